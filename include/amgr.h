@@ -1,0 +1,247 @@
+/*
+ * amgr.h — C-ABI of the B200-native partial-reuse AMG path (libamgr_b200.so).
+ *
+ * This is the drop-in boundary for the reference's C++ solver API
+ * (/root/reference/proj, library `amgreuse`).  Every entry point names the
+ * reference interface it replaces.  The reference's own FFI for this path is
+ * the pybind11 module `_core` declared at proj/CMakeLists.txt:40-82 (its source
+ * python/bindings.cpp is absent from the reference), so the binding a
+ * maintainer adds is a ctypes / pybind / plain C++ stub over these symbols —
+ * see INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or CUDA types in signatures
+ *    (streams are passed as void*, i.e. a cudaStream_t).
+ *  - Index arrays may be int32 or int64 (amgr_csr.index_bits); values are fp64
+ *    (the reference is fp64 throughout, SPEC.md "Real values are 64-bit").
+ *  - Buffers may live on the host or on the device (amgr_csr.location /
+ *    the `location` arguments); device buffers must belong to the context's
+ *    device.  Host buffers are copied in/out inside the call.
+ *  - Errors: every call returns amgr_status.  The message (same text as the
+ *    reference's exception, e.g. "partial update impossible, full rebuild
+ *    required: ...", "level 0: strength_graph: zero diagonal at row 3",
+ *    "setup: coarsening stalled at level ...", "coarse_factorize: singular
+ *    matrix (zero pivot at step k)") is available from amgr_last_error().
+ *    AMGR_E_INVALID_ARGUMENT <-> std::invalid_argument,
+ *    AMGR_E_RUNTIME <-> std::runtime_error.
+ *  - Solver non-convergence / breakdown are NOT errors; they are reported in
+ *    amgr_solve_stats exactly like the reference's SolveStats
+ *    (proj/include/amgreuse/bicgstab.hpp:22-27).
+ *  - Threading: a context (and every hierarchy created from it) is bound to
+ *    one device and one stream; calls on one context must be serialised by
+ *    the caller.  Hierarchies are immutable except through amgr_rebuild
+ *    (the in-place variant of partial_update).
+ */
+#ifndef AMGR_H
+#define AMGR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum amgr_status {
+    AMGR_OK = 0,
+    AMGR_E_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference     */
+    AMGR_E_RUNTIME = 2,          /* std::runtime_error in the reference        */
+    AMGR_E_CUDA = 3,             /* CUDA runtime / launch failure               */
+    AMGR_E_NCCL = 4,             /* NCCL failure (multi-GPU path)               */
+    AMGR_E_DIMENSION = 5         /* partial_update dimension change: the caller
+                                    must do a full setup (reuse.cpp:69-70,84);
+                                    message text identical to the reference's   */
+} amgr_status;
+
+enum { AMGR_HOST = 0, AMGR_DEVICE = 1 };
+
+/* Smoother kinds.  JACOBI is the reference's (smoother.hpp:11-16); SPAI0 and
+ * CHEBYSHEV are north-star extensions with restated oracles (parity unpinned
+ * by the reference). */
+enum { AMGR_SMOOTHER_JACOBI = 0, AMGR_SMOOTHER_SPAI0 = 1, AMGR_SMOOTHER_CHEBYSHEV = 2 };
+/* Coarsening: plain (tentative, piecewise-constant P; the reference's only
+ * kind, coarsening.hpp:48-50) or smoothed aggregation (extension). */
+enum { AMGR_COARSENING_PLAIN = 0, AMGR_COARSENING_SMOOTHED = 1 };
+/* Coarse direct solve: EXACT replays the reference's LU solve order
+ * (dense_lu.cpp:52-73) bit for bit. */
+enum { AMGR_COARSE_EXACT = 0 };
+
+/* CSR input.  Invariants as CsrMatrix (proj/include/amgreuse/csr.hpp:20-27):
+ * row_ptr non-decreasing, row_ptr[0]=0, row_ptr[nrows]=nnz, columns strictly
+ * increasing within a row. */
+typedef struct amgr_csr {
+    int64_t nrows;
+    int64_t ncols;
+    int64_t nnz;
+    const void* row_ptr; /* nrows+1 entries of int32 or int64              */
+    const void* col_idx; /* nnz entries of int32 or int64                  */
+    const double* values;
+    int32_t index_bits;  /* 32 or 64                                       */
+    int32_t location;    /* AMGR_HOST or AMGR_DEVICE                       */
+} amgr_csr;
+
+/* AmgParams (proj/include/amgreuse/hierarchy.hpp:14-21) + extensions. */
+typedef struct amgr_amg_params {
+    double eps;              /* 0.08  strength threshold                    */
+    double omega;            /* 0.72  Jacobi damping                        */
+    int32_t pre_sweeps;      /* 1                                           */
+    int32_t post_sweeps;     /* 1                                           */
+    int64_t coarse_enough;   /* 100                                         */
+    int64_t max_direct_size; /* 2000                                        */
+    int32_t smoother;        /* AMGR_SMOOTHER_*        (extension)          */
+    int32_t coarsening;      /* AMGR_COARSENING_*      (extension)          */
+    double sa_omega;         /* smoothed-aggregation damping (extension)    */
+    int32_t cheb_degree;     /* Chebyshev degree (extension)                */
+    int32_t power_iters;     /* power iterations for lambda_max (extension) */
+    double cheb_lower;       /* lambda_min = cheb_lower * lambda_max        */
+    double cheb_safety;      /* lambda_max safety factor                    */
+} amgr_amg_params;
+
+/* SolveParams (bicgstab.hpp:17-20). */
+typedef struct amgr_solve_params {
+    double tol;       /* 1e-8 */
+    int64_t max_iter; /* 100  */
+} amgr_solve_params;
+
+/* SolveStats (bicgstab.hpp:22-27). */
+typedef struct amgr_solve_stats {
+    int64_t iterations;
+    double relative_residual;
+    int32_t converged;
+    int32_t breakdown;
+} amgr_solve_stats;
+
+/* SetupPhaseTimings (hierarchy.hpp:24-38), seconds, measured with CUDA events
+ * on the context stream. */
+typedef struct amgr_phase_timings {
+    double transfer_ops;
+    double galerkin;
+    double smoother;
+    double coarse_solver;
+} amgr_phase_timings;
+
+typedef struct amgr_ctx amgr_ctx;
+typedef struct amgr_hier amgr_hier;
+
+/* ---- context ------------------------------------------------------------ */
+/* Binds a device and a stream (NULL stream => the library creates its own). */
+amgr_status amgr_ctx_create(int device, void* stream, amgr_ctx** out);
+void amgr_ctx_destroy(amgr_ctx* ctx);
+const char* amgr_last_error(const amgr_ctx* ctx);
+void* amgr_ctx_stream(const amgr_ctx* ctx);
+amgr_status amgr_ctx_synchronize(amgr_ctx* ctx);
+/* Library version string and the compiled architecture ("sm_100a"). */
+const char* amgr_version(void);
+
+/* Defaults of AmgParams / SolveParams (hierarchy.hpp:14-21, bicgstab.hpp:17-20). */
+void amgr_amg_params_default(amgr_amg_params* p);
+void amgr_solve_params_default(amgr_solve_params* p);
+
+/* ---- hierarchy: setup / partial_update / vcycle -------------------------- */
+/* Replaces `Hierarchy setup(const CsrMatrix&, const AmgParams&)`
+ * (hierarchy.hpp:65, hierarchy.cpp:45-105): full AMG setup on the device —
+ * strength graph, exact replay of the sequential greedy aggregation,
+ * P/R, symbolic + numeric Galerkin product, smoothers, coarse LU. */
+amgr_status amgr_setup(amgr_ctx* ctx, const amgr_csr* A, const amgr_amg_params* prm,
+                       amgr_hier** out);
+
+/* Replaces `Hierarchy partial_update(const Hierarchy&, CsrMatrix, const AmgParams&)`
+ * (hierarchy.hpp:71, hierarchy.cpp:107-150): returns a NEW hierarchy that
+ * shares the frozen transfer operators (and the cached Galerkin pattern) of
+ * `h`; level matrices, smoothers and the coarse LU are recomputed from A_new.
+ * A pattern change (same dimensions) re-runs the symbolic product.
+ * Dimension change => AMGR_E_DIMENSION with the reference's message. */
+amgr_status amgr_partial_update(const amgr_hier* h, const amgr_csr* A_new,
+                                const amgr_amg_params* prm, amgr_hier** out);
+
+/* In-place partial update ("rebuild(A)"): same semantics as
+ * amgr_partial_update but overwrites `h` (no allocation on the values-only
+ * path).  This is the per-time-step hot path. */
+amgr_status amgr_rebuild(amgr_hier* h, const amgr_csr* A_new);
+
+/* Values-only rebuild: `values` are the new A_0 entries in the CSR order of
+ * the hierarchy's finest pattern (nnz of level 0 entries).  The caller
+ * asserts the pattern is unchanged. */
+amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location);
+
+/* Replaces `std::vector<double> vcycle(const Hierarchy&, span f, const AmgParams&)`
+ * (hierarchy.hpp:75-76, hierarchy.cpp:152-186) with the smoothing the
+ * reference's documentation specifies.  f/u have
+ * finest_size entries on `location`. */
+amgr_status amgr_vcycle(amgr_hier* h, const double* f, double* u, int location);
+
+void amgr_hier_destroy(amgr_hier* h);
+
+/* ---- Krylov ------------------------------------------------------------- */
+/* Replaces `bicgstab(make_operator(A), make_preconditioner(h), f, u0, prm)`
+ * (bicgstab.hpp:34-44, bicgstab.cpp:21-135): right-preconditioned BiCGStab,
+ * A = the hierarchy's finest matrix, M = one V-cycle.  u0 may equal u. */
+amgr_status amgr_bicgstab(amgr_hier* h, const double* f, const double* u0, double* u,
+                          const amgr_solve_params* prm, amgr_solve_stats* stats, int location);
+
+/* Preconditioned CG (extension; SPEC.md lists CG as a non-goal of the
+ * reference — restated oracle, parity unpinned). */
+amgr_status amgr_cg(amgr_hier* h, const double* f, const double* u0, double* u,
+                    const amgr_solve_params* prm, amgr_solve_stats* stats, int location);
+
+/* y = A_level x (spmv, csr.hpp:77 / csr.cpp:76-85) on one level. */
+amgr_status amgr_spmv(amgr_hier* h, int level, const double* x, double* y, int location);
+
+/* ---- introspection / download (parity dumps) ----------------------------- */
+/* Number of levels, finest first (Hierarchy::num_levels, hierarchy.hpp:54). */
+int amgr_hier_num_levels(const amgr_hier* h);
+/* dims[0]=nrows, dims[1]=nnz, dims[2]=n_coarse (0 on the coarsest level),
+ * dims[3]=has_smoother. */
+amgr_status amgr_hier_level_dims(const amgr_hier* h, int level, int64_t* dims);
+/* A_level as int64 CSR (row_ptr nrows+1, col nnz, values nnz) into host buffers. */
+amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col,
+                              double* values);
+/* Aggregate id of every fine row (= col_idx of the tentative P,
+ * coarsening.cpp:122-132) and R = P^T as CSR (row_ptr n_coarse+1, col n). */
+amgr_status amgr_hier_level_P(const amgr_hier* h, int level, int64_t* agg);
+amgr_status amgr_hier_level_R(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col);
+/* Smoother state: inv_diag (JacobiSmoother::inv_diag, smoother.hpp:11-16). */
+amgr_status amgr_hier_level_smoother(const amgr_hier* h, int level, double* inv_diag);
+/* Coarse LU (DenseFactorization, dense_lu.hpp:12-18): lu n*n row-major, piv n. */
+int64_t amgr_hier_coarse_n(const amgr_hier* h);
+amgr_status amgr_hier_coarse_lu(const amgr_hier* h, double* lu, int64_t* piv);
+/* Hierarchy::operator_complexity (hierarchy.cpp:39-43). */
+double amgr_hier_operator_complexity(const amgr_hier* h);
+/* setup_timings of the last setup / partial update / rebuild. */
+amgr_status amgr_hier_timings(const amgr_hier* h, amgr_phase_timings* t);
+/* Shared-transfer identity check (test_hierarchy.cpp:111-121 analogue):
+ * returns 1 when both hierarchies share the same frozen P/R objects. */
+int amgr_hier_shares_transfer(const amgr_hier* a, const amgr_hier* b, int level);
+
+/* ---- synthetic problem sequences on the device ---------- */
+enum {
+    AMGR_PROBLEM_POISSON = 0,   /* 7-point Laplacian + shift s_k (config C1)     */
+    AMGR_PROBLEM_BLOB = 1,      /* moving high-contrast blob kappa (config C2)  */
+    AMGR_PROBLEM_DAMBREAK = 2,  /* 1000:1 collapsing water column (C3/C4)       */
+    AMGR_PROBLEM_CONVDIFF = 3   /* upwind convection-diffusion (C5)             */
+};
+/* Pattern of the g^3 7-point operator: int32 CSR written to device buffers
+ * (row_ptr n+1, col nnz).  nnz = 7g^3 - 6g^2. */
+int64_t amgr_problem_nnz(int64_t g);
+amgr_status amgr_problem_pattern(amgr_ctx* ctx, int64_t g, int32_t* row_ptr, int32_t* col);
+/* Values of step k of `kind` (same CSR order) into a device buffer. */
+amgr_status amgr_problem_values(amgr_ctx* ctx, int kind, int64_t g, int64_t k, int64_t nsteps,
+                                double* values);
+/* RHS f_i ~ U(0.1, 1.0) from std::mt19937_64(seed) (diffusion.cpp:38-41),
+ * generated on the host and written to `location`. */
+amgr_status amgr_problem_rhs(amgr_ctx* ctx, int64_t n, uint64_t seed, double* out, int location);
+
+/* ---- measurement hooks ----------------------------------------------------- */
+/* Kernel probe: when enabled, every launch of the named kernel family
+ * ("rap", "vcycle_down", "vcycle_up", "spmv", ...) is bracketed by CUDA events
+ * on the launching stream; amgr_probe_read returns launches, total device ms
+ * and the algorithmic bytes those launches moved. */
+amgr_status amgr_probe_enable(amgr_ctx* ctx, const char* family);
+amgr_status amgr_probe_read(amgr_ctx* ctx, int64_t* launches, double* ms, double* bytes);
+/* Number of kernel launches the library issued on this context so far. */
+int64_t amgr_launch_count(const amgr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMGR_H */

@@ -1,0 +1,703 @@
+// Host orchestration of the device AMG hierarchy.  Each function cites the
+// reference function whose semantics (order of phases, error texts, timing
+// buckets) it reproduces.
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "hierarchy.cuh"
+
+namespace amgr {
+
+AmgP to_amgp(const amgr_amg_params* p) {
+    AmgP a;
+    if (!p) return a;
+    a.eps = p->eps;
+    a.omega = p->omega;
+    a.pre = p->pre_sweeps;
+    a.post = p->post_sweeps;
+    a.coarse_enough = p->coarse_enough;
+    a.max_direct = p->max_direct_size;
+    a.smoother = p->smoother;
+    a.coarsening = p->coarsening;
+    a.sa_omega = p->sa_omega;
+    a.cheb_degree = p->cheb_degree;
+    a.power_iters = p->power_iters;
+    a.cheb_lower = p->cheb_lower;
+    a.cheb_safety = p->cheb_safety;
+    return a;
+}
+
+namespace {
+
+// ---- phase timers (SetupPhaseTimings, hierarchy.cpp:17-29) -------------------
+enum Phase { PH_TRANSFER = 0, PH_GALERKIN = 1, PH_SMOOTHER = 2, PH_COARSE = 3 };
+
+struct PhaseClock {
+    Ctx& c;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
+    explicit PhaseClock(Ctx& cc) : c(cc) {}
+    ~PhaseClock() {
+        for (auto& v : ev)
+            for (auto& p : v) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+    }
+    void begin(Phase ph) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, c.stream));
+        ev[ph].push_back({a, b});
+    }
+    void end(Phase ph) { CK(cudaEventRecord(ev[ph].back().second, c.stream)); }
+    // requires the stream to have passed the last event
+    amgr_phase_timings collect() {
+        CK(cudaStreamSynchronize(c.stream));
+        double t[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 4; ++k)
+            for (auto& p : ev[k]) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, p.first, p.second));
+                t[k] += ms * 1e-3;
+            }
+        return amgr_phase_timings{t[0], t[1], t[2], t[3]};
+    }
+};
+
+std::string level_prefix(size_t l) {
+    std::ostringstream os;
+    os << "level " << l << ": ";
+    return os.str();
+}
+
+// Upload / adopt an amgr_csr pattern into int32 device arrays.
+std::shared_ptr<Pattern> make_pattern(Ctx& c, const amgr_csr& A) {
+    auto P = std::make_shared<Pattern>();
+    P->n = A.nrows;
+    P->ncols = A.ncols;
+    P->nnz = A.nnz;
+    if (A.nnz > INT32_MAX - 1 || A.nrows > INT32_MAX - 1 || A.ncols > INT32_MAX - 1)
+        invalid("matrix too large for int32 device indices (> 2^31 entries per GPU)");
+    P->rp.alloc(A.nrows + 1, c.stream);
+    P->col.alloc(A.nnz, c.stream);
+    const bool dev = A.location == AMGR_DEVICE;
+    auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (A.index_bits == 32) {
+        CK(cudaMemcpyAsync(P->rp.get(), A.row_ptr, sizeof(int) * (A.nrows + 1), kind, c.stream));
+        if (A.nnz) CK(cudaMemcpyAsync(P->col.get(), A.col_idx, sizeof(int) * A.nnz, kind, c.stream));
+    } else if (A.index_bits == 64) {
+        DevArray<int> ovf(1, c.stream);
+        CK(cudaMemsetAsync(ovf.get(), 0, sizeof(int), c.stream));
+        DevArray<int64_t> tmp(std::max<int64_t>(A.nrows + 1, A.nnz), c.stream);
+        CK(cudaMemcpyAsync(tmp.get(), A.row_ptr, sizeof(int64_t) * (A.nrows + 1), kind, c.stream));
+        i64_to_i32(c, tmp.get(), P->rp.get(), A.nrows + 1, ovf.get());
+        if (A.nnz) {
+            CK(cudaMemcpyAsync(tmp.get(), A.col_idx, sizeof(int64_t) * A.nnz, kind, c.stream));
+            i64_to_i32(c, tmp.get(), P->col.get(), A.nnz, ovf.get());
+        }
+        if (d2h_scalar(ovf.get(), c.stream)) invalid("index out of int32 range");
+    } else {
+        invalid("amgr_csr.index_bits must be 32 or 64");
+    }
+    P->diag.alloc(A.nrows, c.stream);
+    CsrView v;
+    v.n = P->n;
+    v.ncols = P->ncols;
+    v.nnz = P->nnz;
+    v.rp = P->rp.get();
+    v.col = P->col.get();
+    find_diag(c, v, P->diag.get());
+    return P;
+}
+
+void upload_values(Ctx& c, DevArray<double>& dst, const double* src, int64_t nnz, int location) {
+    if (dst.size() != nnz) dst.alloc(nnz, c.stream);
+    if (nnz == 0) return;
+    CK(cudaMemcpyAsync(dst.get(), src, sizeof(double) * nnz,
+                       location == AMGR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+}
+
+bool same_pattern(Ctx& c, const Pattern& a, const Pattern& b) {
+    if (a.n != b.n || a.ncols != b.ncols || a.nnz != b.nnz) return false;
+    DevArray<int> diff(1, c.stream);
+    CK(cudaMemsetAsync(diff.get(), 0, sizeof(int), c.stream));
+    compare_i32(c, a.rp.get(), b.rp.get(), a.n + 1, diff.get());
+    compare_i32(c, a.col.get(), b.col.get(), a.nnz, diff.get());
+    return d2h_scalar(diff.get(), c.stream) == 0;
+}
+
+// Smoother rebuild of level l (build_smoother, smoother.cpp:8-32; SPAI0 ext.).
+void build_smoother(Ctx& c, Level& L, const AmgP& p, int* bad) {
+    const int64_t n = L.pat->n;
+    if (L.w.size() != n) L.w.alloc(n, c.stream);
+    if (p.smoother == AMGR_SMOOTHER_SPAI0)
+        spai0_rebuild(c, L.view(), L.pat->diag.get(), L.w.get(), bad);
+    else
+        jacobi_rebuild(c, n, L.val.get(), L.pat->diag.get(), L.w.get(), bad);
+    L.has_smoother = true;
+}
+
+void coarse_factorize(Hier& h, int* status) {
+    Ctx& c = *h.ctx;
+    const Level& L = h.lv.back();
+    h.nL = L.pat->n;
+    if (h.lu.size() != h.nL * h.nL) h.lu.alloc(h.nL * h.nL, c.stream);
+    if (h.piv.size() != h.nL) h.piv.alloc(h.nL, c.stream);
+    lu_densify(c, L.view(), h.lu.get());
+    lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
+}
+
+void throw_lu(int st) {
+    std::ostringstream os;
+    os << "coarse_factorize: singular matrix (zero pivot at step " << st << ")";
+    fail(AMGR_E_RUNTIME, os.str());
+}
+
+// Read the per-level smoother bad-row slots and the LU status in one sync
+// and throw the first error in the reference's order.
+void check_rebuild_errors(Hier& h, const char* what) {
+    Work& W = work(h);
+    const size_t L = h.lv.size();
+    std::vector<int> e(L + 1);
+    d2h(e.data(), W.err.get(), static_cast<int64_t>(L + 1), h.ctx->stream);
+    CK(cudaStreamSynchronize(h.ctx->stream));
+    for (size_t l = 0; l + 1 < L; ++l)
+        if (e[l] != 0x7fffffff) {
+            std::ostringstream os;
+            os << level_prefix(l) << what << ": zero diagonal at row " << e[l];
+            invalid(os.str());
+        }
+    if (e[L] >= 0) throw_lu(e[L]);
+}
+
+void reset_err(Hier& h) {
+    Work& W = work(h);
+    std::vector<int> e(h.lv.size() + 1, 0x7fffffff);
+    e.back() = -1;
+    h2d(W.err.get(), e.data(), static_cast<int64_t>(e.size()), h.ctx->stream);
+}
+
+// Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans.
+void numeric_pass(Hier& h, PhaseClock& clk) {
+    Ctx& c = *h.ctx;
+    Work& W = work(h);
+    const size_t L = h.lv.size();
+    for (size_t i = 0; i + 1 < L; ++i) {
+        Level& A = h.lv[i];
+        clk.begin(PH_SMOOTHER);
+        build_smoother(c, A, h.prm, W.err.get() + i);
+        clk.end(PH_SMOOTHER);
+        clk.begin(PH_GALERKIN);
+        Level& B = h.lv[i + 1];
+        if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
+        rap_numeric(c, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.val.get(), B.val.get(), A.pat->nnz);
+        clk.end(PH_GALERKIN);
+    }
+    clk.begin(PH_COARSE);
+    coarse_factorize(h, W.err.get() + L);
+    clk.end(PH_COARSE);
+}
+
+// Symbolic pass with frozen transfers (pattern change under partial reuse).
+void symbolic_pass(Hier& h) {
+    Ctx& c = *h.ctx;
+    for (size_t i = 0; i + 1 < h.lv.size(); ++i) {
+        Level& A = h.lv[i];
+        RapSymbolic s;
+        rap_symbolic(c, A.view(), A.T->agg.get(), A.T->nc, s);
+        auto plan = std::make_shared<RapPlan>();
+        plan->nnz_f = A.pat->nnz;
+        plan->nnz_c = s.nnz_c;
+        plan->cptr = std::move(s.cptr);
+        plan->contrib = std::move(s.contrib);
+        A.rap = plan;
+        auto P = std::make_shared<Pattern>();
+        P->n = A.T->nc;
+        P->ncols = A.T->nc;
+        P->nnz = s.nnz_c;
+        P->rp = std::move(s.rp);
+        P->col = std::move(s.col);
+        P->diag.alloc(P->n, c.stream);
+        Level& B = h.lv[i + 1];
+        B.pat = P;
+        CsrView v = B.view();
+        find_diag(c, v, P->diag.get());
+    }
+}
+
+}  // namespace
+
+Work& work(Hier& h) {
+    Ctx& c = *h.ctx;
+    std::vector<int64_t> shape;
+    for (auto& l : h.lv) shape.push_back(l.pat->n);
+    if (!h.ws || h.ws->shape != shape) {
+        auto W = std::make_shared<Work>();
+        W->shape = shape;
+        const size_t L = h.lv.size();
+        W->u.resize(L);
+        W->t.resize(L);
+        W->f.resize(L);
+        W->r.resize(L);
+        for (size_t i = 0; i < L; ++i) {
+            const int64_t n = h.lv[i].pat->n;
+            W->u[i].alloc(n, c.stream);
+            W->t[i].alloc(n, c.stream);
+            if (i > 0) W->f[i].alloc(n, c.stream);
+            W->r[i].alloc(n, c.stream);
+        }
+        W->st.alloc(1, c.stream);
+        W->partials.alloc(static_cast<int64_t>(dot_grid(c)) * 4, c.stream);
+        W->ticket.alloc(1, c.stream);
+        CK(cudaMemsetAsync(W->ticket.get(), 0, sizeof(unsigned), c.stream));
+        W->err.alloc(static_cast<int64_t>(L + 1), c.stream);
+        h.ws = W;
+    }
+    return *h.ws;
+}
+
+// ---- setup (hierarchy.cpp:45-105) ------------------------------------------------
+std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
+    if (A.nrows != A.ncols) invalid("setup: matrix is not square");
+    if (A.nrows == 0) invalid("setup: empty matrix");
+    auto h = std::make_unique<Hier>();
+    h->ctx = &c;
+    h->prm = p;
+    PhaseClock clk(c);
+
+    Level L0;
+    L0.pat = make_pattern(c, A);
+    upload_values(c, L0.val, A.values, A.nnz, A.location);
+    h->lv.push_back(std::move(L0));
+    DevArray<int> bad(1, c.stream);
+    DevArray<int> lu_status(1, c.stream);
+
+    while (h->lv.back().pat->n > p.coarse_enough) {
+        const size_t l = h->lv.size() - 1;
+        Level& cur = h->lv.back();
+        const CsrView Av = cur.view();
+        auto T = std::make_shared<Transfer>();
+        int64_t nc = 0;
+        clk.begin(PH_TRANSFER);
+        {
+            // strength_graph (coarsening.cpp:11-34) error order: eps, then diagonal
+            if (p.eps < 0.0 || p.eps >= 1.0) invalid(level_prefix(l) + "strength_graph: eps must be in [0, 1)");
+            const int64_t badrow = first_bad_diag(c, Av, cur.pat->diag.get());
+            if (badrow >= 0) {
+                std::ostringstream os;
+                os << level_prefix(l) << "strength_graph: zero diagonal at row " << badrow;
+                invalid(os.str());
+            }
+            GraphDev g;
+            strength_graph(c, Av, cur.pat->diag.get(), p.eps * p.eps, g);
+            int64_t rounds = 0;
+            nc = aggregate(c, g, T->agg, &rounds);
+            h->agg_rounds += rounds;
+            T->nf = Av.n;
+            T->nc = nc;
+            if (nc < Av.n) members(c, Av.n, nc, T->agg.get(), T->mptr, T->midx);
+        }
+        clk.end(PH_TRANSFER);
+        if (nc == Av.n) {
+            // coarsening stalled (hierarchy.cpp:70-77)
+            if (Av.n <= p.max_direct) break;
+            std::ostringstream os;
+            os << "setup: coarsening stalled at level " << l << " with " << Av.n
+               << " unknowns (> max_direct_size " << p.max_direct << ")";
+            fail(AMGR_E_RUNTIME, os.str());
+        }
+        // smoother (hierarchy.cpp:79-87)
+        {
+            const int big = 0x7fffffff;
+            h2d(bad.get(), &big, 1, c.stream);
+            clk.begin(PH_SMOOTHER);
+            build_smoother(c, cur, p, bad.get());
+            clk.end(PH_SMOOTHER);
+            const int b = d2h_scalar(bad.get(), c.stream);
+            if (b != big) {
+                std::ostringstream os;
+                os << level_prefix(l) << "build_smoother: zero diagonal at row " << b;
+                invalid(os.str());
+            }
+        }
+        // Galerkin product (hierarchy.cpp:89-93): symbolic plan + numeric values
+        Level next;
+        clk.begin(PH_GALERKIN);
+        {
+            RapSymbolic s;
+            rap_symbolic(c, Av, T->agg.get(), nc, s);
+            auto plan = std::make_shared<RapPlan>();
+            plan->nnz_f = Av.nnz;
+            plan->nnz_c = s.nnz_c;
+            plan->cptr = std::move(s.cptr);
+            plan->contrib = std::move(s.contrib);
+            auto P = std::make_shared<Pattern>();
+            P->n = nc;
+            P->ncols = nc;
+            P->nnz = s.nnz_c;
+            P->rp = std::move(s.rp);
+            P->col = std::move(s.col);
+            P->diag.alloc(nc, c.stream);
+            next.pat = P;
+            next.val.alloc(s.nnz_c, c.stream);
+            rap_numeric(c, s.nnz_c, plan->cptr.get(), plan->contrib.get(), cur.val.get(), next.val.get(), Av.nnz);
+            CsrView nv = next.view();
+            find_diag(c, nv, P->diag.get());
+            cur.rap = plan;
+        }
+        clk.end(PH_GALERKIN);
+        cur.T = T;
+        h->lv.push_back(std::move(next));
+    }
+    clk.begin(PH_COARSE);
+    coarse_factorize(*h, lu_status.get());
+    clk.end(PH_COARSE);
+    const int st = d2h_scalar(lu_status.get(), c.stream);
+    if (st >= 0) throw_lu(st);
+    h->tm = clk.collect();
+    work(*h);
+    return h;
+}
+
+// ---- partial_update (hierarchy.cpp:107-150) -----------------------------------------
+static void check_dims(const Hier& h, const amgr_csr& A) {
+    const Pattern& P0 = *h.lv.front().pat;
+    if (A.nrows != P0.n || A.ncols != P0.ncols) {
+        std::ostringstream os;
+        os << "partial update impossible, full rebuild required: new matrix is " << A.nrows << "x" << A.ncols
+           << ", hierarchy was built for " << P0.n << "x" << P0.ncols;
+        fail(AMGR_E_DIMENSION, os.str());
+    }
+}
+
+static void rebuild_into(Hier& h, const amgr_csr& A) {
+    Ctx& c = *h.ctx;
+    // pattern: reuse the cached symbolic plan unless the structure changed
+    std::shared_ptr<Pattern> np = make_pattern(c, A);
+    const bool same = same_pattern(c, *np, *h.lv.front().pat);
+    upload_values(c, h.lv.front().val, A.values, A.nnz, A.location);
+    if (!same) {
+        h.lv.front().pat = np;
+        symbolic_pass(h);
+        h.ws.reset();
+    }
+    work(h);
+    reset_err(h);
+    PhaseClock clk(c);
+    numeric_pass(h, clk);
+    check_rebuild_errors(h, "build_smoother");
+    h.tm = clk.collect();
+}
+
+std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const AmgP& p) {
+    if (h.lv.empty()) invalid("partial_update: empty hierarchy");
+    check_dims(h, A);
+    Ctx& c = *h.ctx;
+    auto out = std::make_unique<Hier>();
+    out->ctx = &c;
+    out->prm = p;
+    out->ws = h.ws;
+    out->agg_rounds = 0;
+    for (const Level& L : h.lv) {
+        Level n;
+        n.pat = L.pat;  // shared structure
+        n.T = L.T;      // shared frozen transfer operators
+        n.rap = L.rap;  // shared cached Galerkin plan
+        out->lv.push_back(std::move(n));
+    }
+    for (size_t i = 0; i < out->lv.size(); ++i) out->lv[i].val.alloc(out->lv[i].pat->nnz, c.stream);
+    rebuild_into(*out, A);
+    return out;
+}
+
+void rebuild(Hier& h, const amgr_csr& A) {
+    check_dims(h, A);
+    rebuild_into(h, A);
+}
+
+void rebuild_values(Hier& h, const double* values, int location) {
+    Ctx& c = *h.ctx;
+    upload_values(c, h.lv.front().val, values, h.lv.front().pat->nnz, location);
+    work(h);
+    reset_err(h);
+    PhaseClock clk(c);
+    numeric_pass(h, clk);
+    check_rebuild_errors(h, "build_smoother");
+    h.tm = clk.collect();
+}
+
+// ---- V-cycle (hierarchy.cpp:152-186, smoothing as specified) --------
+void vcycle(Hier& h, const double* f, double* u, Gate g) {
+    Ctx& c = *h.ctx;
+    Work& W = work(h);
+    const size_t L = h.lv.size();
+    const double om = h.om_eff();
+    if (L == 1) {
+        lu_solve(c, h.nL, h.lu.get(), h.piv.get(), f, u, g);
+        return;
+    }
+    std::vector<const double*> fin(L), ufinal(L);
+    fin[0] = f;
+    for (size_t i = 1; i < L; ++i) fin[i] = W.f[i].get();
+    std::vector<double*> cur(L);
+    // down leg
+    for (size_t i = 0; i + 1 < L; ++i) {
+        const Level& Li = h.lv[i];
+        const CsrView A = Li.view();
+        double* a = W.u[i].get();
+        double* b = W.t[i].get();
+        double* r = W.r[i].get();
+        if (h.prm.pre <= 0) {
+            fill(c, a, A.n, 0.0, g);
+            copy(c, r, fin[i], A.n, g);
+            cur[i] = a;
+        } else {
+            vc_down(c, A, fin[i], Li.w.get(), om, a, r, g);
+            double* src = a;
+            double* dst = b;
+            for (int s = 1; s < h.prm.pre; ++s) {
+                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+                std::swap(src, dst);
+            }
+            if (h.prm.pre > 1) residual(c, A, fin[i], src, r, g);
+            cur[i] = src;
+        }
+        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, W.f[i + 1].get(), g);
+    }
+    // coarsest: direct solve (hierarchy.cpp:175)
+    lu_solve(c, h.nL, h.lu.get(), h.piv.get(), W.f[L - 1].get(), W.u[L - 1].get(), g);
+    ufinal[L - 1] = W.u[L - 1].get();
+    // up leg
+    for (size_t i = L - 1; i-- > 0;) {
+        const Level& Li = h.lv[i];
+        const CsrView A = Li.view();
+        double* a = cur[i];
+        double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
+        const int post = h.prm.post;
+        auto target = [&](int k) -> double* {  // output of write k (1-based)
+            if (i == 0 && k == std::max(post, 1)) return u;
+            return (k % 2 == 1) ? b : a;
+        };
+        if (post <= 0) {
+            double* t = target(1);
+            vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], t, g);
+            ufinal[i] = t;
+        } else {
+            double* t = target(1);
+            vc_up(c, A, fin[i], Li.w.get(), om, a, Li.T->agg.get(), ufinal[i + 1], t, g);
+            double* src = t;
+            for (int k = 2; k <= post; ++k) {
+                double* dst = target(k);
+                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+                src = dst;
+            }
+            ufinal[i] = src;
+        }
+    }
+}
+
+// ---- BiCGStab (bicgstab.cpp:21-135) ------------------------------------------------
+namespace {
+
+struct KrylovBufs {
+    double *r, *rt, *p, *v, *s, *t, *ph, *sh;
+};
+
+KrylovBufs krylov_bufs(Hier& h) {
+    Work& W = work(h);
+    Ctx& c = *h.ctx;
+    const int64_t n = h.lv.front().pat->n;
+    if (W.kr.size() != n) {
+        W.kr.alloc(n, c.stream);
+        W.krt.alloc(n, c.stream);
+        W.kp.alloc(n, c.stream);
+        W.kv.alloc(n, c.stream);
+        W.ks.alloc(n, c.stream);
+        W.kt.alloc(n, c.stream);
+        W.kph.alloc(n, c.stream);
+        W.ksh.alloc(n, c.stream);
+    }
+    return {W.kr.get(), W.krt.get(), W.kp.get(), W.kv.get(), W.ks.get(), W.kt.get(), W.kph.get(), W.ksh.get()};
+}
+
+DotSink sink(Hier& h, double* out) {
+    Work& W = work(h);
+    return DotSink{W.partials.get(), W.ticket.get(), out};
+}
+
+KState read_state(Hier& h) {
+    KState s;
+    d2h(&s, work(h).st.get(), 1, h.ctx->stream);
+    CK(cudaStreamSynchronize(h.ctx->stream));
+    return s;
+}
+
+void write_state(Hier& h, const KState& s) {
+    h2d(work(h).st.get(), &s, 1, h.ctx->stream);
+}
+
+#define ST_FIELD(st, f) (&(st)->f)
+
+}  // namespace
+
+void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
+              amgr_solve_stats& out) {
+    if (sp.tol <= 0.0) invalid("bicgstab: tol must be positive");
+    if (sp.max_iter < 1) invalid("bicgstab: max_iter must be >= 1");
+    Ctx& c = *h.ctx;
+    const CsrView A = h.lv.front().view();
+    const int64_t n = A.n;
+    KrylovBufs B = krylov_bufs(h);
+    KState* st = work(h).st.get();
+    out = amgr_solve_stats{0, 0.0, 0, 0};
+
+    KState s0;
+    write_state(h, s0);
+    dot(c, n, f, f, sink(h, ST_FIELD(st, d_true)));
+    KState s = read_state(h);
+    const double normf = std::sqrt(s.d_true);
+    if (normf == 0.0) {
+        fill(c, u, n, 0.0);
+        out.converged = 1;
+        return;
+    }
+    if (u != u0) copy(c, u, u0, n);
+    // r = f - A u ; rtilde = r   (bicgstab.cpp:41-43)
+    resid_norm(c, A, f, u, B.r, B.rt, sink(h, ST_FIELD(st, d_rr)));
+    dot(c, n, B.rt, B.r, sink(h, ST_FIELD(st, d_rtr)));
+    s = read_state(h);
+    out.relative_residual = std::sqrt(s.d_rr) / normf;
+    if (out.relative_residual <= sp.tol) {
+        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+        s = read_state(h);
+        out.relative_residual = std::sqrt(s.d_true) / normf;
+        if (out.relative_residual <= sp.tol) {
+            out.converged = 1;
+            return;
+        }
+    }
+    s.normf = normf;
+    s.floor = 1e-30 * normf * normf;
+    s.tol = sp.tol;
+    s.max_iter = sp.max_iter;
+    s.rho_old = 1.0;
+    s.alpha = 1.0;
+    s.omega = 1.0;
+    s.it = 0;
+    s.flags = 0;
+    write_state(h, s);
+
+    const Gate G = gate_of(st, KF_DONE);
+    const Gate GH = gate_of(st, KF_DONE, KF_HALF);
+    const Gate GF = gate_of(st, KF_DONE | KF_HALF);
+    const Gate GC = gate_of(st, KF_DONE | KF_HALF, KF_CHECK);
+    for (;;) {
+        bicg_begin(c, st);
+        bicg_p(c, st, n, B.r, B.p, B.v);
+        vcycle(h, B.p, B.ph, G);
+        spmv_dot(c, A, B.ph, B.v, B.rt, sink(h, ST_FIELD(st, d_rtv)), G);
+        bicg_alpha(c, st);
+        bicg_s(c, st, n, B.r, B.v, B.s, sink(h, ST_FIELD(st, d_ss)));
+        bicg_half_test(c, st);
+        bicg_half_u(c, st, n, u, B.ph);
+        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GH);
+        bicg_half_check(c, st);
+        bicg_half_r(c, st, n, B.r, B.s);
+        vcycle(h, B.s, B.sh, GF);
+        spmv_dot2(c, A, B.sh, B.t, B.s, sink(h, ST_FIELD(st, d_ts)), GF);
+        bicg_omega(c, st);
+        bicg_update(c, st, n, u, B.ph, B.sh, B.r, B.s, B.t, B.rt, sink(h, ST_FIELD(st, d_rr)));
+        bicg_end_test(c, st);
+        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GC);
+        bicg_end_check(c, st);
+        s = read_state(h);
+        if (s.flags & KF_DONE) break;
+    }
+    out.iterations = s.it;
+    if (s.flags & KF_CONVERGED) {
+        out.converged = 1;
+        out.relative_residual = s.res;
+        return;
+    }
+    out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
+    resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+    s = read_state(h);
+    out.relative_residual = std::sqrt(s.d_true) / normf;
+    out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;
+}
+
+// ---- preconditioned CG (extension; restated oracle in oracle/amg_oracle.c) ------------
+void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
+        amgr_solve_stats& out) {
+    if (sp.tol <= 0.0) invalid("cg: tol must be positive");
+    if (sp.max_iter < 1) invalid("cg: max_iter must be >= 1");
+    Ctx& c = *h.ctx;
+    const CsrView A = h.lv.front().view();
+    const int64_t n = A.n;
+    KrylovBufs B = krylov_bufs(h);
+    KState* st = work(h).st.get();
+    out = amgr_solve_stats{0, 0.0, 0, 0};
+    KState s0;
+    write_state(h, s0);
+    dot(c, n, f, f, sink(h, ST_FIELD(st, d_true)));
+    KState s = read_state(h);
+    const double normf = std::sqrt(s.d_true);
+    if (normf == 0.0) {
+        fill(c, u, n, 0.0);
+        out.converged = 1;
+        return;
+    }
+    if (u != u0) copy(c, u, u0, n);
+    resid_norm(c, A, f, u, B.r, nullptr, sink(h, ST_FIELD(st, d_rr)));
+    s = read_state(h);
+    out.relative_residual = std::sqrt(s.d_rr) / normf;
+    if (out.relative_residual <= sp.tol) {
+        out.converged = 1;
+        return;
+    }
+    // z = M r ; p = z ; rho = r.z
+    vcycle(h, B.r, B.s, {});
+    copy(c, B.p, B.s, n);
+    dot(c, n, B.r, B.s, sink(h, ST_FIELD(st, d_rz)));
+    s = read_state(h);
+    s.normf = normf;
+    s.floor = 1e-30 * normf * normf;
+    s.tol = sp.tol;
+    s.max_iter = sp.max_iter;
+    s.rho = s.d_rz;
+    s.it = 0;
+    s.flags = 0;
+    write_state(h, s);
+    const Gate G = gate_of(st, KF_DONE);
+    const Gate GC = gate_of(st, KF_DONE, KF_CHECK);
+    for (;;) {
+        cg_begin(c, st);
+        spmv_dot(c, A, B.p, B.v, B.p, sink(h, ST_FIELD(st, d_pq)), G);
+        cg_alpha(c, st);
+        cg_update(c, st, n, u, B.r, B.p, B.v, sink(h, ST_FIELD(st, d_rr)));
+        cg_test(c, st);
+        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GC);
+        cg_check(c, st);
+        vcycle(h, B.r, B.s, G);
+        dot(c, n, B.r, B.s, sink(h, ST_FIELD(st, d_rz)), G);
+        cg_beta(c, st);
+        cg_p(c, st, n, B.s, B.p);
+        s = read_state(h);
+        if (s.flags & KF_DONE) break;
+    }
+    out.iterations = s.it;
+    if (s.flags & KF_CONVERGED) {
+        out.converged = 1;
+        out.relative_residual = s.res;
+        return;
+    }
+    out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
+    resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+    s = read_state(h);
+    out.relative_residual = std::sqrt(s.d_true) / normf;
+    out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;
+}
+
+}  // namespace amgr

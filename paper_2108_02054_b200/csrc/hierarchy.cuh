@@ -1,0 +1,108 @@
+// Host-side orchestration of the device hierarchy (C++).  Mirrors the
+// reference's Hierarchy / setup / partial_update / vcycle / bicgstab
+// (proj/include/amgreuse/hierarchy.hpp, bicgstab.hpp) with device storage.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "krylov.cuh"
+#include "setup.cuh"
+
+namespace amgr {
+
+struct AmgP {
+    double eps = 0.08, omega = 0.72;
+    int pre = 1, post = 1;
+    int64_t coarse_enough = 100, max_direct = 2000;
+    int smoother = AMGR_SMOOTHER_JACOBI;
+    int coarsening = AMGR_COARSENING_PLAIN;
+    double sa_omega = 2.0 / 3.0;
+    int cheb_degree = 3, power_iters = 10;
+    double cheb_lower = 1.0 / 30.0, cheb_safety = 1.1;
+};
+AmgP to_amgp(const amgr_amg_params* p);
+
+// Structure of one level's operator (immutable, shared between hierarchies).
+struct Pattern {
+    int64_t n = 0, ncols = 0, nnz = 0;
+    DevArray<int> rp, col, diag;
+};
+// Frozen transfer operators of one level: P (agg) and R = P^T (mptr/midx).
+struct Transfer {
+    int64_t nf = 0, nc = 0;
+    DevArray<int> agg, mptr, midx;
+};
+// Cached Galerkin plan A_i -> A_{i+1}.
+struct RapPlan {
+    int64_t nnz_f = 0, nnz_c = 0;
+    DevArray<int> cptr, contrib;
+};
+
+struct Level {
+    std::shared_ptr<Pattern> pat;
+    DevArray<double> val;  // A_i values
+    DevArray<double> w;    // smoother diagonal (inv_diag for Jacobi)
+    bool has_smoother = false;
+    std::shared_ptr<Transfer> T;   // null on the coarsest level
+    std::shared_ptr<RapPlan> rap;  // null on the coarsest level
+    CsrView view() const {
+        CsrView v;
+        v.n = pat->n;
+        v.ncols = pat->ncols;
+        v.nnz = pat->nnz;
+        v.rp = pat->rp.get();
+        v.col = pat->col.get();
+        v.val = val.get();
+        return v;
+    }
+};
+
+// Per-shape work vectors, shared by hierarchies of the same shape (one
+// context is single-threaded by contract).
+struct Work {
+    std::vector<DevArray<double>> u, t, f, r;
+    DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh;
+    DevArray<KState> st;
+    DevArray<double> partials;
+    DevArray<unsigned> ticket;
+    DevArray<int> err;  // per level bad row (+1 slot for LU status)
+    std::vector<int64_t> shape;
+};
+
+struct Timer {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
+};
+
+struct Hier {
+    Ctx* ctx = nullptr;
+    AmgP prm;
+    std::vector<Level> lv;
+    DevArray<double> lu;
+    DevArray<int64_t> piv;
+    int64_t nL = 0;
+    amgr_phase_timings tm{};
+    std::shared_ptr<Work> ws;
+    int64_t agg_rounds = 0;
+
+    double om_eff() const { return prm.smoother == AMGR_SMOOTHER_SPAI0 ? 1.0 : prm.omega; }
+};
+
+std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p);
+std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const AmgP& p);
+void rebuild(Hier& h, const amgr_csr& A);
+void rebuild_values(Hier& h, const double* values, int location);
+void vcycle(Hier& h, const double* f, double* u, Gate g = {});
+void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
+              amgr_solve_stats& st);
+void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
+        amgr_solve_stats& st);
+Work& work(Hier& h);
+
+// device generators (kernels_gen.cu)
+int64_t problem_nnz(int64_t g);
+void problem_pattern(Ctx& c, int64_t g, int* rp, int* col);
+void problem_values(Ctx& c, int kind, int64_t g, int64_t k, int64_t nsteps, double* val);
+void exclusive_sum_i32(Ctx& c, const int* in, int* out, int64_t n);
+
+}  // namespace amgr

@@ -1,0 +1,97 @@
+// Kernel launchers of libamgr_b200.so (sm_100a).  All arithmetic that the
+// reference performs in a fixed order is replayed in the same order with
+// explicit round-to-nearest intrinsics (the library is also compiled with
+// --fmad=false), so level values, smoother state, the coarse LU and the
+// V-cycle are bit-identical to the reference built with -ffp-contract=off
+// (DESIGN.md §3).
+#pragma once
+
+#include "common.cuh"
+
+namespace amgr {
+
+// Device view of one level's matrix (CSR, int32 indices, fp64 values).
+struct CsrView {
+    int64_t n = 0;     // rows
+    int64_t ncols = 0;
+    int64_t nnz = 0;
+    const int* rp = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
+
+// Deterministic multi-block dot products: per-block partials + last-block
+// fixed-order final sum (no atomics on the values).
+struct DotSink {
+    double* partials = nullptr;   // [grid * ndot]
+    unsigned* ticket = nullptr;   // zero-initialised counter
+    double* out = nullptr;        // [ndot]
+};
+
+// Fixed grid for dot-producing kernels so the reduction order never changes.
+int dot_grid(const Ctx& c);
+
+// ---- row-pass (CSR SpMV family) --------------------------------------------
+void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g = {});
+// r = f - A x
+void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, Gate g = {});
+// V-cycle down leg, first pre-smoothing sweep from a zero guess fused with the
+// residual: u = 0 + (om*w) f ; r = f - A u        (hierarchy.cpp:165-170)
+void vc_down(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* u,
+             double* r, Gate g = {});
+// one more smoothing sweep: out = u + (om*w)(f - A u)     (smoother.cpp:42-47)
+void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
+               const double* u, double* out, Gate g = {});
+// V-cycle up leg: x = u + (0 + uc[agg]) fused with the first post-smoothing
+// sweep: out = x + (om*w)(f - A x)                  (hierarchy.cpp:179-183)
+void vc_up(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
+           const double* u, const int* agg, const double* uc, double* out, Gate g = {});
+// prolongation only (post_sweeps == 0): out = u + (0 + uc[agg])
+void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
+                Gate g = {});
+// restriction fc[I] = sum over members ascending of r[m]   (R spmv, csr.cpp:79-84)
+void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const double* r, double* fc,
+                  Gate g = {});
+
+// Krylov-fused SpMVs (dots land in sink.out):
+// y = A x ; out[0] = a . y
+void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double* a, DotSink s,
+              Gate g = {});
+// y = A x ; out[0] = y . b ; out[1] = y . y
+void spmv_dot2(Ctx& c, const CsrView& A, const double* x, double* y, const double* b, DotSink s,
+               Gate g = {});
+// out[0] = || f - A x ||^2 ; optionally r = f - A x and r2 = r
+void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, double* r2,
+                DotSink s, Gate g = {});
+
+// ---- rebuild ---------------------------------------------------------------
+// Numeric Galerkin product on the cached plan: for every coarse entry c,
+//   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
+//     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
+// (two-level bracket of spmm(R, spmm(A, P)), csr.cpp:145-194)
+void rap_numeric(Ctx& c, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f);
+// Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
+void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
+                    int* bad_row);
+// SPAI0 (extension): w[i] = a_ii / sum_j a_ij^2
+void spai0_rebuild(Ctx& c, const CsrView& A, const int* diag_pos, double* w, int* bad_row);
+
+// ---- coarse direct solver (dense_lu.cpp) ------------------------------------
+void lu_densify(Ctx& c, const CsrView& A, double* dense);
+// in-place LU with partial pivoting; piv[k]; *status = -1 ok, else the zero-pivot step
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status);
+// x = LU \ b in the reference's order; x may alias b
+void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x,
+              Gate g = {});
+
+// ---- misc vector kernels ------------------------------------------------------
+void fill(Ctx& c, double* x, int64_t n, double v, Gate g = {});
+void copy(Ctx& c, double* dst, const double* src, int64_t n, Gate g = {});
+void find_diag(Ctx& c, const CsrView& A, int* diag_pos);
+void i32_to_i64(Ctx& c, const int* src, int64_t* dst, int64_t n);
+void i64_to_i32(Ctx& c, const int64_t* src, int* dst, int64_t n, int* overflow);
+// compare two int32 arrays; *diff set to 1 if any element differs
+void compare_i32(Ctx& c, const int* a, const int* b, int64_t n, int* diff);
+
+}  // namespace amgr

@@ -1,0 +1,577 @@
+// Hot-path kernels of libamgr_b200.so, hand-written for sm_100a.
+//
+//  * k_rowpass<Op>: thread-per-row CSR pass with warp-cooperative staging of
+//    the warp's contiguous nnz range through shared memory (coalesced 8-byte
+//    loads, any row-length distribution, no padding), followed by a strictly
+//    sequential per-row accumulation in column order — the reference's spmv
+//    order (proj/src/csr.cpp:79-84) — so results are bit-identical.  The
+//    Op supplies the on-the-fly operand x_j and the row epilogue, which is how
+//    the V-cycle legs fuse smoothing, residual and prolongation into a single
+//    pass over A_i, and how the Krylov SpMVs fuse their dot products.
+//  * rap_numeric: numeric Galerkin product on the cached contribution plan.
+//  * jacobi/spai0 rebuild, restriction, dense LU factor/solve.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "reduce.cuh"
+
+namespace amgr {
+
+namespace {
+
+constexpr int RP_BLOCK = 256;
+constexpr int RP_WARPS = RP_BLOCK / 32;
+constexpr int RP_CH = 256;  // staged entries per warp per chunk (3 KB)
+
+template <class Op>
+__global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
+    if (gated_off(g)) return;
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    __shared__ double s_val[RP_WARPS][RP_CH];
+    __shared__ int s_col[RP_WARPS][RP_CH];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = static_cast<int>(A.n);
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * RP_WARPS;
+    for (int64_t wid = static_cast<int64_t>(blockIdx.x) * RP_WARPS + w; wid * 32 < n; wid += wstride) {
+        const int r0 = static_cast<int>(wid * 32);
+        const int r1 = min(r0 + 32, n);
+        const int row = r0 + lane;
+        const bool valid = row < n;
+        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + r1);
+        const int rs = valid ? __ldg(A.rp + row) : e1;
+        const int re = valid ? __ldg(A.rp + row + 1) : e1;
+        double sum = 0.0;
+        for (int c0 = e0; c0 < e1; c0 += RP_CH) {
+            const int c1 = min(c0 + RP_CH, e1);
+#pragma unroll 4
+            for (int e = c0 + lane; e < c1; e += 32) {
+                s_val[w][e - c0] = __ldg(A.val + e);
+                s_col[w][e - c0] = __ldg(A.col + e);
+            }
+            __syncwarp();
+            int a = max(rs, c0);
+            const int b = min(re, c1);
+            for (; a + 4 <= b; a += 4) {
+                const int k = a - c0;
+                const double x0 = op.x(s_col[w][k]), x1 = op.x(s_col[w][k + 1]);
+                const double x2 = op.x(s_col[w][k + 2]), x3 = op.x(s_col[w][k + 3]);
+                sum = dadd(sum, dmul(s_val[w][k], x0));
+                sum = dadd(sum, dmul(s_val[w][k + 1], x1));
+                sum = dadd(sum, dmul(s_val[w][k + 2], x2));
+                sum = dadd(sum, dmul(s_val[w][k + 3], x3));
+            }
+            for (; a < b; ++a) sum = dadd(sum, dmul(s_val[w][a - c0], op.x(s_col[w][a - c0])));
+            __syncwarp();
+        }
+        if (valid) op.finish(row, sum, dots);
+    }
+    if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
+}
+
+// ---- row-pass operators ----------------------------------------------------
+struct OpSpmv {
+    static constexpr int NDOT = 0;
+    const double* xv;
+    double* y;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void finish(int i, double s, double*) const { y[i] = s; }
+};
+
+struct OpResidual {
+    static constexpr int NDOT = 0;
+    const double* f;
+    const double* xv;
+    double* r;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void finish(int i, double s, double*) const { r[i] = dsub(f[i], s); }
+};
+
+// hierarchy.cpp:165-170 with smooth() from u = 0 (smoother.cpp:42-47):
+// u_j = 0 + (om*w_j)*(f_j - 0) ; r_i = f_i - sum_j a_ij u_j
+struct OpDown {
+    static constexpr int NDOT = 0;
+    const double* f;
+    const double* w;
+    double om;
+    double* u;
+    double* r;
+    __device__ double x(int j) const { return dadd(0.0, dmul(dmul(om, __ldg(w + j)), __ldg(f + j))); }
+    __device__ void finish(int i, double s, double*) const {
+        u[i] = x(i);
+        r[i] = dsub(f[i], s);
+    }
+};
+
+// one damped sweep: out_i = u_i + (om*w_i)*(f_i - (A u)_i)
+struct OpSmooth {
+    static constexpr int NDOT = 0;
+    const double* f;
+    const double* w;
+    double om;
+    const double* u;
+    double* out;
+    __device__ double x(int j) const { return __ldg(u + j); }
+    __device__ void finish(int i, double s, double*) const {
+        out[i] = dadd(u[i], dmul(dmul(om, w[i]), dsub(f[i], s)));
+    }
+};
+
+// hierarchy.cpp:179-183: x = u + (0 + 1.0*uc[agg]) then one sweep on x.
+struct OpUp {
+    static constexpr int NDOT = 0;
+    const double* f;
+    const double* w;
+    double om;
+    const double* u;
+    const int* agg;
+    const double* uc;
+    double* out;
+    __device__ double x(int j) const { return dadd(__ldg(u + j), dadd(0.0, __ldg(uc + __ldg(agg + j)))); }
+    __device__ void finish(int i, double s, double*) const {
+        out[i] = dadd(x(i), dmul(dmul(om, w[i]), dsub(f[i], s)));
+    }
+};
+
+struct OpSpmvDot {
+    static constexpr int NDOT = 1;
+    const double* xv;
+    double* y;
+    const double* a;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void finish(int i, double s, double* d) const {
+        y[i] = s;
+        d[0] = __fma_rn(a[i], s, d[0]);
+    }
+};
+
+struct OpSpmvDot2 {
+    static constexpr int NDOT = 2;
+    const double* xv;
+    double* y;
+    const double* b;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void finish(int i, double s, double* d) const {
+        y[i] = s;
+        d[0] = __fma_rn(s, b[i], d[0]);
+        d[1] = __fma_rn(s, s, d[1]);
+    }
+};
+
+struct OpResidNorm {
+    static constexpr int NDOT = 1;
+    const double* f;
+    const double* xv;
+    double* r;
+    double* r2;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void finish(int i, double s, double* d) const {
+        const double t = dsub(f[i], s);
+        if (r) r[i] = t;
+        if (r2) r2[i] = t;
+        d[0] = __fma_rn(t, t, d[0]);
+    }
+};
+
+template <class Op>
+void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g,
+                    DotSink s, bool fixed_grid) {
+    if (A.n == 0) return;
+    const int64_t warps = (A.n + 31) / 32;
+    unsigned grid = grid_for(warps, RP_WARPS);
+    if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
+    LAUNCH(c, fam, bytes, k_rowpass<Op>, grid, RP_BLOCK, 0, A, op, g, s);
+}
+
+double spmv_bytes(const CsrView& A) {
+    // 12 B/nnz (value + int32 column) + row_ptr + x read once + y written once
+    return 12.0 * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
+}
+
+// ---- restriction / prolongation ------------------------------------------
+__global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __restrict__ midx,
+                           const double* __restrict__ r, double* __restrict__ fc, Gate g) {
+    if (gated_off(g)) return;
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        const int p0 = mptr[I], p1 = mptr[I + 1];
+        double s = 0.0;
+        for (int p = p0; p < p1; ++p) s = dadd(s, __ldg(r + __ldg(midx + p)));
+        fc[I] = s;
+    }
+}
+
+__global__ void k_prolong(int n, const double* __restrict__ u, const int* __restrict__ agg,
+                          const double* __restrict__ uc, double* __restrict__ out, Gate g) {
+    if (gated_off(g)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = dadd(u[i], dadd(0.0, uc[agg[i]]));
+}
+
+// ---- numeric RAP ----------------------------------------------------------
+__global__ void k_rap(int64_t nnz_c, const int* __restrict__ cptr, const int* __restrict__ contrib,
+                      const double* __restrict__ af, double* __restrict__ ac) {
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nnz_c;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p0 = __ldg(cptr + c), p1 = __ldg(cptr + c + 1);
+        double acc = 0.0, part = 0.0;
+        int p = p0;
+        for (; p + 2 <= p1; p += 2) {
+            const int e0 = __ldg(contrib + p), e1 = __ldg(contrib + p + 1);
+            const double v0 = __ldg(af + (e0 & 0x7fffffff)), v1 = __ldg(af + (e1 & 0x7fffffff));
+            part = dadd(part, v0);
+            if (e0 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
+            }
+            part = dadd(part, v1);
+            if (e1 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
+            }
+        }
+        if (p < p1) {
+            const int e0 = __ldg(contrib + p);
+            part = dadd(part, __ldg(af + (e0 & 0x7fffffff)));
+            if (e0 < 0) acc = dadd(acc, part);
+        }
+        ac[c] = acc;
+    }
+}
+
+__global__ void k_jacobi(int n, const double* __restrict__ val, const int* __restrict__ dpos,
+                         double* __restrict__ w, int* bad) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int k = dpos[i];
+        const double d = k >= 0 ? val[k] : 0.0;
+        if (d == 0.0) {
+            atomicMin(bad, i);
+            w[i] = 0.0;
+        } else {
+            w[i] = __ddiv_rn(1.0, d);
+        }
+    }
+}
+
+__global__ void k_spai0(CsrView A, const int* __restrict__ dpos, double* __restrict__ w, int* bad) {
+    const int n = static_cast<int>(A.n);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) s = dadd(s, dmul(A.val[k], A.val[k]));
+        const int k = dpos[i];
+        const double d = k >= 0 ? A.val[k] : 0.0;
+        if (d == 0.0) {
+            atomicMin(bad, i);
+            w[i] = 0.0;
+        } else {
+            w[i] = __ddiv_rn(d, s);
+        }
+    }
+}
+
+// ---- dense LU (coarse_factorize / coarse_solve, dense_lu.cpp:10-73) --------
+__global__ void k_densify(CsrView A, double* dense) {
+    const int64_t n = A.n;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dense[t] = 0.0;
+}
+__global__ void k_densify_fill(CsrView A, double* dense) {
+    const int64_t n = A.n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) dense[i * n + A.col[k]] = A.val[k];
+}
+
+constexpr int LU_THREADS = 1024;
+
+__global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int64_t* piv, int* status,
+                                                          int use_smem) {
+    extern __shared__ double sm[];
+    __shared__ double rbest[LU_THREADS / 32];
+    __shared__ int ridx[LU_THREADS / 32];
+    __shared__ int s_p;
+    __shared__ double s_pivot;
+    double* m = use_smem ? sm : gm;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nn = n * n;
+    if (use_smem)
+        for (int t = tid; t < nn; t += blockDim.x) m[t] = gm[t];
+    if (tid == 0) *status = -1;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        // pivot: lowest row attaining max |m[i][k]| over i >= k (strict '>' scan)
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = k + tid; i < n; i += blockDim.x) {
+            const double v = fabs(m[i * n + k]);
+            if (v > best) {
+                best = v;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, off);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            rbest[w] = best;
+            ridx[w] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double b = rbest[0];
+            int p = ridx[0];
+            for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+                if (rbest[q] > b || (rbest[q] == b && ridx[q] < p)) {
+                    b = rbest[q];
+                    p = ridx[q];
+                }
+            if (p == 0x7fffffff) p = k;  // all NaN: the reference keeps p = k
+            // the reference starts from best=|m[k][k]|, p=k: ties keep k
+            if (!(fabs(m[k * n + k]) < b)) p = k;
+            s_p = p;
+            piv[k] = p;
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (p != k)
+            for (int j = tid; j < n; j += blockDim.x) {
+                const double t = m[k * n + j];
+                m[k * n + j] = m[p * n + j];
+                m[p * n + j] = t;
+            }
+        __syncthreads();
+        if (tid == 0) s_pivot = m[k * n + k];
+        __syncthreads();
+        const double pivot = s_pivot;
+        if (pivot == 0.0) {
+            if (tid == 0) *status = k;
+            break;
+        }
+        for (int i = k + 1 + tid; i < n; i += blockDim.x) m[i * n + k] = __ddiv_rn(m[i * n + k], pivot);
+        __syncthreads();
+        const int rows = n - k - 1;
+        const int tot = rows * rows;
+        for (int t = tid; t < tot; t += blockDim.x) {
+            const int i = k + 1 + t / rows, j = k + 1 + t % rows;
+            m[i * n + j] = dsub(m[i * n + j], dmul(m[i * n + k], m[k * n + j]));
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (use_smem)
+        for (int t = tid; t < nn; t += blockDim.x) gm[t] = m[t];
+}
+
+constexpr int LS_THREADS = 256;
+
+__global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __restrict__ m,
+                                                         const int64_t* __restrict__ piv,
+                                                         const double* b, double* x, Gate g) {
+    if (gated_off(g)) return;
+    extern __shared__ double xs[];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += blockDim.x) xs[i] = b[i];
+    __syncthreads();
+    if (tid == 0)
+        for (int k = 0; k < n; ++k) {
+            const int p = static_cast<int>(piv[k]);
+            if (p != k) {
+                const double t = xs[k];
+                xs[k] = xs[p];
+                xs[p] = t;
+            }
+        }
+    __syncthreads();
+    // forward, unit L: column-oriented sweep subtracts in ascending j for every
+    // row, i.e. exactly the reference's row-oriented order.
+    for (int j = 0; j < n - 1; ++j) {
+        const double xj = xs[j];
+        for (int i = j + 1 + tid; i < n; i += blockDim.x) xs[i] = dsub(xs[i], dmul(m[i * n + j], xj));
+        __syncthreads();
+    }
+    // backward: the reference subtracts ascending j from i+1, so each row must
+    // wait for x[i+1]; one thread walks it.
+    if (tid == 0)
+        for (int i = n - 1; i >= 0; --i) {
+            double s = xs[i];
+            const double* mi = m + static_cast<int64_t>(i) * n;
+            for (int j = i + 1; j < n; ++j) s = dsub(s, dmul(mi[j], xs[j]));
+            xs[i] = __ddiv_rn(s, mi[i]);
+        }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) x[i] = xs[i];
+}
+
+// ---- misc ---------------------------------------------------------------------
+__global__ void k_fill(double* x, int64_t n, double v, Gate g) {
+    if (gated_off(g)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] = v;
+}
+__global__ void k_copy(double* d, const double* s, int64_t n, Gate g) {
+    if (gated_off(g)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        d[i] = s[i];
+}
+__global__ void k_find_diag(CsrView A, int* dpos) {
+    const int n = static_cast<int>(A.n);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int lo = A.rp[i], hi = A.rp[i + 1] - 1, found = -1;
+        while (lo <= hi) {
+            const int mid = (lo + hi) >> 1;
+            const int cm = A.col[mid];
+            if (cm == i) {
+                found = mid;
+                break;
+            }
+            if (cm < i) lo = mid + 1;
+            else hi = mid - 1;
+        }
+        dpos[i] = found;
+    }
+}
+__global__ void k_i32_to_i64(const int* s, int64_t* d, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        d[i] = s[i];
+}
+__global__ void k_i64_to_i32(const int64_t* s, int* d, int64_t n, int* ovf) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t v = s[i];
+        if (v < INT32_MIN || v > INT32_MAX) *ovf = 1;
+        d[i] = static_cast<int>(v);
+    }
+}
+__global__ void k_compare_i32(const int* a, const int* b, int64_t n, int* diff) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (a[i] != b[i]) *diff = 1;
+}
+
+}  // namespace
+
+int dot_grid(const Ctx& c) { return c.num_sms * 4; }
+
+// ---- launchers -----------------------------------------------------------------
+void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g) {
+    launch_rowpass(c, "spmv", spmv_bytes(A), A, OpSpmv{x, y}, g, {}, false);
+}
+void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, Gate g) {
+    launch_rowpass(c, "residual", spmv_bytes(A) + 16.0 * A.n, A, OpResidual{f, x, r}, g, {}, false);
+}
+void vc_down(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* u,
+             double* r, Gate g) {
+    // A + f, w read once, u and r written once
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n + 16.0 * A.n;
+    launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, w, om, u, r}, g, {}, false);
+}
+void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
+               const double* u, double* out, Gate g) {
+    launch_rowpass(c, "vcycle_smooth", spmv_bytes(A) + 16.0 * A.n, A, OpSmooth{f, w, om, u, out}, g, {},
+                   false);
+}
+void vc_up(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
+           const int* agg, const double* uc, double* out, Gate g) {
+    // A + u, agg, f, w read once + uc (coarse) + out written once
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 28.0 * A.n + 8.0 * A.n;
+    launch_rowpass(c, "vcycle_up", bytes, A, OpUp{f, w, om, u, agg, uc, out}, g, {}, false);
+}
+void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
+                Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "prolong", 20.0 * n, k_prolong, grid_for(n, 256, c.num_sms * 16), 256, 0,
+           static_cast<int>(n), u, agg, uc, out, g);
+}
+void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const double* r, double* fc,
+                  Gate g) {
+    if (nc == 0) return;
+    LAUNCH(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc),
+           mptr, midx, r, fc, g);
+}
+void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double* a, DotSink s, Gate g) {
+    launch_rowpass(c, "spmv_dot", spmv_bytes(A) + 8.0 * A.n, A, OpSpmvDot{x, y, a}, g, s, true);
+}
+void spmv_dot2(Ctx& c, const CsrView& A, const double* x, double* y, const double* b, DotSink s,
+               Gate g) {
+    launch_rowpass(c, "spmv_dot2", spmv_bytes(A) + 8.0 * A.n, A, OpSpmvDot2{x, y, b}, g, s, true);
+}
+void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, double* r2,
+                DotSink s, Gate g) {
+    launch_rowpass(c, "resid_norm", spmv_bytes(A), A, OpResidNorm{f, x, r, r2}, g, s, true);
+}
+
+void rap_numeric(Ctx& c, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f) {
+    if (nnz_c == 0) return;
+    const double bytes = 12.0 * nnz_f + 12.0 * nnz_c;
+    LAUNCH(c, "rap", bytes, k_rap, grid_for(nnz_c, 256, c.num_sms * 32), 256, 0, nnz_c, cptr, contrib, af, ac);
+}
+void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
+    if (n == 0) return;
+    LAUNCH(c, "smoother", 20.0 * n, k_jacobi, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n),
+           val, dpos, w, bad);
+}
+void spai0_rebuild(Ctx& c, const CsrView& A, const int* dpos, double* w, int* bad) {
+    if (A.n == 0) return;
+    LAUNCH(c, "smoother", 8.0 * A.nnz + 12.0 * A.n, k_spai0, grid_for(A.n, 256, c.num_sms * 16), 256, 0, A,
+           dpos, w, bad);
+}
+
+void lu_densify(Ctx& c, const CsrView& A, double* dense) {
+    if (A.n == 0) return;
+    LAUNCH(c, "coarse", 0.0, k_densify, grid_for(A.n * A.n, 256, c.num_sms * 8), 256, 0, A, dense);
+    LAUNCH(c, "coarse", 0.0, k_densify_fill, grid_for(A.n, 128, c.num_sms * 8), 128, 0, A, dense);
+}
+
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
+    if (n == 0) return;
+    const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
+    int use_smem = sm <= 200 * 1024 ? 1 : 0;
+    if (use_smem) CK(cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    LAUNCH(c, "coarse", 0.0, k_lu_factor, 1, LU_THREADS, use_smem ? sm : 0, static_cast<int>(n), m, piv, status,
+           use_smem);
+}
+
+void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g) {
+    if (n == 0) return;
+    const size_t sm = sizeof(double) * static_cast<size_t>(n);
+    LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, g);
+}
+
+void fill(Ctx& c, double* x, int64_t n, double v, Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "vec", 8.0 * n, k_fill, grid_for(n, 256, c.num_sms * 16), 256, 0, x, n, v, g);
+}
+void copy(Ctx& c, double* d, const double* s, int64_t n, Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "vec", 16.0 * n, k_copy, grid_for(n, 256, c.num_sms * 16), 256, 0, d, s, n, g);
+}
+void find_diag(Ctx& c, const CsrView& A, int* dpos) {
+    if (A.n == 0) return;
+    LAUNCH(c, "setup", 0.0, k_find_diag, grid_for(A.n, 256, c.num_sms * 16), 256, 0, A, dpos);
+}
+void i32_to_i64(Ctx& c, const int* s, int64_t* d, int64_t n) {
+    if (n == 0) return;
+    LAUNCH(c, "io", 0.0, k_i32_to_i64, grid_for(n, 256, c.num_sms * 16), 256, 0, s, d, n);
+}
+void i64_to_i32(Ctx& c, const int64_t* s, int* d, int64_t n, int* ovf) {
+    if (n == 0) return;
+    LAUNCH(c, "io", 0.0, k_i64_to_i32, grid_for(n, 256, c.num_sms * 16), 256, 0, s, d, n, ovf);
+}
+void compare_i32(Ctx& c, const int* a, const int* b, int64_t n, int* diff) {
+    if (n == 0) return;
+    LAUNCH(c, "io", 0.0, k_compare_i32, grid_for(n, 256, c.num_sms * 16), 256, 0, a, b, n, diff);
+}
+
+}  // namespace amgr

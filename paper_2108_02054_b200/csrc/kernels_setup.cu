@@ -1,0 +1,427 @@
+// Setup kernels (sm_100a).  Sorting and prefix sums of the one-time setup use
+// CUB's device primitives; everything else — the strength test, the exact
+// aggregation replay, P/R and the Galerkin plan construction — is hand-written.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "setup.cuh"
+
+namespace amgr {
+
+namespace {
+
+constexpr int SB = 256;
+
+int bits_for(int64_t n) {
+    int b = 1;
+    while ((int64_t{1} << b) < n) ++b;
+    return b;
+}
+
+template <class T>
+void exclusive_sum(Ctx& c, const T* in, T* out, int64_t n) {
+    if (n <= 0) return;
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c.stream));
+    DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, in, out, n, c.stream));
+    ++c.launches;
+}
+
+// Stable LSD radix sort of (key, value) pairs on the low end_bit bits.
+// Returns pointers to the sorted arrays (one of the two buffers).
+void sort_pairs(Ctx& c, uint64_t* k0, uint64_t* k1, int* v0, int* v1, int64_t n, int end_bit,
+                uint64_t** ko, int** vo) {
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<int> vb(v0, v1);
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, c.stream));
+    DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kb, vb, n, 0, end_bit, c.stream));
+    c.launches += 1;
+    *ko = kb.Current();
+    *vo = vb.Current();
+}
+
+void sort_keys(Ctx& c, uint64_t* k0, uint64_t* k1, int64_t n, int end_bit, uint64_t** ko) {
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kb, n, 0, end_bit, c.stream));
+    DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
+    CK(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, kb, n, 0, end_bit, c.stream));
+    c.launches += 1;
+    *ko = kb.Current();
+}
+
+#define GRID_STRIDE(i, n) \
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (n); \
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+__global__ void k_bad_diag(CsrView A, const int* dpos, int* bad) {
+    GRID_STRIDE(i, A.n) {
+        const int k = dpos[i];
+        if (k < 0 || A.val[k] == 0.0) atomicMin(bad, static_cast<int>(i));
+    }
+}
+
+// coarsening.cpp:36-46: edge iff j != i and v*v > eps2*|d_i*d_j|, both directions.
+__global__ void k_strong_count(CsrView A, const int* dpos, double eps2, int64_t* cnt) {
+    GRID_STRIDE(i, A.n) {
+        const double di = A.val[dpos[i]];
+        int64_t c = 0;
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int j = A.col[k];
+            if (j == i) continue;
+            const double v = A.val[k];
+            const double dj = A.val[dpos[j]];
+            if (__dmul_rn(v, v) > __dmul_rn(eps2, fabs(__dmul_rn(di, dj)))) c += 2;
+        }
+        cnt[i] = c;
+    }
+}
+
+__global__ void k_strong_emit(CsrView A, const int* dpos, double eps2, const int64_t* off, int b,
+                              uint64_t* keys) {
+    GRID_STRIDE(i, A.n) {
+        const double di = A.val[dpos[i]];
+        int64_t o = off[i];
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int j = A.col[k];
+            if (j == i) continue;
+            const double v = A.val[k];
+            const double dj = A.val[dpos[j]];
+            if (__dmul_rn(v, v) > __dmul_rn(eps2, fabs(__dmul_rn(di, dj)))) {
+                keys[o++] = (static_cast<uint64_t>(i) << b) | static_cast<uint64_t>(j);
+                keys[o++] = (static_cast<uint64_t>(j) << b) | static_cast<uint64_t>(i);
+            }
+        }
+    }
+}
+
+__global__ void k_heads(const uint64_t* keys, int64_t m, int64_t* head) {
+    GRID_STRIDE(p, m) head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_compact_keys(const uint64_t* keys, const int64_t* head, const int64_t* pos, int64_t m,
+                               uint64_t* out) {
+    GRID_STRIDE(p, m) if (head[p]) out[pos[p]] = keys[p];
+}
+
+// ptr[i] = lower_bound(ukeys, i << b); adj = low bits
+__global__ void k_graph_ptr(const uint64_t* ukeys, int64_t m, int64_t n, int b, int* ptr) {
+    GRID_STRIDE(i, n + 1) {
+        const uint64_t target = static_cast<uint64_t>(i) << b;
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (ukeys[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[i] = static_cast<int>(lo);
+    }
+}
+__global__ void k_graph_adj(const uint64_t* ukeys, int64_t m, uint64_t mask, int* adj) {
+    GRID_STRIDE(p, m) adj[p] = static_cast<int>(ukeys[p] & mask);
+}
+
+// ---- aggregation replay ------------------------------------------------------
+// state: 0 undecided, 1 root, 2 non-root.  Node i is a pass-1 root iff
+//  (a) no root among its lower-indexed neighbours, and
+//  (b) some neighbour j > i has no root in N(j) ∩ [0, i)
+// (DESIGN.md §3.2).  Decisions are final, so reading states
+// written by other threads in the same round is safe.
+__device__ __forceinline__ int ld_state(const int* s, int i) {
+    return *reinterpret_cast<const volatile int*>(s + i);
+}
+
+__global__ void __launch_bounds__(SB) k_agg_round(int n, const int* __restrict__ ptr, const int* __restrict__ adj,
+                                                  int* state, int* undecided) {
+    int local = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (ld_state(state, i) != 0) continue;
+        const int p0 = ptr[i], p1 = ptr[i + 1];
+        if (p0 == p1) {  // isolated: never a pass-1 root
+            reinterpret_cast<volatile int*>(state)[i] = 2;
+            continue;
+        }
+        int decision = 0;
+        bool blocked = false;
+        int p = p0;
+        for (; p < p1; ++p) {
+            const int j = adj[p];
+            if (j > i) break;
+            const int s = ld_state(state, j);
+            if (s == 1) {
+                decision = 2;
+                break;
+            }
+            if (s == 0) blocked = true;
+        }
+        if (decision == 0 && !blocked) {
+            bool unknown = false, free_found = false;
+            for (int q = p; q < p1 && !free_found; ++q) {
+                const int j = adj[q];
+                bool taken = false, junk = false;
+                for (int t = ptr[j]; t < ptr[j + 1]; ++t) {
+                    const int x = adj[t];
+                    if (x >= i) break;
+                    const int s = ld_state(state, x);
+                    if (s == 1) {
+                        taken = true;
+                        break;
+                    }
+                    if (s == 0) junk = true;
+                }
+                if (!taken && !junk) free_found = true;
+                else if (!taken) unknown = true;
+            }
+            if (free_found) decision = 1;
+            else if (!unknown) decision = 2;
+        }
+        if (decision) reinterpret_cast<volatile int*>(state)[i] = decision;
+        else ++local;
+    }
+    // block-aggregate the undecided count
+    __shared__ int s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    if (local) atomicAdd(&s_cnt, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(undecided, s_cnt);
+}
+
+__global__ void k_root_flags(const int* state, int64_t n, int64_t* rf) {
+    GRID_STRIDE(i, n) rf[i] = state[i] == 1 ? 1 : 0;
+}
+
+// pass 1: roots take their id; absorbed nodes take the id of their
+// lowest-indexed root neighbour; -2 isolated, -1 pass-2 leftover.
+__global__ void k_assign1(int64_t n, const int* ptr, const int* adj, const int* state, const int64_t* rid,
+                          int* agg, int64_t* iso) {
+    GRID_STRIDE(i, n) {
+        int a = -1;
+        int64_t is = 0;
+        if (state[i] == 1) {
+            a = static_cast<int>(rid[i]);
+        } else if (ptr[i] == ptr[i + 1]) {
+            a = -2;
+            is = 1;
+        } else {
+            for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
+                const int j = adj[p];
+                if (state[j] == 1) {
+                    a = static_cast<int>(rid[j]);
+                    break;
+                }
+            }
+        }
+        agg[i] = a;
+        iso[i] = is;
+    }
+}
+
+// pass 2 (coarsening.cpp:103-116): isolated -> new singleton ids after all
+// roots in ascending order; leftover -> aggregate of the lowest-indexed
+// neighbour (always assigned in pass 1).
+__global__ void k_assign2(int64_t n, const int* ptr, const int* adj, int64_t n_roots, const int64_t* isorank,
+                          int* agg, int* err) {
+    GRID_STRIDE(i, n) {
+        const int a = agg[i];
+        if (a == -2) {
+            agg[i] = static_cast<int>(n_roots + isorank[i]);
+        } else if (a == -1) {
+            const int j = adj[ptr[i]];
+            const int aj = agg[j];
+            if (aj < 0) *err = 1;
+            agg[i] = aj;
+        }
+    }
+}
+
+__global__ void k_hist(const int* agg, int64_t n, int* cnt) {
+    GRID_STRIDE(i, n) atomicAdd(cnt + agg[i], 1);
+}
+__global__ void k_iota(int* v, int64_t n) {
+    GRID_STRIDE(i, n) v[i] = static_cast<int>(i);
+}
+__global__ void k_agg_keys(const int* agg, int64_t n, uint64_t* k) {
+    GRID_STRIDE(i, n) k[i] = static_cast<uint64_t>(agg[i]);
+}
+__global__ void k_i64_to_i32(const int64_t* s, int* d, int64_t n) {
+    GRID_STRIDE(i, n) d[i] = static_cast<int>(s[i]);
+}
+
+// ---- symbolic RAP -------------------------------------------------------------
+__global__ void k_rap_keys(CsrView A, const int* agg, int b, uint64_t* keys, int* vals, int* rowof) {
+    GRID_STRIDE(i, A.n) {
+        const uint64_t I = static_cast<uint64_t>(agg[i]) << b;
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            keys[k] = I | static_cast<uint64_t>(agg[A.col[k]]);
+            vals[k] = k;
+            rowof[k] = static_cast<int>(i);
+        }
+    }
+}
+__global__ void k_rap_plan(const uint64_t* keys, const int* vals, const int* rowof, const int64_t* head,
+                           const int64_t* pos, int64_t m, int* contrib, int* cptr, uint64_t* ukeys) {
+    GRID_STRIDE(p, m) {
+        const int e = vals[p];
+        bool last = true;
+        if (p + 1 < m && keys[p + 1] == keys[p] && rowof[vals[p + 1]] == rowof[e]) last = false;
+        contrib[p] = last ? (e | static_cast<int>(0x80000000u)) : e;
+        if (head[p]) {
+            cptr[pos[p]] = static_cast<int>(p);
+            ukeys[pos[p]] = keys[p];
+        }
+    }
+}
+__global__ void k_coarse_col(const uint64_t* ukeys, int64_t nnz_c, uint64_t mask, int* col) {
+    GRID_STRIDE(c, nnz_c) col[c] = static_cast<int>(ukeys[c] & mask);
+}
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
+}  // namespace
+
+int64_t first_bad_diag(Ctx& c, const CsrView& A, const int* dpos) {
+    DevArray<int> bad(1, c.stream);
+    const int big = 0x7fffffff;
+    h2d(bad.get(), &big, 1, c.stream);
+    LAUNCH(c, "setup", 0.0, k_bad_diag, grid_for(A.n, SB, c.num_sms * 16), SB, 0, A, dpos, bad.get());
+    const int r = d2h_scalar(bad.get(), c.stream);
+    return r == big ? -1 : r;
+}
+
+void strength_graph(Ctx& c, const CsrView& A, const int* dpos, double eps2, GraphDev& g) {
+    const int64_t n = A.n;
+    const int b = bits_for(n);
+    DevArray<int64_t> cnt(n + 1, c.stream), off(n + 1, c.stream);
+    CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int64_t) * (n + 1), c.stream));
+    LAUNCH(c, "setup", 0.0, k_strong_count, grid_for(n, SB, c.num_sms * 16), SB, 0, A, dpos, eps2, cnt.get());
+    exclusive_sum(c, cnt.get(), off.get(), n + 1);
+    const int64_t m2 = d2h_scalar(off.get() + n, c.stream);
+    g.n = n;
+    g.ptr.alloc(n + 1, c.stream);
+    if (m2 == 0) {
+        CK(cudaMemsetAsync(g.ptr.get(), 0, sizeof(int) * (n + 1), c.stream));
+        g.m = 0;
+        g.adj.alloc(1, c.stream);
+        return;
+    }
+    DevArray<uint64_t> k0(m2, c.stream), k1(m2, c.stream);
+    LAUNCH(c, "setup", 0.0, k_strong_emit, grid_for(n, SB, c.num_sms * 16), SB, 0, A, dpos, eps2, off.get(), b,
+           k0.get());
+    uint64_t* ks = nullptr;
+    sort_keys(c, k0.get(), k1.get(), m2, 2 * b, &ks);
+    DevArray<int64_t> head(m2, c.stream), pos(m2, c.stream);
+    LAUNCH(c, "setup", 0.0, k_heads, grid_for(m2, SB, c.num_sms * 16), SB, 0, ks, m2, head.get());
+    exclusive_sum(c, head.get(), pos.get(), m2);
+    const int64_t m = d2h_scalar(pos.get() + m2 - 1, c.stream) + d2h_scalar(head.get() + m2 - 1, c.stream);
+    uint64_t* other = (ks == k0.get()) ? k1.get() : k0.get();
+    LAUNCH(c, "setup", 0.0, k_compact_keys, grid_for(m2, SB, c.num_sms * 16), SB, 0, ks, head.get(), pos.get(), m2,
+           other);
+    g.m = m;
+    g.adj.alloc(m, c.stream);
+    LAUNCH(c, "setup", 0.0, k_graph_ptr, grid_for(n + 1, SB, c.num_sms * 16), SB, 0, other, m, n, b, g.ptr.get());
+    LAUNCH(c, "setup", 0.0, k_graph_adj, grid_for(m, SB, c.num_sms * 16), SB, 0, other, m,
+           (uint64_t{1} << b) - 1, g.adj.get());
+}
+
+int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds) {
+    const int64_t n = g.n;
+    DevArray<int> state(n, c.stream);
+    CK(cudaMemsetAsync(state.get(), 0, sizeof(int) * n, c.stream));
+    constexpr int BATCH = 16;
+    DevArray<int> cnt(BATCH, c.stream);
+    int64_t r = 0;
+    const unsigned grid = grid_for(n, SB, c.num_sms * 8);
+    for (;;) {
+        CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int) * BATCH, c.stream));
+        for (int k = 0; k < BATCH; ++k)
+            LAUNCH(c, "setup", 0.0, k_agg_round, grid, SB, 0, static_cast<int>(n), g.ptr.get(), g.adj.get(),
+                   state.get(), cnt.get() + k);
+        r += BATCH;
+        int h[BATCH];
+        d2h(h, cnt.get(), BATCH, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        int done_at = -1;
+        for (int k = 0; k < BATCH; ++k)
+            if (h[k] == 0) {
+                done_at = k;
+                break;
+            }
+        if (done_at >= 0) {
+            r = r - BATCH + done_at + 1;
+            break;
+        }
+    }
+    if (rounds) *rounds = r;
+
+    DevArray<int64_t> rf(n + 1, c.stream), rid(n + 1, c.stream), iso(n + 1, c.stream), isor(n + 1, c.stream);
+    CK(cudaMemsetAsync(rf.get() + n, 0, sizeof(int64_t), c.stream));
+    LAUNCH(c, "setup", 0.0, k_root_flags, grid_for(n, SB, c.num_sms * 16), SB, 0, state.get(), n, rf.get());
+    exclusive_sum(c, rf.get(), rid.get(), n + 1);
+    const int64_t n_roots = d2h_scalar(rid.get() + n, c.stream);
+    agg.alloc(n, c.stream);
+    CK(cudaMemsetAsync(iso.get() + n, 0, sizeof(int64_t), c.stream));
+    LAUNCH(c, "setup", 0.0, k_assign1, grid_for(n, SB, c.num_sms * 16), SB, 0, n, g.ptr.get(), g.adj.get(),
+           state.get(), rid.get(), agg.get(), iso.get());
+    exclusive_sum(c, iso.get(), isor.get(), n + 1);
+    const int64_t n_iso = d2h_scalar(isor.get() + n, c.stream);
+    DevArray<int> err(1, c.stream);
+    CK(cudaMemsetAsync(err.get(), 0, sizeof(int), c.stream));
+    LAUNCH(c, "setup", 0.0, k_assign2, grid_for(n, SB, c.num_sms * 16), SB, 0, n, g.ptr.get(), g.adj.get(), n_roots,
+           isor.get(), agg.get(), err.get());
+    if (d2h_scalar(err.get(), c.stream)) fail(AMGR_E_RUNTIME, "aggregate: internal error (unassigned neighbour)");
+    return n_roots + n_iso;
+}
+
+void members(Ctx& c, int64_t nf, int64_t nc, const int* agg, DevArray<int>& mptr, DevArray<int>& midx) {
+    const int b = bits_for(nc);
+    DevArray<int> cnt(nc + 1, c.stream);
+    CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int) * (nc + 1), c.stream));
+    LAUNCH(c, "setup", 0.0, k_hist, grid_for(nf, SB, c.num_sms * 16), SB, 0, agg, nf, cnt.get());
+    mptr.alloc(nc + 1, c.stream);
+    exclusive_sum(c, cnt.get(), mptr.get(), nc + 1);
+    DevArray<uint64_t> k0(nf, c.stream), k1(nf, c.stream);
+    DevArray<int> v0(nf, c.stream), v1(nf, c.stream);
+    LAUNCH(c, "setup", 0.0, k_agg_keys, grid_for(nf, SB, c.num_sms * 16), SB, 0, agg, nf, k0.get());
+    LAUNCH(c, "setup", 0.0, k_iota, grid_for(nf, SB, c.num_sms * 16), SB, 0, v0.get(), nf);
+    uint64_t* ko;
+    int* vo;
+    sort_pairs(c, k0.get(), k1.get(), v0.get(), v1.get(), nf, b, &ko, &vo);
+    midx.alloc(nf, c.stream);
+    d2d(midx.get(), vo, nf, c.stream);
+}
+
+void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbolic& out) {
+    const int64_t m = A.nnz;
+    const int b = bits_for(nc);
+    const uint64_t mask = (uint64_t{1} << b) - 1;
+    out.contrib.alloc(m, c.stream);
+    DevArray<uint64_t> k0(m, c.stream), k1(m, c.stream);
+    DevArray<int> v0(m, c.stream), v1(m, c.stream), rowof(m, c.stream);
+    LAUNCH(c, "setup", 0.0, k_rap_keys, grid_for(A.n, SB, c.num_sms * 16), SB, 0, A, agg, b, k0.get(), v0.get(),
+           rowof.get());
+    uint64_t* ks;
+    int* vs;
+    sort_pairs(c, k0.get(), k1.get(), v0.get(), v1.get(), m, 2 * b, &ks, &vs);
+    DevArray<int64_t> head(m, c.stream), pos(m, c.stream);
+    LAUNCH(c, "setup", 0.0, k_heads, grid_for(m, SB, c.num_sms * 16), SB, 0, ks, m, head.get());
+    exclusive_sum(c, head.get(), pos.get(), m);
+    const int64_t nnz_c = d2h_scalar(pos.get() + m - 1, c.stream) + d2h_scalar(head.get() + m - 1, c.stream);
+    out.nnz_c = nnz_c;
+    out.cptr.alloc(nnz_c + 1, c.stream);
+    uint64_t* ukeys = (ks == k0.get()) ? k1.get() : k0.get();
+    LAUNCH(c, "setup", 0.0, k_rap_plan, grid_for(m, SB, c.num_sms * 16), SB, 0, ks, vs, rowof.get(), head.get(),
+           pos.get(), m, out.contrib.get(), out.cptr.get(), ukeys);
+    LAUNCH(c, "setup", 0.0, k_set_int, 1, 1, 0, out.cptr.get() + nnz_c, static_cast<int>(m));
+    out.col.alloc(nnz_c, c.stream);
+    LAUNCH(c, "setup", 0.0, k_coarse_col, grid_for(nnz_c, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, mask,
+           out.col.get());
+    out.rp.alloc(nc + 1, c.stream);
+    LAUNCH(c, "setup", 0.0, k_graph_ptr, grid_for(nc + 1, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, nc, b,
+           out.rp.get());
+}
+
+}  // namespace amgr

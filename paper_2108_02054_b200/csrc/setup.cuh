@@ -1,0 +1,40 @@
+// Device-side full AMG setup (hierarchy.cpp:45-105): strength graph, exact
+// parallel replay of the sequential greedy aggregation, P/R, and the symbolic
+// Galerkin plan that partial rebuilds reuse.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace amgr {
+
+struct GraphDev {
+    int64_t n = 0, m = 0;
+    DevArray<int> ptr, adj;
+};
+
+// First row (ascending) whose diagonal is missing or zero, or -1.
+// (strength_graph, coarsening.cpp:19-32; build_smoother, smoother.cpp:12-28)
+int64_t first_bad_diag(Ctx& c, const CsrView& A, const int* dpos);
+
+// Symmetrised strong-coupling graph, adjacency sorted and unique
+// (coarsening.cpp:11-75).  eps2 = eps*eps as the reference computes it.
+void strength_graph(Ctx& c, const CsrView& A, const int* dpos, double eps2, GraphDev& g);
+
+// Two-pass greedy aggregation (coarsening.cpp:77-120) replayed exactly in
+// parallel rounds.  Returns n_coarse; agg has g.n entries.
+int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds);
+
+// R = P^T: member lists per aggregate, ascending fine index (csr.cpp:93-113).
+void members(Ctx& c, int64_t nf, int64_t nc, const int* agg, DevArray<int>& mptr, DevArray<int>& midx);
+
+// Symbolic RAP + numeric plan.  Coarse pattern (sorted columns, structural,
+// csr.cpp:115-143) and for every coarse entry its contributing fine entries in
+// the reference's summation order with row-break flags.
+struct RapSymbolic {
+    int64_t nnz_c = 0;
+    DevArray<int> rp, col;       // coarse pattern
+    DevArray<int> cptr, contrib; // plan
+};
+void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbolic& out);
+
+}  // namespace amgr

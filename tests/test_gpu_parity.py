@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference itself
+(oracle/_ref, the unmodified reference compiled from /root/reference sources).
+
+Bar (BASELINE.json north_star): hierarchy structure bit-exact (aggregates,
+patterns of P, R and every A_i); level values within 1e-12 relative — we
+assert bit-exactness, which holds because the device replays the reference's
+summation order; solve: iteration count within +-1 and final
+residual <= tol against the fixed-V-cycle oracle.
+"""
+import numpy as np
+import pytest
+
+from oracle import problems as P
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+amg = pytest.importorskip("paper_2108_02054_b200")
+
+
+def _bits(a):
+    return np.asarray(a, np.float64).view(np.int64)
+
+
+def assert_same_hierarchy(g, r, values=True):
+    assert g.num_levels() == len(r.levels), (g.num_levels(), len(r.levels))
+    for l, RL in enumerate(r.levels):
+        rp, ci, v = g.level_A(l)
+        np.testing.assert_array_equal(rp, RL.A[0], err_msg=f"level {l} row_ptr")
+        np.testing.assert_array_equal(ci, RL.A[1], err_msg=f"level {l} col_idx")
+        if values:
+            np.testing.assert_array_equal(_bits(v), _bits(RL.A[2]), err_msg=f"level {l} values")
+        if RL.agg is not None:
+            np.testing.assert_array_equal(g.level_agg(l), RL.agg, err_msg=f"level {l} aggregates")
+            rrp, rci = g.level_R(l)
+            np.testing.assert_array_equal(rrp, RL.R[0], err_msg=f"level {l} R row_ptr")
+            np.testing.assert_array_equal(rci, RL.R[1], err_msg=f"level {l} R col_idx")
+        if RL.inv_diag is not None and values:
+            np.testing.assert_array_equal(_bits(g.level_smoother(l)), _bits(RL.inv_diag),
+                                          err_msg=f"level {l} inv_diag")
+    if values:
+        lu, piv = g.coarse_lu()
+        np.testing.assert_array_equal(piv, r.piv)
+        np.testing.assert_array_equal(_bits(lu), _bits(r.lu))
+
+
+CASES = {
+    "poisson1d_64_ce10": (lambda: P.poisson1d(64), dict(coarse_enough=10)),
+    "poisson2d_16": (lambda: P.poisson2d(16), {}),
+    "poisson2d_40": (lambda: P.poisson2d(40), {}),
+    "poisson2d_64": (lambda: P.poisson2d(64), {}),
+    "poisson3d_12": (lambda: P.grid3d_values("poisson", 12, 3), {}),
+    "dambreak_16": (lambda: P.grid3d_values("dambreak", 16, 0), {}),
+    "dambreak_24_k20": (lambda: P.grid3d_values("dambreak", 24, 20), {}),
+    "blob_20": (lambda: P.grid3d_values("blob", 20, 5), {}),
+    "random_300": (lambda: P.random_csr(300, 300, 0.02, 7, diag=3.0), {}),
+    "random_500_eps0": (lambda: P.random_csr(500, 500, 0.01, 11, diag=2.0), dict(eps=0.0)),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_setup_bit_exact(ctx, name):
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    assert_same_hierarchy(h, r)
+
+
+@pytest.mark.parametrize("name", ["poisson2d_40", "dambreak_24_k20", "random_300"])
+def test_partial_update_bit_exact(ctx, name):
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    rp, ci, v = A
+    rng = np.random.default_rng(5)
+    B = (rp, ci, v * (1.0 + 0.1 * rng.random(len(v))))
+    hu = amg.partial_update(h, B)
+    ru = ref.partial_update(r, B, ref.params(**kw))
+    assert_same_hierarchy(hu, ru)
+    for l in range(h.num_levels() - 1):
+        assert hu.shares_transfer(h, l)
+    # in-place rebuild gives the same hierarchy
+    h.rebuild(B)
+    assert_same_hierarchy(h, ru)
+
+
+def test_partial_update_fixed_point(ctx):
+    A = P.grid3d_values("dambreak", 16, 7)
+    h = amg.setup(A, ctx=ctx)
+    r = ref.setup(A)
+    assert_same_hierarchy(amg.partial_update(h, A), r)
+
+
+def test_dambreak_sequence_partial_reuse(ctx):
+    # values drift, pattern fixed: device rebuild == reference partial_update
+    A0 = P.grid3d_values("dambreak", 20, 0)
+    h = amg.setup(A0, ctx=ctx)
+    r = ref.setup(A0)
+    for k in (5, 17, 49):
+        Ak = P.grid3d_values("dambreak", 20, k)
+        h.rebuild_values(Ak[2])
+        r = ref.partial_update(r, Ak)
+        assert_same_hierarchy(h, r)
+
+
+def test_pattern_change_same_dims(ctx):
+    A = P.random_csr(200, 200, 0.03, 1, diag=2.0)
+    B = P.random_csr(200, 200, 0.03, 2, diag=2.0)
+    h = amg.setup(A, ctx=ctx)
+    r = ref.setup(A)
+    assert_same_hierarchy(amg.partial_update(h, B), ref.partial_update(r, B))
+
+
+@pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "blob_20", "random_300"])
+def test_vcycle_bit_exact(ctx, name):
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    f = np.random.default_rng(3).uniform(-1, 1, len(A[0]) - 1)
+    u = amg.vcycle(h, f)
+    ur = ref.vcycle(r, f, fixed=True, prm=ref.params(**kw))
+    np.testing.assert_array_equal(_bits(u), _bits(ur))
+
+
+@pytest.mark.parametrize("pre,post", [(0, 0), (2, 1), (1, 3)])
+def test_vcycle_sweeps(ctx, pre, post):
+    A = P.poisson2d(32)
+    h = amg.setup(A, amg.AmgParams(pre_sweeps=pre, post_sweeps=post), ctx=ctx)
+    r = ref.setup(A, ref.params(pre_sweeps=pre, post_sweeps=post))
+    f = np.random.default_rng(4).uniform(-1, 1, 32 * 32)
+    u = amg.vcycle(h, f)
+    ur = ref.vcycle(r, f, fixed=True, prm=ref.params(pre_sweeps=pre, post_sweeps=post))
+    np.testing.assert_array_equal(_bits(u), _bits(ur))
+
+
+@pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "blob_20", "poisson3d_12"])
+def test_bicgstab_parity(ctx, name):
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    f = P.rhs(len(A[0]) - 1)
+    u, st = amg.bicgstab(h, f)
+    rs = ref.bicgstab(r, f, fixed=True, prm=ref.params(**kw))
+    assert st.converged and rs.converged
+    assert abs(st.iterations - rs.iterations) <= 1, (st.iterations, rs.iterations)
+    assert st.relative_residual <= 1e-8
+    # true residual from the reference's own spmv
+    res = np.linalg.norm(f - ref.spmv(A, u)) / np.linalg.norm(f)
+    assert res <= 1e-8
+
+
+def test_bicgstab_zero_rhs(ctx):
+    A = P.poisson2d(8)
+    h = amg.setup(A, ctx=ctx)
+    u, st = amg.bicgstab(h, np.zeros(64))
+    assert st.converged and st.iterations == 0 and np.all(u == 0)
+
+
+def test_errors_match_reference(ctx):
+    # dimension change (hierarchy.cpp:110-116)
+    h = amg.setup(P.poisson2d(12), ctx=ctx)
+    with pytest.raises(amg.DimensionChange, match="partial update impossible, full rebuild required"):
+        amg.partial_update(h, P.poisson2d(13))
+    # zero diagonal with level prefix (hierarchy.cpp:31-35)
+    A = (np.array([0, 2, 3]), np.array([0, 1, 0]), np.array([1.0, 1.0, 1.0]))
+    with pytest.raises(amg.InvalidArgument, match="level 0"):
+        amg.setup(A, amg.AmgParams(coarse_enough=1), ctx=ctx)
+    # stall beyond the direct budget (hierarchy.cpp:70-77)
+    D = P.diagonal(np.full(20, 2.0))
+    with pytest.raises(amg.RuntimeFailure, match="coarsening stalled"):
+        amg.setup(D, amg.AmgParams(coarse_enough=5, max_direct_size=10), ctx=ctx)
+    hd = amg.setup(D, amg.AmgParams(coarse_enough=5, max_direct_size=50), ctx=ctx)
+    assert hd.num_levels() == 1
+    # singular coarse matrix (dense_lu.cpp:38-42)
+    S = (np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([1.0, 1.0, 1.0, 1.0]))
+    with pytest.raises(amg.RuntimeFailure, match="singular"):
+        amg.setup(S, ctx=ctx)
