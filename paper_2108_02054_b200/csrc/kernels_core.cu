@@ -22,9 +22,11 @@ namespace {
 constexpr int RP_BLOCK = 256;
 constexpr int RP_WARPS = RP_BLOCK / 32;
 constexpr int RP_CH = 256;  // staged entries per warp per chunk (3 KB)
+constexpr int RP_BATCH = 8; // operand gathers in flight per thread
+constexpr int RP_MINB = 5;  // resident blocks per SM the register budget targets
 
 template <class Op>
-__global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
+__global__ void __launch_bounds__(RP_BLOCK, RP_MINB) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
     __shared__ double s_val[RP_WARPS][RP_CH];
@@ -54,16 +56,19 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             __syncwarp();
             int a = max(rs, c0);
             const int b = min(re, c1);
-            for (; a + 4 <= b; a += 4) {
+            // issue up to RP_BATCH independent operand gathers, then accumulate
+            // them strictly in column order
+            while (a < b) {
+                const int cnt = min(RP_BATCH, b - a);
                 const int k = a - c0;
-                const double x0 = op.x(s_col[w][k]), x1 = op.x(s_col[w][k + 1]);
-                const double x2 = op.x(s_col[w][k + 2]), x3 = op.x(s_col[w][k + 3]);
-                sum = dadd(sum, dmul(s_val[w][k], x0));
-                sum = dadd(sum, dmul(s_val[w][k + 1], x1));
-                sum = dadd(sum, dmul(s_val[w][k + 2], x2));
-                sum = dadd(sum, dmul(s_val[w][k + 3], x3));
+                double xv[RP_BATCH];
+#pragma unroll
+                for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][k + t]) : 0.0;
+#pragma unroll
+                for (int t = 0; t < RP_BATCH; ++t)
+                    if (t < cnt) sum = dadd(sum, dmul(s_val[w][k + t], xv[t]));
+                a += cnt;
             }
-            for (; a < b; ++a) sum = dadd(sum, dmul(s_val[w][a - c0], op.x(s_col[w][a - c0])));
             __syncwarp();
         }
         if (valid) op.finish(row, sum, dots);
@@ -195,9 +200,20 @@ __global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __re
                            const double* __restrict__ r, double* __restrict__ fc, Gate g) {
     if (gated_off(g)) return;
     for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
-        const int p0 = mptr[I], p1 = mptr[I + 1];
+        int p = __ldg(mptr + I);
+        const int p1 = __ldg(mptr + I + 1);
         double s = 0.0;
-        for (int p = p0; p < p1; ++p) s = dadd(s, __ldg(r + __ldg(midx + p)));
+        while (p < p1) {
+            const int cnt = min(4, p1 - p);
+            double rv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t < cnt) rv[t] = __ldg(r + __ldg(midx + p + t));
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t < cnt) s = dadd(s, rv[t]);
+            p += cnt;
+        }
         fc[I] = s;
     }
 }
@@ -372,14 +388,28 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
 
 constexpr int LS_THREADS = 256;
 
+// x = LU \\ b replaying dense_lu.cpp:52-73 bit for bit.  The factor is staged
+// in shared memory; the forward sweep is column-oriented over one warp (each
+// row still subtracts in ascending j), the backward sweep is the reference's
+// row-oriented chain (row i needs x[i+1] first), run by one thread with its
+// operand loads issued ahead of the dependent subtractions.
 __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __restrict__ m,
                                                          const int64_t* __restrict__ piv,
-                                                         const double* b, double* x, Gate g) {
+                                                         const double* b, double* x, int use_smem, Gate g) {
     if (gated_off(g)) return;
-    extern __shared__ double xs[];
+    extern __shared__ double sm[];
+    double* xs = sm;
+    const double* M = m;
     const int tid = threadIdx.x;
     for (int i = tid; i < n; i += blockDim.x) xs[i] = b[i];
+    if (use_smem) {
+        double* ms = sm + n;
+        const int nn = n * n;
+        for (int t = tid; t < nn; t += blockDim.x) ms[t] = m[t];
+        M = ms;
+    }
     __syncthreads();
+    if (tid >= 32) return;
     if (tid == 0)
         for (int k = 0; k < n; ++k) {
             const int p = static_cast<int>(piv[k]);
@@ -389,25 +419,30 @@ __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __
                 xs[p] = t;
             }
         }
-    __syncthreads();
-    // forward, unit L: column-oriented sweep subtracts in ascending j for every
-    // row, i.e. exactly the reference's row-oriented order.
+    __syncwarp();
     for (int j = 0; j < n - 1; ++j) {
         const double xj = xs[j];
-        for (int i = j + 1 + tid; i < n; i += blockDim.x) xs[i] = dsub(xs[i], dmul(m[i * n + j], xj));
-        __syncthreads();
+        for (int i = j + 1 + tid; i < n; i += 32) xs[i] = dsub(xs[i], dmul(M[i * n + j], xj));
+        __syncwarp();
     }
-    // backward: the reference subtracts ascending j from i+1, so each row must
-    // wait for x[i+1]; one thread walks it.
     if (tid == 0)
         for (int i = n - 1; i >= 0; --i) {
+            const double* mi = M + static_cast<int64_t>(i) * n;
             double s = xs[i];
-            const double* mi = m + static_cast<int64_t>(i) * n;
-            for (int j = i + 1; j < n; ++j) s = dsub(s, dmul(mi[j], xs[j]));
+            int j = i + 1;
+            for (; j + 4 <= n; j += 4) {
+                const double p0 = dmul(mi[j], xs[j]), p1 = dmul(mi[j + 1], xs[j + 1]);
+                const double p2 = dmul(mi[j + 2], xs[j + 2]), p3 = dmul(mi[j + 3], xs[j + 3]);
+                s = dsub(s, p0);
+                s = dsub(s, p1);
+                s = dsub(s, p2);
+                s = dsub(s, p3);
+            }
+            for (; j < n; ++j) s = dsub(s, dmul(mi[j], xs[j]));
             xs[i] = __ddiv_rn(s, mi[i]);
         }
-    __syncthreads();
-    for (int i = tid; i < n; i += blockDim.x) x[i] = xs[i];
+    __syncwarp();
+    for (int i = tid; i < n; i += 32) x[i] = xs[i];
 }
 
 // ---- misc ---------------------------------------------------------------------
@@ -545,8 +580,11 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
 
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g) {
     if (n == 0) return;
-    const size_t sm = sizeof(double) * static_cast<size_t>(n);
-    LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, g);
+    const size_t full = sizeof(double) * static_cast<size_t>(n * n + n);
+    const int use_smem = full <= 200 * 1024 ? 1 : 0;
+    const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(n);
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }
 
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g) {
