@@ -53,7 +53,12 @@ typedef enum amgr_status {
                                     message text identical to the reference's   */
 } amgr_status;
 
-enum { AMGR_HOST = 0, AMGR_DEVICE = 1 };
+enum { AMGR_HOST = 0, AMGR_DEVICE = 1,
+       /* amgr_rebuild_values only: the hierarchy adopts the device buffer
+        * (zero copy) until the next rebuild; it must stay valid and
+        * unmodified, be 16-byte aligned and have >= 32 bytes of slack past
+        * the last value (read by 16-byte TMA bulk copies). */
+       AMGR_DEVICE_ADOPT = 2 };
 
 /* Smoother kinds.  JACOBI is the reference's (smoother.hpp:11-16); SPAI0 and
  * CHEBYSHEV are north-star extensions with restated oracles (parity unpinned

@@ -29,7 +29,7 @@ __all__ = [
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libamgr_b200.so")
 
-HOST, DEVICE = 0, 1
+HOST, DEVICE, DEVICE_ADOPT = 0, 1, 2
 SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}
 COARSENING = {"plain": 0, "smoothed": 1}
 PROBLEM = {"poisson": 0, "blob": 1, "dambreak": 2, "convdiff": 3}
@@ -379,9 +379,12 @@ class Hierarchy:
         c = A._c()
         _check(lib().amgr_rebuild(self._p, C.byref(c)), self.ctx.ptr)
 
-    def rebuild_values(self, values, location=None):
+    def rebuild_values(self, values, adopt: bool = False):
+        """Values-only rebuild (amgr_rebuild_values).  A device pointer may be
+        adopted zero-copy (AMGR_DEVICE_ADOPT): it must stay valid until the next
+        rebuild and carry >= 32 bytes of slack."""
         if isinstance(values, int):
-            _check(lib().amgr_rebuild_values(self._p, values, DEVICE), self.ctx.ptr)
+            _check(lib().amgr_rebuild_values(self._p, values, DEVICE_ADOPT if adopt else DEVICE), self.ctx.ptr)
         else:
             v = _f64(values)
             _check(lib().amgr_rebuild_values(self._p, v.ctypes.data, HOST), self.ctx.ptr)

@@ -97,7 +97,8 @@ class DevArray {
         release();
         stream_ = s;
         n_ = n;
-        if (n > 0) CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), sizeof(T) * static_cast<size_t>(n), s));
+        // +8 elements of slack: TMA bulk copies read 16-byte-rounded ranges
+        if (n > 0) CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), sizeof(T) * static_cast<size_t>(n + 8), s));
     }
     void release() {
         if (p_) cudaFreeAsync(p_, stream_);

@@ -135,7 +135,7 @@ void build_smoother(Ctx& c, Level& L, const AmgP& p, int* bad) {
     if (p.smoother == AMGR_SMOOTHER_SPAI0)
         spai0_rebuild(c, L.view(), L.pat->diag.get(), L.w.get(), bad);
     else
-        jacobi_rebuild(c, n, L.val.get(), L.pat->diag.get(), L.w.get(), bad);
+        jacobi_rebuild(c, n, L.view().val, L.pat->diag.get(), L.w.get(), bad);
     L.has_smoother = true;
 }
 
@@ -192,7 +192,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         clk.begin(PH_GALERKIN);
         Level& B = h.lv[i + 1];
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
-        rap_numeric(c, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.val.get(), B.val.get(), A.pat->nnz);
+        rap_numeric(c, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz);
         clk.end(PH_GALERKIN);
     }
     clk.begin(PH_COARSE);
@@ -249,7 +249,7 @@ Work& work(Hier& h) {
             W->r[i].alloc(n, c.stream);
         }
         W->st.alloc(1, c.stream);
-        W->partials.alloc(static_cast<int64_t>(dot_grid(c)) * 4, c.stream);
+        W->partials.alloc(static_cast<int64_t>(dot_grid(c)) * 4 + 64, c.stream);
         W->ticket.alloc(1, c.stream);
         CK(cudaMemsetAsync(W->ticket.get(), 0, sizeof(unsigned), c.stream));
         W->err.alloc(static_cast<int64_t>(L + 1), c.stream);
@@ -377,6 +377,7 @@ static void rebuild_into(Hier& h, const amgr_csr& A) {
     // pattern: reuse the cached symbolic plan unless the structure changed
     std::shared_ptr<Pattern> np = make_pattern(c, A);
     const bool same = same_pattern(c, *np, *h.lv.front().pat);
+    h.lv.front().ext_val = nullptr;
     upload_values(c, h.lv.front().val, A.values, A.nnz, A.location);
     if (!same) {
         h.lv.front().pat = np;
@@ -419,7 +420,13 @@ void rebuild(Hier& h, const amgr_csr& A) {
 
 void rebuild_values(Hier& h, const double* values, int location) {
     Ctx& c = *h.ctx;
-    upload_values(c, h.lv.front().val, values, h.lv.front().pat->nnz, location);
+    if (location == AMGR_DEVICE_ADOPT) {
+        if (reinterpret_cast<uintptr_t>(values) % 16 != 0) invalid("rebuild_values: adopted buffer must be 16-byte aligned");
+        h.lv.front().ext_val = values;
+    } else {
+        h.lv.front().ext_val = nullptr;
+        upload_values(c, h.lv.front().val, values, h.lv.front().pat->nnz, location);
+    }
     work(h);
     reset_err(h);
     PhaseClock clk(c);

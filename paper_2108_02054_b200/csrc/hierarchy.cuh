@@ -42,6 +42,7 @@ struct RapPlan {
 struct Level {
     std::shared_ptr<Pattern> pat;
     DevArray<double> val;  // A_i values
+    const double* ext_val = nullptr;  // adopted (zero-copy) A_0 values, see AMGR_DEVICE_ADOPT
     DevArray<double> w;    // smoother diagonal (inv_diag for Jacobi)
     bool has_smoother = false;
     std::shared_ptr<Transfer> T;   // null on the coarsest level
@@ -53,7 +54,7 @@ struct Level {
         v.nnz = pat->nnz;
         v.rp = pat->rp.get();
         v.col = pat->col.get();
-        v.val = val.get();
+        v.val = ext_val ? ext_val : val.get();
         return v;
     }
 };

@@ -19,114 +19,230 @@ namespace amgr {
 
 namespace {
 
-constexpr int RP_BLOCK = 256;
-constexpr int RP_WARPS = RP_BLOCK / 32;
-constexpr int RP_CH = 256;  // staged entries per warp per chunk (3 KB)
-constexpr int RP_BATCH = 8; // operand gathers in flight per thread
-constexpr int RP_MINB = 5;  // resident blocks per SM the register budget targets
+constexpr int RP_WARPS = 4;                 // warps per block
+constexpr int RP_BLOCK = RP_WARPS * 32;
+constexpr int RP_CH = 256;                  // entries per TMA chunk (multiple of 4)
+constexpr int RP_BATCH = 8;                 // operand gathers in flight per thread
+constexpr int RP_BLOCKS_PER_SM = 8;         // persistent grid: 32 warps per SM
 
+// ---- TMA 1-D bulk copy + mbarrier helpers (sm_90+/sm_100a PTX) ----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Each warp owns a contiguous row range; the nnz stream of that range
+// (values + int32 columns) is double-buffered into shared memory with TMA
+// 1-D bulk copies completing on per-stage mbarriers, so DRAM reads of the
+// matrix are always one chunk ahead of the consumer.  Threads own rows
+// (32 consecutive rows per group) and accumulate strictly in column order
+// (csr.cpp:79-84), gathering up to RP_BATCH operands at a time.  Row
+// pointers and the per-row epilogue operands are prefetched one group ahead.
+// The operand x_i of the row's own diagonal is captured during accumulation
+// (the V-cycle epilogues need it: u_i, or u_i + P u_c).
 template <class Op>
-__global__ void __launch_bounds__(RP_BLOCK, RP_MINB) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
+__global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink, int rows_per_warp,
+                                                      int nnz_pad) {
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
-    __shared__ double s_val[RP_WARPS][RP_CH];
-    __shared__ int s_col[RP_WARPS][RP_CH];
+    __shared__ __align__(128) double s_val[RP_WARPS][2][RP_CH];
+    __shared__ __align__(128) int s_col[RP_WARPS][2][RP_CH];
+    __shared__ __align__(8) uint64_t s_bar[RP_WARPS][2];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = static_cast<int>(A.n);
     double dots[ND];
 #pragma unroll
     for (int k = 0; k < ND; ++k) dots[k] = 0.0;
-    const int64_t wstride = static_cast<int64_t>(gridDim.x) * RP_WARPS;
-    for (int64_t wid = static_cast<int64_t>(blockIdx.x) * RP_WARPS + w; wid * 32 < n; wid += wstride) {
-        const int r0 = static_cast<int>(wid * 32);
-        const int r1 = min(r0 + 32, n);
-        const int row = r0 + lane;
-        const bool valid = row < n;
-        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + r1);
-        const int rs = valid ? __ldg(A.rp + row) : e1;
-        const int re = valid ? __ldg(A.rp + row + 1) : e1;
-        double sum = 0.0;
-        for (int c0 = e0; c0 < e1; c0 += RP_CH) {
-            const int c1 = min(c0 + RP_CH, e1);
-#pragma unroll 4
-            for (int e = c0 + lane; e < c1; e += 32) {
-                s_val[w][e - c0] = __ldg(A.val + e);
-                s_col[w][e - c0] = __ldg(A.col + e);
-            }
-            __syncwarp();
-            int a = max(rs, c0);
-            const int b = min(re, c1);
-            // issue up to RP_BATCH independent operand gathers, then accumulate
-            // them strictly in column order
-            while (a < b) {
-                const int cnt = min(RP_BATCH, b - a);
-                const int k = a - c0;
-                double xv[RP_BATCH];
-#pragma unroll
-                for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][k + t]) : 0.0;
-#pragma unroll
-                for (int t = 0; t < RP_BATCH; ++t)
-                    if (t < cnt) sum = dadd(sum, dmul(s_val[w][k + t], xv[t]));
-                a += cnt;
-            }
-            __syncwarp();
+
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * RP_WARPS + w;
+    const int R0 = static_cast<int>(gw * rows_per_warp < n ? gw * rows_per_warp : static_cast<int64_t>(n));
+    const int R1 = static_cast<int>(static_cast<int64_t>(R0) + rows_per_warp < n ? static_cast<int64_t>(R0) + rows_per_warp : static_cast<int64_t>(n));
+    if (R0 < R1) {
+        const int E0 = __ldg(A.rp + R0), E1 = __ldg(A.rp + R1);
+        const int cfirst = E0 / RP_CH;
+        const int clast = E1 > E0 ? (E1 - 1) / RP_CH : cfirst;
+        uint64_t* bar = s_bar[w];
+        if (lane == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            mbar_fence_init();
         }
-        if (valid) op.finish(row, sum, dots);
+        __syncwarp();
+        auto issue = [&](int c, int st) {
+            const int base = c * RP_CH;
+            const int cnt = min(RP_CH, nnz_pad - base);
+            const uint32_t bv = static_cast<uint32_t>(cnt) * 8u, bc = static_cast<uint32_t>(cnt) * 4u;
+            mbar_expect_tx(&bar[st], bv + bc);
+            tma_load_1d(&s_val[w][st][0], A.val + base, bv, &bar[st]);
+            tma_load_1d(&s_col[w][st][0], A.col + base, bc, &bar[st]);
+        };
+        const bool any = E1 > E0;
+        if (lane == 0 && any) {
+            issue(cfirst, 0);
+            if (cfirst + 1 <= clast) issue(cfirst + 1, 1);
+        }
+        int cur = cfirst, st = 0;
+        uint32_t phase = 0;  // bit s = parity to wait for on stage s
+        if (any) {
+            mbar_wait(&bar[0], 0);
+            phase ^= 1u;
+        }
+        auto advance = [&]() {
+            __syncwarp();
+            if (lane == 0 && cur + 2 <= clast) {
+                fence_proxy_async();
+                issue(cur + 2, st);
+            }
+            ++cur;
+            st ^= 1;
+            mbar_wait(&bar[st], (phase >> st) & 1u);
+            phase ^= (1u << st);
+        };
+
+        int row = R0 + lane;
+        int rs = row < R1 ? __ldg(A.rp + row) : E1;
+        int re = row < R1 ? __ldg(A.rp + row + 1) : E1;
+        typename Op::Row rw;
+        if (row < R1) rw = op.load(row);
+        for (int r0 = R0; r0 < R1; r0 += 32) {
+            // prefetch the next group's row pointers and epilogue operands
+            const int nrow = r0 + 32 + lane;
+            const bool nvalid = nrow < R1;
+            const int nrs = nvalid ? __ldg(A.rp + nrow) : E1;
+            const int nre = nvalid ? __ldg(A.rp + nrow + 1) : E1;
+            typename Op::Row nrw;
+            if (nvalid) nrw = op.load(nrow);
+
+            const bool valid = row < R1;
+            const int g0 = __shfl_sync(0xffffffffu, rs, 0);
+            const int ge = __shfl_sync(0xffffffffu, re, 31);
+            double sum = 0.0, xdiag = 0.0;
+            if (ge > g0) {
+                while (g0 >= (cur + 1) * RP_CH && cur < clast) advance();
+                for (;;) {
+                    const int c0 = cur * RP_CH, c1 = c0 + RP_CH;
+                    int a = max(rs, c0);
+                    const int b = min(re, c1);
+                    while (a < b) {
+                        const int cnt = min(RP_BATCH, b - a);
+                        const int k = a - c0;
+                        double xv[RP_BATCH];
+#pragma unroll
+                        for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
+#pragma unroll
+                        for (int t = 0; t < RP_BATCH; ++t)
+                            if (t < cnt) {
+                                sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
+                                if (s_col[w][st][k + t] == row) xdiag = xv[t];
+                            }
+                        a += cnt;
+                    }
+                    if (ge <= c1 || cur >= clast) break;
+                    advance();
+                }
+            }
+            if (valid) op.finish(row, sum, xdiag, rw, dots);
+            row = nrow;
+            rs = nrs;
+            re = nre;
+            rw = nrw;
+        }
+        __syncwarp();
     }
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
 
 // ---- row-pass operators ----------------------------------------------------
+struct NoRow {};
+struct Row1 {
+    double a;
+};
+struct Row2 {
+    double f, w;
+};
+
 struct OpSpmv {
     static constexpr int NDOT = 0;
+    using Row = NoRow;
     const double* xv;
     double* y;
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void finish(int i, double s, double*) const { y[i] = s; }
+    __device__ Row load(int) const { return {}; }
+    __device__ void finish(int i, double s, double, const Row&, double*) const { y[i] = s; }
 };
 
 struct OpResidual {
     static constexpr int NDOT = 0;
+    using Row = Row1;
     const double* f;
     const double* xv;
     double* r;
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void finish(int i, double s, double*) const { r[i] = dsub(f[i], s); }
+    __device__ Row load(int i) const { return {__ldg(f + i)}; }
+    __device__ void finish(int i, double s, double, const Row& q, double*) const { r[i] = dsub(q.a, s); }
 };
 
 // hierarchy.cpp:165-170 with smooth() from u = 0 (smoother.cpp:42-47):
 // u_j = 0 + (om*w_j)*(f_j - 0) ; r_i = f_i - sum_j a_ij u_j
 struct OpDown {
     static constexpr int NDOT = 0;
+    using Row = Row2;
     const double* f;
     const double* w;
     double om;
     double* u;
     double* r;
     __device__ double x(int j) const { return dadd(0.0, dmul(dmul(om, __ldg(w + j)), __ldg(f + j))); }
-    __device__ void finish(int i, double s, double*) const {
-        u[i] = x(i);
-        r[i] = dsub(f[i], s);
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
+    __device__ void finish(int i, double s, double, const Row& q, double*) const {
+        u[i] = dadd(0.0, dmul(dmul(om, q.w), q.f));
+        r[i] = dsub(q.f, s);
     }
 };
 
 // one damped sweep: out_i = u_i + (om*w_i)*(f_i - (A u)_i)
 struct OpSmooth {
     static constexpr int NDOT = 0;
+    using Row = Row2;
     const double* f;
     const double* w;
     double om;
     const double* u;
     double* out;
     __device__ double x(int j) const { return __ldg(u + j); }
-    __device__ void finish(int i, double s, double*) const {
-        out[i] = dadd(u[i], dmul(dmul(om, w[i]), dsub(f[i], s)));
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
+    __device__ void finish(int i, double s, double xi, const Row& q, double*) const {
+        out[i] = dadd(xi, dmul(dmul(om, q.w), dsub(q.f, s)));
     }
 };
 
 // hierarchy.cpp:179-183: x = u + (0 + 1.0*uc[agg]) then one sweep on x.
 struct OpUp {
     static constexpr int NDOT = 0;
+    using Row = Row2;
     const double* f;
     const double* w;
     double om;
@@ -135,59 +251,72 @@ struct OpUp {
     const double* uc;
     double* out;
     __device__ double x(int j) const { return dadd(__ldg(u + j), dadd(0.0, __ldg(uc + __ldg(agg + j)))); }
-    __device__ void finish(int i, double s, double*) const {
-        out[i] = dadd(x(i), dmul(dmul(om, w[i]), dsub(f[i], s)));
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
+    __device__ void finish(int i, double s, double xi, const Row& q, double*) const {
+        out[i] = dadd(xi, dmul(dmul(om, q.w), dsub(q.f, s)));
     }
 };
 
 struct OpSpmvDot {
     static constexpr int NDOT = 1;
+    using Row = Row1;
     const double* xv;
     double* y;
     const double* a;
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void finish(int i, double s, double* d) const {
+    __device__ Row load(int i) const { return {__ldg(a + i)}; }
+    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
         y[i] = s;
-        d[0] = __fma_rn(a[i], s, d[0]);
+        d[0] = __fma_rn(q.a, s, d[0]);
     }
 };
 
 struct OpSpmvDot2 {
     static constexpr int NDOT = 2;
+    using Row = Row1;
     const double* xv;
     double* y;
     const double* b;
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void finish(int i, double s, double* d) const {
+    __device__ Row load(int i) const { return {__ldg(b + i)}; }
+    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
         y[i] = s;
-        d[0] = __fma_rn(s, b[i], d[0]);
+        d[0] = __fma_rn(s, q.a, d[0]);
         d[1] = __fma_rn(s, s, d[1]);
     }
 };
 
 struct OpResidNorm {
     static constexpr int NDOT = 1;
+    using Row = Row1;
     const double* f;
     const double* xv;
     double* r;
     double* r2;
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void finish(int i, double s, double* d) const {
-        const double t = dsub(f[i], s);
+    __device__ Row load(int i) const { return {__ldg(f + i)}; }
+    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
+        const double t = dsub(q.a, s);
         if (r) r[i] = t;
         if (r2) r2[i] = t;
         d[0] = __fma_rn(t, t, d[0]);
     }
 };
 
+int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
+
 template <class Op>
 void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g,
-                    DotSink s, bool fixed_grid) {
+                    DotSink s, bool) {
     if (A.n == 0) return;
-    const int64_t warps = (A.n + 31) / 32;
-    unsigned grid = grid_for(warps, RP_WARPS);
-    if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
-    LAUNCH(c, fam, bytes, k_rowpass<Op>, grid, RP_BLOCK, 0, A, op, g, s);
+    const int64_t groups = (A.n + 31) / 32;
+    const int64_t max_warps = static_cast<int64_t>(persistent_grid(c)) * RP_WARPS;
+    const int64_t gpw = (groups + max_warps - 1) / max_warps;  // groups per warp
+    const int rows_per_warp = static_cast<int>(gpw * 32);
+    const int64_t warps = (A.n + rows_per_warp - 1) / rows_per_warp;
+    unsigned grid = static_cast<unsigned>((warps + RP_WARPS - 1) / RP_WARPS);
+    const int nnz_pad = static_cast<int>((A.nnz + 3) & ~int64_t{3});
+    LAUNCH(c, fam, bytes, k_rowpass<Op>, grid, RP_BLOCK, 0, A, op, g, s, rows_per_warp, nnz_pad);
 }
 
 double spmv_bytes(const CsrView& A) {
@@ -302,58 +431,49 @@ __global__ void k_densify_fill(CsrView A, double* dense) {
 
 constexpr int LU_THREADS = 1024;
 
+// coarse_factorize (dense_lu.cpp:10-50) replayed bit for bit: pivot = lowest
+// row attaining the largest |m[i][k]| (the reference's strict '>' scan), row
+// swap, l = m[i][k] / pivot, m[i][j] -= l*m[k][j] (no FMA).  One CTA; the
+// factor lives in shared memory when it fits; a 32x32 thread tile walks the
+// trailing submatrix without integer division; 3 barriers per step.
 __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int64_t* piv, int* status,
                                                           int use_smem) {
     extern __shared__ double sm[];
-    __shared__ double rbest[LU_THREADS / 32];
-    __shared__ int ridx[LU_THREADS / 32];
+    __shared__ double s_l[2048 + 1];
     __shared__ int s_p;
-    __shared__ double s_pivot;
     double* m = use_smem ? sm : gm;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nn = n * n;
     if (use_smem)
         for (int t = tid; t < nn; t += blockDim.x) m[t] = gm[t];
     if (tid == 0) *status = -1;
     __syncthreads();
     for (int k = 0; k < n; ++k) {
-        // pivot: lowest row attaining max |m[i][k]| over i >= k (strict '>' scan)
-        double best = -1.0;
-        int bi = 0x7fffffff;
-        for (int i = k + tid; i < n; i += blockDim.x) {
-            const double v = fabs(m[i * n + k]);
-            if (v > best) {
-                best = v;
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double ob = __shfl_down_sync(0xffffffffu, best, off);
-            const int oi = __shfl_down_sync(0xffffffffu, bi, off);
-            if (ob > best || (ob == best && oi < bi)) {
-                best = ob;
-                bi = oi;
-            }
-        }
-        if (lane == 0) {
-            rbest[w] = best;
-            ridx[w] = bi;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double b = rbest[0];
-            int p = ridx[0];
-            for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
-                if (rbest[q] > b || (rbest[q] == b && ridx[q] < p)) {
-                    b = rbest[q];
-                    p = ridx[q];
+        if (wid == 0) {
+            double best = -1.0;
+            int bi = 0x7fffffff;
+            for (int i = k + lane; i < n; i += 32) {
+                const double v = fabs(m[i * n + k]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
                 }
-            if (p == 0x7fffffff) p = k;  // all NaN: the reference keeps p = k
-            // the reference starts from best=|m[k][k]|, p=k: ties keep k
-            if (!(fabs(m[k * n + k]) < b)) p = k;
-            s_p = p;
-            piv[k] = p;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, best, off);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                int p = bi;
+                if (p == 0x7fffffff || !(fabs(m[k * n + k]) < best)) p = k;  // ties / NaN keep k
+                s_p = p;
+                piv[k] = p;
+            }
         }
         __syncthreads();
         const int p = s_p;
@@ -364,20 +484,21 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
                 m[p * n + j] = t;
             }
         __syncthreads();
-        if (tid == 0) s_pivot = m[k * n + k];
-        __syncthreads();
-        const double pivot = s_pivot;
+        const double pivot = m[k * n + k];
         if (pivot == 0.0) {
             if (tid == 0) *status = k;
             break;
         }
-        for (int i = k + 1 + tid; i < n; i += blockDim.x) m[i * n + k] = __ddiv_rn(m[i * n + k], pivot);
+        for (int i = k + 1 + tid; i < n; i += blockDim.x) {
+            const double l = __ddiv_rn(m[i * n + k], pivot);
+            s_l[i] = l;
+            m[i * n + k] = l;
+        }
         __syncthreads();
-        const int rows = n - k - 1;
-        const int tot = rows * rows;
-        for (int t = tid; t < tot; t += blockDim.x) {
-            const int i = k + 1 + t / rows, j = k + 1 + t % rows;
-            m[i * n + j] = dsub(m[i * n + j], dmul(m[i * n + k], m[k * n + j]));
+        const int ty = tid >> 5, tx = tid & 31;
+        for (int i = k + 1 + ty; i < n; i += 32) {
+            const double l = s_l[i];
+            for (int j = k + 1 + tx; j < n; j += 32) m[i * n + j] = dsub(m[i * n + j], dmul(l, m[k * n + j]));
         }
         __syncthreads();
     }
@@ -386,30 +507,38 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
         for (int t = tid; t < nn; t += blockDim.x) gm[t] = m[t];
 }
 
-constexpr int LS_THREADS = 256;
+constexpr int LS_THREADS = 32;
 
-// x = LU \\ b replaying dense_lu.cpp:52-73 bit for bit.  The factor is staged
-// in shared memory; the forward sweep is column-oriented over one warp (each
-// row still subtracts in ascending j), the backward sweep is the reference's
-// row-oriented chain (row i needs x[i+1] first), run by one thread with its
-// operand loads issued ahead of the dependent subtractions.
+// x = LU \ b replaying dense_lu.cpp:52-73 bit for bit.  The factor is staged
+// into shared memory with one TMA bulk copy; the forward sweep is
+// column-oriented over one warp (each row still subtracts in ascending j);
+// the backward sweep keeps the reference's row-oriented order (row i needs
+// x[i+1] first): lanes form the products m[i][j]*x[j] in parallel, lane 0
+// runs the dependent subtraction chain over them.
 __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __restrict__ m,
                                                          const int64_t* __restrict__ piv,
                                                          const double* b, double* x, int use_smem, Gate g) {
     if (gated_off(g)) return;
-    extern __shared__ double sm[];
-    double* xs = sm;
-    const double* M = m;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bar;
+    double* xs = sm;          // n
+    double* ps = sm + n;      // n products
+    double* ms = sm + 2 * n;  // n*n factor (when staged)
     const int tid = threadIdx.x;
-    for (int i = tid; i < n; i += blockDim.x) xs[i] = b[i];
+    if (tid >= 32) return;
+    const double* M = m;
     if (use_smem) {
-        double* ms = sm + n;
-        const int nn = n * n;
-        for (int t = tid; t < nn; t += blockDim.x) ms[t] = m[t];
+        if (tid == 0) {
+            mbar_init(&bar, 1);
+            mbar_fence_init();
+            const uint32_t bytes = static_cast<uint32_t>(((n * n + 1) & ~1) * 8);
+            mbar_expect_tx(&bar, bytes);
+            tma_load_1d(ms, m, bytes, &bar);
+        }
         M = ms;
     }
-    __syncthreads();
-    if (tid >= 32) return;
+    for (int i = tid; i < n; i += 32) xs[i] = b[i];
+    __syncwarp();
     if (tid == 0)
         for (int k = 0; k < n; ++k) {
             const int p = static_cast<int>(piv[k]);
@@ -419,29 +548,32 @@ __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __
                 xs[p] = t;
             }
         }
+    if (use_smem) mbar_wait(&bar, 0);
     __syncwarp();
     for (int j = 0; j < n - 1; ++j) {
         const double xj = xs[j];
         for (int i = j + 1 + tid; i < n; i += 32) xs[i] = dsub(xs[i], dmul(M[i * n + j], xj));
         __syncwarp();
     }
-    if (tid == 0)
-        for (int i = n - 1; i >= 0; --i) {
-            const double* mi = M + static_cast<int64_t>(i) * n;
+    for (int i = n - 1; i >= 0; --i) {
+        const double* mi = M + static_cast<int64_t>(i) * n;
+        for (int j = i + 1 + tid; j < n; j += 32) ps[j] = dmul(mi[j], xs[j]);
+        __syncwarp();
+        if (tid == 0) {
             double s = xs[i];
             int j = i + 1;
-            for (; j + 4 <= n; j += 4) {
-                const double p0 = dmul(mi[j], xs[j]), p1 = dmul(mi[j + 1], xs[j + 1]);
-                const double p2 = dmul(mi[j + 2], xs[j + 2]), p3 = dmul(mi[j + 3], xs[j + 3]);
-                s = dsub(s, p0);
-                s = dsub(s, p1);
-                s = dsub(s, p2);
-                s = dsub(s, p3);
+            for (; j + 8 <= n; j += 8) {
+                double q[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) q[t] = ps[j + t];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) s = dsub(s, q[t]);
             }
-            for (; j < n; ++j) s = dsub(s, dmul(mi[j], xs[j]));
+            for (; j < n; ++j) s = dsub(s, ps[j]);
             xs[i] = __ddiv_rn(s, mi[i]);
         }
-    __syncwarp();
+        __syncwarp();
+    }
     for (int i = tid; i < n; i += 32) x[i] = xs[i];
 }
 
@@ -496,7 +628,7 @@ __global__ void k_compare_i32(const int* a, const int* b, int64_t n, int* diff) 
 
 }  // namespace
 
-int dot_grid(const Ctx& c) { return c.num_sms * 4; }
+int dot_grid(const Ctx& c) { return c.num_sms * 8; }
 
 // ---- launchers -----------------------------------------------------------------
 void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g) {
@@ -571,18 +703,19 @@ void lu_densify(Ctx& c, const CsrView& A, double* dense) {
 
 void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
     if (n == 0) return;
+    if (n > 2048) invalid("coarse_factorize: coarse system larger than 2048 unknowns is not supported on device");
     const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
-    int use_smem = sm <= 200 * 1024 ? 1 : 0;
-    if (use_smem) CK(cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int use_smem = sm <= 180 * 1024 ? 1 : 0;
+    if (use_smem) CK(cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
     LAUNCH(c, "coarse", 0.0, k_lu_factor, 1, LU_THREADS, use_smem ? sm : 0, static_cast<int>(n), m, piv, status,
            use_smem);
 }
 
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g) {
     if (n == 0) return;
-    const size_t full = sizeof(double) * static_cast<size_t>(n * n + n);
+    const size_t full = sizeof(double) * static_cast<size_t>(n * n + 2 * n + 2);
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
-    const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(n);
+    const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(2 * n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }

@@ -25,7 +25,7 @@ def main():
     nnz = int(L.amgr_problem_nnz(g))
     rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
     ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
-    vals = [torch.empty(nnz, dtype=torch.float64, device="cuda") for _ in range(steps + 1)]
+    vals = [torch.empty(nnz + 8, dtype=torch.float64, device="cuda") for _ in range(steps + 1)]
     torch.cuda.synchronize()
     amg._check(L.amgr_problem_pattern(ctx.ptr, g, rp.data_ptr(), ci.data_ptr()), ctx.ptr)
     for k, v in enumerate(vals):
@@ -49,7 +49,7 @@ def main():
     for k in range(1, steps + 1):
         ctx.synchronize()
         t0 = time.perf_counter()
-        h.rebuild_values(vals[k].data_ptr())
+        h.rebuild_values(vals[k].data_ptr(), adopt=True)
         ctx.synchronize()
         t_rb = time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -61,7 +61,7 @@ def main():
     # per-family device time for one rebuild + solve
     for fam in fams:
         ctx.probe(fam)
-        h.rebuild_values(vals[1].data_ptr())
+        h.rebuild_values(vals[1].data_ptr(), adopt=True)
         u.zero_()
         torch.cuda.synchronize()
         _, st = amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()))
