@@ -109,6 +109,7 @@ std::shared_ptr<Pattern> make_pattern(Ctx& c, const amgr_csr& A) {
     v.rp = P->rp.get();
     v.col = P->col.get();
     find_diag(c, v, P->diag.get());
+    P->max_span = max_group_span(c, P->rp.get(), P->n);
     return P;
 }
 
@@ -224,6 +225,7 @@ void symbolic_pass(Hier& h) {
         B.pat = P;
         CsrView v = B.view();
         find_diag(c, v, P->diag.get());
+        P->max_span = max_group_span(c, P->rp.get(), P->n);
     }
 }
 
@@ -345,6 +347,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             rap_numeric(c, s.nnz_c, plan->cptr.get(), plan->contrib.get(), cur.val.get(), next.val.get(), Av.nnz);
             CsrView nv = next.view();
             find_diag(c, nv, P->diag.get());
+            P->max_span = max_group_span(c, P->rp.get(), P->n);
             cur.rap = plan;
         }
         clk.end(PH_GALERKIN);

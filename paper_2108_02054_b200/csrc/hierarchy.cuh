@@ -26,6 +26,7 @@ AmgP to_amgp(const amgr_amg_params* p);
 // Structure of one level's operator (immutable, shared between hierarchies).
 struct Pattern {
     int64_t n = 0, ncols = 0, nnz = 0;
+    int max_span = 0;
     DevArray<int> rp, col, diag;
 };
 // Frozen transfer operators of one level: P (agg) and R = P^T (mptr/midx).
@@ -55,6 +56,7 @@ struct Level {
         v.rp = pat->rp.get();
         v.col = pat->col.get();
         v.val = ext_val ? ext_val : val.get();
+        v.max_span = pat->max_span;
         return v;
     }
 };

@@ -18,6 +18,7 @@ struct CsrView {
     const int* rp = nullptr;
     const int* col = nullptr;
     const double* val = nullptr;
+    int max_span = 0;  // widest 16-byte-aligned nnz span of a 32-row group (row-pass chunk sizing)
 };
 
 // Deterministic multi-block dot products: per-block partials + last-block
@@ -92,6 +93,8 @@ void find_diag(Ctx& c, const CsrView& A, int* diag_pos);
 void i32_to_i64(Ctx& c, const int* src, int64_t* dst, int64_t n);
 void i64_to_i32(Ctx& c, const int64_t* src, int* dst, int64_t n, int* overflow);
 // compare two int32 arrays; *diff set to 1 if any element differs
+// widest aligned nnz span over 32-row groups
+int max_group_span(Ctx& c, const int* rp, int64_t n);
 void compare_i32(Ctx& c, const int* a, const int* b, int64_t n, int* diff);
 
 }  // namespace amgr

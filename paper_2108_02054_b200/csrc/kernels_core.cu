@@ -12,6 +12,9 @@
 //  * jacobi/spai0 rebuild, restriction, dense LU factor/solve.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "kernels.cuh"
 #include "reduce.cuh"
 
@@ -54,36 +57,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Each warp owns a contiguous row range; the nnz stream of that range
-// (values + int32 columns) is double-buffered into shared memory with TMA
-// 1-D bulk copies completing on per-stage mbarriers, so DRAM reads of the
-// matrix are always one chunk ahead of the consumer.  Threads own rows
-// (32 consecutive rows per group) and accumulate strictly in column order
-// (csr.cpp:79-84), gathering up to RP_BATCH operands at a time.  Row
-// pointers and the per-row epilogue operands are prefetched one group ahead.
-// The operand x_i of the row's own diagonal is captured during accumulation
-// (the V-cycle epilogues need it: u_i, or u_i + P u_c).
-template <class Op>
-__global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink, int rows_per_warp,
-                                                      int nnz_pad) {
+// Interleaved TMA pipeline.  Warp w of W processes the 32-row groups
+// w, w+W, w+2W, ... so all warps sweep the matrix as one narrow band (the
+// +-g^2 z-neighbour gathers stay L2-resident).  While group G is consumed,
+// the group G+W's contiguous nnz range (values + int32 columns) is already
+// in flight into the other shared-memory stage via two TMA 1-D bulk copies
+// completing on that stage's mbarrier, and the row pointers of G+2W and the
+// epilogue operands of G+W are in flight into registers.  Threads own rows
+// and accumulate strictly in column order (csr.cpp:79-84), gathering up to
+// RP_BATCH operands at a time; the row's own diagonal operand is captured
+// for the V-cycle epilogues.  Groups wider than CH entries (pathological
+// rows) are streamed synchronously from global memory instead.
+template <class Op, int CH>
+__global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
-    __shared__ __align__(128) double s_val[RP_WARPS][2][RP_CH];
-    __shared__ __align__(128) int s_col[RP_WARPS][2][RP_CH];
-    __shared__ __align__(8) uint64_t s_bar[RP_WARPS][2];
+    extern __shared__ __align__(128) unsigned char rp_smem[];
+    auto s_val = reinterpret_cast<double(*)[2][CH]>(rp_smem);
+    auto s_col = reinterpret_cast<int(*)[2][CH]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH);
+    auto s_bar = reinterpret_cast<uint64_t(*)[2]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH +
+                                                  sizeof(int) * RP_WARPS * 2 * CH);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = static_cast<int>(A.n);
+    const int ngroups = (n + 31) >> 5;
+    const int W = gridDim.x * RP_WARPS;
     double dots[ND];
 #pragma unroll
     for (int k = 0; k < ND; ++k) dots[k] = 0.0;
 
-    const int64_t gw = static_cast<int64_t>(blockIdx.x) * RP_WARPS + w;
-    const int R0 = static_cast<int>(gw * rows_per_warp < n ? gw * rows_per_warp : static_cast<int64_t>(n));
-    const int R1 = static_cast<int>(static_cast<int64_t>(R0) + rows_per_warp < n ? static_cast<int64_t>(R0) + rows_per_warp : static_cast<int64_t>(n));
-    if (R0 < R1) {
-        const int E0 = __ldg(A.rp + R0), E1 = __ldg(A.rp + R1);
-        const int cfirst = E0 / RP_CH;
-        const int clast = E1 > E0 ? (E1 - 1) / RP_CH : cfirst;
+    int G = blockIdx.x * RP_WARPS + w;
+    if (G < ngroups) {
         uint64_t* bar = s_bar[w];
         if (lane == 0) {
             mbar_init(&bar[0], 1);
@@ -91,86 +94,158 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             mbar_fence_init();
         }
         __syncwarp();
-        auto issue = [&](int c, int st) {
-            const int base = c * RP_CH;
-            const int cnt = min(RP_CH, nnz_pad - base);
-            const uint32_t bv = static_cast<uint32_t>(cnt) * 8u, bc = static_cast<uint32_t>(cnt) * 4u;
-            mbar_expect_tx(&bar[st], bv + bc);
-            tma_load_1d(&s_val[w][st][0], A.val + base, bv, &bar[st]);
-            tma_load_1d(&s_col[w][st][0], A.col + base, bc, &bar[st]);
-        };
-        const bool any = E1 > E0;
-        if (lane == 0 && any) {
-            issue(cfirst, 0);
-            if (cfirst + 1 <= clast) issue(cfirst + 1, 1);
-        }
-        int cur = cfirst, st = 0;
-        uint32_t phase = 0;  // bit s = parity to wait for on stage s
-        if (any) {
-            mbar_wait(&bar[0], 0);
-            phase ^= 1u;
-        }
-        auto advance = [&]() {
-            __syncwarp();
-            if (lane == 0 && cur + 2 <= clast) {
+        // returns true when the group's aligned span fits a stage and a TMA was issued
+        auto issue = [&](int gs, int ge, int st) -> bool {
+            const int a0 = gs & ~3, a1 = (ge + 3) & ~3;
+            const int cnt = a1 - a0;
+            if (cnt > CH) return false;
+            if (lane == 0 && cnt > 0) {
                 fence_proxy_async();
-                issue(cur + 2, st);
+                const uint32_t bv = static_cast<uint32_t>(cnt) * 8u, bc = static_cast<uint32_t>(cnt) * 4u;
+                mbar_expect_tx(&bar[st], bv + bc);
+                tma_load_1d(&s_val[w][st][0], A.val + a0, bv, &bar[st]);
+                tma_load_1d(&s_col[w][st][0], A.col + a0, bc, &bar[st]);
             }
-            ++cur;
-            st ^= 1;
-            mbar_wait(&bar[st], (phase >> st) & 1u);
-            phase ^= (1u << st);
+            return cnt > 0;
         };
-
-        int row = R0 + lane;
-        int rs = row < R1 ? __ldg(A.rp + row) : E1;
-        int re = row < R1 ? __ldg(A.rp + row + 1) : E1;
+        auto rows_of = [&](int grp, int& rs, int& re) {
+            const int row = grp * 32 + lane;
+            const int last = min(grp * 32 + 32, n);
+            rs = row < n ? __ldg(A.rp + row) : __ldg(A.rp + last);
+            re = row < n ? __ldg(A.rp + row + 1) : rs;
+        };
+        int rs, re;
+        rows_of(G, rs, re);
         typename Op::Row rw;
-        if (row < R1) rw = op.load(row);
-        for (int r0 = R0; r0 < R1; r0 += 32) {
-            // prefetch the next group's row pointers and epilogue operands
-            const int nrow = r0 + 32 + lane;
-            const bool nvalid = nrow < R1;
-            const int nrs = nvalid ? __ldg(A.rp + nrow) : E1;
-            const int nre = nvalid ? __ldg(A.rp + nrow + 1) : E1;
+        if (G * 32 + lane < n) rw = op.load(G * 32 + lane);
+        int st = 0;
+        uint32_t phase = 0;
+        bool tma_cur = issue(__shfl_sync(0xffffffffu, rs, 0), __shfl_sync(0xffffffffu, re, 31), 0);
+        int nrs = 0, nre = 0;
+        if (G + W < ngroups) rows_of(G + W, nrs, nre);
+        for (; G < ngroups; G += W) {
+            const int NG = G + W;
+            // 1. next group's matrix chunk -> other stage
+            bool tma_nxt = false;
+            if (NG < ngroups)
+                tma_nxt = issue(__shfl_sync(0xffffffffu, nrs, 0), __shfl_sync(0xffffffffu, nre, 31), st ^ 1);
+            // 2. row pointers two groups ahead, epilogue operands one group ahead
+            int nnrs = 0, nnre = 0;
+            if (NG + W < ngroups) rows_of(NG + W, nnrs, nnre);
             typename Op::Row nrw;
-            if (nvalid) nrw = op.load(nrow);
-
-            const bool valid = row < R1;
-            const int g0 = __shfl_sync(0xffffffffu, rs, 0);
-            const int ge = __shfl_sync(0xffffffffu, re, 31);
+            if (NG < ngroups && NG * 32 + lane < n) nrw = op.load(NG * 32 + lane);
+            // 3. consume group G
+            const int row = G * 32 + lane;
+            const int gs = __shfl_sync(0xffffffffu, rs, 0), ge = __shfl_sync(0xffffffffu, re, 31);
             double sum = 0.0, xdiag = 0.0;
-            if (ge > g0) {
-                while (g0 >= (cur + 1) * RP_CH && cur < clast) advance();
-                for (;;) {
-                    const int c0 = cur * RP_CH, c1 = c0 + RP_CH;
-                    int a = max(rs, c0);
-                    const int b = min(re, c1);
-                    while (a < b) {
-                        const int cnt = min(RP_BATCH, b - a);
-                        const int k = a - c0;
-                        double xv[RP_BATCH];
+            if (tma_cur) {
+                mbar_wait(&bar[st], (phase >> st) & 1u);
+                phase ^= (1u << st);
+                const int a0 = gs & ~3;
+                int a = rs;
+                const int b = re;
+                while (a < b) {
+                    const int cnt = min(RP_BATCH, b - a);
+                    const int k = a - a0;
+                    double xv[RP_BATCH];
 #pragma unroll
-                        for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
+                    for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
 #pragma unroll
-                        for (int t = 0; t < RP_BATCH; ++t)
-                            if (t < cnt) {
-                                sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
-                                if (s_col[w][st][k + t] == row) xdiag = xv[t];
-                            }
-                        a += cnt;
-                    }
-                    if (ge <= c1 || cur >= clast) break;
-                    advance();
+                    for (int t = 0; t < RP_BATCH; ++t)
+                        if (t < cnt) {
+                            sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
+                            if (s_col[w][st][k + t] == row) xdiag = xv[t];
+                        }
+                    a += cnt;
+                }
+            } else if (ge > gs) {
+                // wide group: synchronous row-major walk from global memory
+                int a = rs;
+                while (a < re) {
+                    const int cnt = min(RP_BATCH, re - a);
+                    double xv[RP_BATCH];
+#pragma unroll
+                    for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(__ldg(A.col + a + t)) : 0.0;
+#pragma unroll
+                    for (int t = 0; t < RP_BATCH; ++t)
+                        if (t < cnt) {
+                            sum = dadd(sum, dmul(__ldg(A.val + a + t), xv[t]));
+                            if (__ldg(A.col + a + t) == row) xdiag = xv[t];
+                        }
+                    a += cnt;
                 }
             }
-            if (valid) op.finish(row, sum, xdiag, rw, dots);
-            row = nrow;
+            if (row < n) op.finish(row, sum, xdiag, rw, dots);
+            __syncwarp();
+            st ^= 1;
+            tma_cur = tma_nxt;
             rs = nrs;
             re = nre;
+            nrs = nnrs;
+            nre = nnre;
             rw = nrw;
         }
-        __syncwarp();
+    }
+    if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
+}
+
+constexpr int RS_BLOCK = 256;  // simple variant: one 32-row group per warp, synchronous staging
+constexpr int RS_WARPS = RS_BLOCK / 32;
+constexpr int RS_CH = 256;
+constexpr int RS_MINB = 5;
+
+template <class Op>
+__global__ void __launch_bounds__(RS_BLOCK, RS_MINB) k_rowpass_simple(CsrView A, Op op, Gate g, DotSink sink) {
+    if (gated_off(g)) return;
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    __shared__ double s_val[RS_WARPS][RS_CH];
+    __shared__ int s_col[RS_WARPS][RS_CH];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = static_cast<int>(A.n);
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * RS_WARPS;
+    for (int64_t wid = static_cast<int64_t>(blockIdx.x) * RS_WARPS + w; wid * 32 < n; wid += wstride) {
+        const int r0 = static_cast<int>(wid * 32);
+        const int r1 = min(r0 + 32, n);
+        const int row = r0 + lane;
+        const bool valid = row < n;
+        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + r1);
+        const int rs = valid ? __ldg(A.rp + row) : e1;
+        const int re = valid ? __ldg(A.rp + row + 1) : e1;
+        double sum = 0.0, xdiag = 0.0;
+        typename Op::Row rw;
+        if (valid) rw = op.load(row);
+        for (int c0 = e0; c0 < e1; c0 += RS_CH) {
+            const int c1 = min(c0 + RS_CH, e1);
+#pragma unroll 4
+            for (int e = c0 + lane; e < c1; e += 32) {
+                s_val[w][e - c0] = __ldg(A.val + e);
+                s_col[w][e - c0] = __ldg(A.col + e);
+            }
+            __syncwarp();
+            int a = max(rs, c0);
+            const int b = min(re, c1);
+            // issue up to RP_BATCH independent operand gathers, then accumulate
+            // them strictly in column order
+            while (a < b) {
+                const int cnt = min(RP_BATCH, b - a);
+                const int k = a - c0;
+                double xv[RP_BATCH];
+#pragma unroll
+                for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][k + t]) : 0.0;
+#pragma unroll
+                for (int t = 0; t < RP_BATCH; ++t)
+                    if (t < cnt) {
+                        sum = dadd(sum, dmul(s_val[w][k + t], xv[t]));
+                        if (s_col[w][k + t] == row) xdiag = xv[t];
+                    }
+                a += cnt;
+            }
+            __syncwarp();
+        }
+        if (valid) op.finish(row, sum, xdiag, rw, dots);
     }
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
@@ -305,18 +380,50 @@ struct OpResidNorm {
 
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
+int rowpass_variant() {
+    static int v = [] {
+        const char* e = getenv("AMGR_ROWPASS");
+        return (e && std::string(e) == "simple") ? 1 : 0;
+    }();
+    return v;
+}
+
+template <class Op, int CH>
+void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
+                unsigned grid) {
+    constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * CH * 12 + RP_WARPS * 2 * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(k_rowpass<Op, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        configured = true;
+    }
+    LAUNCH(c, fam, bytes, (k_rowpass<Op, CH>), grid, RP_BLOCK, smem, A, op, g, s);
+}
+
 template <class Op>
 void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g,
-                    DotSink s, bool) {
+                    DotSink s, bool fixed_grid) {
     if (A.n == 0) return;
     const int64_t groups = (A.n + 31) / 32;
-    const int64_t max_warps = static_cast<int64_t>(persistent_grid(c)) * RP_WARPS;
-    const int64_t gpw = (groups + max_warps - 1) / max_warps;  // groups per warp
-    const int rows_per_warp = static_cast<int>(gpw * 32);
-    const int64_t warps = (A.n + rows_per_warp - 1) / rows_per_warp;
-    unsigned grid = static_cast<unsigned>((warps + RP_WARPS - 1) / RP_WARPS);
-    const int nnz_pad = static_cast<int>((A.nnz + 3) & ~int64_t{3});
-    LAUNCH(c, fam, bytes, k_rowpass<Op>, grid, RP_BLOCK, 0, A, op, g, s, rows_per_warp, nnz_pad);
+    if (rowpass_variant() == 1) {
+        unsigned grid = grid_for(groups, RS_WARPS);
+        if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
+        LAUNCH(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
+        return;
+    }
+    const int span = A.max_span;
+    int per_sm = span <= 256 ? 8 : (span <= 512 ? 4 : 2);
+    int64_t want = (groups + RP_WARPS - 1) / RP_WARPS;
+    int64_t cap = static_cast<int64_t>(c.num_sms) * per_sm;
+    unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+    if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order per level
+    if (span <= 256)
+        launch_tma<Op, 256>(c, fam, bytes, A, op, g, s, grid);
+    else if (span <= 512)
+        launch_tma<Op, 512>(c, fam, bytes, A, op, g, s, grid);
+    else
+        launch_tma<Op, 1024>(c, fam, bytes, A, op, g, s, grid);
 }
 
 double spmv_bytes(const CsrView& A) {
@@ -620,6 +727,17 @@ __global__ void k_i64_to_i32(const int64_t* s, int* d, int64_t n, int* ovf) {
         d[i] = static_cast<int>(v);
     }
 }
+__global__ void k_max_span(const int* rp, int64_t n, int* out) {
+    const int64_t groups = (n + 31) / 32;
+    int m = 0;
+    for (int64_t gi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; gi < groups;
+         gi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t last = gi * 32 + 32 < n ? gi * 32 + 32 : n;
+        const int span = ((rp[last] + 3) & ~3) - (rp[gi * 32] & ~3);
+        m = max(m, span);
+    }
+    atomicMax(out, m);
+}
 __global__ void k_compare_i32(const int* a, const int* b, int64_t n, int* diff) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -739,6 +857,13 @@ void i32_to_i64(Ctx& c, const int* s, int64_t* d, int64_t n) {
 void i64_to_i32(Ctx& c, const int64_t* s, int* d, int64_t n, int* ovf) {
     if (n == 0) return;
     LAUNCH(c, "io", 0.0, k_i64_to_i32, grid_for(n, 256, c.num_sms * 16), 256, 0, s, d, n, ovf);
+}
+int max_group_span(Ctx& c, const int* rp, int64_t n) {
+    if (n == 0) return 0;
+    DevArray<int> m(1, c.stream);
+    CK(cudaMemsetAsync(m.get(), 0, sizeof(int), c.stream));
+    LAUNCH(c, "setup", 0.0, k_max_span, grid_for((n + 31) / 32, 256, c.num_sms * 8), 256, 0, rp, n, m.get());
+    return d2h_scalar(m.get(), c.stream);
 }
 void compare_i32(Ctx& c, const int* a, const int* b, int64_t n, int* diff) {
     if (n == 0) return;
