@@ -2,6 +2,8 @@
 // reference function whose semantics (order of phases, error texts, timing
 // buckets) it reproduces.
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <sstream>
 
@@ -438,6 +440,14 @@ void rebuild_values(Hier& h, const double* values, int location) {
     h.tm = clk.collect();
 }
 
+static bool upleg_split() {
+    static int v = [] {
+        const char* e = getenv("AMGR_UPLEG");
+        return (e && std::string(e) == "fused") ? 0 : 1;
+    }();
+    return v != 0;
+}
+
 // ---- V-cycle (hierarchy.cpp:152-186, smoothing as specified) --------
 void vcycle(Hier& h, const double* f, double* u, Gate g) {
     Ctx& c = *h.ctx;
@@ -494,6 +504,17 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
             double* t = target(1);
             vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], t, g);
             ufinal[i] = t;
+        } else if (upleg_split()) {
+            // x = u + P u_c materialised by a coalesced pass (into b), then the
+            // post-smoothing sweeps; the sweep's operand gather is one level deep
+            vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
+            double* src = b;
+            for (int k = 1; k <= post; ++k) {
+                double* dst = (i == 0 && k == post) ? u : (src == b ? a : b);
+                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+                src = dst;
+            }
+            ufinal[i] = src;
         } else {
             double* t = target(1);
             vc_up(c, A, fin[i], Li.w.get(), om, a, Li.T->agg.get(), ufinal[i + 1], t, g);
