@@ -57,17 +57,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Interleaved TMA pipeline.  Warp w of W processes the 32-row groups
+// Interleaved TMA chunk stream.  Warp w of W processes the 32-row groups
 // w, w+W, w+2W, ... so all warps sweep the matrix as one narrow band (the
-// +-g^2 z-neighbour gathers stay L2-resident).  While group G is consumed,
-// the group G+W's contiguous nnz range (values + int32 columns) is already
-// in flight into the other shared-memory stage via two TMA 1-D bulk copies
-// completing on that stage's mbarrier, and the row pointers of G+2W and the
-// epilogue operands of G+W are in flight into registers.  Threads own rows
-// and accumulate strictly in column order (csr.cpp:79-84), gathering up to
-// RP_BATCH operands at a time; the row's own diagonal operand is captured
-// for the V-cycle epilogues.  Groups wider than CH entries (pathological
-// rows) are streamed synchronously from global memory instead.
+// +-g^2 z-neighbour gathers stay L2-resident).  A group's 16-byte-aligned nnz
+// range (values + int32 columns) is cut into CH-entry chunks; the chunk
+// sequence of the warp is double-buffered in shared memory by TMA 1-D bulk
+// copies completing on per-stage mbarriers, always one chunk ahead of the
+// consumer (the next chunk of the same group, or the first chunk of the next
+// group).  Row pointers and epilogue operands of the next group are prefetched
+// into registers.  Threads own rows and accumulate strictly in column order
+// (csr.cpp:79-84), gathering up to RP_BATCH operands at a time; the row's own
+// diagonal operand is captured for the V-cycle epilogues.
 template <class Op, int CH>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     if (gated_off(g)) return;
@@ -94,19 +94,15 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             mbar_fence_init();
         }
         __syncwarp();
-        // returns true when the group's aligned span fits a stage and a TMA was issued
-        auto issue = [&](int gs, int ge, int st) -> bool {
-            const int a0 = gs & ~3, a1 = (ge + 3) & ~3;
-            const int cnt = a1 - a0;
-            if (cnt > CH) return false;
-            if (lane == 0 && cnt > 0) {
+        auto issue = [&](int base, int end, int st) {  // [base, min(base+CH, end)), base/end 4-aligned
+            const int cnt = min(CH, end - base);
+            if (lane == 0) {
                 fence_proxy_async();
                 const uint32_t bv = static_cast<uint32_t>(cnt) * 8u, bc = static_cast<uint32_t>(cnt) * 4u;
                 mbar_expect_tx(&bar[st], bv + bc);
-                tma_load_1d(&s_val[w][st][0], A.val + a0, bv, &bar[st]);
-                tma_load_1d(&s_col[w][st][0], A.col + a0, bc, &bar[st]);
+                tma_load_1d(&s_val[w][st][0], A.val + base, bv, &bar[st]);
+                tma_load_1d(&s_col[w][st][0], A.col + base, bc, &bar[st]);
             }
-            return cnt > 0;
         };
         auto rows_of = [&](int grp, int& rs, int& re) {
             const int row = grp * 32 + lane;
@@ -114,39 +110,53 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             rs = row < n ? __ldg(A.rp + row) : __ldg(A.rp + last);
             re = row < n ? __ldg(A.rp + row + 1) : rs;
         };
-        int rs, re;
+        int rs, re, nrs = 0, nre = 0;
         rows_of(G, rs, re);
-        typename Op::Row rw;
+        typename Op::Row rw, nrw;
         if (G * 32 + lane < n) rw = op.load(G * 32 + lane);
+        int NG = G + W;
+        if (NG < ngroups) {
+            rows_of(NG, nrs, nre);
+            if (NG * 32 + lane < n) nrw = op.load(NG * 32 + lane);
+        }
+        // group range (aligned) of the current group
+        int gs = __shfl_sync(0xffffffffu, rs, 0), ge = __shfl_sync(0xffffffffu, re, 31);
+        int ab = gs & ~3, ae = (ge + 3) & ~3;
         int st = 0;
         uint32_t phase = 0;
-        bool tma_cur = issue(__shfl_sync(0xffffffffu, rs, 0), __shfl_sync(0xffffffffu, re, 31), 0);
-        int nrs = 0, nre = 0;
-        if (G + W < ngroups) rows_of(G + W, nrs, nre);
-        for (; G < ngroups; G += W) {
-            const int NG = G + W;
-            // 1. next group's matrix chunk -> other stage
-            bool tma_nxt = false;
-            if (NG < ngroups)
-                tma_nxt = issue(__shfl_sync(0xffffffffu, nrs, 0), __shfl_sync(0xffffffffu, nre, 31), st ^ 1);
-            // 2. row pointers two groups ahead, epilogue operands one group ahead
-            int nnrs = 0, nnre = 0;
-            if (NG + W < ngroups) rows_of(NG + W, nnrs, nnre);
-            typename Op::Row nrw;
-            if (NG < ngroups && NG * 32 + lane < n) nrw = op.load(NG * 32 + lane);
-            // 3. consume group G
+        int cb = ab;                     // base of the chunk to consume next
+        bool ready = false;              // chunk cb is in flight in stage st
+        if (ae > ab) {
+            issue(cb, ae, st);
+            ready = true;
+        }
+        double sum = 0.0, xdiag = 0.0;
+        while (G < ngroups) {
             const int row = G * 32 + lane;
-            const int gs = __shfl_sync(0xffffffffu, rs, 0), ge = __shfl_sync(0xffffffffu, re, 31);
-            double sum = 0.0, xdiag = 0.0;
-            if (tma_cur) {
+            // ---- consume chunk cb (if the group has entries) ----
+            bool group_done;
+            if (ae > ab) {
+                if (!ready) issue(cb, ae, st);
+                // prefetch the following chunk into the other stage
+                int pb = -1, pe = 0;
+                if (cb + CH < ae) {
+                    pb = cb + CH;
+                    pe = ae;
+                } else if (NG < ngroups) {
+                    const int ngs = __shfl_sync(0xffffffffu, nrs, 0), nge = __shfl_sync(0xffffffffu, nre, 31);
+                    if (nge > ngs) {
+                        pb = ngs & ~3;
+                        pe = (nge + 3) & ~3;
+                    }
+                }
+                if (pb >= 0) issue(pb, pe, st ^ 1);
                 mbar_wait(&bar[st], (phase >> st) & 1u);
                 phase ^= (1u << st);
-                const int a0 = gs & ~3;
-                int a = rs;
-                const int b = re;
+                int a = max(rs, cb);
+                const int b = min(re, cb + CH);
                 while (a < b) {
                     const int cnt = min(RP_BATCH, b - a);
-                    const int k = a - a0;
+                    const int k = a - cb;
                     double xv[RP_BATCH];
 #pragma unroll
                     for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
@@ -158,32 +168,37 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                         }
                     a += cnt;
                 }
-            } else if (ge > gs) {
-                // wide group: synchronous row-major walk from global memory
-                int a = rs;
-                while (a < re) {
-                    const int cnt = min(RP_BATCH, re - a);
-                    double xv[RP_BATCH];
-#pragma unroll
-                    for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(__ldg(A.col + a + t)) : 0.0;
-#pragma unroll
-                    for (int t = 0; t < RP_BATCH; ++t)
-                        if (t < cnt) {
-                            sum = dadd(sum, dmul(__ldg(A.val + a + t), xv[t]));
-                            if (__ldg(A.col + a + t) == row) xdiag = xv[t];
-                        }
-                    a += cnt;
-                }
+                __syncwarp();
+                group_done = cb + CH >= ae;
+                st ^= 1;
+                ready = pb >= 0;
+                cb = pb;
+            } else {
+                group_done = true;
             }
+            if (!group_done) continue;
+            // ---- epilogue of group G and rotation to G+W ----
             if (row < n) op.finish(row, sum, xdiag, rw, dots);
-            __syncwarp();
-            st ^= 1;
-            tma_cur = tma_nxt;
+            sum = 0.0;
+            xdiag = 0.0;
+            G = NG;
             rs = nrs;
             re = nre;
-            nrs = nnrs;
-            nre = nnre;
             rw = nrw;
+            if (G >= ngroups) break;
+            gs = __shfl_sync(0xffffffffu, rs, 0);
+            ge = __shfl_sync(0xffffffffu, re, 31);
+            ab = gs & ~3;
+            ae = (ge + 3) & ~3;
+            if (!ready || cb != ab) {  // first chunk of the new group not prefetched
+                cb = ab;
+                ready = false;
+            }
+            NG = G + W;
+            if (NG < ngroups) {
+                rows_of(NG, nrs, nre);
+                if (NG * 32 + lane < n) nrw = op.load(NG * 32 + lane);
+            }
         }
     }
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
@@ -412,18 +427,11 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
         LAUNCH(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
         return;
     }
-    const int span = A.max_span;
-    int per_sm = span <= 256 ? 8 : (span <= 512 ? 4 : 2);
     int64_t want = (groups + RP_WARPS - 1) / RP_WARPS;
-    int64_t cap = static_cast<int64_t>(c.num_sms) * per_sm;
+    int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-    if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order per level
-    if (span <= 256)
-        launch_tma<Op, 256>(c, fam, bytes, A, op, g, s, grid);
-    else if (span <= 512)
-        launch_tma<Op, 512>(c, fam, bytes, A, op, g, s, grid);
-    else
-        launch_tma<Op, 1024>(c, fam, bytes, A, op, g, s, grid);
+    if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
+    launch_tma<Op, RP_CH>(c, fam, bytes, A, op, g, s, grid);
 }
 
 double spmv_bytes(const CsrView& A) {
@@ -614,25 +622,30 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
         for (int t = tid; t < nn; t += blockDim.x) gm[t] = m[t];
 }
 
-constexpr int LS_THREADS = 32;
+constexpr int LS_THREADS = 64;
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // x = LU \ b replaying dense_lu.cpp:52-73 bit for bit.  The factor is staged
-// into shared memory with one TMA bulk copy; the forward sweep is
-// column-oriented over one warp (each row still subtracts in ascending j);
-// the backward sweep keeps the reference's row-oriented order (row i needs
-// x[i+1] first): lanes form the products m[i][j]*x[j] in parallel, lane 0
-// runs the dependent subtraction chain over them.
+// into shared memory with one TMA bulk copy.  Forward sweep: column-oriented
+// over warp 0 (each row still subtracts in ascending j).  Backward sweep: the
+// reference's row-oriented chain (row i needs x[i+1] as its FIRST term, so the
+// rows cannot overlap): warp 1 forms the products m[i-1][j]*x[j], j > i, of the
+// next row while lane 0 of warp 0 runs row i's dependent subtraction chain;
+// one named barrier per row.
 __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __restrict__ m,
                                                          const int64_t* __restrict__ piv,
                                                          const double* b, double* x, int use_smem, Gate g) {
     if (gated_off(g)) return;
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bar;
-    double* xs = sm;          // n
-    double* ps = sm + n;      // n products
-    double* ms = sm + 2 * n;  // n*n factor (when staged)
-    const int tid = threadIdx.x;
-    if (tid >= 32) return;
+    const int nn2 = use_smem ? ((n * n + 1) & ~1) : 0;
+    double* ms = sm;              // n*n factor (when staged; 16-byte aligned TMA target)
+    double* xs = sm + nn2;        // n
+    double* ps = sm + nn2 + n;    // 2 x n products (double buffer)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const double* M = m;
     if (use_smem) {
         if (tid == 0) {
@@ -644,44 +657,57 @@ __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __
         }
         M = ms;
     }
-    for (int i = tid; i < n; i += 32) xs[i] = b[i];
-    __syncwarp();
-    if (tid == 0)
-        for (int k = 0; k < n; ++k) {
-            const int p = static_cast<int>(piv[k]);
-            if (p != k) {
-                const double t = xs[k];
-                xs[k] = xs[p];
-                xs[p] = t;
+    for (int i = tid; i < n; i += LS_THREADS) xs[i] = b[i];
+    __syncthreads();
+    if (wid == 0) {
+        if (lane == 0)
+            for (int k = 0; k < n; ++k) {
+                const int p = static_cast<int>(piv[k]);
+                if (p != k) {
+                    const double t = xs[k];
+                    xs[k] = xs[p];
+                    xs[p] = t;
+                }
             }
-        }
-    if (use_smem) mbar_wait(&bar, 0);
-    __syncwarp();
-    for (int j = 0; j < n - 1; ++j) {
-        const double xj = xs[j];
-        for (int i = j + 1 + tid; i < n; i += 32) xs[i] = dsub(xs[i], dmul(M[i * n + j], xj));
+        if (use_smem) mbar_wait(&bar, 0);
         __syncwarp();
+        for (int j = 0; j < n - 1; ++j) {
+            const double xj = xs[j];
+            for (int i = j + 1 + lane; i < n; i += 32) xs[i] = dsub(xs[i], dmul(M[i * n + j], xj));
+            __syncwarp();
+        }
+    } else if (use_smem) {
+        mbar_wait(&bar, 0);
     }
+    __syncthreads();
+    // backward
     for (int i = n - 1; i >= 0; --i) {
-        const double* mi = M + static_cast<int64_t>(i) * n;
-        for (int j = i + 1 + tid; j < n; j += 32) ps[j] = dmul(mi[j], xs[j]);
-        __syncwarp();
-        if (tid == 0) {
-            double s = xs[i];
-            int j = i + 1;
-            for (; j + 8 <= n; j += 8) {
-                double q[8];
+        if (wid == 0) {
+            if (lane == 0) {
+                const double* mi = M + static_cast<int64_t>(i) * n;
+                const double* pr = ps + (i & 1) * n;
+                double s = xs[i];
+                if (i + 1 < n) s = dsub(s, dmul(mi[i + 1], xs[i + 1]));
+                int j = i + 2;
+                for (; j + 8 <= n; j += 8) {
+                    double q[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) q[t] = ps[j + t];
+                    for (int t = 0; t < 8; ++t) q[t] = pr[j + t];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) s = dsub(s, q[t]);
+                    for (int t = 0; t < 8; ++t) s = dsub(s, q[t]);
+                }
+                for (; j < n; ++j) s = dsub(s, pr[j]);
+                xs[i] = __ddiv_rn(s, mi[i]);
             }
-            for (; j < n; ++j) s = dsub(s, ps[j]);
-            xs[i] = __ddiv_rn(s, mi[i]);
+        } else if (i > 0) {
+            // products of row i-1 for j > i (x_j final)
+            const double* mi = M + static_cast<int64_t>(i - 1) * n;
+            double* pw = ps + ((i - 1) & 1) * n;
+            for (int j = i + 1 + lane; j < n; j += 32) pw[j] = dmul(mi[j], xs[j]);
         }
-        __syncwarp();
+        named_bar(1, LS_THREADS);
     }
-    for (int i = tid; i < n; i += 32) x[i] = xs[i];
+    for (int i = tid; i < n; i += LS_THREADS) x[i] = xs[i];
 }
 
 // ---- misc ---------------------------------------------------------------------
@@ -831,9 +857,9 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
 
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g) {
     if (n == 0) return;
-    const size_t full = sizeof(double) * static_cast<size_t>(n * n + 2 * n + 2);
+    const size_t full = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + 3 * n);
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
-    const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(2 * n);
+    const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }
