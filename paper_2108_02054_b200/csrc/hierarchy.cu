@@ -440,15 +440,10 @@ void rebuild_values(Hier& h, const double* values, int location) {
     h.tm = clk.collect();
 }
 
-static bool upleg_split() {
-    static int v = [] {
-        const char* e = getenv("AMGR_UPLEG");
-        return (e && std::string(e) == "fused") ? 0 : 1;
-    }();
-    return v != 0;
-}
-
 // ---- V-cycle (hierarchy.cpp:152-186, smoothing as specified) --------
+// Down leg per level: [premul on level 0] -> vc_down (r = f - A u0) ->
+// restriction (also writing the next level's u0).  Up leg per level:
+// prolongation x = u + P u_c (coalesced pass) -> post-smoothing sweeps.
 void vcycle(Hier& h, const double* f, double* u, Gate g) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
@@ -462,29 +457,36 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     fin[0] = f;
     for (size_t i = 1; i < L; ++i) fin[i] = W.f[i].get();
     std::vector<double*> cur(L);
+    const int pre = h.prm.pre, post = h.prm.post;
+    if (pre >= 1) vc_premul(c, h.lv[0].pat->n, f, h.lv[0].w.get(), om, W.u[0].get(), g);
     // down leg
     for (size_t i = 0; i + 1 < L; ++i) {
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
-        double* a = W.u[i].get();
+        double* a = W.u[i].get();  // holds u0 (premul / previous restriction) when pre >= 1
         double* b = W.t[i].get();
         double* r = W.r[i].get();
-        if (h.prm.pre <= 0) {
+        if (pre <= 0) {
             fill(c, a, A.n, 0.0, g);
             copy(c, r, fin[i], A.n, g);
             cur[i] = a;
         } else {
-            vc_down(c, A, fin[i], Li.w.get(), om, a, r, g);
             double* src = a;
-            double* dst = b;
-            for (int s = 1; s < h.prm.pre; ++s) {
-                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
-                std::swap(src, dst);
+            if (pre == 1) {
+                vc_down(c, A, fin[i], a, r, g);
+            } else {
+                double* dst = b;
+                for (int s = 1; s < pre; ++s) {
+                    vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+                    std::swap(src, dst);
+                }
+                residual(c, A, fin[i], src, r, g);
             }
-            if (h.prm.pre > 1) residual(c, A, fin[i], src, r, g);
             cur[i] = src;
         }
-        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, W.f[i + 1].get(), g);
+        const bool next_smoothed = pre >= 1 && i + 2 < L;
+        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, W.f[i + 1].get(),
+                     next_smoothed ? h.lv[i + 1].w.get() : nullptr, om, next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
     // coarsest: direct solve (hierarchy.cpp:175)
     lu_solve(c, h.nL, h.lu.get(), h.piv.get(), W.f[L - 1].get(), W.u[L - 1].get(), g);
@@ -495,37 +497,21 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
         const CsrView A = Li.view();
         double* a = cur[i];
         double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
-        const int post = h.prm.post;
-        auto target = [&](int k) -> double* {  // output of write k (1-based)
-            if (i == 0 && k == std::max(post, 1)) return u;
-            return (k % 2 == 1) ? b : a;
-        };
         if (post <= 0) {
-            double* t = target(1);
+            double* t = (i == 0) ? u : b;
             vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], t, g);
             ufinal[i] = t;
-        } else if (upleg_split()) {
-            // x = u + P u_c materialised by a coalesced pass (into b), then the
-            // post-smoothing sweeps; the sweep's operand gather is one level deep
-            vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
-            double* src = b;
-            for (int k = 1; k <= post; ++k) {
-                double* dst = (i == 0 && k == post) ? u : (src == b ? a : b);
-                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
-                src = dst;
-            }
-            ufinal[i] = src;
-        } else {
-            double* t = target(1);
-            vc_up(c, A, fin[i], Li.w.get(), om, a, Li.T->agg.get(), ufinal[i + 1], t, g);
-            double* src = t;
-            for (int k = 2; k <= post; ++k) {
-                double* dst = target(k);
-                vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
-                src = dst;
-            }
-            ufinal[i] = src;
+            continue;
         }
+        // x = u + P u_c into b, then the post-smoothing sweeps
+        vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
+        double* src = b;
+        for (int k = 1; k <= post; ++k) {
+            double* dst = (i == 0 && k == post) ? u : (src == b ? a : b);
+            vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+            src = dst;
+        }
+        ufinal[i] = src;
     }
 }
 

@@ -36,23 +36,21 @@ int dot_grid(const Ctx& c);
 void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g = {});
 // r = f - A x
 void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, Gate g = {});
-// V-cycle down leg, first pre-smoothing sweep from a zero guess fused with the
-// residual: u = 0 + (om*w) f ; r = f - A u        (hierarchy.cpp:165-170)
-void vc_down(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* u,
-             double* r, Gate g = {});
-// one more smoothing sweep: out = u + (om*w)(f - A u)     (smoother.cpp:42-47)
+// V-cycle down leg (hierarchy.cpp:165-172).  The first pre-smoothing sweep
+// from a zero guess is u0 = 0 + (om*w) f: written by vc_premul on level 0 and
+// by restrict_sum for coarser levels; vc_down then forms r = f - A u0.
+void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, double* u0, Gate g = {});
+void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g = {});
+// one smoothing sweep: out = u + (om*w)(f - A u)     (smoother.cpp:42-47)
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
                const double* u, double* out, Gate g = {});
-// V-cycle up leg: x = u + (0 + uc[agg]) fused with the first post-smoothing
-// sweep: out = x + (om*w)(f - A x)                  (hierarchy.cpp:179-183)
-void vc_up(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
-           const double* u, const int* agg, const double* uc, double* out, Gate g = {});
-// prolongation only (post_sweeps == 0): out = u + (0 + uc[agg])
+// prolongation (hierarchy.cpp:179-182): out = u + (0 + uc[agg])
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
                 Gate g = {});
-// restriction fc[I] = sum over members ascending of r[m]   (R spmv, csr.cpp:79-84)
+// restriction fc[I] = sum over members ascending of r[m] (R spmv, csr.cpp:79-84);
+// if u0c != nullptr also u0c = 0 + (om*wc) fc for the coarse level's pre-smoothing
 void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const double* r, double* fc,
-                  Gate g = {});
+                  const double* wc, double om, double* u0c, Gate g = {});
 
 // Krylov-fused SpMVs (dots land in sink.out):
 // y = A x ; out[0] = a . y

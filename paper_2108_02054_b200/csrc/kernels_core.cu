@@ -66,8 +66,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // consumer (the next chunk of the same group, or the first chunk of the next
 // group).  Row pointers and epilogue operands of the next group are prefetched
 // into registers.  Threads own rows and accumulate strictly in column order
-// (csr.cpp:79-84), gathering up to RP_BATCH operands at a time; the row's own
-// diagonal operand is captured for the V-cycle epilogues.
+// (csr.cpp:79-84): per chunk, lanes first form the products a_e * x_col(e)
+// entry-parallel (all gathers of a lane in flight at once, written in place
+// over the staged values), then each lane sums its row's products in column
+// order from shared memory.
 template <class Op, int CH>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     if (gated_off(g)) return;
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             issue(cb, ae, st);
             ready = true;
         }
-        double sum = 0.0, xdiag = 0.0;
+        double sum = 0.0;
         while (G < ngroups) {
             const int row = G * 32 + lane;
             // ---- consume chunk cb (if the group has entries) ----
@@ -152,21 +154,40 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                 if (pb >= 0) issue(pb, pe, st ^ 1);
                 mbar_wait(&bar[st], (phase >> st) & 1u);
                 phase ^= (1u << st);
-                int a = max(rs, cb);
-                const int b = min(re, cb + CH);
-                while (a < b) {
-                    const int cnt = min(RP_BATCH, b - a);
-                    const int k = a - cb;
-                    double xv[RP_BATCH];
+                // phase 1 (entry-parallel): p_e = a_e * x_col(e), in place over the
+                // staged values; every lane issues its CH/32 gathers at once
+                {
+                    constexpr int PER = CH / 32;
+                    const int lo = max(gs, cb) - cb, hi = min(ge, cb + CH) - cb;
+                    int cidx[PER];
+                    double xv[PER];
 #pragma unroll
-                    for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
+                    for (int t = 0; t < PER; ++t) {
+                        const int k = lane + 32 * t;
+                        cidx[t] = (k >= lo && k < hi) ? s_col[w][st][k] : -1;
+                    }
 #pragma unroll
-                    for (int t = 0; t < RP_BATCH; ++t)
-                        if (t < cnt) {
-                            sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
-                            if (s_col[w][st][k + t] == row) xdiag = xv[t];
-                        }
-                    a += cnt;
+                    for (int t = 0; t < PER; ++t) xv[t] = cidx[t] >= 0 ? op.x(cidx[t]) : 0.0;
+#pragma unroll
+                    for (int t = 0; t < PER; ++t) {
+                        const int k = lane + 32 * t;
+                        if (cidx[t] >= 0) s_val[w][st][k] = dmul(s_val[w][st][k], xv[t]);
+                    }
+                }
+                __syncwarp();
+                // phase 2 (row-parallel): sequential sum in column order
+                {
+                    int a = max(rs, cb) - cb;
+                    const int b = min(re, cb + CH) - cb;
+                    const double* pv = s_val[w][st];
+                    for (; a + 4 <= b; a += 4) {
+                        const double p0 = pv[a], p1 = pv[a + 1], p2 = pv[a + 2], p3 = pv[a + 3];
+                        sum = dadd(sum, p0);
+                        sum = dadd(sum, p1);
+                        sum = dadd(sum, p2);
+                        sum = dadd(sum, p3);
+                    }
+                    for (; a < b; ++a) sum = dadd(sum, pv[a]);
                 }
                 __syncwarp();
                 group_done = cb + CH >= ae;
@@ -178,9 +199,8 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             }
             if (!group_done) continue;
             // ---- epilogue of group G and rotation to G+W ----
-            if (row < n) op.finish(row, sum, xdiag, rw, dots);
+            if (row < n) op.finish(row, sum, rw, dots);
             sum = 0.0;
-            xdiag = 0.0;
             G = NG;
             rs = nrs;
             re = nre;
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(RS_BLOCK, RS_MINB) k_rowpass_simple(CsrView A,
             }
             __syncwarp();
         }
-        if (valid) op.finish(row, sum, xdiag, rw, dots);
+        if (valid) op.finish(row, sum, rw, dots);
     }
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
@@ -270,8 +290,8 @@ struct NoRow {};
 struct Row1 {
     double a;
 };
-struct Row2 {
-    double f, w;
+struct Row3 {
+    double f, w, x;
 };
 
 struct OpSpmv {
@@ -281,7 +301,7 @@ struct OpSpmv {
     double* y;
     __device__ double x(int j) const { return __ldg(xv + j); }
     __device__ Row load(int) const { return {}; }
-    __device__ void finish(int i, double s, double, const Row&, double*) const { y[i] = s; }
+    __device__ void finish(int i, double s, const Row&, double*) const { y[i] = s; }
 };
 
 struct OpResidual {
@@ -292,58 +312,37 @@ struct OpResidual {
     double* r;
     __device__ double x(int j) const { return __ldg(xv + j); }
     __device__ Row load(int i) const { return {__ldg(f + i)}; }
-    __device__ void finish(int i, double s, double, const Row& q, double*) const { r[i] = dsub(q.a, s); }
+    __device__ void finish(int i, double s, const Row& q, double*) const { r[i] = dsub(q.a, s); }
 };
 
-// hierarchy.cpp:165-170 with smooth() from u = 0 (smoother.cpp:42-47):
-// u_j = 0 + (om*w_j)*(f_j - 0) ; r_i = f_i - sum_j a_ij u_j
+// V-cycle down leg (hierarchy.cpp:165-170): the first pre-smoothing sweep from
+// u = 0 gives u = 0 + (om*w)*(f - A*0) = u0, which the producer of f (the
+// restriction, or premul on level 0) has already written; this pass forms the
+// residual r = f - A u0.
 struct OpDown {
     static constexpr int NDOT = 0;
-    using Row = Row2;
+    using Row = Row1;
     const double* f;
-    const double* w;
-    double om;
-    double* u;
+    const double* u0;
     double* r;
-    __device__ double x(int j) const { return dadd(0.0, dmul(dmul(om, __ldg(w + j)), __ldg(f + j))); }
-    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
-    __device__ void finish(int i, double s, double, const Row& q, double*) const {
-        u[i] = dadd(0.0, dmul(dmul(om, q.w), q.f));
-        r[i] = dsub(q.f, s);
-    }
+    __device__ double x(int j) const { return __ldg(u0 + j); }
+    __device__ Row load(int i) const { return {__ldg(f + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const { r[i] = dsub(q.a, s); }
 };
 
-// one damped sweep: out_i = u_i + (om*w_i)*(f_i - (A u)_i)
+// one damped sweep (smoother.cpp:42-47): out_i = x_i + (om*w_i)*(f_i - (A x)_i)
 struct OpSmooth {
     static constexpr int NDOT = 0;
-    using Row = Row2;
+    using Row = Row3;
     const double* f;
     const double* w;
     double om;
     const double* u;
     double* out;
     __device__ double x(int j) const { return __ldg(u + j); }
-    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
-    __device__ void finish(int i, double s, double xi, const Row& q, double*) const {
-        out[i] = dadd(xi, dmul(dmul(om, q.w), dsub(q.f, s)));
-    }
-};
-
-// hierarchy.cpp:179-183: x = u + (0 + 1.0*uc[agg]) then one sweep on x.
-struct OpUp {
-    static constexpr int NDOT = 0;
-    using Row = Row2;
-    const double* f;
-    const double* w;
-    double om;
-    const double* u;
-    const int* agg;
-    const double* uc;
-    double* out;
-    __device__ double x(int j) const { return dadd(__ldg(u + j), dadd(0.0, __ldg(uc + __ldg(agg + j)))); }
-    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i)}; }
-    __device__ void finish(int i, double s, double xi, const Row& q, double*) const {
-        out[i] = dadd(xi, dmul(dmul(om, q.w), dsub(q.f, s)));
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i), __ldg(u + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const {
+        out[i] = dadd(q.x, dmul(dmul(om, q.w), dsub(q.f, s)));
     }
 };
 
@@ -355,7 +354,7 @@ struct OpSpmvDot {
     const double* a;
     __device__ double x(int j) const { return __ldg(xv + j); }
     __device__ Row load(int i) const { return {__ldg(a + i)}; }
-    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
         y[i] = s;
         d[0] = __fma_rn(q.a, s, d[0]);
     }
@@ -369,7 +368,7 @@ struct OpSpmvDot2 {
     const double* b;
     __device__ double x(int j) const { return __ldg(xv + j); }
     __device__ Row load(int i) const { return {__ldg(b + i)}; }
-    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
         y[i] = s;
         d[0] = __fma_rn(s, q.a, d[0]);
         d[1] = __fma_rn(s, s, d[1]);
@@ -385,7 +384,7 @@ struct OpResidNorm {
     double* r2;
     __device__ double x(int j) const { return __ldg(xv + j); }
     __device__ Row load(int i) const { return {__ldg(f + i)}; }
-    __device__ void finish(int i, double s, double, const Row& q, double* d) const {
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
         const double t = dsub(q.a, s);
         if (r) r[i] = t;
         if (r2) r2[i] = t;
@@ -440,8 +439,12 @@ double spmv_bytes(const CsrView& A) {
 }
 
 // ---- restriction / prolongation ------------------------------------------
+// restriction f_c = R r (spmv with R = P^T, csr.cpp:79-84: members ascending,
+// 1.0*r exact) and, for a coarse level that is smoothed next, its first
+// pre-smoothing iterate u0_c = 0 + (om*w_c)*f_c.
 __global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __restrict__ midx,
-                           const double* __restrict__ r, double* __restrict__ fc, Gate g) {
+                           const double* __restrict__ r, double* __restrict__ fc, const double* __restrict__ wc,
+                           double om, double* __restrict__ u0c, Gate g) {
     if (gated_off(g)) return;
     for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
         int p = __ldg(mptr + I);
@@ -451,15 +454,23 @@ __global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __re
             const int cnt = min(4, p1 - p);
             double rv[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (t < cnt) rv[t] = __ldg(r + __ldg(midx + p + t));
+            for (int t = 0; t < 4; ++t) rv[t] = t < cnt ? __ldg(r + __ldg(midx + p + t)) : 0.0;
 #pragma unroll
             for (int t = 0; t < 4; ++t)
                 if (t < cnt) s = dadd(s, rv[t]);
             p += cnt;
         }
         fc[I] = s;
+        if (u0c) u0c[I] = dadd(0.0, dmul(dmul(om, wc[I]), s));
     }
+}
+
+// u0 = 0 + (om*w)*f : first pre-smoothing iterate from a zero guess
+__global__ void k_premul(int n, const double* __restrict__ f, const double* __restrict__ w, double om,
+                         double* __restrict__ u0, Gate g) {
+    if (gated_off(g)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        u0[i] = dadd(0.0, dmul(dmul(om, w[i]), f[i]));
 }
 
 __global__ void k_prolong(int n, const double* __restrict__ u, const int* __restrict__ agg,
@@ -781,22 +792,20 @@ void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g) {
 void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, Gate g) {
     launch_rowpass(c, "residual", spmv_bytes(A) + 16.0 * A.n, A, OpResidual{f, x, r}, g, {}, false);
 }
-void vc_down(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* u,
-             double* r, Gate g) {
-    // A + f, w read once, u and r written once
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n + 16.0 * A.n;
-    launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, w, om, u, r}, g, {}, false);
+void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, double* u0, Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "vcycle_premul", 24.0 * n, k_premul, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f,
+           w, om, u0, g);
 }
-void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
-               const double* u, double* out, Gate g) {
-    launch_rowpass(c, "vcycle_smooth", spmv_bytes(A) + 16.0 * A.n, A, OpSmooth{f, w, om, u, out}, g, {},
-                   false);
+void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g) {
+    // A + f read once, u0 gathered (read once), r written once
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, u0, r}, g, {}, false);
 }
-void vc_up(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
-           const int* agg, const double* uc, double* out, Gate g) {
-    // A + u, agg, f, w read once + uc (coarse) + out written once
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 28.0 * A.n + 8.0 * A.n;
-    launch_rowpass(c, "vcycle_up", bytes, A, OpUp{f, w, om, u, agg, uc, out}, g, {}, false);
+void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
+               double* out, Gate g) {
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;
+    launch_rowpass(c, "vcycle_smooth", bytes, A, OpSmooth{f, w, om, u, out}, g, {}, false);
 }
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
                 Gate g) {
@@ -805,10 +814,10 @@ void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double
            static_cast<int>(n), u, agg, uc, out, g);
 }
 void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const double* r, double* fc,
-                  Gate g) {
+                  const double* wc, double om, double* u0c, Gate g) {
     if (nc == 0) return;
-    LAUNCH(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc),
-           mptr, midx, r, fc, g);
+    LAUNCH(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc), mptr,
+           midx, r, fc, wc, om, u0c, g);
 }
 void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double* a, DotSink s, Gate g) {
     launch_rowpass(c, "spmv_dot", spmv_bytes(A) + 8.0 * A.n, A, OpSpmvDot{x, y, a}, g, s, true);
