@@ -66,10 +66,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // consumer (the next chunk of the same group, or the first chunk of the next
 // group).  Row pointers and epilogue operands of the next group are prefetched
 // into registers.  Threads own rows and accumulate strictly in column order
-// (csr.cpp:79-84): per chunk, lanes first form the products a_e * x_col(e)
-// entry-parallel (all gathers of a lane in flight at once, written in place
-// over the staged values), then each lane sums its row's products in column
-// order from shared memory.
+// (csr.cpp:79-84), gathering up to RP_BATCH operands at a time.
 template <class Op, int CH>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     if (gated_off(g)) return;
@@ -154,40 +151,23 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                 if (pb >= 0) issue(pb, pe, st ^ 1);
                 mbar_wait(&bar[st], (phase >> st) & 1u);
                 phase ^= (1u << st);
-                // phase 1 (entry-parallel): p_e = a_e * x_col(e), in place over the
-                // staged values; every lane issues its CH/32 gathers at once
+                // row-parallel: lane l gathers the k-th operand of 32 consecutive rows
+                // (contiguous for stencil-like matrices), RP_BATCH at a time, then
+                // accumulates them strictly in column order
                 {
-                    constexpr int PER = CH / 32;
-                    const int lo = max(gs, cb) - cb, hi = min(ge, cb + CH) - cb;
-                    int cidx[PER];
-                    double xv[PER];
+                    int a = max(rs, cb);
+                    const int b = min(re, cb + CH);
+                    while (a < b) {
+                        const int cnt = min(RP_BATCH, b - a);
+                        const int k = a - cb;
+                        double xv[RP_BATCH];
 #pragma unroll
-                    for (int t = 0; t < PER; ++t) {
-                        const int k = lane + 32 * t;
-                        cidx[t] = (k >= lo && k < hi) ? s_col[w][st][k] : -1;
-                    }
+                        for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
 #pragma unroll
-                    for (int t = 0; t < PER; ++t) xv[t] = cidx[t] >= 0 ? op.x(cidx[t]) : 0.0;
-#pragma unroll
-                    for (int t = 0; t < PER; ++t) {
-                        const int k = lane + 32 * t;
-                        if (cidx[t] >= 0) s_val[w][st][k] = dmul(s_val[w][st][k], xv[t]);
+                        for (int t = 0; t < RP_BATCH; ++t)
+                            if (t < cnt) sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
+                        a += cnt;
                     }
-                }
-                __syncwarp();
-                // phase 2 (row-parallel): sequential sum in column order
-                {
-                    int a = max(rs, cb) - cb;
-                    const int b = min(re, cb + CH) - cb;
-                    const double* pv = s_val[w][st];
-                    for (; a + 4 <= b; a += 4) {
-                        const double p0 = pv[a], p1 = pv[a + 1], p2 = pv[a + 2], p3 = pv[a + 3];
-                        sum = dadd(sum, p0);
-                        sum = dadd(sum, p1);
-                        sum = dadd(sum, p2);
-                        sum = dadd(sum, p3);
-                    }
-                    for (; a < b; ++a) sum = dadd(sum, pv[a]);
                 }
                 __syncwarp();
                 group_done = cb + CH >= ae;
