@@ -68,8 +68,10 @@ enum { AMGR_SMOOTHER_JACOBI = 0, AMGR_SMOOTHER_SPAI0 = 1, AMGR_SMOOTHER_CHEBYSHE
  * kind, coarsening.hpp:48-50) or smoothed aggregation (extension). */
 enum { AMGR_COARSENING_PLAIN = 0, AMGR_COARSENING_SMOOTHED = 1 };
 /* Coarse direct solve: EXACT replays the reference's LU solve order
- * (dense_lu.cpp:52-73) bit for bit. */
-enum { AMGR_COARSE_EXACT = 0 };
+ * (dense_lu.cpp:52-73) bit for bit; INVERSE (extension) applies the explicit
+ * inverse formed from the same LU factors at rebuild time (a parallel matvec,
+ * rounding differs at the 1e-16 level). */
+enum { AMGR_COARSE_EXACT = 0, AMGR_COARSE_INVERSE = 1 };
 
 /* CSR input.  Invariants as CsrMatrix (proj/include/amgreuse/csr.hpp:20-27):
  * row_ptr non-decreasing, row_ptr[0]=0, row_ptr[nrows]=nnz, columns strictly
@@ -100,6 +102,8 @@ typedef struct amgr_amg_params {
     int32_t power_iters;     /* power iterations for lambda_max (extension) */
     double cheb_lower;       /* lambda_min = cheb_lower * lambda_max        */
     double cheb_safety;      /* lambda_max safety factor                    */
+    int32_t coarse_solve;    /* AMGR_COARSE_*          (extension)          */
+    int32_t reserved;
 } amgr_amg_params;
 
 /* SolveParams (bicgstab.hpp:17-20). */

@@ -32,6 +32,7 @@ LIB_PATH = os.path.join(_HERE, "libamgr_b200.so")
 HOST, DEVICE, DEVICE_ADOPT = 0, 1, 2
 SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}
 COARSENING = {"plain": 0, "smoothed": 1}
+COARSE_SOLVE = {"exact": 0, "inverse": 1}
 PROBLEM = {"poisson": 0, "blob": 1, "dambreak": 2, "convdiff": 3}
 
 
@@ -69,7 +70,7 @@ class _AmgParams(C.Structure):
                 ("post_sweeps", C.c_int32), ("coarse_enough", C.c_int64), ("max_direct_size", C.c_int64),
                 ("smoother", C.c_int32), ("coarsening", C.c_int32), ("sa_omega", C.c_double),
                 ("cheb_degree", C.c_int32), ("power_iters", C.c_int32), ("cheb_lower", C.c_double),
-                ("cheb_safety", C.c_double)]
+                ("cheb_safety", C.c_double), ("coarse_solve", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _SolveParams(C.Structure):
@@ -162,11 +163,13 @@ class AmgParams:
     power_iters: int = 10
     cheb_lower: float = 1.0 / 30.0
     cheb_safety: float = 1.1
+    coarse_solve: str = "exact"
 
     def _c(self) -> _AmgParams:
         return _AmgParams(self.eps, self.omega, self.pre_sweeps, self.post_sweeps, self.coarse_enough,
                           self.max_direct_size, SMOOTHER[self.smoother], COARSENING[self.coarsening],
-                          self.sa_omega, self.cheb_degree, self.power_iters, self.cheb_lower, self.cheb_safety)
+                          self.sa_omega, self.cheb_degree, self.power_iters, self.cheb_lower, self.cheb_safety,
+                          COARSE_SOLVE[self.coarse_solve], 0)
 
 
 @dataclass

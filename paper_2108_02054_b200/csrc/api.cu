@@ -80,6 +80,8 @@ void amgr_amg_params_default(amgr_amg_params* p) {
     p->power_iters = 10;
     p->cheb_lower = 1.0 / 30.0;
     p->cheb_safety = 1.1;
+    p->coarse_solve = AMGR_COARSE_EXACT;
+    p->reserved = 0;
 }
 
 void amgr_solve_params_default(amgr_solve_params* p) {

@@ -3,6 +3,7 @@
 // buckets) it reproduces.
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <cstring>
 #include <sstream>
@@ -27,6 +28,7 @@ AmgP to_amgp(const amgr_amg_params* p) {
     a.power_iters = p->power_iters;
     a.cheb_lower = p->cheb_lower;
     a.cheb_safety = p->cheb_safety;
+    a.coarse_solve = p->coarse_solve;
     return a;
 }
 
@@ -150,6 +152,17 @@ void coarse_factorize(Hier& h, int* status) {
     if (h.piv.size() != h.nL) h.piv.alloc(h.nL, c.stream);
     lu_densify(c, L.view(), h.lu.get());
     lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
+    if (h.prm.coarse_solve == AMGR_COARSE_INVERSE) {
+        if (h.inv.size() != h.nL * h.nL) h.inv.alloc(h.nL * h.nL, c.stream);
+        lu_inverse(c, h.nL, h.lu.get(), h.piv.get(), h.inv.get());
+    }
+}
+
+static void coarse_solve(Hier& h, const double* b, double* x, Gate g) {
+    if (h.prm.coarse_solve == AMGR_COARSE_INVERSE)
+        inv_apply(*h.ctx, h.nL, h.inv.get(), b, x, g);
+    else
+        lu_solve(*h.ctx, h.nL, h.lu.get(), h.piv.get(), b, x, g);
 }
 
 void throw_lu(int st) {
@@ -450,7 +463,7 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     const size_t L = h.lv.size();
     const double om = h.om_eff();
     if (L == 1) {
-        lu_solve(c, h.nL, h.lu.get(), h.piv.get(), f, u, g);
+        coarse_solve(h, f, u, g);
         return;
     }
     std::vector<const double*> fin(L), ufinal(L);
@@ -489,7 +502,7 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
                      next_smoothed ? h.lv[i + 1].w.get() : nullptr, om, next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
     // coarsest: direct solve (hierarchy.cpp:175)
-    lu_solve(c, h.nL, h.lu.get(), h.piv.get(), W.f[L - 1].get(), W.u[L - 1].get(), g);
+    coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
     ufinal[L - 1] = W.u[L - 1].get();
     // up leg
     for (size_t i = L - 1; i-- > 0;) {
@@ -559,6 +572,59 @@ void write_state(Hier& h, const KState& s) {
 
 }  // namespace
 
+// Run gated Krylov iterations: the per-iteration kernel sequence is captured
+// once into a CUDA graph (every kernel is gated on the device-side solver
+// flags, so the sequence is static), then replayed with one iteration in
+// flight ahead of the host's convergence check (flags copied to pinned memory
+// and signalled by an event).  Falls back to direct launches while a kernel
+// probe is active (probe events must bracket individual launches).
+static void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& out) {
+    Ctx& c = *h.ctx;
+    KState* st = work(h).st.get();
+    static thread_local KState* pinned = nullptr;
+    if (!pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&pinned), 2 * sizeof(KState)));
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    cudaGraphExec_t exec = nullptr;
+    int64_t per_iter = 0;
+    const bool use_graph = c.probe.family.empty() && !getenv("AMGR_NO_GRAPH");
+    if (use_graph) {
+        cudaGraph_t graph;
+        const int64_t l0 = c.launches;
+        CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+        enqueue_iter();
+        CK(cudaStreamEndCapture(c.stream, &graph));
+        per_iter = c.launches - l0;
+        c.launches = l0;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+    }
+    auto launch = [&](int slot) {
+        if (use_graph) {
+            CK(cudaGraphLaunch(exec, c.stream));
+            c.launches += per_iter;
+        } else {
+            enqueue_iter();
+        }
+        CK(cudaMemcpyAsync(&pinned[slot], st, sizeof(KState), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaEventRecord(ev[slot], c.stream));
+    };
+    int64_t k = 0;
+    launch(0);
+    for (;;) {
+        ++k;
+        launch(static_cast<int>(k & 1));  // one iteration ahead (gated off if already done)
+        CK(cudaEventSynchronize(ev[(k - 1) & 1]));
+        if (pinned[(k - 1) & 1].flags & KF_DONE) break;
+    }
+    CK(cudaStreamSynchronize(c.stream));
+    if (exec) CK(cudaGraphExecDestroy(exec));
+    CK(cudaEventDestroy(ev[0]));
+    CK(cudaEventDestroy(ev[1]));
+    out = read_state(h);
+}
+
 void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
               amgr_solve_stats& out) {
     if (sp.tol <= 0.0) invalid("bicgstab: tol must be positive");
@@ -610,7 +676,7 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
     const Gate GH = gate_of(st, KF_DONE, KF_HALF);
     const Gate GF = gate_of(st, KF_DONE | KF_HALF);
     const Gate GC = gate_of(st, KF_DONE | KF_HALF, KF_CHECK);
-    for (;;) {
+    auto iter = [&]() {
         bicg_begin(c, st);
         bicg_p(c, st, n, B.r, B.p, B.v);
         vcycle(h, B.p, B.ph, G);
@@ -629,9 +695,8 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
         bicg_end_test(c, st);
         resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GC);
         bicg_end_check(c, st);
-        s = read_state(h);
-        if (s.flags & KF_DONE) break;
-    }
+    };
+    run_iterations(h, iter, s);
     out.iterations = s.it;
     if (s.flags & KF_CONVERGED) {
         out.converged = 1;
@@ -689,7 +754,7 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
     write_state(h, s);
     const Gate G = gate_of(st, KF_DONE);
     const Gate GC = gate_of(st, KF_DONE, KF_CHECK);
-    for (;;) {
+    auto iter = [&]() {
         cg_begin(c, st);
         spmv_dot(c, A, B.p, B.v, B.p, sink(h, ST_FIELD(st, d_pq)), G);
         cg_alpha(c, st);
@@ -701,9 +766,8 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
         dot(c, n, B.r, B.s, sink(h, ST_FIELD(st, d_rz)), G);
         cg_beta(c, st);
         cg_p(c, st, n, B.s, B.p);
-        s = read_state(h);
-        if (s.flags & KF_DONE) break;
-    }
+    };
+    run_iterations(h, iter, s);
     out.iterations = s.it;
     if (s.flags & KF_CONVERGED) {
         out.converged = 1;

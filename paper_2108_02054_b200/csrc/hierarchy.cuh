@@ -20,6 +20,7 @@ struct AmgP {
     double sa_omega = 2.0 / 3.0;
     int cheb_degree = 3, power_iters = 10;
     double cheb_lower = 1.0 / 30.0, cheb_safety = 1.1;
+    int coarse_solve = AMGR_COARSE_EXACT;
 };
 AmgP to_amgp(const amgr_amg_params* p);
 
@@ -83,6 +84,7 @@ struct Hier {
     std::vector<Level> lv;
     DevArray<double> lu;
     DevArray<int64_t> piv;
+    DevArray<double> inv;  // AMGR_COARSE_INVERSE
     int64_t nL = 0;
     amgr_phase_timings tm{};
     std::shared_ptr<Work> ws;

@@ -84,6 +84,10 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status);
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x,
               Gate g = {});
 
+// FAST mode (extension): explicit inverse from the LU factors, applied as a matvec
+void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv);
+void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g = {});
+
 // ---- misc vector kernels ------------------------------------------------------
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g = {});
 void copy(Ctx& c, double* dst, const double* src, int64_t n, Gate g = {});

@@ -701,6 +701,76 @@ __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __
     for (int i = tid; i < n; i += LS_THREADS) x[i] = xs[i];
 }
 
+// ---- FAST coarse solve (AMGR_COARSE_INVERSE, extension) -------------------
+// Inverse of the coarsest matrix from its LU factors: warp per column,
+// column-oriented forward and backward sweeps on the unit vectors (rounding
+// differs from the reference's row-oriented solve; tolerance-level parity).
+__global__ void __launch_bounds__(1024) k_lu_inverse(int n, const double* __restrict__ m,
+                                                     const int64_t* __restrict__ piv, double* __restrict__ inv,
+                                                     double* __restrict__ scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int col = blockIdx.x * nw + wid; col < n; col += gridDim.x * nw) {
+        double* x = scratch + static_cast<int64_t>(col) * n;
+        for (int i = lane; i < n; i += 32) x[i] = (i == col) ? 1.0 : 0.0;
+        __syncwarp();
+        if (lane == 0)
+            for (int k = 0; k < n; ++k) {
+                const int p = static_cast<int>(piv[k]);
+                if (p != k) {
+                    const double t = x[k];
+                    x[k] = x[p];
+                    x[p] = t;
+                }
+            }
+        __syncwarp();
+        for (int j = 0; j < n - 1; ++j) {
+            const double xj = x[j];
+            for (int i = j + 1 + lane; i < n; i += 32) x[i] = x[i] - m[static_cast<int64_t>(i) * n + j] * xj;
+            __syncwarp();
+        }
+        for (int j = n - 1; j >= 0; --j) {
+            if (lane == 0) x[j] = x[j] / m[static_cast<int64_t>(j) * n + j];
+            __syncwarp();
+            const double xj = x[j];
+            for (int i = lane; i < j; i += 32) x[i] = x[i] - m[static_cast<int64_t>(i) * n + j] * xj;
+            __syncwarp();
+        }
+        for (int i = lane; i < n; i += 32) inv[static_cast<int64_t>(i) * n + col] = x[i];
+    }
+}
+
+// x = inv * b, warp per row, fixed-order lane partials + shuffle tree
+__global__ void __launch_bounds__(1024) k_inv_apply(int n, const double* __restrict__ inv, const double* b,
+                                                    double* x, Gate g) {
+    if (gated_off(g)) return;
+    extern __shared__ double bs[];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) bs[i] = b[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int row = wid; row < n; row += nw) {
+        const double* r = inv + static_cast<int64_t>(row) * n;
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s = __fma_rn(r[j], bs[j], s);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) x[row] = s;
+    }
+}
+
+void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv) {
+    if (n == 0) return;
+    DevArray<double> scratch(n * n, c.stream);
+    LAUNCH(c, "coarse", 0.0, k_lu_inverse, grid_for(n, 32, 64), 1024, 0, static_cast<int>(n), m, piv, inv,
+           scratch.get());
+}
+
+void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g) {
+    if (n == 0) return;
+    const size_t sm = sizeof(double) * static_cast<size_t>(n);
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    LAUNCH(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
+}
+
 // ---- misc ---------------------------------------------------------------------
 __global__ void k_fill(double* x, int64_t n, double v, Gate g) {
     if (gated_off(g)) return;

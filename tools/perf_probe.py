@@ -36,7 +36,8 @@ def main():
     ctx.synchronize()
     A = amg.DeviceCsr(n, n, nnz, rp.data_ptr(), ci.data_ptr(), vals[0].data_ptr())
     t0 = time.perf_counter()
-    h = amg.setup(A, ctx=ctx)
+    cs = os.environ.get("AMGR_COARSE", "exact")
+    h = amg.setup(A, amg.AmgParams(coarse_solve=cs), ctx=ctx)
     ctx.synchronize()
     t_setup = time.perf_counter() - t0
     print(f"g={g} kind={kind} n={n} nnz={nnz} setup {t_setup*1e3:.1f} ms levels={h.num_levels()} "
