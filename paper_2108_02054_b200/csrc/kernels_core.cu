@@ -757,20 +757,6 @@ __global__ void __launch_bounds__(1024) k_inv_apply(int n, const double* __restr
     }
 }
 
-void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv) {
-    if (n == 0) return;
-    DevArray<double> scratch(n * n, c.stream);
-    LAUNCH(c, "coarse", 0.0, k_lu_inverse, grid_for(n, 32, 64), 1024, 0, static_cast<int>(n), m, piv, inv,
-           scratch.get());
-}
-
-void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g) {
-    if (n == 0) return;
-    const size_t sm = sizeof(double) * static_cast<size_t>(n);
-    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    LAUNCH(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
-}
-
 // ---- misc ---------------------------------------------------------------------
 __global__ void k_fill(double* x, int64_t n, double v, Gate g) {
     if (gated_off(g)) return;
@@ -921,6 +907,20 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
+}
+
+void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv) {
+    if (n == 0) return;
+    DevArray<double> scratch(n * n, c.stream);
+    LAUNCH(c, "coarse", 0.0, k_lu_inverse, grid_for(n, 32, 64), 1024, 0, static_cast<int>(n), m, piv, inv,
+           scratch.get());
+}
+
+void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g) {
+    if (n == 0) return;
+    const size_t sm = sizeof(double) * static_cast<size_t>(n);
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    LAUNCH(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
 }
 
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g) {
