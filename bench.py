@@ -1,0 +1,402 @@
+"""Benchmark: partial-reuse AMG rebuild ms/step + solve ms/step (BASELINE.json
+`metric`) on the synthetic two-fluid dam-break pressure Poisson problem
+(configs[2], "C3": 256^3, 1000:1 density jump on a collapsing water column,
+partial reuse, 1 B200).
+
+One step = one time step of the sequence: partial rebuild of the hierarchy
+from A_k (numeric Galerkin RAP on the frozen transfers + smoothers + coarse
+LU, `amgr_rebuild_values`) followed by the AMG-preconditioned BiCGStab solve
+(`amgr_bicgstab`, tol 1e-8, <= 100 iterations) from the previous step's
+solution — exactly the reference's `run_sequence` partial-reuse step
+(proj/src/reuse.cpp:85-114).  The matrices A_k are generated on the device
+before the timed region (ingestion is excluded, reuse.cpp:65) and are larger
+than L2 (0.94 GB of values), so no explicit flush is needed.
+
+value        = device time of K steps / K (CUDA events on the library stream,
+               barrier + synchronize both sides, max over ranks)      [ms/step]
+e2e          = the same through the C-ABI with HOST buffers: per step the
+               H2D copy of A_k's values and f from pinned memory and the D2H
+               read of the solution are inside the timed region
+roofline     = the dominant kernel (level-0 post-smoothing sweep, the largest
+               single kernel of the step) probed with CUDA events on its stream
+cpu_baseline = the unmodified reference (oracle/_ref, single-threaded as
+               shipped) on a bounded sample of the same workload
+--impl reference runs that reference arm alone (rank 0).
+
+Multi-GPU (torchrun, N>1): each rank runs an independent 256^3 system
+(replicas; the row-partitioned NCCL path is not built yet) — see DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "partial-reuse AMG rebuild ms/step + solve ms/step, 256^3 Poisson; HBM GB/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+ITER_RECORD = os.path.join(ROOT, "profiles", "c3_iterations.json")
+TRAFFIC_RECORD = os.path.join(ROOT, "profiles", "r01_traffic.json")
+
+
+def args_parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--size", type=int, default=256)
+    p.add_argument("--problem", default="dambreak")
+    p.add_argument("--nsteps", type=int, default=50, help="length of the time sequence (configs[2]: 50)")
+    p.add_argument("--coarse", default="exact", choices=["exact", "inverse"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# --------------------------------------------------------------------------------------
+# reference arm / CPU baseline (TEST INFRASTRUCTURE: oracle/_ref is the checker and the
+# reported CPU baseline, never part of the measured GPU path)
+# --------------------------------------------------------------------------------------
+def reference_sample(A0, Ak_list, f, iters, max_steps):
+    """Time the unmodified reference on the host: setup(A0) untimed, then per
+    step partial_update(A_k) (timed in full) + fixed-V BiCGStab sampled for 2
+    iterations (per-iteration time).  ms/step = rebuild + per_iter * iters."""
+    from oracle import ref
+
+    p = ref.params()
+    t0 = time.perf_counter()
+    h = ref.setup(A0, p)
+    t_setup = time.perf_counter() - t0
+    rebuild, per_iter = [], []
+    for Ak in Ak_list[:max_steps]:
+        hk = ref.partial_update(h, Ak, p)
+        rebuild.append(hk.seconds)
+        s = ref.bicgstab(hk, f, fixed=True, max_iter=2, prm=p)
+        per_iter.append(s.seconds / max(s.iterations, 1))
+        hk.free()
+    h.free()
+    rb = float(np.mean(rebuild)) * 1e3
+    it = float(np.mean(per_iter)) * 1e3
+    return {"value": rb + it * iters, "rebuild_ms": rb, "per_iteration_ms": it, "setup_s": t_setup,
+            "steps": len(rebuild)}
+
+
+def host_problem(g, kind, k, nsteps):
+    from oracle import problems as P
+
+    return P.grid3d_values(kind, g, k, nsteps)
+
+
+def run_reference_arm(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    g = a.size
+    try:
+        rec = json.load(open(ITER_RECORD))
+        iters = float(rec["avg_iterations"])
+        src = f"avg BiCGStab iterations of the same sequence recorded in {os.path.relpath(ITER_RECORD, ROOT)}"
+    except Exception:
+        iters, src = 80.0, "assumed 80 iterations/step (no recorded count)"
+    import numpy as np  # noqa: F811
+
+    from oracle import problems as P
+
+    ks = list(range(1 + a.warmup, 1 + a.warmup + min(a.steps, 3)))
+    A0 = host_problem(g, a.problem, 0, a.nsteps)
+    Aks = [host_problem(g, a.problem, k, a.nsteps) for k in ks]
+    f = P.rhs(g ** 3)
+    r = reference_sample(A0, Aks, f, iters, len(ks))
+    cores = 1
+    sample = (f"{r['steps']} partial_update steps of the {g}^3 {a.problem} sequence timed in full + fixed-V "
+              f"BiCGStab timed for 2 iterations per step; solve = per-iteration time x {iters:.1f} ({src}); "
+              f"reference setup {r['setup_s']:.1f} s untimed; single-threaded as shipped")
+    out = {"metric": METRIC, "value": r["value"], "unit": "ms/step", "impl": "reference", "n_gpus": a.gpus,
+           "steps": r["steps"], "warmup": 0, "ms_per_step": r["value"], "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"C3 dam-break {g}^3 partial reuse", "problem": a.problem, "grid": g,
+                      "reuse": "partial"},
+           "rebuild_ms_per_step": r["rebuild_ms"], "solve_ms_per_step": r["per_iteration_ms"] * iters,
+           "cpu_baseline": {"value": r["value"], "unit": "ms/step", "cores": cores, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": r["value"], "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+def main():
+    a = args_parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+        return
+    rank, world, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2108_02054_b200 as amg
+
+    L = amg.lib()
+    ctx = amg.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    g, kind = a.size, amg.PROBLEM[a.problem]
+    n, nnz = g ** 3, int(L.amgr_problem_nnz(g))
+    W, K = max(a.warmup, 0), max(a.steps, 1)
+    ksteps = list(range(0, 1 + W + K))  # step 0 = full setup
+
+    # ---- inputs resident in HBM (generation excluded from timing) ----
+    rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(nnz + 8, dtype=torch.int32, device="cuda")
+    vals = [torch.empty(nnz + 8, dtype=torch.float64, device="cuda") for _ in ksteps]
+    torch.cuda.synchronize()
+    amg._check(L.amgr_problem_pattern(ctx.ptr, g, rp.data_ptr(), ci.data_ptr()), ctx.ptr)
+    for k, v in zip(ksteps, vals):
+        amg._check(L.amgr_problem_values(ctx.ptr, kind, g, k % a.nsteps, a.nsteps, v.data_ptr()), ctx.ptr)
+    f = torch.empty(n, dtype=torch.float64, device="cuda")
+    amg._check(L.amgr_problem_rhs(ctx.ptr, n, 42, f.data_ptr(), amg.DEVICE), ctx.ptr)
+    u = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ctx.synchronize()
+
+    prm = amg.AmgParams(coarse_solve=a.coarse)
+    A0 = amg.DeviceCsr(n, n, nnz, rp.data_ptr(), ci.data_ptr(), vals[0].data_ptr())
+    t0 = time.perf_counter()
+    h = amg.setup(A0, prm, ctx=ctx)
+    ctx.synchronize()
+    setup_s = time.perf_counter() - t0
+    sp = amg.SolveParams()
+
+    def step(k):
+        h.rebuild_values(vals[k].data_ptr(), adopt=True)
+        _, st = amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()), sp)
+        return st
+
+    st0 = amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()), sp)[1]  # step 0 solve
+    for k in range(1, 1 + W):
+        step(k)
+    ctx.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # ---- timed region ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 1)]
+    iters, conv = [], []
+    launches0 = ctx.launches()
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for j, k in enumerate(range(1 + W, 1 + W + K)):
+            h.rebuild_values(vals[k].data_ptr(), adopt=True)
+            ev[2 * j + 1].record(stream)
+            _, st = amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()), sp)
+            ev[2 * j + 2].record(stream)
+            iters.append(st.iterations)
+            conv.append(st.converged)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launches() - launches0
+    total_ms = ev[0].elapsed_time(ev[2 * K])
+    rebuild_ms = sum(ev[2 * j].elapsed_time(ev[2 * j + 1]) for j in range(K)) / K
+    solve_ms = sum(ev[2 * j + 1].elapsed_time(ev[2 * j + 2]) for j in range(K)) / K
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+
+    # ---- roofline probe: dominant kernel = level-0 post-smoothing sweep ----
+    peak, peak_kind = hbm_peak()
+    ctx.probe("vcycle_smooth@0")
+    k_probe = 1 + W + K - 1
+    step(k_probe)
+    cnt, pms, pbytes = ctx.probe_read()
+    ctx.probe(None)
+    achieved = (pbytes / cnt) / (pms / cnt) / 1e6 if cnt else None  # GB/s
+    # rebuild kernels (numeric RAP on level 0) for the north-star rebuild roofline
+    extra = {}
+    for fam in ("rap@0", "vcycle_down@0", "spmv_dot"):
+        ctx.probe(fam)
+        step(k_probe)
+        c2, m2, b2 = ctx.probe_read()
+        if c2:
+            extra[fam] = {"launches": c2, "avg_us": 1e3 * m2 / c2, "GB_s": b2 / m2 / 1e6, "frac": b2 / m2 / 1e6 / peak}
+    ctx.probe(None)
+    traffic = None
+    try:
+        traffic = json.load(open(TRAFFIC_RECORD)).get("vcycle_smooth@0")
+    except Exception:
+        pass
+    lvl0 = h.level_dims(0)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "k_rowpass<OpSmooth> level 0 (post-smoothing sweep)",
+                "bytes_per_launch": pbytes / cnt if cnt else None,
+                "bytes_formula": "12*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads)",
+                "nnz": lvl0["nnz"], "n": lvl0["nrows"], "peak_source": peak_kind, "kernels": extra}
+
+    # ---- e2e through the C-ABI with host buffers ----
+    e2e = None
+    if not a.no_e2e:
+        hv = []
+        for k in range(1 + W, 1 + W + K):
+            t = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
+            t.copy_(vals[k][:nnz])
+            hv.append(t)
+        fh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        fh.copy_(f)
+        uh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        uh.copy_(u)
+        torch.cuda.synchronize()
+        hb = L.amgr_bicgstab
+        spc = amg._SolveParams(sp.tol, sp.max_iter)
+        stc = amg._SolveStats()
+        import ctypes
+
+        ctx.synchronize()
+        barrier()
+        e0 = time.perf_counter()
+        for t in hv:
+            amg._check(L.amgr_rebuild_values(h._p, t.data_ptr(), amg.HOST), ctx.ptr)
+            amg._check(hb(h._p, fh.data_ptr(), uh.data_ptr(), uh.data_ptr(), ctypes.byref(spc), ctypes.byref(stc),
+                          amg.HOST), ctx.ptr)
+        ctx.synchronize()
+        e_ms = (time.perf_counter() - e0) * 1e3 / K
+        e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": 8 * nnz + 16 * n,
+               "d2h_bytes_per_step": 8 * n, "timer": "host wall clock around the C-ABI calls (sync both sides)"}
+
+    # ---- CPU baseline (rank 0, N=1) ----
+    cpu = None
+    avg_it = float(np.mean(iters))
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            A0h = host_problem(g, a.problem, 0, a.nsteps)
+            k1 = 1 + W
+            Akh = host_problem(g, a.problem, k1 % a.nsteps, a.nsteps)
+            fh_np = f.cpu().numpy()
+            r = reference_sample(A0h, [Akh], fh_np, avg_it, 1)
+            cpu = {"value": r["value"], "unit": "ms/step", "cores": 1, "kind": "reference",
+                   "sample": (f"1 partial_update of step {k1} timed in full ({r['rebuild_ms']:.0f} ms) + fixed-V "
+                              f"BiCGStab timed for 2 iterations ({r['per_iteration_ms']:.0f} ms/iteration) x "
+                              f"{avg_it:.1f} iterations (this run's average); reference setup "
+                              f"{r['setup_s']:.1f} s untimed; unmodified reference, single-threaded as shipped")}
+        except Exception as e:  # never let the baseline kill the bench line
+            cpu = {"value": None, "unit": "ms/step", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        # record the per-step iteration count of this sequence for the reference arm
+        try:
+            os.makedirs(os.path.dirname(ITER_RECORD), exist_ok=True)
+            if not os.path.exists(ITER_RECORD):
+                json.dump({"workload": f"{a.problem} {g}^3 steps {1 + W}..{W + K}", "iterations": iters,
+                           "avg_iterations": avg_it}, open(ITER_RECORD, "w"))
+        except Exception:
+            pass
+        out = {"metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": world, "steps": K,
+               "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated dam-break sequence)",
+               "config": {"workload": f"C3 dam-break {g}^3, partial reuse (BASELINE.json configs[2])",
+                          "problem": a.problem, "grid": g, "n": n, "nnz": nnz, "sequence_steps": a.nsteps,
+                          "timed_steps": f"{1 + W}..{W + K}", "reuse": "partial", "smoother": "jacobi",
+                          "coarse_solve": a.coarse, "levels": h.num_levels(),
+                          "operator_complexity": h.operator_complexity(),
+                          "parallelism": "replicas" if world > 1 else "single",
+                          "l2": "inputs larger than L2 (A_k values 0.94 GB/step)"},
+               "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
+               "converged": all(conv), "setup_s": setup_s, "step0_iterations": st0.iterations,
+               "clocks": clk.summary(), "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
+               "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -17,8 +17,12 @@ struct amgr_hier {
 
 namespace amgr {
 
+static bool probe_match(const Ctx& c, const char* family) {
+    if (c.probe.family.empty() || c.probe.family != family) return false;
+    return c.probe.level < 0 || c.probe.level == c.cur_level;
+}
 void probe_begin(Ctx& c, const char* family, double bytes) {
-    if (c.probe.family.empty() || c.probe.family != family) return;
+    if (!probe_match(c, family)) return;
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
@@ -27,7 +31,7 @@ void probe_begin(Ctx& c, const char* family, double bytes) {
     c.probe.bytes.push_back(bytes);
 }
 void probe_end(Ctx& c, const char* family) {
-    if (c.probe.family.empty() || c.probe.family != family) return;
+    if (!probe_match(c, family)) return;
     CK(cudaEventRecord(c.probe.events.back().second, c.stream));
 }
 
@@ -423,7 +427,15 @@ amgr_status amgr_probe_enable(amgr_ctx* ctx, const char* family) {
         }
         ctx->c.probe.events.clear();
         ctx->c.probe.bytes.clear();
-        ctx->c.probe.family = family ? family : "";
+        std::string f = family ? family : "";
+        int level = -1;
+        const auto at = f.find('@');
+        if (at != std::string::npos) {
+            level = std::stoi(f.substr(at + 1));
+            f = f.substr(0, at);
+        }
+        ctx->c.probe.family = f;
+        ctx->c.probe.level = level;
     });
 }
 

@@ -40,6 +40,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // for the roofline probe (amgr_probe_enable).
 struct Probe {
     std::string family;                 // "" = disabled
+    int level = -1;                     // >= 0: only launches on this hierarchy level
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
     std::vector<double> bytes;
 };
@@ -56,6 +57,7 @@ struct Ctx {
     int64_t launches = 0;
     Probe probe;
     int num_sms = 148;
+    int cur_level = -1;  // hierarchy level the orchestration is currently launching for
 };
 
 #define LAUNCH(ctx, family, bytes, kernel, grid, block, smem, ...)                  \

@@ -201,6 +201,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     Work& W = work(h);
     const size_t L = h.lv.size();
     for (size_t i = 0; i + 1 < L; ++i) {
+        c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
         clk.begin(PH_SMOOTHER);
         build_smoother(c, A, h.prm, W.err.get() + i);
@@ -211,9 +212,11 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         rap_numeric(c, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz);
         clk.end(PH_GALERKIN);
     }
+    c.cur_level = static_cast<int>(L - 1);
     clk.begin(PH_COARSE);
     coarse_factorize(h, W.err.get() + L);
     clk.end(PH_COARSE);
+    c.cur_level = -1;
 }
 
 // Symbolic pass with frozen transfers (pattern change under partial reuse).
@@ -474,6 +477,7 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     if (pre >= 1) vc_premul(c, h.lv[0].pat->n, f, h.lv[0].w.get(), om, W.u[0].get(), g);
     // down leg
     for (size_t i = 0; i + 1 < L; ++i) {
+        c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
         double* a = W.u[i].get();  // holds u0 (premul / previous restriction) when pre >= 1
@@ -502,10 +506,12 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
                      next_smoothed ? h.lv[i + 1].w.get() : nullptr, om, next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
     // coarsest: direct solve (hierarchy.cpp:175)
+    c.cur_level = static_cast<int>(L - 1);
     coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
     ufinal[L - 1] = W.u[L - 1].get();
     // up leg
     for (size_t i = L - 1; i-- > 0;) {
+        c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
         double* a = cur[i];
@@ -526,6 +532,7 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
         }
         ufinal[i] = src;
     }
+    c.cur_level = -1;
 }
 
 // ---- BiCGStab (bicgstab.cpp:21-135) ------------------------------------------------
