@@ -196,20 +196,33 @@ void reset_err(Hier& h) {
 }
 
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans.
+// Level 0's smoother is rebuilt by its own kernel; for every coarser smoothed
+// level the Jacobi rebuild is fused into the Galerkin kernel that produces it
+// (its time is therefore booked under `galerkin`).
 void numeric_pass(Hier& h, PhaseClock& clk) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
+    const bool jacobi = h.prm.smoother != AMGR_SMOOTHER_SPAI0;
     for (size_t i = 0; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
-        clk.begin(PH_SMOOTHER);
-        build_smoother(c, A, h.prm, W.err.get() + i);
-        clk.end(PH_SMOOTHER);
+        if (i == 0 || !jacobi) {
+            clk.begin(PH_SMOOTHER);
+            build_smoother(c, A, h.prm, W.err.get() + i);
+            clk.end(PH_SMOOTHER);
+        }
         clk.begin(PH_GALERKIN);
         Level& B = h.lv[i + 1];
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
-        rap_numeric(c, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz);
+        const bool fuse = jacobi && i + 2 < L;
+        if (fuse) {
+            if (B.w.size() != B.pat->n) B.w.alloc(B.pat->n, c.stream);
+            B.has_smoother = true;
+        }
+        rap_numeric(c, A.pat->n, B.pat->n, B.pat->rp.get(), B.pat->diag.get(), A.rap->nnz_c, A.rap->cptr.get(),
+                    A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz, fuse ? B.w.get() : nullptr,
+                    W.err.get() + i + 1);
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
@@ -362,9 +375,10 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             P->diag.alloc(nc, c.stream);
             next.pat = P;
             next.val.alloc(s.nnz_c, c.stream);
-            rap_numeric(c, s.nnz_c, plan->cptr.get(), plan->contrib.get(), cur.val.get(), next.val.get(), Av.nnz);
             CsrView nv = next.view();
             find_diag(c, nv, P->diag.get());
+            rap_numeric(c, Av.n, nc, P->rp.get(), P->diag.get(), s.nnz_c, plan->cptr.get(), plan->contrib.get(),
+                        Av.val, next.val.get(), Av.nnz, nullptr, nullptr);
             P->max_span = max_group_span(c, P->rp.get(), P->n);
             cur.rap = plan;
         }

@@ -64,12 +64,12 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
                 DotSink s, Gate g = {});
 
 // ---- rebuild ---------------------------------------------------------------
-// Numeric Galerkin product on the cached plan: for every coarse entry c,
-//   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
-//     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
-// (two-level bracket of spmm(R, spmm(A, P)), csr.cpp:145-194)
-void rap_numeric(Ctx& c, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
-                 double* ac, int64_t nnz_f);
+// Numeric Galerkin product on the cached plan (two-level bracket of
+// spmm(R, spmm(A, P)), csr.cpp:145-194), coarse row group per warp.  With wc
+// != nullptr the coarse level's Jacobi weights 1/a_II are written too (fused
+// smoother rebuild; first bad row -> *bad).
+void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
+                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);

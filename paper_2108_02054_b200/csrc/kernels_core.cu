@@ -461,33 +461,70 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 }
 
 // ---- numeric RAP ----------------------------------------------------------
-__global__ void k_rap(int64_t nnz_c, const int* __restrict__ cptr, const int* __restrict__ contrib,
-                      const double* __restrict__ af, double* __restrict__ ac) {
-    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nnz_c;
-         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int p0 = __ldg(cptr + c), p1 = __ldg(cptr + c + 1);
-        double acc = 0.0, part = 0.0;
-        int p = p0;
-        for (; p + 2 <= p1; p += 2) {
-            const int e0 = __ldg(contrib + p), e1 = __ldg(contrib + p + 1);
-            const double v0 = __ldg(af + (e0 & 0x7fffffff)), v1 = __ldg(af + (e1 & 0x7fffffff));
-            part = dadd(part, v0);
-            if (e0 < 0) {
-                acc = dadd(acc, part);
-                part = 0.0;
+// Warp per 32-coarse-row group, groups dispatched in order (no grid-stride) so
+// the fine values gathered by all resident warps stay in a narrow L2 band.
+// Lanes take 32 consecutive coarse entries at a time; each entry replays the
+// reference's two-level bracket (csr.cpp:145-194):
+//   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
+//     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
+// The plan arrays and the output are streamed with evict-first hints.  When
+// the coarse level is smoothed next, its Jacobi rebuild (smoother.cpp:8-32,
+// inv_diag = 1.0/a_II) is fused: the lane owning row I picks the diagonal
+// entry's value out of the warp with a shuffle.
+__global__ void __launch_bounds__(128) k_rap(int nc, const int* __restrict__ crp, const int* __restrict__ cdiag,
+                                             const int* __restrict__ cptr, const int* __restrict__ contrib,
+                                             const double* __restrict__ af, double* __restrict__ ac,
+                                             double* __restrict__ wc, int* bad) {
+    const int lane = threadIdx.x & 31;
+    const int G = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int r0 = G * 32;
+    if (r0 >= nc) return;
+    const int row = r0 + lane;
+    const bool valid = row < nc;
+    const int dl = (wc && valid) ? __ldg(cdiag + row) : -1;
+    const int e0 = __ldg(crp + r0);
+    const int e1 = __ldg(crp + min(r0 + 32, nc));
+    if (wc && valid && dl < 0) atomicMin(bad, row);
+    for (int base = e0; base < e1; base += 32) {
+        const int e = base + lane;
+        double acc = 0.0;
+        if (e < e1) {
+            int p = __ldcs(cptr + e);
+            const int p1 = __ldcs(cptr + e + 1);
+            double part = 0.0;
+            for (; p + 2 <= p1; p += 2) {
+                const int q0 = __ldcs(contrib + p), q1 = __ldcs(contrib + p + 1);
+                const double v0 = __ldg(af + (q0 & 0x7fffffff)), v1 = __ldg(af + (q1 & 0x7fffffff));
+                part = dadd(part, v0);
+                if (q0 < 0) {
+                    acc = dadd(acc, part);
+                    part = 0.0;
+                }
+                part = dadd(part, v1);
+                if (q1 < 0) {
+                    acc = dadd(acc, part);
+                    part = 0.0;
+                }
             }
-            part = dadd(part, v1);
-            if (e1 < 0) {
-                acc = dadd(acc, part);
-                part = 0.0;
+            if (p < p1) {
+                const int q0 = __ldcs(contrib + p);
+                part = dadd(part, __ldg(af + (q0 & 0x7fffffff)));
+                if (q0 < 0) acc = dadd(acc, part);
+            }
+            __stcs(ac + e, acc);
+        }
+        if (wc) {
+            const int src = dl - base;
+            const double v = __shfl_sync(0xffffffffu, acc, src & 31);
+            if (dl >= 0 && src >= 0 && src < 32) {
+                if (v == 0.0) {
+                    atomicMin(bad, row);
+                    wc[row] = 0.0;
+                } else {
+                    wc[row] = __ddiv_rn(1.0, v);
+                }
             }
         }
-        if (p < p1) {
-            const int e0 = __ldg(contrib + p);
-            part = dadd(part, __ldg(af + (e0 & 0x7fffffff)));
-            if (e0 < 0) acc = dadd(acc, part);
-        }
-        ac[c] = acc;
     }
 }
 
@@ -867,11 +904,15 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
     launch_rowpass(c, "resid_norm", spmv_bytes(A), A, OpResidNorm{f, x, r, r2}, g, s, true);
 }
 
-void rap_numeric(Ctx& c, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
-                 double* ac, int64_t nnz_f) {
+void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
+                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad) {
     if (nnz_c == 0) return;
-    const double bytes = 12.0 * nnz_f + 12.0 * nnz_c;
-    LAUNCH(c, "rap", bytes, k_rap, grid_for(nnz_c, 256, c.num_sms * 32), 256, 0, nnz_c, cptr, contrib, af, ac);
+    // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1),
+    // plus the fused Jacobi rebuild of level i+1: 20*n_{i+1}
+    const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1) + (wc ? 20.0 * nc : 0.0);
+    const int64_t groups = (nc + 31) / 32;
+    LAUNCH(c, "rap", bytes, k_rap, grid_for(groups, 4), 128, 0, static_cast<int>(nc), crp, cdiag, cptr, contrib, af,
+           ac, wc, bad);
 }
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;

@@ -179,3 +179,83 @@ def test_errors_match_reference(ctx):
     S = (np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([1.0, 1.0, 1.0, 1.0]))
     with pytest.raises(amg.RuntimeFailure, match="singular"):
         amg.setup(S, ctx=ctx)
+
+
+@pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "random_300"])
+def test_inverse_coarse_mode_solve_parity(ctx, name):
+    """AMGR_COARSE_INVERSE (extension): same hierarchy bits, V-cycle within
+    1e-12 of the exact mode, solve within +-1 iteration of the reference."""
+    make, kw = CASES[name]
+    A = make()
+    he = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    hi = amg.setup(A, amg.AmgParams(coarse_solve="inverse", **kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    assert_same_hierarchy(hi, r)
+    f = np.random.default_rng(3).uniform(-1, 1, len(A[0]) - 1)
+    ue, ui = amg.vcycle(he, f), amg.vcycle(hi, f)
+    assert np.linalg.norm(ue - ui) <= 1e-12 * np.linalg.norm(ue)
+    fr = P.rhs(len(A[0]) - 1)
+    _, st = amg.bicgstab(hi, fr)
+    rs = ref.bicgstab(r, fr, fixed=True, prm=ref.params(**kw))
+    assert st.converged and abs(st.iterations - rs.iterations) <= 1
+
+
+def test_device_generator_matches_host(ctx):
+    """The device dam-break / Poisson generators (used by bench.py) produce the
+    same bits as the host restatement the parity tests feed the reference."""
+    import torch
+
+    L = amg.lib()
+    g = 20
+    n, nnz = g ** 3, int(L.amgr_problem_nnz(g))
+    rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    v = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    amg._check(L.amgr_problem_pattern(ctx.ptr, g, rp.data_ptr(), ci.data_ptr()), ctx.ptr)
+    for kind, k in (("dambreak", 0), ("dambreak", 31), ("poisson", 4), ("convdiff", 7)):
+        amg._check(L.amgr_problem_values(ctx.ptr, amg.PROBLEM[kind], g, k, 50, v.data_ptr()), ctx.ptr)
+        ctx.synchronize()
+        hrp, hci, hv = P.grid3d_values(kind, g, k, 50)
+        np.testing.assert_array_equal(rp.cpu().numpy(), hrp)
+        np.testing.assert_array_equal(ci.cpu().numpy(), hci)
+        if kind == "convdiff":  # exp() may differ in the last bit between libm and CUDA
+            np.testing.assert_allclose(v.cpu().numpy(), hv, rtol=1e-14)
+        else:
+            np.testing.assert_array_equal(v.cpu().numpy().view(np.int64), hv.view(np.int64))
+
+
+def test_rebuild_adopted_device_values(ctx):
+    import torch
+
+    A0 = P.grid3d_values("dambreak", 16, 2)
+    A1 = P.grid3d_values("dambreak", 16, 40)
+    h = amg.setup(A0, ctx=ctx)
+    buf = torch.zeros(len(A1[2]) + 8, dtype=torch.float64, device="cuda")
+    buf[: len(A1[2])] = torch.from_numpy(A1[2]).cuda()
+    torch.cuda.synchronize()
+    h.rebuild_values(buf.data_ptr(), adopt=True)
+    r = ref.partial_update(ref.setup(A0), A1)
+    assert_same_hierarchy(h, r)
+
+
+def test_cg_extension_converges(ctx):
+    from oracle import oracle as O
+
+    A = P.grid3d_values("poisson", 16, 0)
+    h = amg.setup(A, ctx=ctx)
+    f = P.rhs(16 ** 3)
+    u, st = amg.cg(h, f)
+    so = O.cg(O.setup(A), f)
+    assert st.converged and so.converged
+    assert abs(st.iterations - so.iterations) <= 1
+    res = np.linalg.norm(f - ref.spmv(A, u)) / np.linalg.norm(f)
+    assert res <= 1e-8
+
+
+def test_many_levels_and_launch_count(ctx):
+    A = P.grid3d_values("dambreak", 32, 10)
+    h = amg.setup(A, ctx=ctx)
+    l0 = ctx.launches()
+    amg.vcycle(h, P.rhs(32 ** 3))
+    assert ctx.launches() > l0 + 3 * (h.num_levels() - 1)
