@@ -306,7 +306,7 @@ amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, i
             amgr::d2h(col, t.get(), L.pat->nnz, c.stream);
             CK(cudaStreamSynchronize(c.stream));
         }
-        if (values) amgr::d2h(values, L.val.get(), L.pat->nnz, c.stream);
+        if (values) amgr::d2h(values, L.view().val, L.pat->nnz, c.stream);
         CK(cudaStreamSynchronize(c.stream));
     });
 }

@@ -461,22 +461,33 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 }
 
 // ---- numeric RAP ----------------------------------------------------------
-// Warp per 32-coarse-row group, groups dispatched in order (no grid-stride) so
-// the fine values gathered by all resident warps stay in a narrow L2 band.
-// Lanes take 32 consecutive coarse entries at a time; each entry replays the
-// reference's two-level bracket (csr.cpp:145-194):
+// Warp per 32-coarse-row group, groups dispatched in order so the fine values
+// gathered by all resident warps stay in a narrow L2 band.  The group's
+// contribution range [cptr[e0], cptr[e1]) is contiguous: in one pass the warp
+// streams it (coalesced, evict-first) and gathers the fine values it names
+// into shared memory, all loads in flight at once; then lanes take 32
+// consecutive coarse entries at a time and replay the reference's two-level
+// bracket (csr.cpp:145-194) from shared memory:
 //   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
 //     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
-// The plan arrays and the output are streamed with evict-first hints.  When
-// the coarse level is smoothed next, its Jacobi rebuild (smoother.cpp:8-32,
+// Groups with more than RAP_CAP contributions take the direct path.  When the
+// coarse level is smoothed next, its Jacobi rebuild (smoother.cpp:8-32,
 // inv_diag = 1.0/a_II) is fused: the lane owning row I picks the diagonal
 // entry's value out of the warp with a shuffle.
-__global__ void __launch_bounds__(128) k_rap(int nc, const int* __restrict__ crp, const int* __restrict__ cdiag,
-                                             const int* __restrict__ cptr, const int* __restrict__ contrib,
-                                             const double* __restrict__ af, double* __restrict__ ac,
-                                             double* __restrict__ wc, int* bad) {
-    const int lane = threadIdx.x & 31;
-    const int G = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+constexpr int RAP_WARPS = 4;
+constexpr int RAP_CAP = 1536;
+
+__global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int nc, const int* __restrict__ crp,
+                                                        const int* __restrict__ cdiag, const int* __restrict__ cptr,
+                                                        const int* __restrict__ contrib,
+                                                        const double* __restrict__ af, double* __restrict__ ac,
+                                                        double* __restrict__ wc, int* bad) {
+    extern __shared__ __align__(16) unsigned char rap_smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* sv = reinterpret_cast<double*>(rap_smem) + w * RAP_CAP;
+    unsigned* sf = reinterpret_cast<unsigned*>(reinterpret_cast<double*>(rap_smem) + RAP_WARPS * RAP_CAP) +
+                   w * (RAP_CAP / 32);
+    const int G = blockIdx.x * RAP_WARPS + w;
     const int r0 = G * 32;
     if (r0 >= nc) return;
     const int row = r0 + lane;
@@ -485,6 +496,37 @@ __global__ void __launch_bounds__(128) k_rap(int nc, const int* __restrict__ crp
     const int e0 = __ldg(crp + r0);
     const int e1 = __ldg(crp + min(r0 + 32, nc));
     if (wc && valid && dl < 0) atomicMin(bad, row);
+    const int q0 = __ldg(cptr + e0), q1 = __ldg(cptr + e1);
+    const bool staged = q1 - q0 <= RAP_CAP;
+    if (staged) {
+        // stage values (and the row-break bits) of the whole group
+        constexpr int PER = RAP_CAP / 32;
+        const int nq = q1 - q0;
+#pragma unroll 4
+        for (int t = 0; t < PER; t += 4) {
+            int qi[4];
+            double vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = lane + 32 * (t + u);
+                qi[u] = k < nq ? __ldcs(contrib + q0 + k) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = lane + 32 * (t + u);
+                vv[u] = k < nq ? __ldg(af + (qi[u] & 0x7fffffff)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = lane + 32 * (t + u);
+                if (k < nq) sv[k] = vv[u];
+                const unsigned bits = __ballot_sync(0xffffffffu, k < nq && qi[u] < 0);
+                if (lane == 0) sf[t + u] = bits;
+            }
+            if (32 * (t + 4) >= nq) break;
+        }
+        __syncwarp();
+    }
     for (int base = e0; base < e1; base += 32) {
         const int e = base + lane;
         double acc = 0.0;
@@ -492,24 +534,24 @@ __global__ void __launch_bounds__(128) k_rap(int nc, const int* __restrict__ crp
             int p = __ldcs(cptr + e);
             const int p1 = __ldcs(cptr + e + 1);
             double part = 0.0;
-            for (; p + 2 <= p1; p += 2) {
-                const int q0 = __ldcs(contrib + p), q1 = __ldcs(contrib + p + 1);
-                const double v0 = __ldg(af + (q0 & 0x7fffffff)), v1 = __ldg(af + (q1 & 0x7fffffff));
-                part = dadd(part, v0);
-                if (q0 < 0) {
-                    acc = dadd(acc, part);
-                    part = 0.0;
+            if (staged) {
+                for (; p < p1; ++p) {
+                    const int k = p - q0;
+                    part = dadd(part, sv[k]);
+                    if ((sf[k >> 5] >> (k & 31)) & 1u) {
+                        acc = dadd(acc, part);
+                        part = 0.0;
+                    }
                 }
-                part = dadd(part, v1);
-                if (q1 < 0) {
-                    acc = dadd(acc, part);
-                    part = 0.0;
+            } else {
+                for (; p < p1; ++p) {
+                    const int q = __ldcs(contrib + p);
+                    part = dadd(part, __ldg(af + (q & 0x7fffffff)));
+                    if (q < 0) {
+                        acc = dadd(acc, part);
+                        part = 0.0;
+                    }
                 }
-            }
-            if (p < p1) {
-                const int q0 = __ldcs(contrib + p);
-                part = dadd(part, __ldg(af + (q0 & 0x7fffffff)));
-                if (q0 < 0) acc = dadd(acc, part);
             }
             __stcs(ac + e, acc);
         }
@@ -911,8 +953,14 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdia
     // plus the fused Jacobi rebuild of level i+1: 20*n_{i+1}
     const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1) + (wc ? 20.0 * nc : 0.0);
     const int64_t groups = (nc + 31) / 32;
-    LAUNCH(c, "rap", bytes, k_rap, grid_for(groups, 4), 128, 0, static_cast<int>(nc), crp, cdiag, cptr, contrib, af,
-           ac, wc, bad);
+    constexpr size_t smem = static_cast<size_t>(RAP_WARPS) * RAP_CAP * 8 + RAP_WARPS * (RAP_CAP / 32) * 4;
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(k_rap, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = true;
+    }
+    LAUNCH(c, "rap", bytes, k_rap, grid_for(groups, RAP_WARPS), RAP_WARPS * 32, smem, static_cast<int>(nc), crp, cdiag,
+           cptr, contrib, af, ac, wc, bad);
 }
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
