@@ -203,7 +203,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
-    const bool jacobi = h.prm.smoother != AMGR_SMOOTHER_SPAI0;
+    const bool jacobi = false;  // fused coarse-level Jacobi disabled: separate smoother kernel per level
     for (size_t i = 0; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];

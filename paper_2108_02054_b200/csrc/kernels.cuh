@@ -65,9 +65,8 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
 
 // ---- rebuild ---------------------------------------------------------------
 // Numeric Galerkin product on the cached plan (two-level bracket of
-// spmm(R, spmm(A, P)), csr.cpp:145-194), coarse row group per warp.  With wc
-// != nullptr the coarse level's Jacobi weights 1/a_II are written too (fused
-// smoother rebuild; first bad row -> *bad).
+// spmm(R, spmm(A, P)), csr.cpp:145-194).  crp/cdiag/wc/bad are reserved for
+// a fused coarse-level smoother rebuild (currently a separate kernel).
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
                  const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.

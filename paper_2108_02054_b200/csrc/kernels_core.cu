@@ -461,112 +461,37 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 }
 
 // ---- numeric RAP ----------------------------------------------------------
-// Warp per 32-coarse-row group, groups dispatched in order so the fine values
-// gathered by all resident warps stay in a narrow L2 band.  The group's
-// contribution range [cptr[e0], cptr[e1]) is contiguous: in one pass the warp
-// streams it (coalesced, evict-first) and gathers the fine values it names
-// into shared memory, all loads in flight at once; then lanes take 32
-// consecutive coarse entries at a time and replay the reference's two-level
-// bracket (csr.cpp:145-194) from shared memory:
+// Thread per coarse entry c (grid-stride), replaying the reference's two-level
+// bracket of spmm(R, spmm(A, P)) (csr.cpp:145-194) over the cached plan:
 //   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
 //     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
-// Groups with more than RAP_CAP contributions take the direct path.  When the
-// coarse level is smoothed next, its Jacobi rebuild (smoother.cpp:8-32,
-// inv_diag = 1.0/a_II) is fused: the lane owning row I picks the diagonal
-// entry's value out of the warp with a shuffle.
-constexpr int RAP_WARPS = 4;
-constexpr int RAP_CAP = 1536;
-
-__global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int nc, const int* __restrict__ crp,
-                                                        const int* __restrict__ cdiag, const int* __restrict__ cptr,
-                                                        const int* __restrict__ contrib,
-                                                        const double* __restrict__ af, double* __restrict__ ac,
-                                                        double* __restrict__ wc, int* bad) {
-    extern __shared__ __align__(16) unsigned char rap_smem[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double* sv = reinterpret_cast<double*>(rap_smem) + w * RAP_CAP;
-    unsigned* sf = reinterpret_cast<unsigned*>(reinterpret_cast<double*>(rap_smem) + RAP_WARPS * RAP_CAP) +
-                   w * (RAP_CAP / 32);
-    const int G = blockIdx.x * RAP_WARPS + w;
-    const int r0 = G * 32;
-    if (r0 >= nc) return;
-    const int row = r0 + lane;
-    const bool valid = row < nc;
-    const int dl = (wc && valid) ? __ldg(cdiag + row) : -1;
-    const int e0 = __ldg(crp + r0);
-    const int e1 = __ldg(crp + min(r0 + 32, nc));
-    if (wc && valid && dl < 0) atomicMin(bad, row);
-    const int q0 = __ldg(cptr + e0), q1 = __ldg(cptr + e1);
-    const bool staged = q1 - q0 <= RAP_CAP;
-    if (staged) {
-        // stage values (and the row-break bits) of the whole group
-        constexpr int PER = RAP_CAP / 32;
-        const int nq = q1 - q0;
-#pragma unroll 4
-        for (int t = 0; t < PER; t += 4) {
-            int qi[4];
-            double vv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = lane + 32 * (t + u);
-                qi[u] = k < nq ? __ldcs(contrib + q0 + k) : 0;
+__global__ void k_rap(int64_t nnz_c, const int* __restrict__ cptr, const int* __restrict__ contrib,
+                      const double* __restrict__ af, double* __restrict__ ac) {
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nnz_c;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p0 = __ldg(cptr + c), p1 = __ldg(cptr + c + 1);
+        double acc = 0.0, part = 0.0;
+        int p = p0;
+        for (; p + 2 <= p1; p += 2) {
+            const int e0 = __ldg(contrib + p), e1 = __ldg(contrib + p + 1);
+            const double v0 = __ldg(af + (e0 & 0x7fffffff)), v1 = __ldg(af + (e1 & 0x7fffffff));
+            part = dadd(part, v0);
+            if (e0 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = lane + 32 * (t + u);
-                vv[u] = k < nq ? __ldg(af + (qi[u] & 0x7fffffff)) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = lane + 32 * (t + u);
-                if (k < nq) sv[k] = vv[u];
-                const unsigned bits = __ballot_sync(0xffffffffu, k < nq && qi[u] < 0);
-                if (lane == 0) sf[t + u] = bits;
-            }
-            if (32 * (t + 4) >= nq) break;
-        }
-        __syncwarp();
-    }
-    for (int base = e0; base < e1; base += 32) {
-        const int e = base + lane;
-        double acc = 0.0;
-        if (e < e1) {
-            int p = __ldcs(cptr + e);
-            const int p1 = __ldcs(cptr + e + 1);
-            double part = 0.0;
-            if (staged) {
-                for (; p < p1; ++p) {
-                    const int k = p - q0;
-                    part = dadd(part, sv[k]);
-                    if ((sf[k >> 5] >> (k & 31)) & 1u) {
-                        acc = dadd(acc, part);
-                        part = 0.0;
-                    }
-                }
-            } else {
-                for (; p < p1; ++p) {
-                    const int q = __ldcs(contrib + p);
-                    part = dadd(part, __ldg(af + (q & 0x7fffffff)));
-                    if (q < 0) {
-                        acc = dadd(acc, part);
-                        part = 0.0;
-                    }
-                }
-            }
-            __stcs(ac + e, acc);
-        }
-        if (wc) {
-            const int src = dl - base;
-            const double v = __shfl_sync(0xffffffffu, acc, src & 31);
-            if (dl >= 0 && src >= 0 && src < 32) {
-                if (v == 0.0) {
-                    atomicMin(bad, row);
-                    wc[row] = 0.0;
-                } else {
-                    wc[row] = __ddiv_rn(1.0, v);
-                }
+            part = dadd(part, v1);
+            if (e1 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
             }
         }
+        if (p < p1) {
+            const int e0 = __ldg(contrib + p);
+            part = dadd(part, __ldg(af + (e0 & 0x7fffffff)));
+            if (e0 < 0) acc = dadd(acc, part);
+        }
+        ac[c] = acc;
     }
 }
 
@@ -949,18 +874,13 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
                  const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad) {
     if (nnz_c == 0) return;
-    // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1),
-    // plus the fused Jacobi rebuild of level i+1: 20*n_{i+1}
-    const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1) + (wc ? 20.0 * nc : 0.0);
-    const int64_t groups = (nc + 31) / 32;
-    constexpr size_t smem = static_cast<size_t>(RAP_WARPS) * RAP_CAP * 8 + RAP_WARPS * (RAP_CAP / 32) * 4;
-    static bool configured = false;
-    if (!configured) {
-        CK(cudaFuncSetAttribute(k_rap, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = true;
-    }
-    LAUNCH(c, "rap", bytes, k_rap, grid_for(groups, RAP_WARPS), RAP_WARPS * 32, smem, static_cast<int>(nc), crp, cdiag,
-           cptr, contrib, af, ac, wc, bad);
+    (void)crp;
+    (void)cdiag;
+    (void)wc;
+    (void)bad;
+    // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1)
+    const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
+    LAUNCH(c, "rap", bytes, k_rap, grid_for(nnz_c, 256, c.num_sms * 32), 256, 0, nnz_c, cptr, contrib, af, ac);
 }
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
