@@ -196,6 +196,51 @@ amgr_status amgr_cg(amgr_hier* h, const double* f, const double* u0, double* u,
 /* y = A_level x (spmv, csr.hpp:77 / csr.cpp:76-85) on one level. */
 amgr_status amgr_spmv(amgr_hier* h, int level, const double* x, double* y, int location);
 
+/* ---- reuse driver (proj/include/amgreuse/reuse.hpp:13-81, src/reuse.cpp) -- */
+/* StrategyKind (reuse.hpp:13) */
+enum { AMGR_REUSE_NONE = 0, AMGR_REUSE_FULL = 1, AMGR_REUSE_PARTIAL = 2 };
+/* StepAction (reuse.hpp:31) */
+enum { AMGR_ACTION_FULL_BUILD = 0, AMGR_ACTION_PARTIAL_UPDATE = 1, AMGR_ACTION_REUSED_UNCHANGED = 2 };
+
+/* StrategyConfig (reuse.hpp:20-28).  rebuild_every <= 0 means "absent". */
+typedef struct amgr_strategy {
+    int32_t kind;
+    int32_t pad;
+    int64_t reuse_iter_limit;
+    int64_t rebuild_every;
+} amgr_strategy;
+
+/* StepMetrics (reuse.hpp:33-41); times in seconds (CUDA events on the stream). */
+typedef struct amgr_step_metrics {
+    int64_t step;
+    double setup_time;
+    double solve_time;
+    int64_t iterations;
+    int32_t converged;
+    int32_t action;
+    amgr_phase_timings phase_timings;
+} amgr_step_metrics;
+
+/* ProblemSequence::step(k) (sequence.hpp:11-23): fill *A and *rhs for step k
+ * (host or device buffers, valid until the next call).  Return 0 on success. */
+typedef int (*amgr_step_fn)(void* user, int64_t k, amgr_csr* A, const double** rhs, int32_t* rhs_location);
+/* Optional per-step solution sink: u has n entries on the device. */
+typedef void (*amgr_solution_fn)(void* user, int64_t k, const double* u_device, int64_t n);
+
+/* Replaces `RunResult run_sequence(const ProblemSequence&, const StrategyConfig&,
+ * const AmgParams&, const SolveParams&)` (reuse.hpp:70-71, reuse.cpp:46-136):
+ * same actions, chaining of the previous solution as the initial guess, the
+ * full-reuse rebuild flag, the dimension-change fallback.  metrics: nsteps
+ * entries.  Solver non-convergence is recorded, not raised. */
+amgr_status amgr_run_sequence(amgr_ctx* ctx, int64_t nsteps, amgr_step_fn step, void* user,
+                              const amgr_strategy* strategy, const amgr_amg_params* amg,
+                              const amgr_solve_params* solve, amgr_step_metrics* metrics,
+                              amgr_solution_fn sink, void* sink_user);
+
+/* speedup_percent (reuse.cpp:138-147): (t_base / t_other - 1) * 100, +inf
+ * when t_other == 0. */
+double amgr_speedup_percent(double t_base, double t_other);
+
 /* ---- introspection / download (parity dumps) ----------------------------- */
 /* Number of levels, finest first (Hierarchy::num_levels, hierarchy.hpp:54). */
 int amgr_hier_num_levels(const amgr_hier* h);
@@ -247,6 +292,9 @@ amgr_status amgr_problem_rhs(amgr_ctx* ctx, int64_t n, uint64_t seed, double* ou
  * and the algorithmic bytes those launches moved. */
 amgr_status amgr_probe_enable(amgr_ctx* ctx, const char* family);
 amgr_status amgr_probe_read(amgr_ctx* ctx, int64_t* launches, double* ms, double* bytes);
+/* Stream-ordered device -> host copy on the context stream (synchronous). */
+amgr_status amgr_copy_to_host(amgr_ctx* ctx, void* host, const void* device, size_t bytes);
+
 /* Number of kernel launches the library issued on this context so far. */
 int64_t amgr_launch_count(const amgr_ctx* ctx);
 

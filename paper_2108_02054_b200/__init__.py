@@ -126,6 +126,9 @@ PROTOTYPES = {
     "amgr_probe_enable": (_I, [_V, C.c_char_p]),
     "amgr_probe_read": (_I, [_V, _P(_L), _P(_D), _P(_D)]),
     "amgr_launch_count": (_L, [_V]),
+    "amgr_copy_to_host": (_I, [_V, _V, _V, C.c_size_t]),
+    "amgr_run_sequence": (_I, [_V, _L, _V, _V, _V, _V, _V, _V, _V, _V]),
+    "amgr_speedup_percent": (_D, [_D, _D]),
 }
 
 _lib = None
@@ -486,5 +489,6 @@ def cg(h: Hierarchy, f, u0=None, prm: SolveParams | None = None):
 
 
 def run_sequence(*args, **kwargs):
+    """RunResult run_sequence(systems, StrategyConfig, AmgParams, SolveParams) — reuse.hpp:70-71."""
     from .reuse import run_sequence as _rs
     return _rs(*args, **kwargs)

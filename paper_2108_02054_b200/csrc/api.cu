@@ -8,9 +8,6 @@
 
 #include "hierarchy.cuh"
 
-struct amgr_ctx {
-    amgr::Ctx c;
-};
 struct amgr_hier {
     std::unique_ptr<amgr::Hier> h;
 };
@@ -453,6 +450,14 @@ amgr_status amgr_probe_read(amgr_ctx* ctx, int64_t* launches, double* ms, double
         if (launches) *launches = static_cast<int64_t>(ctx->c.probe.events.size());
         if (ms) *ms = t;
         if (bytes) *bytes = b;
+    });
+}
+
+amgr_status amgr_copy_to_host(amgr_ctx* ctx, void* host, const void* device, size_t bytes) {
+    if (!ctx || (!host && bytes)) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] {
+        if (bytes) CK(cudaMemcpyAsync(host, device, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
+        CK(cudaStreamSynchronize(ctx->c.stream));
     });
 }
 

@@ -169,3 +169,8 @@ enum : int {
 };
 
 }  // namespace amgr
+
+// Opaque C-ABI context handle (include/amgr.h): wraps the library context.
+struct amgr_ctx {
+    amgr::Ctx c;
+};

@@ -1,0 +1,225 @@
+"""Reuse driver — mirror of the reference's run_sequence / RunReport API
+(proj/include/amgreuse/reuse.hpp:13-81, proj/src/reuse.cpp) over
+`amgr_run_sequence`.  The per-step loop (action choice, setup / in-place
+partial update, BiCGStab from the previous solution, the full-reuse rebuild
+flag) runs in the library's C++; Python only adapts the problem sequence.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import (AmgParams, Context, CsrMatrix, DeviceCsr, InvalidArgument, PhaseTimings, SolveParams, _check,
+               _Csr, _SolveParams, _Timings, default_context, lib)
+
+
+class StrategyKind(enum.IntEnum):
+    """reuse.hpp:13"""
+    none = 0
+    full = 1
+    partial = 2
+
+
+def strategy_kind_from_string(name: str) -> StrategyKind:
+    """reuse.cpp:31-36"""
+    try:
+        return StrategyKind[name]
+    except KeyError:
+        raise InvalidArgument(f"unknown strategy '{name}' (expected none, full or partial)") from None
+
+
+class StepAction(enum.IntEnum):
+    """reuse.hpp:31"""
+    full_build = 0
+    partial_update = 1
+    reused_unchanged = 2
+
+
+@dataclass
+class StrategyConfig:
+    """reuse.hpp:20-28"""
+    kind: StrategyKind = StrategyKind.none
+    reuse_iter_limit: int = 0
+    rebuild_every: int | None = None
+
+
+@dataclass
+class StepMetrics:
+    """reuse.hpp:33-41"""
+    step: int
+    setup_time: float
+    solve_time: float
+    iterations: int
+    converged: bool
+    action: StepAction
+    phase_timings: PhaseTimings
+
+
+@dataclass
+class RunReport:
+    """reuse.hpp:43-50"""
+    strategy: StrategyConfig
+    steps: list = field(default_factory=list)
+    total_setup: float = 0.0
+    total_solve: float = 0.0
+    full_rebuilds: int = 0
+    avg_iterations: float = 0.0
+
+
+@dataclass
+class RunResult:
+    solutions: list
+    report: RunReport
+
+
+class _Strategy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("reuse_iter_limit", C.c_int64),
+                ("rebuild_every", C.c_int64)]
+
+
+class _StepMetrics(C.Structure):
+    _fields_ = [("step", C.c_int64), ("setup_time", C.c_double), ("solve_time", C.c_double),
+                ("iterations", C.c_int64), ("converged", C.c_int32), ("action", C.c_int32),
+                ("phase_timings", _Timings)]
+
+
+STEP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(_Csr), C.POINTER(C.c_void_p), C.POINTER(C.c_int32))
+SINK_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64)
+
+
+def run_sequence(systems, strategy: StrategyConfig, amg: AmgParams | None = None, solve: SolveParams | None = None,
+                 ctx: Context | None = None, keep_solutions: bool = True) -> RunResult:
+    """RunResult run_sequence(const ProblemSequence&, const StrategyConfig&,
+    const AmgParams&, const SolveParams&) — reuse.hpp:70-71.
+
+    `systems` needs size() and step(k) -> (A, rhs); A is a host CSR tuple /
+    CsrMatrix or a DeviceCsr, rhs a numpy array or a device pointer (int)."""
+    ctx = ctx or default_context()
+    amg = amg or AmgParams()
+    solve = solve or SolveParams()
+    if strategy.rebuild_every is not None and strategy.rebuild_every < 1:
+        raise InvalidArgument("run_sequence: rebuild_every must be >= 1")
+    n_steps = systems.size()
+    keep = {}
+    solutions = []
+    errors = []
+
+    def step_cb(_user, k, a_out, rhs_out, loc_out):
+        try:
+            A, rhs = systems.step(int(k))
+            A = A if isinstance(A, DeviceCsr) else CsrMatrix.of(A)
+            if isinstance(rhs, int):
+                rhs_ptr, loc = rhs, 1
+            else:
+                rhs = np.ascontiguousarray(rhs, np.float64)
+                if len(rhs) != A.nrows:
+                    raise InvalidArgument("run_sequence: RHS length does not match matrix size")
+                rhs_ptr, loc = rhs.ctypes.data, 0
+            keep["A"], keep["rhs"] = A, rhs
+            a_out[0] = A._c()
+            rhs_out[0] = rhs_ptr
+            loc_out[0] = loc
+            return 0
+        except Exception as e:  # surfaced after the call
+            errors.append(e)
+            return 1
+
+    def sink_cb(_user, k, u_dev, n):
+        host = np.empty(int(n))
+        _check(lib().amgr_copy_to_host(ctx.ptr, host.ctypes.data, u_dev, 8 * int(n)), ctx.ptr)
+        solutions.append(host)
+
+    step_fn = STEP_FN(step_cb)
+    sink_fn = SINK_FN(sink_cb) if keep_solutions else SINK_FN()
+    st = _Strategy(int(strategy.kind), 0, strategy.reuse_iter_limit,
+                   strategy.rebuild_every if strategy.rebuild_every is not None else 0)
+    metrics = (_StepMetrics * n_steps)()
+    p = amg._c()
+    sp = _SolveParams(solve.tol, solve.max_iter)
+    rc = lib().amgr_run_sequence(ctx.ptr, n_steps, step_fn, None, C.byref(st), C.byref(p), C.byref(sp), metrics,
+                                 sink_fn, None)
+    if errors:
+        raise errors[0]
+    _check(rc, ctx.ptr)
+    rep = RunReport(strategy=strategy)
+    for m in metrics:
+        pt = m.phase_timings
+        rep.steps.append(StepMetrics(int(m.step), m.setup_time, m.solve_time, int(m.iterations), bool(m.converged),
+                                     StepAction(m.action),
+                                     PhaseTimings(pt.transfer_ops, pt.galerkin, pt.smoother, pt.coarse_solver)))
+    # totals (reuse.cpp:126-134)
+    rep.total_setup = sum(s.setup_time for s in rep.steps)
+    rep.total_solve = sum(s.solve_time for s in rep.steps)
+    rep.full_rebuilds = sum(1 for s in rep.steps if s.action == StepAction.full_build)
+    rep.avg_iterations = sum(s.iterations for s in rep.steps) / len(rep.steps)
+    return RunResult(solutions, rep)
+
+
+class SpeedupBasis(enum.IntEnum):
+    total = 0
+    setup = 1
+
+
+def speedup_percent(base: RunReport, other: RunReport, which: SpeedupBasis = SpeedupBasis.total) -> float:
+    """reuse.cpp:138-147: (t_base / t_other - 1) * 100, +inf when t_other == 0."""
+    if len(base.steps) != len(other.steps):
+        raise InvalidArgument("speedup_percent: reports cover different step counts")
+    tb = base.total_setup + (base.total_solve if which == SpeedupBasis.total else 0.0)
+    to = other.total_setup + (other.total_solve if which == SpeedupBasis.total else 0.0)
+    return float(lib().amgr_speedup_percent(tb, to))
+
+
+def speedup_from_times(t_base: float, t_other: float) -> float:
+    return math.inf if t_other == 0.0 else (t_base / t_other - 1.0) * 100.0
+
+
+def full_build_phase_totals(report: RunReport) -> PhaseTimings:
+    """reuse.cpp:149-154"""
+    t = PhaseTimings()
+    for s in report.steps:
+        if s.action == StepAction.full_build:
+            t.transfer_ops += s.phase_timings.transfer_ops
+            t.galerkin += s.phase_timings.galerkin
+            t.smoother += s.phase_timings.smoother
+            t.coarse_solver += s.phase_timings.coarse_solver
+    return t
+
+
+class DeviceGridSequence:
+    """ProblemSequence (sequence.hpp:17-23) generated on the device: the 3D
+    synthetic sequences of SURVEY.md 8(d) (poisson / blob / dambreak /
+    convdiff), fixed RHS U(0.1, 1) from std::mt19937_64(seed)."""
+
+    def __init__(self, kind: str, g: int, steps: int, seed: int = 42, ctx: Context | None = None):
+        import torch
+
+        from . import DEVICE, PROBLEM
+
+        self.ctx = ctx or default_context()
+        self.kind, self.g, self.steps = PROBLEM[kind], g, steps
+        L = lib()
+        n, nnz = g ** 3, int(L.amgr_problem_nnz(g))
+        self.n, self.nnz = n, nnz
+        dev = torch.device("cuda", self.ctx.device)
+        self.rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        self.ci = torch.empty(nnz + 8, dtype=torch.int32, device=dev)
+        self.v = torch.empty(nnz + 8, dtype=torch.float64, device=dev)
+        self.f = torch.empty(n, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        _check(L.amgr_problem_pattern(self.ctx.ptr, g, self.rp.data_ptr(), self.ci.data_ptr()), self.ctx.ptr)
+        _check(L.amgr_problem_rhs(self.ctx.ptr, n, seed, self.f.data_ptr(), DEVICE), self.ctx.ptr)
+        self.ctx.synchronize()
+
+    def size(self) -> int:
+        return self.steps
+
+    def step(self, k: int):
+        L = lib()
+        _check(L.amgr_problem_values(self.ctx.ptr, self.kind, self.g, k, self.steps, self.v.data_ptr()), self.ctx.ptr)
+        self.ctx.synchronize()
+        return DeviceCsr(self.n, self.n, self.nnz, self.rp.data_ptr(), self.ci.data_ptr(), self.v.data_ptr()), \
+            self.f.data_ptr()

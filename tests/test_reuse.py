@@ -1,0 +1,115 @@
+"""Reuse driver (run_sequence, reuse.cpp:46-154).  CPU: speedup arithmetic
+(SPEC.md Table-2 examples).  GPU: the device driver against the restated
+run_sequence over the C oracle on the same host sequences."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import problems as P
+
+
+def test_speedup_arithmetic_table2():
+    import paper_2108_02054_b200 as amg
+
+    L = amg.lib()
+    # SPEC.md:411-423 / PAPER.md Table 2 level-set OpenMP row
+    assert L.amgr_speedup_percent(1.235, 0.021) == pytest.approx(5781.0, abs=1.0)
+    assert L.amgr_speedup_percent(1.235 + 2.893, 0.021 + 3.132) == pytest.approx(31.0, abs=1.0)
+    assert L.amgr_speedup_percent(1.235 + 2.893, 0.423 + 2.794) == pytest.approx(28.0, abs=1.0)
+    assert L.amgr_speedup_percent(2.0, 2.0) == 0.0
+    assert math.isinf(L.amgr_speedup_percent(1.0, 0.0))
+
+
+class HostSeq:
+    def __init__(self, mats, rhs):
+        self.mats, self.rhs = mats, rhs
+
+    def size(self):
+        return len(self.mats)
+
+    def step(self, k):
+        return self.mats[k], self.rhs[k] if isinstance(self.rhs, list) else self.rhs
+
+
+def dambreak_seq(g, ks):
+    return HostSeq([P.grid3d_values("dambreak", g, k) for k in ks], P.rhs(g ** 3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,extra", [("none", {}), ("partial", {}), ("partial", {"rebuild_every": 2}),
+                                        ("full", {}), ("full", {"reuse_iter_limit": 10})])
+def test_run_sequence_matches_oracle(ctx, kind, extra):
+    import paper_2108_02054_b200 as amg
+    from paper_2108_02054_b200 import reuse as R
+    from oracle import reuse_oracle as RO
+
+    seq = dambreak_seq(14, [0, 10, 20, 30, 40, 49])
+    st = R.StrategyConfig(R.StrategyKind[kind], extra.get("reuse_iter_limit", 0), extra.get("rebuild_every"))
+    res = R.run_sequence(seq, st, ctx=ctx)
+    ref = RO.run_sequence(seq, kind, extra.get("reuse_iter_limit", 0), extra.get("rebuild_every"))
+    assert [int(s.action) for s in res.report.steps] == [r[0] for r in ref]
+    for s, r in zip(res.report.steps, ref):
+        assert abs(s.iterations - r[1]) <= 1 and s.converged == r[2]
+    for u, r, k in zip(res.solutions, ref, range(6)):
+        A = seq.mats[k]
+        res_true = np.linalg.norm(seq.rhs - P_spmv(A, u)) / np.linalg.norm(seq.rhs)
+        assert res_true <= 1e-8
+    rep = res.report
+    assert rep.full_rebuilds == sum(1 for s in rep.steps if s.action == R.StepAction.full_build)
+    assert rep.avg_iterations == pytest.approx(np.mean([s.iterations for s in rep.steps]))
+    if kind == "none":
+        assert rep.full_rebuilds == 6
+    if kind == "partial" and not extra:
+        assert rep.full_rebuilds == 1
+        assert all(s.phase_timings.transfer_ops == 0.0 for s in rep.steps[1:])
+
+
+def P_spmv(A, x):
+    from oracle import ref
+
+    return ref.spmv(A, x)
+
+
+@pytest.mark.gpu
+def test_constant_sequence_partial_identical_iterations(ctx):
+    from paper_2108_02054_b200 import reuse as R
+
+    A = P.grid3d_values("dambreak", 12, 5)
+    f = P.rhs(12 ** 3)
+    seq = HostSeq([A] * 4, [f, f * 1.5, f * 0.5, f])  # fresh solves: vary the RHS
+    res = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.partial), ctx=ctx)
+    assert [s.action for s in res.report.steps] == [R.StepAction.full_build] + [R.StepAction.partial_update] * 3
+    res_full = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.full, reuse_iter_limit=100), ctx=ctx)
+    assert res_full.report.full_rebuilds == 1
+
+
+@pytest.mark.gpu
+def test_dimension_change_falls_back_to_full_build(ctx):
+    from paper_2108_02054_b200 import reuse as R
+
+    seq = HostSeq([P.grid3d_values("poisson", 10, 0), P.grid3d_values("poisson", 11, 1),
+                   P.grid3d_values("poisson", 11, 2)], None)
+    seq.rhs = None
+
+    class S(HostSeq):
+        def step(self, k):
+            A = self.mats[k]
+            return A, P.rhs(len(A[0]) - 1)
+
+    s = S(seq.mats, None)
+    res = R.run_sequence(s, R.StrategyConfig(R.StrategyKind.partial), ctx=ctx)
+    assert [s_.action for s_ in res.report.steps] == [R.StepAction.full_build, R.StepAction.full_build,
+                                                      R.StepAction.partial_update]
+
+
+@pytest.mark.gpu
+def test_device_generated_sequence(ctx):
+    from paper_2108_02054_b200 import reuse as R
+
+    seq = R.DeviceGridSequence("dambreak", 24, 4, ctx=ctx)
+    res = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.partial), ctx=ctx, keep_solutions=False)
+    assert res.report.full_rebuilds == 1 and all(s.converged for s in res.report.steps)
+    base = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.none), ctx=ctx, keep_solutions=False)
+    assert base.report.full_rebuilds == 4
+    assert R.speedup_percent(base.report, res.report, R.SpeedupBasis.setup) > 0.0
