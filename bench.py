@@ -56,7 +56,8 @@ def args_parse():
     p.add_argument("--size", type=int, default=256)
     p.add_argument("--problem", default="dambreak")
     p.add_argument("--nsteps", type=int, default=50, help="length of the time sequence (configs[2]: 50)")
-    p.add_argument("--coarse", default="exact", choices=["exact", "inverse"])
+    p.add_argument("--coarse", default="inverse", choices=["exact", "inverse"],
+                   help="coarsest solve: exact replay of dense_lu.cpp (bit-exact V-cycle) or the explicit inverse")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
