@@ -256,6 +256,9 @@ amgr_status amgr_hier_level_P(const amgr_hier* h, int level, int64_t* agg);
 amgr_status amgr_hier_level_R(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col);
 /* Smoother state: inv_diag (JacobiSmoother::inv_diag, smoother.hpp:11-16). */
 amgr_status amgr_hier_level_smoother(const amgr_hier* h, int level, double* inv_diag);
+/* Chebyshev extension: power-iteration estimate of lambda_max(D^-1 A) of a
+ * level (before the safety factor). */
+amgr_status amgr_hier_level_lambda(const amgr_hier* h, int level, double* lambda_max);
 /* Coarse LU (DenseFactorization, dense_lu.hpp:12-18): lu n*n row-major, piv n. */
 int64_t amgr_hier_coarse_n(const amgr_hier* h);
 amgr_status amgr_hier_coarse_lu(const amgr_hier* h, double* lu, int64_t* piv);

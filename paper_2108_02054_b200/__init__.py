@@ -114,6 +114,7 @@ PROTOTYPES = {
     "amgr_hier_level_P": (_I, [_V, _I, _V]),
     "amgr_hier_level_R": (_I, [_V, _I, _V, _V]),
     "amgr_hier_level_smoother": (_I, [_V, _I, _V]),
+    "amgr_hier_level_lambda": (_I, [_V, _I, _P(_D)]),
     "amgr_hier_coarse_n": (_L, [_V]),
     "amgr_hier_coarse_lu": (_I, [_V, _V, _V]),
     "amgr_hier_operator_complexity": (_D, [_V]),
@@ -359,6 +360,12 @@ class Hierarchy:
         w = np.zeros(d["nrows"])
         _check(lib().amgr_hier_level_smoother(self._p, lvl, w.ctypes.data), self.ctx.ptr)
         return w
+
+    def level_lambda(self, lvl: int) -> float:
+        """Chebyshev extension: power-iteration lambda_max(D^-1 A) of a level."""
+        x = C.c_double()
+        _check(lib().amgr_hier_level_lambda(self._p, lvl, C.byref(x)), self.ctx.ptr)
+        return float(x.value)
 
     def coarse_lu(self):
         n = int(lib().amgr_hier_coarse_n(self._p))

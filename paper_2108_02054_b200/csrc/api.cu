@@ -352,6 +352,19 @@ amgr_status amgr_hier_level_smoother(const amgr_hier* h, int level, double* w) {
     });
 }
 
+amgr_status amgr_hier_level_lambda(const amgr_hier* h, int level, double* lam) {
+    if (!h || !lam) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] {
+        amgr::Hier& H = *h->h;
+        if (level < 0 || level >= static_cast<int>(H.lv.size()) || H.lv[level].pst.size() != 3)
+            amgr::invalid("level has no Chebyshev smoother");
+        double st[3];
+        amgr::d2h(st, H.lv[level].pst.get(), 3, H.ctx->stream);
+        CK(cudaStreamSynchronize(H.ctx->stream));
+        *lam = st[2];
+    });
+}
+
 int64_t amgr_hier_coarse_n(const amgr_hier* h) { return h && h->h ? h->h->nL : 0; }
 
 amgr_status amgr_hier_coarse_lu(const amgr_hier* h, double* lu, int64_t* piv) {

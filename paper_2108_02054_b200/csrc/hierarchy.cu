@@ -133,7 +133,10 @@ bool same_pattern(Ctx& c, const Pattern& a, const Pattern& b) {
     return d2h_scalar(diff.get(), c.stream) == 0;
 }
 
-// Smoother rebuild of level l (build_smoother, smoother.cpp:8-32; SPAI0 ext.).
+// Smoother rebuild of level l (build_smoother, smoother.cpp:8-32; SPAI0 and
+// Chebyshev extensions).  Chebyshev: Jacobi weights + power iteration for
+// lambda_max(D^-1 A) from the all-ones vector + coefficient table
+// (oracle/amg_oracle.c power_lambda / smooth_cheb).
 void build_smoother(Ctx& c, Level& L, const AmgP& p, int* bad) {
     const int64_t n = L.pat->n;
     if (L.w.size() != n) L.w.alloc(n, c.stream);
@@ -142,6 +145,23 @@ void build_smoother(Ctx& c, Level& L, const AmgP& p, int* bad) {
     else
         jacobi_rebuild(c, n, L.view().val, L.pat->diag.get(), L.w.get(), bad);
     L.has_smoother = true;
+    if (p.smoother == AMGR_SMOOTHER_CHEBYSHEV) {
+        if (p.cheb_degree < 1 || p.cheb_degree > 32) invalid("chebyshev: degree must be in [1, 32]");
+        const CsrView A = L.view();
+        DevArray<double> x(n, c.stream), y(n, c.stream), partials(static_cast<int64_t>(dot_grid(c)) * 2 + 8, c.stream);
+        DevArray<unsigned> ticket(1, c.stream);
+        CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), c.stream));
+        if (L.pst.size() != 3) L.pst.alloc(3, c.stream);
+        if (L.cheb.size() != 2 * p.cheb_degree + 1) L.cheb.alloc(2 * p.cheb_degree + 1, c.stream);
+        fill(c, x.get(), n, 1.0);
+        const double init[3] = {0.0, static_cast<double>(n), 0.0};
+        h2d(L.pst.get(), init, 3, c.stream);
+        for (int it = 0; it < p.power_iters; ++it) {
+            power_step(c, A, L.w.get(), x.get(), y.get(), DotSink{partials.get(), ticket.get(), L.pst.get()});
+            power_norm(c, n, y.get(), x.get(), L.pst.get(), DotSink{partials.get(), ticket.get(), L.pst.get() + 1});
+        }
+        cheb_coef(c, L.pst.get(), p.cheb_safety, p.cheb_lower, p.cheb_degree, L.cheb.get());
+    }
 }
 
 void coarse_factorize(Hier& h, int* status) {
@@ -272,6 +292,8 @@ Work& work(Hier& h) {
         const size_t L = h.lv.size();
         W->u.resize(L);
         W->t.resize(L);
+        W->d0.resize(L);
+        W->d1.resize(L);
         W->f.resize(L);
         W->r.resize(L);
         for (size_t i = 0; i < L; ++i) {
@@ -474,6 +496,94 @@ void rebuild_values(Hier& h, const double* values, int location) {
 // Down leg per level: [premul on level 0] -> vc_down (r = f - A u0) ->
 // restriction (also writing the next level's u0).  Up leg per level:
 // prolongation x = u + P u_c (coalesced pass) -> post-smoothing sweeps.
+// One Chebyshev sweep (oracle smooth_cheb) on level i from x (zero when
+// from_zero) into *out; returns the buffer holding the result.
+static double* cheb_sweep(Hier& h, size_t i, const double* f, double* x, double* other, bool from_zero, Gate g) {
+    Ctx& c = *h.ctx;
+    Work& W = work(h);
+    const Level& Li = h.lv[i];
+    const CsrView A = Li.view();
+    const int64_t n = A.n;
+    if (W.d0[i].size() != n) W.d0[i].alloc(n, c.stream);
+    if (W.d1[i].size() != n) W.d1[i].alloc(n, c.stream);
+    double* d = W.d0[i].get();
+    double* dn = W.d1[i].get();
+    if (from_zero) {
+        fill(c, x, n, 0.0, g);
+        cheb_zero(c, n, f, Li.w.get(), Li.cheb.get(), d, g);
+    } else {
+        cheb_start(c, A, f, Li.w.get(), x, Li.cheb.get(), d, g);
+    }
+    double* xs = x;
+    double* xo = other;
+    for (int k = 1; k < h.prm.cheb_degree; ++k) {
+        cheb_step(c, A, f, Li.w.get(), xs, d, Li.cheb.get(), k, xo, dn, g);
+        std::swap(xs, xo);
+        std::swap(d, dn);
+    }
+    axpy1(c, n, xs, d, g);
+    return xs;
+}
+
+// V-cycle with the Chebyshev smoother (extension): generic sweeps, residual,
+// restriction, prolongation (hierarchy.cpp:152-186 structure).
+static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
+    Ctx& c = *h.ctx;
+    Work& W = work(h);
+    const size_t L = h.lv.size();
+    if (W.d0.size() != L) {
+        W.d0.resize(L);
+        W.d1.resize(L);
+    }
+    std::vector<const double*> fin(L), ufinal(L);
+    fin[0] = f;
+    for (size_t i = 1; i < L; ++i) fin[i] = W.f[i].get();
+    std::vector<double*> cur(L);
+    for (size_t i = 0; i + 1 < L; ++i) {
+        c.cur_level = static_cast<int>(i);
+        const Level& Li = h.lv[i];
+        const CsrView A = Li.view();
+        double* a = W.u[i].get();
+        double* b = W.t[i].get();
+        double* x = a;
+        if (h.prm.pre <= 0) {
+            fill(c, a, A.n, 0.0, g);
+        } else {
+            for (int s = 0; s < h.prm.pre; ++s) {
+                double* other = (x == a) ? b : a;
+                x = cheb_sweep(h, i, fin[i], x, other, s == 0, g);
+            }
+        }
+        cur[i] = x;
+        residual(c, A, fin[i], x, W.r[i].get(), g);
+        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), W.r[i].get(), W.f[i + 1].get(), nullptr, 0.0,
+                     nullptr, g);
+    }
+    c.cur_level = static_cast<int>(L - 1);
+    coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
+    ufinal[L - 1] = W.u[L - 1].get();
+    for (size_t i = L - 1; i-- > 0;) {
+        c.cur_level = static_cast<int>(i);
+        const Level& Li = h.lv[i];
+        const CsrView A = Li.view();
+        double* a = cur[i];
+        double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
+        vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
+        double* x = b;
+        for (int s = 0; s < h.prm.post; ++s) {
+            double* other = (x == a) ? b : a;
+            x = cheb_sweep(h, i, fin[i], x, other, false, g);
+        }
+        if (i == 0) {
+            copy(c, u, x, A.n, g);
+            ufinal[i] = u;
+        } else {
+            ufinal[i] = x;
+        }
+    }
+    c.cur_level = -1;
+}
+
 void vcycle(Hier& h, const double* f, double* u, Gate g) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
@@ -481,6 +591,10 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     const double om = h.om_eff();
     if (L == 1) {
         coarse_solve(h, f, u, g);
+        return;
+    }
+    if (h.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV) {
+        vcycle_cheb(h, f, u, g);
         return;
     }
     std::vector<const double*> fin(L), ufinal(L);

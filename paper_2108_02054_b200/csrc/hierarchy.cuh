@@ -46,6 +46,8 @@ struct Level {
     DevArray<double> val;  // A_i values
     const double* ext_val = nullptr;  // adopted (zero-copy) A_0 values, see AMGR_DEVICE_ADOPT
     DevArray<double> w;    // smoother diagonal (inv_diag for Jacobi)
+    DevArray<double> cheb; // Chebyshev coefficients (extension): theta, c1/c2 per step, hi
+    DevArray<double> pst;  // power-iteration state {yy, xx, lam}
     bool has_smoother = false;
     std::shared_ptr<Transfer> T;   // null on the coarsest level
     std::shared_ptr<RapPlan> rap;  // null on the coarsest level
@@ -66,6 +68,7 @@ struct Level {
 // context is single-threaded by contract).
 struct Work {
     std::vector<DevArray<double>> u, t, f, r;
+    std::vector<DevArray<double>> d0, d1;  // Chebyshev direction vectors (lazily allocated)
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh;
     DevArray<KState> st;
     DevArray<double> partials;

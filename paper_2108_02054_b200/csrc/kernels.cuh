@@ -87,6 +87,20 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
 void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv);
 void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g = {});
 
+// ---- Chebyshev smoother (extension; oracle/amg_oracle.c smooth_cheb / power_lambda) ----
+// power iteration step y = D^-1 A x with y.y -> s.out[0]; normalisation x = y/|y|,
+// st = {yy, xx, lam} (lam = |y|/|x_prev|), x.x -> s.out (= st[1])
+void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s);
+void power_norm(Ctx& c, int64_t n, const double* y, double* x, double* st, DotSink s);
+// coef[0] = theta, coef[2k-1], coef[2k] = c1, c2 of step k, coef[2*degree] = hi
+void cheb_coef(Ctx& c, const double* st, double safety, double lower, int degree, double* coef);
+void cheb_start(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* coef,
+                double* d, Gate g = {});
+void cheb_zero(Ctx& c, int64_t n, const double* f, const double* w, const double* coef, double* d, Gate g = {});
+void cheb_step(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* d,
+               const double* coef, int k, double* xout, double* dout, Gate g = {});
+void axpy1(Ctx& c, int64_t n, double* x, const double* d, Gate g = {});
+
 // ---- misc vector kernels ------------------------------------------------------
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g = {});
 void copy(Ctx& c, double* dst, const double* src, int64_t n, Gate g = {});

@@ -372,6 +372,66 @@ struct OpResidNorm {
     }
 };
 
+// ---- Chebyshev smoother + power iteration (extension, oracle/amg_oracle.c) --
+// power step: y = D^-1 A x (w = 1/a_ii), out[0] = y . y
+struct OpPower {
+    static constexpr int NDOT = 1;
+    using Row = Row1;
+    const double* xv;
+    const double* w;
+    double* y;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ Row load(int i) const { return {__ldg(w + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
+        const double t = dmul(q.a, s);
+        y[i] = t;
+        d[0] = __fma_rn(t, t, d[0]);
+    }
+};
+
+struct Row4 {
+    double f, w, x, d;
+};
+
+// first Chebyshev step: r = w*(f - A x); d = r / theta
+struct OpChebStart {
+    static constexpr int NDOT = 0;
+    using Row = Row3;
+    const double* f;
+    const double* w;
+    const double* xv;
+    const double* coef;  // coef[0] = theta
+    double* dout;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i), 0.0}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const {
+        const double r = dmul(q.w, dsub(q.f, s));
+        dout[i] = __ddiv_rn(r, coef[0]);
+    }
+};
+
+// Chebyshev step k (>= 1): x' = x + d; r = w*(f - A x'); d' = c1*d + c2*r
+struct OpChebStep {
+    static constexpr int NDOT = 0;
+    using Row = Row4;
+    const double* f;
+    const double* w;
+    const double* xv;
+    const double* dv;
+    const double* coef;  // c1 = coef[2k-1], c2 = coef[2k]
+    int k;
+    double* xout;
+    double* dout;
+    __device__ double x(int j) const { return dadd(__ldg(xv + j), __ldg(dv + j)); }
+    __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i), __ldg(xv + i), __ldg(dv + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const {
+        const double xn = dadd(q.x, q.d);
+        const double r = dmul(q.w, dsub(q.f, s));
+        xout[i] = xn;
+        dout[i] = dadd(dmul(coef[2 * k - 1], q.d), dmul(coef[2 * k], r));
+    }
+};
+
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
 int rowpass_variant() {
@@ -761,6 +821,53 @@ __global__ void __launch_bounds__(1024) k_inv_apply(int n, const double* __restr
     }
 }
 
+// power normalisation: lam = sqrt(yy)/sqrt(xx); x = y * (1/sqrt(yy)); xx' = x.x
+// st = {yy, xx, lam}
+__global__ void __launch_bounds__(256) k_power_norm(int n, const double* __restrict__ y, double* __restrict__ x,
+                                                    double* st, DotSink ds) {
+    const double yy = st[0];
+    const double sc = 1.0 / sqrt(yy);
+    double d[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double t = y[i] * sc;
+        x[i] = t;
+        d[0] = __fma_rn(t, t, d[0]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) st[2] = sqrt(yy) / sqrt(st[1]);
+    block_dots<1>(d, ds);
+}
+
+// Chebyshev coefficients from lam (oracle smooth_cheb): hi = lam*safety,
+// lo = hi*lower, theta, delta, sigma; rho recursion for the degree-1 steps.
+__global__ void k_cheb_coef(const double* st, double safety, double lower, int degree, double* coef) {
+    const double hi = st[2] * safety, lo = hi * lower;
+    const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo);
+    const double sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    coef[0] = theta;
+    for (int k = 1; k < degree; ++k) {
+        const double rho_new = 1.0 / (2.0 * sigma - rho);
+        coef[2 * k - 1] = rho_new * rho;
+        coef[2 * k] = 2.0 * rho_new / delta;
+        rho = rho_new;
+    }
+    coef[2 * degree] = hi;
+}
+
+__global__ void k_axpy1(int n, double* __restrict__ x, const double* __restrict__ d, Gate g) {
+    if (gated_off(g)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = dadd(x[i], d[i]);
+}
+
+// d = (w*(f - 0)) / theta  (Chebyshev start from a zero iterate; A*0 = 0)
+__global__ void k_cheb_zero(int n, const double* __restrict__ f, const double* __restrict__ w,
+                            const double* __restrict__ coef, double* __restrict__ d, Gate g) {
+    if (gated_off(g)) return;
+    const double theta = coef[0];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        d[i] = __ddiv_rn(dmul(w[i], dsub(f[i], 0.0)), theta);
+}
+
 // ---- misc ---------------------------------------------------------------------
 __global__ void k_fill(double* x, int64_t n, double v, Gate g) {
     if (gated_off(g)) return;
@@ -930,6 +1037,34 @@ void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x,
     const size_t sm = sizeof(double) * static_cast<size_t>(n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     LAUNCH(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
+}
+
+void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s) {
+    launch_rowpass(c, "power", spmv_bytes(A) + 8.0 * A.n, A, OpPower{x, w, y}, Gate{}, s, true);
+}
+void power_norm(Ctx& c, int64_t n, const double* y, double* x, double* st, DotSink s) {
+    LAUNCH(c, "power", 16.0 * n, k_power_norm, dot_grid(c), 256, 0, static_cast<int>(n), y, x, st, s);
+}
+void cheb_coef(Ctx& c, const double* st, double safety, double lower, int degree, double* coef) {
+    LAUNCH(c, "smoother", 0.0, k_cheb_coef, 1, 1, 0, st, safety, lower, degree, coef);
+}
+void cheb_start(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* coef,
+                double* d, Gate g) {
+    launch_rowpass(c, "cheb", spmv_bytes(A) + 16.0 * A.n, A, OpChebStart{f, w, x, coef, d}, g, {}, false);
+}
+void cheb_zero(Ctx& c, int64_t n, const double* f, const double* w, const double* coef, double* d, Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "cheb", 24.0 * n, k_cheb_zero, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f, w,
+           coef, d, g);
+}
+void cheb_step(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* d,
+               const double* coef, int k, double* xout, double* dout, Gate g) {
+    launch_rowpass(c, "cheb", spmv_bytes(A) + 40.0 * A.n, A, OpChebStep{f, w, x, d, coef, k, xout, dout}, g, {},
+                   false);
+}
+void axpy1(Ctx& c, int64_t n, double* x, const double* d, Gate g) {
+    if (n == 0) return;
+    LAUNCH(c, "cheb", 24.0 * n, k_axpy1, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), x, d, g);
 }
 
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g) {

@@ -259,3 +259,46 @@ def test_many_levels_and_launch_count(ctx):
     l0 = ctx.launches()
     amg.vcycle(h, P.rhs(32 ** 3))
     assert ctx.launches() > l0 + 3 * (h.num_levels() - 1)
+
+
+# ---------------------------------------------------------------- extensions vs the restated oracle
+@pytest.mark.parametrize("problem", ["poisson", "convdiff"])
+def test_chebyshev_smoother_vs_oracle(ctx, problem):
+    """Chebyshev + power iteration (extension, parity unpinned by the
+    reference): same hierarchy bits as the oracle, lambda_max within 1e-12,
+    V-cycle within 1e-10 (lambda comes from parallel dots), solve +-1 iter."""
+    from oracle import oracle as O
+
+    g = 16
+    A = P.grid3d_values(problem, g, 3) if problem == "poisson" else O.grid3d(problem, g, 3)
+    kw = dict(smoother="chebyshev", cheb_degree=3, power_iters=12)
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    o = O.setup(A, O.params(**kw))
+    assert h.num_levels() == len(o.levels)
+    for l, L in enumerate(o.levels[:-1]):
+        np.testing.assert_array_equal(_bits(h.level_A(l)[2]), _bits(L.A[2]))
+        assert h.level_lambda(l) * 1.1 == pytest.approx(L.lam_max, rel=1e-12)
+    f = np.random.default_rng(5).uniform(-1, 1, g ** 3)
+    u, uo = amg.vcycle(h, f), O.vcycle(o, f)
+    assert np.linalg.norm(u - uo) <= 1e-10 * np.linalg.norm(uo)
+    fr = P.rhs(g ** 3)
+    _, st = amg.bicgstab(h, fr)
+    so = O.bicgstab(o, fr)
+    assert st.converged == so.converged and abs(st.iterations - so.iterations) <= 1
+
+
+def test_spai0_smoother_vs_oracle(ctx):
+    from oracle import oracle as O
+
+    A = P.grid3d_values("dambreak", 16, 12)
+    h = amg.setup(A, amg.AmgParams(smoother="spai0"), ctx=ctx)
+    o = O.setup(A, O.params(smoother="spai0"))
+    for l, L in enumerate(o.levels[:-1]):
+        np.testing.assert_array_equal(_bits(h.level_A(l)[2]), _bits(L.A[2]))
+        np.testing.assert_array_equal(_bits(h.level_smoother(l)), _bits(L.w))
+    f = np.random.default_rng(6).uniform(-1, 1, 16 ** 3)
+    np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(O.vcycle(o, f)))
+    fr = P.rhs(16 ** 3)
+    _, st = amg.bicgstab(h, fr)
+    so = O.bicgstab(o, fr)
+    assert st.converged and abs(st.iterations - so.iterations) <= 1
