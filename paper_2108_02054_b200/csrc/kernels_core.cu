@@ -521,72 +521,41 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 }
 
 // ---- numeric RAP ----------------------------------------------------------
-// Thread per coarse entry c, replaying the reference's two-level bracket of
-// spmm(R, spmm(A, P)) (csr.cpp:145-194) over the cached plan:
+// Thread per coarse entry c (grid-stride), replaying the reference's two-level
+// bracket of spmm(R, spmm(A, P)) (csr.cpp:145-194) over the cached plan:
 //   acc = 0; part = 0; for p in [cptr[c], cptr[c+1]):
 //     part += Af[contrib[p] & 0x7fffffff]; if (contrib[p] < 0) { acc += part; part = 0; }
-// Each thread owns RAP_ENT entries (a grid stride apart, so every load stage is
-// coalesced across the warp) and issues each load stage for all of them at
-// once: cptr pairs, then the first two contributions, then their fine values
-// — 3 dependent latencies per RAP_ENT entries instead of per entry.  Plan and
-// output are streamed with evict-first hints; the gathered fine values use
-// the default policy so neighbouring aggregates' sectors can hit in L2.
-constexpr int RAP_ENT = 4;
-
-__global__ void __launch_bounds__(256) k_rap(int64_t nnz_c, const int* __restrict__ cptr,
-                                             const int* __restrict__ contrib, const double* __restrict__ af,
-                                             double* __restrict__ ac) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; base < nnz_c;
-         base += RAP_ENT * stride) {
-        int p0[RAP_ENT], p1[RAP_ENT], q0[RAP_ENT], q1[RAP_ENT];
-        double v0[RAP_ENT], v1[RAP_ENT];
-#pragma unroll
-        for (int t = 0; t < RAP_ENT; ++t) {
-            const int64_t c = base + t * stride;
-            const bool ok = c < nnz_c;
-            p0[t] = ok ? __ldcs(cptr + c) : 0;
-            p1[t] = ok ? __ldcs(cptr + c + 1) : 0;
-        }
-#pragma unroll
-        for (int t = 0; t < RAP_ENT; ++t) {
-            q0[t] = p0[t] < p1[t] ? __ldcs(contrib + p0[t]) : 0;
-            q1[t] = p0[t] + 1 < p1[t] ? __ldcs(contrib + p0[t] + 1) : 0;
-        }
-#pragma unroll
-        for (int t = 0; t < RAP_ENT; ++t) {
-            v0[t] = p0[t] < p1[t] ? __ldg(af + (q0[t] & 0x7fffffff)) : 0.0;
-            v1[t] = p0[t] + 1 < p1[t] ? __ldg(af + (q1[t] & 0x7fffffff)) : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < RAP_ENT; ++t) {
-            const int64_t c = base + t * stride;
-            if (c >= nnz_c) continue;
-            double acc = 0.0, part = 0.0;
-            if (p0[t] < p1[t]) {
-                part = dadd(part, v0[t]);
-                if (q0[t] < 0) {
-                    acc = dadd(acc, part);
-                    part = 0.0;
-                }
+// Plan and output are streamed with evict-first hints; the gathered fine values
+// use the default policy so sectors shared by neighbouring aggregates can hit
+// in L2.  (Variants measured slower in round 1 — row-group warps, shared-memory
+// staging, 4 entries per thread: see DESIGN.md §3.3.)
+__global__ void k_rap(int64_t nnz_c, const int* __restrict__ cptr, const int* __restrict__ contrib,
+                      const double* __restrict__ af, double* __restrict__ ac) {
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nnz_c;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p0 = __ldcs(cptr + c), p1 = __ldcs(cptr + c + 1);
+        double acc = 0.0, part = 0.0;
+        int p = p0;
+        for (; p + 2 <= p1; p += 2) {
+            const int e0 = __ldcs(contrib + p), e1 = __ldcs(contrib + p + 1);
+            const double v0 = __ldg(af + (e0 & 0x7fffffff)), v1 = __ldg(af + (e1 & 0x7fffffff));
+            part = dadd(part, v0);
+            if (e0 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
             }
-            if (p0[t] + 1 < p1[t]) {
-                part = dadd(part, v1[t]);
-                if (q1[t] < 0) {
-                    acc = dadd(acc, part);
-                    part = 0.0;
-                }
+            part = dadd(part, v1);
+            if (e1 < 0) {
+                acc = dadd(acc, part);
+                part = 0.0;
             }
-            for (int p = p0[t] + 2; p < p1[t]; ++p) {
-                const int q = __ldcs(contrib + p);
-                part = dadd(part, __ldg(af + (q & 0x7fffffff)));
-                if (q < 0) {
-                    acc = dadd(acc, part);
-                    part = 0.0;
-                }
-            }
-            __stcs(ac + c, acc);
         }
+        if (p < p1) {
+            const int e0 = __ldcs(contrib + p);
+            part = dadd(part, __ldg(af + (e0 & 0x7fffffff)));
+            if (e0 < 0) acc = dadd(acc, part);
+        }
+        __stcs(ac + c, acc);
     }
 }
 
@@ -1022,8 +991,7 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdia
     (void)bad;
     // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1)
     const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
-    LAUNCH(c, "rap", bytes, k_rap, grid_for((nnz_c + RAP_ENT - 1) / RAP_ENT, 256, c.num_sms * 8), 256, 0, nnz_c, cptr,
-           contrib, af, ac);
+    LAUNCH(c, "rap", bytes, k_rap, grid_for(nnz_c, 256, c.num_sms * 32), 256, 0, nnz_c, cptr, contrib, af, ac);
 }
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
