@@ -241,6 +241,44 @@ amgr_status amgr_run_sequence(amgr_ctx* ctx, int64_t nsteps, amgr_step_fn step, 
  * when t_other == 0. */
 double amgr_speedup_percent(double t_base, double t_other);
 
+/* ---- row-partitioned multi-GPU solve ---------------------- */
+/* One rank per GPU.  Every rank builds the same global hierarchy with
+ * amgr_setup; levels 0..top are then row-partitioned (aggregate-consistent
+ * ownership computed host-side by paper_2108_02054_b200/partition.py), levels
+ * top+1.. are replicated.  Halo exchange: ncclSend/ncclRecv; dots: allgather
+ * of per-rank partials summed in rank order (identical on every rank). */
+typedef struct amgr_dist amgr_dist;
+typedef struct amgr_dist_level {
+    int64_t n_own, n_halo, nnz, n_coarse_owned;
+    const int64_t* row_ptr;  /* n_own+1, local CSR rows = owned rows ascending   */
+    const int64_t* col;      /* nnz, local column ids: owned [0,n_own) | halo      */
+    const int64_t* nnz_map;  /* nnz, local entry -> global entry of level A_i      */
+    const int64_t* owned;    /* n_own, global row ids                              */
+    const int64_t* agg;      /* n_own, local coarse id (global id at level top)    */
+    const int64_t* mptr;     /* n_coarse_owned+1, members of owned coarse rows     */
+    const int64_t* midx;     /* local fine ids, ascending                          */
+    int32_t n_send_peers, n_recv_peers;
+    const int32_t* send_peer;
+    const int64_t* send_cnt;
+    const int64_t* send_idx; /* concatenated per send peer: local owned ids        */
+    const int32_t* recv_peer;
+    const int64_t* recv_off; /* offset of the peer's block inside the halo         */
+    const int64_t* recv_cnt;
+} amgr_dist_level;
+
+amgr_status amgr_nccl_unique_id(void* out128);
+/* t_counts[r]: level-(top+1) rows restricted by rank r (contiguous, rank order). */
+amgr_status amgr_dist_create(amgr_hier* global, const void* nccl_id128, int rank, int world, int top,
+                             const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
+                             amgr_dist** out);
+/* Global rebuild on every rank + gather of the local values (round 1). */
+amgr_status amgr_dist_rebuild_values(amgr_dist* d, const double* global_values, int location);
+/* f/u: device vectors over the owned level-0 rows. */
+amgr_status amgr_dist_vcycle(amgr_dist* d, const double* f_local, double* u_local);
+amgr_status amgr_dist_bicgstab(amgr_dist* d, const double* f_local, double* u_local,
+                               const amgr_solve_params* prm, amgr_solve_stats* stats);
+void amgr_dist_destroy(amgr_dist* d);
+
 /* ---- introspection / download (parity dumps) ----------------------------- */
 /* Number of levels, finest first (Hierarchy::num_levels, hierarchy.hpp:54). */
 int amgr_hier_num_levels(const amgr_hier* h);

@@ -130,6 +130,12 @@ PROTOTYPES = {
     "amgr_copy_to_host": (_I, [_V, _V, _V, C.c_size_t]),
     "amgr_run_sequence": (_I, [_V, _L, _V, _V, _V, _V, _V, _V, _V, _V]),
     "amgr_speedup_percent": (_D, [_D, _D]),
+    "amgr_nccl_unique_id": (_I, [_V]),
+    "amgr_dist_create": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
+    "amgr_dist_rebuild_values": (_I, [_V, _V, _I]),
+    "amgr_dist_vcycle": (_I, [_V, _V, _V]),
+    "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),
+    "amgr_dist_destroy": (None, [_V]),
 }
 
 _lib = None
@@ -250,7 +256,7 @@ class DeviceCsr:
 
 def _check(st: int, ctx_ptr):
     if st != 0:
-        msg = lib().amgr_last_error(ctx_ptr)
+        msg = lib().amgr_last_error(ctx_ptr) if ctx_ptr is not None else b""
         msg = msg.decode() if msg else ""
         raise _ERR.get(st, AmgrError)(msg)
 

@@ -8,9 +8,6 @@
 
 #include "hierarchy.cuh"
 
-struct amgr_hier {
-    std::unique_ptr<amgr::Hier> h;
-};
 
 namespace amgr {
 

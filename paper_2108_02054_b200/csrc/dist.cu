@@ -1,0 +1,469 @@
+// Row-partitioned multi-GPU solve — one process per GPU,
+// NCCL over NVLink for the data path.
+//
+//  * Setup is replicated: every rank builds the same global hierarchy
+//    (deterministic), then adopts the aggregate-consistent partition computed
+//    by paper_2108_02054_b200/partition.py (levels 0..T partitioned, T+1..
+//    replicated).  Rebuild in round 1 is the global rebuild on every rank
+//    followed by gathers of the local values (the rebuild is ~1% of a step);
+//    the solve is partitioned.
+//  * Partitioned levels run the same row-pass kernels on local CSR matrices
+//    whose columns index [owned | halo]; before every pass whose operand is
+//    gathered, the halo is exchanged with ncclSend/ncclRecv in one group.
+//    Restriction and prolongation are local (aggregate-consistent ownership).
+//  * Transition: each rank restricts onto its contiguous range of level-T+1
+//    rows; one ncclAllGather (padded blocks) replicates f_{T+1}; the coarse
+//    levels run through vcycle_from(T+1) on every rank.
+//  * Dots: every rank's partial (deterministic block reduction) is
+//    allgathered and summed in rank order on the device, so all ranks take
+//    identical control-flow decisions.
+#include <nccl.h>
+
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+#include "hierarchy.cuh"
+#include "reduce.cuh"
+
+namespace amgr {
+
+#define NK(x)                                                                                         \
+    do {                                                                                              \
+        ncclResult_t r_ = (x);                                                                        \
+        if (r_ != ncclSuccess) ::amgr::fail(AMGR_E_NCCL, std::string("NCCL: ") + ncclGetErrorString(r_)); \
+    } while (0)
+
+namespace {
+
+__global__ void k_gather_d(int64_t n, const double* __restrict__ src, const int* __restrict__ idx,
+                           double* __restrict__ dst, Gate g) {
+    if (gated_off(g)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// padded allgather blocks (W x pad) -> global vector (block r at displ[r], count[r])
+__global__ void k_unpad(int world, int64_t pad, const double* __restrict__ buf, const int64_t* __restrict__ displ,
+                        const int64_t* __restrict__ cnt, double* __restrict__ out) {
+    for (int r = 0; r < world; ++r)
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < cnt[r];
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            out[displ[r] + i] = buf[r * pad + i];
+}
+
+// sum the W gathered partials of each of k dots in rank order
+__global__ void k_rank_sum(int world, int k, const double* __restrict__ parts, double* const* outs) {
+    const int t = threadIdx.x;
+    if (t >= k) return;
+    double s = 0.0;
+    for (int r = 0; r < world; ++r) s = __dadd_rn(s, parts[r * k + t]);
+    *outs[t] = s;
+}
+
+}  // namespace
+
+struct DistLevel {
+    int64_t n_own = 0, n_halo = 0, nnz = 0, n_cown = 0;
+    DevArray<int> rp, col, nnz_map, owned, agg, mptr, midx;
+    DevArray<double> val, w;
+    DevArray<double> u0, x, out, f, r;  // u0/x carry halo space
+    std::vector<int> send_peer, recv_peer;
+    std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
+    DevArray<int> send_idx;
+    DevArray<double> send_buf;
+    int max_span = 0;
+    CsrView view() const {
+        CsrView v;
+        v.n = n_own;
+        v.ncols = n_own + n_halo;
+        v.nnz = nnz;
+        v.rp = rp.get();
+        v.col = col.get();
+        v.val = val.get();
+        v.max_span = max_span;
+        return v;
+    }
+};
+
+struct DistHier {
+    Hier* g = nullptr;
+    Ctx* ctx = nullptr;
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, T = -1;
+    std::vector<DistLevel> lv;
+    // transition (level T -> T+1)
+    std::vector<int64_t> tcnt, tdispl;
+    int64_t tpad = 0;
+    DevArray<double> tsend, tgather, fT, uT;
+    DevArray<int64_t> tcnt_d, tdispl_d;
+    // Krylov (level 0 local)
+    DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh, ku;
+    DevArray<double> dloc, dall;  // local dot results (up to 2) and the gathered partials
+    DevArray<double*> douts;
+};
+
+static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
+    Ctx& c = *d.ctx;
+    if (L.send_idx.size() > 0)
+        LAUNCH(c, "halo_pack", 16.0 * L.send_idx.size(), k_gather_d, grid_for(L.send_idx.size(), 256, c.num_sms * 8),
+               256, 0, L.send_idx.size(), x, L.send_idx.get(), L.send_buf.get(), g);
+    if (d.world == 1 || (L.send_peer.empty() && L.recv_peer.empty())) return;
+    NK(ncclGroupStart());
+    for (size_t k = 0; k < L.send_peer.size(); ++k)
+        NK(ncclSend(L.send_buf.get() + L.send_off[k], static_cast<size_t>(L.send_cnt[k]), ncclDouble, L.send_peer[k],
+                    d.comm, c.stream));
+    for (size_t k = 0; k < L.recv_peer.size(); ++k)
+        NK(ncclRecv(x + L.n_own + L.recv_off[k], static_cast<size_t>(L.recv_cnt[k]), ncclDouble, L.recv_peer[k],
+                    d.comm, c.stream));
+    NK(ncclGroupEnd());
+}
+
+// deterministic cross-rank sum of k local dots (d.dloc[0..k)) into outs
+static void allsum(DistHier& d, int k, std::initializer_list<double*> outs) {
+    Ctx& c = *d.ctx;
+    std::vector<double*> o(outs);
+    h2d(d.douts.get(), o.data(), static_cast<int64_t>(o.size()), c.stream);
+    if (d.world > 1)
+        NK(ncclAllGather(d.dloc.get(), d.dall.get(), static_cast<size_t>(k), ncclDouble, d.comm, c.stream));
+    else
+        d2d(d.dall.get(), d.dloc.get(), k, c.stream);
+    LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), d.douts.get());
+}
+
+static DotSink local_sink(DistHier& d, int slot) {
+    Work& W = work(*d.g);
+    return DotSink{W.partials.get(), W.ticket.get(), d.dloc.get() + slot};
+}
+
+// ---- V-cycle on the partition (hierarchy.cpp:152-186 semantics) -------------
+static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
+    Ctx& c = *d.ctx;
+    Hier& h = *d.g;
+    const double om = h.om_eff();
+    const int T = d.T;
+    std::vector<const double*> fin(T + 1);
+    fin[0] = f0;
+    for (int i = 1; i <= T; ++i) fin[i] = d.lv[i].f.get();
+    vc_premul(c, d.lv[0].n_own, f0, d.lv[0].w.get(), om, d.lv[0].u0.get(), g);
+    for (int i = 0; i <= T; ++i) {
+        c.cur_level = i;
+        DistLevel& L = d.lv[i];
+        halo(d, L, L.u0.get(), g);
+        vc_down(c, L.view(), fin[i], L.u0.get(), L.r.get(), g);
+        if (i < T) {
+            DistLevel& N = d.lv[i + 1];
+            restrict_sum(c, L.n_cown, L.mptr.get(), L.midx.get(), L.r.get(), N.f.get(), N.w.get(), om, N.u0.get(), g);
+        } else {
+            restrict_sum(c, L.n_cown, L.mptr.get(), L.midx.get(), L.r.get(), d.tsend.get(), nullptr, 0.0, nullptr, g);
+        }
+    }
+    // transition: replicate f_{T+1}, then the coarse levels on every rank
+    if (d.world > 1)
+        NK(ncclAllGather(d.tsend.get(), d.tgather.get(), static_cast<size_t>(d.tpad), ncclDouble, d.comm, c.stream));
+    else
+        d2d(d.tgather.get(), d.tsend.get(), d.tpad, c.stream);
+    LAUNCH(c, "dist", 0.0, k_unpad, grid_for(d.tpad, 256, 64), 256, 0, d.world, d.tpad, d.tgather.get(),
+           d.tdispl_d.get(), d.tcnt_d.get(), d.fT.get());
+    vcycle_from(h, static_cast<size_t>(T + 1), d.fT.get(), d.uT.get(), g);
+    const double* uc = d.uT.get();
+    for (int i = T; i >= 0; --i) {
+        c.cur_level = i;
+        DistLevel& L = d.lv[i];
+        vc_prolong(c, L.n_own, L.u0.get(), L.agg.get(), uc, L.x.get(), g);
+        halo(d, L, L.x.get(), g);
+        double* out = (i == 0) ? u_out : L.out.get();
+        vc_smooth(c, L.view(), fin[i], L.w.get(), om, L.x.get(), out, g);
+        uc = out;
+    }
+    c.cur_level = -1;
+}
+
+static void gather_local(DistHier& d) {
+    Ctx& c = *d.ctx;
+    Hier& h = *d.g;
+    for (int i = 0; i <= d.T; ++i) {
+        DistLevel& L = d.lv[i];
+        const Level& G = h.lv[i];
+        LAUNCH(c, "dist", 0.0, k_gather_d, grid_for(L.nnz, 256, c.num_sms * 16), 256, 0, L.nnz, G.view().val,
+               L.nnz_map.get(), L.val.get(), Gate{});
+        LAUNCH(c, "dist", 0.0, k_gather_d, grid_for(L.n_own, 256, c.num_sms * 16), 256, 0, L.n_own, G.w.get(),
+               L.owned.get(), L.w.get(), Gate{});
+    }
+}
+
+}  // namespace amgr
+
+// ---- C-ABI ----------------------------------------------------------------------
+struct amgr_dist {
+    std::unique_ptr<amgr::DistHier> d;
+};
+
+extern "C" {
+
+amgr_status amgr_nccl_unique_id(void* out128) {
+    if (!out128) return AMGR_E_INVALID_ARGUMENT;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return AMGR_E_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof(id));
+    return AMGR_OK;
+}
+
+amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, int world, int top,
+                             const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
+                             amgr_dist** out) {
+    if (!hg || !nccl_id128 || !out || (top >= 0 && !levels) || world < 1) return AMGR_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    amgr::Hier& H = *hg->h;
+    amgr::Ctx& c = *H.ctx;
+    try {
+        CK(cudaSetDevice(c.device));
+        if (top < 0 || top + 1 >= static_cast<int>(H.lv.size()))
+            amgr::invalid("amgr_dist_create: need 0 <= top < num_levels - 1");
+        if (H.prm.pre != 1 || H.prm.post != 1 || H.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV)
+            amgr::invalid("amgr_dist_create: the partitioned solve supports 1+1 Jacobi/SPAI0 sweeps");
+        auto d = std::make_unique<amgr::DistHier>();
+        d->g = &H;
+        d->ctx = &c;
+        d->rank = rank;
+        d->world = world;
+        d->T = top;
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof(id));
+        NK(ncclCommInitRank(&d->comm, world, id, rank));
+        auto up32 = [&](amgr::DevArray<int>& dst, const int64_t* src, int64_t n) {
+            std::vector<int> tmp(static_cast<size_t>(n));
+            for (int64_t k = 0; k < n; ++k) tmp[k] = static_cast<int>(src[k]);
+            dst.alloc(n, c.stream);
+            amgr::h2d(dst.get(), tmp.data(), n, c.stream);
+        };
+        d->lv.resize(static_cast<size_t>(top + 1));
+        for (int i = 0; i <= top; ++i) {
+            const amgr_dist_level& s = levels[i];
+            amgr::DistLevel& L = d->lv[i];
+            L.n_own = s.n_own;
+            L.n_halo = s.n_halo;
+            L.nnz = s.nnz;
+            L.n_cown = s.n_coarse_owned;
+            up32(L.rp, s.row_ptr, s.n_own + 1);
+            up32(L.col, s.col, s.nnz);
+            up32(L.nnz_map, s.nnz_map, s.nnz);
+            up32(L.owned, s.owned, s.n_own);
+            up32(L.agg, s.agg, s.n_own);
+            up32(L.mptr, s.mptr, s.n_coarse_owned + 1);
+            up32(L.midx, s.midx, s.mptr[s.n_coarse_owned]);
+            L.val.alloc(s.nnz, c.stream);
+            L.w.alloc(s.n_own, c.stream);
+            L.u0.alloc(s.n_own + s.n_halo, c.stream);
+            L.x.alloc(s.n_own + s.n_halo, c.stream);
+            L.out.alloc(s.n_own, c.stream);
+            L.f.alloc(s.n_own, c.stream);
+            L.r.alloc(s.n_own, c.stream);
+            int64_t off = 0;
+            for (int k = 0; k < s.n_send_peers; ++k) {
+                L.send_peer.push_back(s.send_peer[k]);
+                L.send_off.push_back(off);
+                L.send_cnt.push_back(s.send_cnt[k]);
+                off += s.send_cnt[k];
+            }
+            up32(L.send_idx, s.send_idx, off);
+            L.send_buf.alloc(off, c.stream);
+            for (int k = 0; k < s.n_recv_peers; ++k) {
+                L.recv_peer.push_back(s.recv_peer[k]);
+                L.recv_off.push_back(s.recv_off[k]);
+                L.recv_cnt.push_back(s.recv_cnt[k]);
+            }
+            L.max_span = amgr::max_group_span(c, L.rp.get(), L.n_own);
+        }
+        // transition allgather layout
+        int64_t disp = 0;
+        for (int r = 0; r < world; ++r) {
+            d->tcnt.push_back(t_counts[r]);
+            d->tdispl.push_back(disp);
+            disp += t_counts[r];
+            d->tpad = std::max<int64_t>(d->tpad, t_counts[r]);
+        }
+        if (disp != t_count_total || disp != H.lv[top + 1].pat->n)
+            amgr::invalid("amgr_dist_create: transition counts do not cover level top+1");
+        d->tsend.alloc(std::max<int64_t>(d->tpad, 1), c.stream);
+        d->tgather.alloc(std::max<int64_t>(d->tpad * world, 1), c.stream);
+        d->tcnt_d.alloc(world, c.stream);
+        d->tdispl_d.alloc(world, c.stream);
+        amgr::h2d(d->tcnt_d.get(), d->tcnt.data(), world, c.stream);
+        amgr::h2d(d->tdispl_d.get(), d->tdispl.data(), world, c.stream);
+        d->fT.alloc(disp, c.stream);
+        d->uT.alloc(disp, c.stream);
+        const int64_t n0 = d->lv[0].n_own, h0 = d->lv[0].n_halo;
+        for (auto* v : {&d->kr, &d->krt, &d->kp, &d->kv, &d->ks, &d->kt}) v->alloc(n0, c.stream);
+        for (auto* v : {&d->kph, &d->ksh, &d->ku}) v->alloc(n0 + h0, c.stream);
+        d->dloc.alloc(4, c.stream);
+        d->dall.alloc(4 * world, c.stream);
+        d->douts.alloc(4, c.stream);
+        amgr::work(H);
+        amgr::gather_local(*d);
+        CK(cudaStreamSynchronize(c.stream));
+        auto* o = new amgr_dist();
+        o->d = std::move(d);
+        *out = o;
+        return AMGR_OK;
+    } catch (const amgr::Error& e) {
+        c.last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        c.last_error = e.what();
+        return AMGR_E_RUNTIME;
+    }
+}
+
+void amgr_dist_destroy(amgr_dist* d) {
+    if (!d) return;
+    if (d->d && d->d->comm) ncclCommDestroy(d->d->comm);
+    delete d;
+}
+
+static amgr_status dist_guard(amgr_dist* d, const std::function<void()>& fn) {
+    if (!d || !d->d) return AMGR_E_INVALID_ARGUMENT;
+    amgr::Ctx& c = *d->d->ctx;
+    try {
+        CK(cudaSetDevice(c.device));
+        fn();
+        return AMGR_OK;
+    } catch (const amgr::Error& e) {
+        c.last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        c.last_error = e.what();
+        return AMGR_E_RUNTIME;
+    }
+}
+
+amgr_status amgr_dist_rebuild_values(amgr_dist* d, const double* global_values, int location) {
+    return dist_guard(d, [&] {
+        amgr::rebuild_values(*d->d->g, global_values, location);
+        amgr::gather_local(*d->d);
+    });
+}
+
+amgr_status amgr_dist_vcycle(amgr_dist* d, const double* f_local, double* u_local) {
+    return dist_guard(d, [&] { amgr::dist_vcycle(*d->d, f_local, u_local, amgr::Gate{}); });
+}
+
+}  // extern "C"
+
+namespace amgr {
+
+// BiCGStab (bicgstab.cpp:21-135) on the partition: local vectors of the owned
+// level-0 rows, halo exchange before every level-0 SpMV, rank-ordered dots.
+void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_params& sp, amgr_solve_stats& out) {
+    Ctx& c = *d.ctx;
+    Hier& h = *d.g;
+    DistLevel& L0 = d.lv[0];
+    const CsrView A = L0.view();
+    const int64_t n = L0.n_own;
+    KState* st = work(h).st.get();
+    out = amgr_solve_stats{0, 0.0, 0, 0};
+    auto rd = [&]() {
+        KState s;
+        d2h(&s, st, 1, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        return s;
+    };
+    KState s0;
+    h2d(st, &s0, 1, c.stream);
+    dot(c, n, f, f, local_sink(d, 0));
+    allsum(d, 1, {&st->d_true});
+    KState s = rd();
+    const double normf = std::sqrt(s.d_true);
+    if (normf == 0.0) {
+        fill(c, u, n, 0.0);
+        out.converged = 1;
+        return;
+    }
+    copy(c, d.ku.get(), u, n);  // u (with halo space) starts from the caller's guess
+    double* uu = d.ku.get();
+    halo(d, L0, uu, Gate{});
+    resid_norm(c, A, f, uu, d.kr.get(), d.krt.get(), local_sink(d, 0));
+    dot(c, n, d.krt.get(), d.kr.get(), local_sink(d, 1));
+    allsum(d, 2, {&st->d_rr, &st->d_rtr});
+    s = rd();
+    out.relative_residual = std::sqrt(s.d_rr) / normf;
+    if (out.relative_residual <= sp.tol) {
+        out.converged = 1;
+        copy(c, u, uu, n);
+        return;
+    }
+    s.normf = normf;
+    s.floor = 1e-30 * normf * normf;
+    s.tol = sp.tol;
+    s.max_iter = sp.max_iter;
+    s.rho_old = s.alpha = s.omega = 1.0;
+    s.it = 0;
+    s.flags = 0;
+    h2d(st, &s, 1, c.stream);
+    const Gate G = gate_of(st, KF_DONE);
+    const Gate GH = gate_of(st, KF_DONE, KF_HALF);
+    const Gate GF = gate_of(st, KF_DONE | KF_HALF);
+    const Gate GC = gate_of(st, KF_DONE | KF_HALF, KF_CHECK);
+    for (;;) {
+        bicg_begin(c, st);
+        bicg_p(c, st, n, d.kr.get(), d.kp.get(), d.kv.get());
+        dist_vcycle(d, d.kp.get(), d.kph.get(), G);
+        halo(d, L0, d.kph.get(), G);
+        spmv_dot(c, A, d.kph.get(), d.kv.get(), d.krt.get(), local_sink(d, 0), G);
+        allsum(d, 1, {&st->d_rtv});
+        bicg_alpha(c, st);
+        bicg_s(c, st, n, d.kr.get(), d.kv.get(), d.ks.get(), local_sink(d, 0));
+        allsum(d, 1, {&st->d_ss});
+        bicg_half_test(c, st);
+        bicg_half_u(c, st, n, uu, d.kph.get());
+        halo(d, L0, uu, GH);
+        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GH);
+        allsum(d, 1, {&st->d_true});
+        bicg_half_check(c, st);
+        bicg_half_r(c, st, n, d.kr.get(), d.ks.get());
+        dist_vcycle(d, d.ks.get(), d.ksh.get(), GF);
+        halo(d, L0, d.ksh.get(), GF);
+        spmv_dot2(c, A, d.ksh.get(), d.kt.get(), d.ks.get(), local_sink(d, 0), GF);
+        allsum(d, 2, {&st->d_ts, &st->d_tt});
+        bicg_omega(c, st);
+        bicg_update(c, st, n, uu, d.kph.get(), d.ksh.get(), d.kr.get(), d.ks.get(), d.kt.get(), d.krt.get(),
+                    local_sink(d, 0));
+        allsum(d, 2, {&st->d_rr, &st->d_rtr});
+        bicg_end_test(c, st);
+        halo(d, L0, uu, GC);
+        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GC);
+        allsum(d, 1, {&st->d_true});
+        bicg_end_check(c, st);
+        s = rd();
+        if (s.flags & KF_DONE) break;
+    }
+    out.iterations = s.it;
+    if (s.flags & KF_CONVERGED) {
+        out.converged = 1;
+        out.relative_residual = s.res;
+    } else {
+        out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
+        halo(d, L0, uu, Gate{});
+        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0));
+        allsum(d, 1, {&st->d_true});
+        s = rd();
+        out.relative_residual = std::sqrt(s.d_true) / normf;
+        out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;
+    }
+    copy(c, u, uu, n);
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace amgr
+
+extern "C" amgr_status amgr_dist_bicgstab(amgr_dist* d, const double* f_local, double* u_local,
+                                          const amgr_solve_params* prm, amgr_solve_stats* stats) {
+    if (!stats) return AMGR_E_INVALID_ARGUMENT;
+    return dist_guard(d, [&] {
+        amgr_solve_params sp{1e-8, 100};
+        if (prm) sp = *prm;
+        amgr::dist_bicgstab(*d->d, f_local, u_local, sp, *stats);
+    });
+}

@@ -584,27 +584,31 @@ static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
     c.cur_level = -1;
 }
 
-void vcycle(Hier& h, const double* f, double* u, Gate g) {
+// V-cycle over levels s..L-1 (s = 0: the whole hierarchy); f and u live on
+// level s.  The partitioned multi-GPU solve runs the replicated coarse levels
+// through this with s = T+1.
+void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
     const double om = h.om_eff();
-    if (L == 1) {
+    if (s + 1 == L) {
         coarse_solve(h, f, u, g);
         return;
     }
     if (h.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV) {
+        if (s != 0) invalid("vcycle_from: Chebyshev smoother supports s = 0 only");
         vcycle_cheb(h, f, u, g);
         return;
     }
     std::vector<const double*> fin(L), ufinal(L);
-    fin[0] = f;
-    for (size_t i = 1; i < L; ++i) fin[i] = W.f[i].get();
+    fin[s] = f;
+    for (size_t i = s + 1; i < L; ++i) fin[i] = W.f[i].get();
     std::vector<double*> cur(L);
     const int pre = h.prm.pre, post = h.prm.post;
-    if (pre >= 1) vc_premul(c, h.lv[0].pat->n, f, h.lv[0].w.get(), om, W.u[0].get(), g);
+    if (pre >= 1) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
     // down leg
-    for (size_t i = 0; i + 1 < L; ++i) {
+    for (size_t i = s; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
@@ -638,14 +642,14 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
     ufinal[L - 1] = W.u[L - 1].get();
     // up leg
-    for (size_t i = L - 1; i-- > 0;) {
+    for (size_t i = L - 1; i-- > s;) {
         c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
         double* a = cur[i];
         double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
         if (post <= 0) {
-            double* t = (i == 0) ? u : b;
+            double* t = (i == s) ? u : b;
             vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], t, g);
             ufinal[i] = t;
             continue;
@@ -654,7 +658,7 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
         vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
         double* src = b;
         for (int k = 1; k <= post; ++k) {
-            double* dst = (i == 0 && k == post) ? u : (src == b ? a : b);
+            double* dst = (i == s && k == post) ? u : (src == b ? a : b);
             vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
             src = dst;
         }
@@ -662,6 +666,8 @@ void vcycle(Hier& h, const double* f, double* u, Gate g) {
     }
     c.cur_level = -1;
 }
+
+void vcycle(Hier& h, const double* f, double* u, Gate g) { vcycle_from(h, 0, f, u, g); }
 
 // ---- BiCGStab (bicgstab.cpp:21-135) ------------------------------------------------
 namespace {

@@ -101,6 +101,7 @@ std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const Amg
 void rebuild(Hier& h, const amgr_csr& A);
 void rebuild_values(Hier& h, const double* values, int location);
 void vcycle(Hier& h, const double* f, double* u, Gate g = {});
+void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g = {});
 void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
               amgr_solve_stats& st);
 void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
@@ -114,3 +115,8 @@ void problem_values(Ctx& c, int kind, int64_t g, int64_t k, int64_t nsteps, doub
 void exclusive_sum_i32(Ctx& c, const int* in, int* out, int64_t n);
 
 }  // namespace amgr
+
+// Opaque C-ABI hierarchy handle (include/amgr.h).
+struct amgr_hier {
+    std::unique_ptr<amgr::Hier> h;
+};
