@@ -17,6 +17,7 @@
 //  * Dots: every rank's partial (deterministic block reduction) is
 //    allgathered and summed in rank order on the device, so all ranks take
 //    identical control-flow decisions.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -28,10 +29,57 @@
 
 namespace amgr {
 
+// NCCL is bound at run time (dlopen), not at link time: the process usually
+// already holds torch's bundled libnccl.so.2, and a link-time NEEDED entry
+// would let the system copy claim that SONAME first when this library loads
+// before torch.  RTLD_NOLOAD picks the already-loaded copy when present.
+struct NcclApi {
+    decltype(&::ncclGetUniqueId) GetUniqueId;
+    decltype(&::ncclCommInitRank) CommInitRank;
+    decltype(&::ncclCommDestroy) CommDestroy;
+    decltype(&::ncclGroupStart) GroupStart;
+    decltype(&::ncclGroupEnd) GroupEnd;
+    decltype(&::ncclSend) Send;
+    decltype(&::ncclRecv) Recv;
+    decltype(&::ncclAllGather) AllGather;
+    decltype(&::ncclGetErrorString) GetErrorString;
+};
+
+static const NcclApi* nccl_api() {
+    static NcclApi api{};
+    static bool ok = [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        bool good = true;
+        auto sym = [&](auto& f, const char* name) {
+            f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+            good = good && f != nullptr;
+        };
+        sym(api.GetUniqueId, "ncclGetUniqueId");
+        sym(api.CommInitRank, "ncclCommInitRank");
+        sym(api.CommDestroy, "ncclCommDestroy");
+        sym(api.GroupStart, "ncclGroupStart");
+        sym(api.GroupEnd, "ncclGroupEnd");
+        sym(api.Send, "ncclSend");
+        sym(api.Recv, "ncclRecv");
+        sym(api.AllGather, "ncclAllGather");
+        sym(api.GetErrorString, "ncclGetErrorString");
+        return good;
+    }();
+    return ok ? &api : nullptr;
+}
+
+static const NcclApi& N() {
+    const NcclApi* a = nccl_api();
+    if (!a) fail(AMGR_E_NCCL, "NCCL: libnccl.so.2 could not be loaded");
+    return *a;
+}
+
 #define NK(x)                                                                                         \
     do {                                                                                              \
         ncclResult_t r_ = (x);                                                                        \
-        if (r_ != ncclSuccess) ::amgr::fail(AMGR_E_NCCL, std::string("NCCL: ") + ncclGetErrorString(r_)); \
+        if (r_ != ncclSuccess) ::amgr::fail(AMGR_E_NCCL, std::string("NCCL: ") + ::amgr::N().GetErrorString(r_)); \
     } while (0)
 
 namespace {
@@ -110,14 +158,14 @@ static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
         LAUNCH(c, "halo_pack", 16.0 * L.send_idx.size(), k_gather_d, grid_for(L.send_idx.size(), 256, c.num_sms * 8),
                256, 0, L.send_idx.size(), x, L.send_idx.get(), L.send_buf.get(), g);
     if (d.world == 1 || (L.send_peer.empty() && L.recv_peer.empty())) return;
-    NK(ncclGroupStart());
+    NK(N().GroupStart());
     for (size_t k = 0; k < L.send_peer.size(); ++k)
-        NK(ncclSend(L.send_buf.get() + L.send_off[k], static_cast<size_t>(L.send_cnt[k]), ncclDouble, L.send_peer[k],
+        NK(N().Send(L.send_buf.get() + L.send_off[k], static_cast<size_t>(L.send_cnt[k]), ncclDouble, L.send_peer[k],
                     d.comm, c.stream));
     for (size_t k = 0; k < L.recv_peer.size(); ++k)
-        NK(ncclRecv(x + L.n_own + L.recv_off[k], static_cast<size_t>(L.recv_cnt[k]), ncclDouble, L.recv_peer[k],
+        NK(N().Recv(x + L.n_own + L.recv_off[k], static_cast<size_t>(L.recv_cnt[k]), ncclDouble, L.recv_peer[k],
                     d.comm, c.stream));
-    NK(ncclGroupEnd());
+    NK(N().GroupEnd());
 }
 
 // deterministic cross-rank sum of k local dots (d.dloc[0..k)) into outs
@@ -126,7 +174,7 @@ static void allsum(DistHier& d, int k, std::initializer_list<double*> outs) {
     std::vector<double*> o(outs);
     h2d(d.douts.get(), o.data(), static_cast<int64_t>(o.size()), c.stream);
     if (d.world > 1)
-        NK(ncclAllGather(d.dloc.get(), d.dall.get(), static_cast<size_t>(k), ncclDouble, d.comm, c.stream));
+        NK(N().AllGather(d.dloc.get(), d.dall.get(), static_cast<size_t>(k), ncclDouble, d.comm, c.stream));
     else
         d2d(d.dall.get(), d.dloc.get(), k, c.stream);
     LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), d.douts.get());
@@ -161,7 +209,7 @@ static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
     }
     // transition: replicate f_{T+1}, then the coarse levels on every rank
     if (d.world > 1)
-        NK(ncclAllGather(d.tsend.get(), d.tgather.get(), static_cast<size_t>(d.tpad), ncclDouble, d.comm, c.stream));
+        NK(N().AllGather(d.tsend.get(), d.tgather.get(), static_cast<size_t>(d.tpad), ncclDouble, d.comm, c.stream));
     else
         d2d(d.tgather.get(), d.tsend.get(), d.tpad, c.stream);
     LAUNCH(c, "dist", 0.0, k_unpad, grid_for(d.tpad, 256, 64), 256, 0, d.world, d.tpad, d.tgather.get(),
@@ -205,7 +253,8 @@ extern "C" {
 amgr_status amgr_nccl_unique_id(void* out128) {
     if (!out128) return AMGR_E_INVALID_ARGUMENT;
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return AMGR_E_NCCL;
+    const amgr::NcclApi* api = amgr::nccl_api();
+    if (!api || api->GetUniqueId(&id) != ncclSuccess) return AMGR_E_NCCL;
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     std::memcpy(out128, &id, sizeof(id));
     return AMGR_OK;
@@ -232,7 +281,7 @@ amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, in
         d->T = top;
         ncclUniqueId id;
         std::memcpy(&id, nccl_id128, sizeof(id));
-        NK(ncclCommInitRank(&d->comm, world, id, rank));
+        NK(::amgr::N().CommInitRank(&d->comm, world, id, rank));
         auto up32 = [&](amgr::DevArray<int>& dst, const int64_t* src, int64_t n) {
             std::vector<int> tmp(static_cast<size_t>(n));
             for (int64_t k = 0; k < n; ++k) tmp[k] = static_cast<int>(src[k]);
@@ -319,7 +368,7 @@ amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, in
 
 void amgr_dist_destroy(amgr_dist* d) {
     if (!d) return;
-    if (d->d && d->d->comm) ncclCommDestroy(d->d->comm);
+    if (d->d && d->d->comm) amgr::nccl_api()->CommDestroy(d->d->comm);
     delete d;
 }
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 
 import numpy as np
+import torch  # noqa: F401  -- loads torch's libnccl.so.2 before the library binds NCCL
 
 from . import Hierarchy, SolveParams, SolveStats, _check, _SolveParams, _SolveStats, lib
 from . import partition as PT
