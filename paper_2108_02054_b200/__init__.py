@@ -373,6 +373,9 @@ class Hierarchy:
         _check(lib().amgr_hier_level_lambda(self._p, lvl, C.byref(x)), self.ctx.ptr)
         return float(x.value)
 
+    def coarse_n(self) -> int:
+        return int(lib().amgr_hier_coarse_n(self._p))
+
     def coarse_lu(self):
         n = int(lib().amgr_hier_coarse_n(self._p))
         lu = np.zeros(max(n * n, 1))

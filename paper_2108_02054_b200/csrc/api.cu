@@ -132,6 +132,12 @@ void amgr_ctx_destroy(amgr_ctx* ctx) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    if (ctx->c.side) {
+        cudaStreamSynchronize(ctx->c.side);
+        cudaStreamDestroy(ctx->c.side);
+        cudaEventDestroy(ctx->c.fork_ev);
+        cudaEventDestroy(ctx->c.join_ev);
+    }
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
 }
@@ -368,6 +374,8 @@ amgr_status amgr_hier_coarse_lu(const amgr_hier* h, double* lu, int64_t* piv) {
     if (!h || !lu || !piv) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] {
         amgr::Hier& H = *h->h;
+        if (!H.lu_formed)
+            amgr::invalid("amgr_hier_coarse_lu: no LU factor is formed in the inverse coarse-solve mode");
         amgr::d2h(lu, H.lu.get(), H.nL * H.nL, H.ctx->stream);
         amgr::d2h(piv, H.piv.get(), H.nL, H.ctx->stream);
         CK(cudaStreamSynchronize(H.ctx->stream));

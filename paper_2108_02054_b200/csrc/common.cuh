@@ -58,7 +58,40 @@ struct Ctx {
     Probe probe;
     int num_sms = 148;
     int cur_level = -1;  // hierarchy level the orchestration is currently launching for
+    // auxiliary stream for independent work inside one call (created lazily,
+    // joined back into `stream` before the call returns)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
+
+// Run fn with c.stream temporarily redirected to the side stream, ordered
+// after everything already queued on the main stream; returns with the side
+// work NOT yet joined (call join_side).
+template <class F>
+void on_side(Ctx& c, F&& fn) {
+    if (!c.side) {
+        CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c.fork_ev, c.stream));
+    CK(cudaStreamWaitEvent(c.side, c.fork_ev, 0));
+    cudaStream_t main = c.stream;
+    c.stream = c.side;
+    try {
+        fn();
+    } catch (...) {
+        c.stream = main;
+        throw;
+    }
+    c.stream = main;
+}
+
+inline void join_side(Ctx& c) {
+    if (!c.side) return;
+    CK(cudaEventRecord(c.join_ev, c.side));
+    CK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
+}
 
 #define LAUNCH(ctx, family, bytes, kernel, grid, block, smem, ...)                  \
     do {                                                                              \

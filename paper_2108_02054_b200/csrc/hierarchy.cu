@@ -171,11 +171,19 @@ void coarse_factorize(Hier& h, int* status) {
     if (h.lu.size() != h.nL * h.nL) h.lu.alloc(h.nL * h.nL, c.stream);
     if (h.piv.size() != h.nL) h.piv.alloc(h.nL, c.stream);
     lu_densify(c, L.view(), h.lu.get());
-    lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
+    h.lu_formed = true;
     if (h.prm.coarse_solve == AMGR_COARSE_INVERSE) {
         if (h.inv.size() != h.nL * h.nL) h.inv.alloc(h.nL * h.nL, c.stream);
+        // small systems: direct Gauss-Jordan inverse, no LU factor is formed
+        if (dense_inverse_direct(c, h.nL, h.lu.get(), h.inv.get(), h.piv.get(), status)) {
+            h.lu_formed = false;
+            return;
+        }
+        lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
         lu_inverse(c, h.nL, h.lu.get(), h.piv.get(), h.inv.get());
+        return;
     }
+    lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
 }
 
 static void coarse_solve(Hier& h, const double* b, double* x, Gate g) {
@@ -224,14 +232,13 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     Work& W = work(h);
     const size_t L = h.lv.size();
     const bool jacobi = false;  // fused coarse-level Jacobi disabled: separate smoother kernel per level
+    // Galerkin chain first; then the coarsest dense factorization (one CTA)
+    // runs on the side stream concurrently with the per-level smoother
+    // rebuilds, which do not depend on it.  Errors are still reported in the
+    // reference's order (check_rebuild_errors reads every slot).
     for (size_t i = 0; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
-        if (i == 0 || !jacobi) {
-            clk.begin(PH_SMOOTHER);
-            build_smoother(c, A, h.prm, W.err.get() + i);
-            clk.end(PH_SMOOTHER);
-        }
         clk.begin(PH_GALERKIN);
         Level& B = h.lv[i + 1];
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
@@ -246,9 +253,19 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
-    clk.begin(PH_COARSE);
-    coarse_factorize(h, W.err.get() + L);
-    clk.end(PH_COARSE);
+    on_side(c, [&] {
+        clk.begin(PH_COARSE);
+        coarse_factorize(h, W.err.get() + L);
+        clk.end(PH_COARSE);
+    });
+    for (size_t i = 0; i + 1 < L; ++i) {
+        if (i > 0 && jacobi) continue;
+        c.cur_level = static_cast<int>(i);
+        clk.begin(PH_SMOOTHER);
+        build_smoother(c, h.lv[i], h.prm, W.err.get() + i);
+        clk.end(PH_SMOOTHER);
+    }
+    join_side(c);
     c.cur_level = -1;
 }
 

@@ -86,6 +86,7 @@ struct Hier {
     AmgP prm;
     std::vector<Level> lv;
     DevArray<double> lu;
+    bool lu_formed = false;   // false in the inverse mode when the direct Gauss-Jordan kernel ran
     DevArray<int64_t> piv;
     DevArray<double> inv;  // AMGR_COARSE_INVERSE
     int64_t nL = 0;

@@ -85,6 +85,9 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
 
 // FAST mode (extension): explicit inverse from the LU factors, applied as a matvec
 void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv);
+// Gauss-Jordan inverse of the dense matrix a (n <= 160) straight into inv;
+// false when n is outside the register-resident kernel's range.
+bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status);
 void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g = {});
 
 // ---- Chebyshev smoother (extension; oracle/amg_oracle.c smooth_cheb / power_lambda) ----

@@ -681,6 +681,210 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
         for (int t = tid; t < nn; t += blockDim.x) gm[t] = m[t];
 }
 
+// Register-resident dense elimination for small coarsest systems (n <= 160,
+// the usual case: the coarsening stalls at ~150 rows).  512 threads; thread
+// (ty, tx) holds rows ty + 16q and columns tx + 32m of the matrix in
+// registers.  Rows are never moved: lp[] maps logical -> physical row and
+// posof[] is its inverse, so the reference's row swaps (dense_lu.cpp:21-46)
+// cost two integer stores.  Per step the pivot column and the pivot row are
+// broadcast through shared memory (3 barriers).  The step loop is split into
+// an unrolled loop over the 32-column group mb and a runtime loop over the
+// lane kl, so every register access uses a compile-time index (no local
+// memory) and column groups left of the pivot are skipped at compile time.
+//   GJ = false: LU with the reference's pivot rule and operation order
+//               (l = m[i][k] / pivot; m[i][j] -= l * m[k][j]).  Each row's
+//               multipliers and, when it becomes the pivot row, its final U
+//               part go to a shared-memory history Ls (by physical row), so
+//               the register update is a bare DMUL + DADD on every row with
+//               no predicates (finished rows just accumulate garbage); the
+//               factor is written from Ls in the reference's swapped order.
+//   GJ = true : in-place Gauss-Jordan inverse for AMGR_COARSE_INVERSE
+//               (tolerance-level extension; output inv = A^{-1}).
+constexpr int DR_ROWS = 10, DR_COLS = 5, DR_THREADS = 512, DR_MAXN = 160;
+
+// predicated select in PTX: keeps NVVM from turning "for q: if (q == x) use
+// a[q]" into a dynamically indexed (local-memory) access to the register tile
+__device__ __forceinline__ double dr_sel(bool p, double a, double b) {
+    double r;
+    asm("{.reg .pred q; setp.ne.b32 q, %1, 0; selp.f64 %0, %2, %3, q;}" : "=d"(r) : "r"(static_cast<int>(p)), "d"(a),
+        "d"(b));
+    return r;
+}
+
+template <bool GJ>
+__global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double* gin, double* gout,
+                                                             int64_t* piv, int* status) {
+    extern __shared__ double Ls[];  // LU: n x n multiplier history, row = physical row
+    __shared__ double colbuf[2][DR_MAXN], coll[DR_MAXN], rowbuf[DR_MAXN], lbuf[DR_MAXN];
+    __shared__ int lp[DR_MAXN], posof[DR_MAXN];
+    __shared__ int s_r, s_stop;
+    __shared__ double s_piv;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, lane = tx;
+    double a[DR_ROWS][DR_COLS];
+    for (int i = tid; i < DR_MAXN; i += DR_THREADS) {
+        colbuf[0][i] = 0.0;
+        colbuf[1][i] = 0.0;
+        lbuf[i] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < DR_ROWS; ++q)
+#pragma unroll
+        for (int m = 0; m < DR_COLS; ++m) {
+            const int i = ty + 16 * q, j = tx + 32 * m;
+            a[q][m] = (i < n && j < n) ? gin[static_cast<int64_t>(i) * n + j] : 0.0;
+        }
+    for (int i = tid; i < DR_MAXN; i += DR_THREADS) {
+        lp[i] = i;
+        posof[i] = i;
+        rowbuf[i] = 0.0;  // columns >= n stay 0
+    }
+    if (tid == 0) {
+        *status = -1;
+        s_stop = 0;
+    }
+    __syncthreads();
+    bool stop = false;
+#pragma unroll
+    for (int mb = 0; mb < DR_COLS; ++mb) {
+        for (int kl = 0; kl < 32; ++kl) {
+            const int k = 32 * mb + kl;
+            if (k >= n) break;
+            double* cb = colbuf[k & 1];
+            // 1. pivot column -> smem, by physical row (cb) and logical row (coll)
+            if (tx == kl) {
+#pragma unroll
+                for (int q = 0; q < DR_ROWS; ++q) {
+                    const int i = ty + 16 * q;
+                    if (i < n) {
+                        cb[i] = a[q][mb];
+                        coll[posof[i]] = a[q][mb];
+                    }
+                }
+            }
+            __syncthreads();
+            // 2. pivot: first maximum of |.| over logical rows k..n-1
+            if (ty == 0) {
+                double best = -1.0;
+                int bi = 0x7fffffff;
+                for (int i = k + lane; i < n; i += 32) {
+                    const double v = fabs(coll[i]);
+                    if (v > best) {
+                        best = v;
+                        bi = i;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ob = __shfl_down_sync(0xffffffffu, best, off);
+                    const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+                    if (ob > best || (ob == best && oi < bi)) {
+                        best = ob;
+                        bi = oi;
+                    }
+                }
+                if (lane == 0) {
+                    int p = bi;
+                    if (p == 0x7fffffff || !(fabs(coll[k]) < best)) p = k;  // ties / NaN keep k
+                    if (p != k) {
+                        const int rk = lp[k], rp = lp[p];
+                        lp[k] = rp;
+                        lp[p] = rk;
+                        posof[rp] = k;
+                        posof[rk] = p;
+                    }
+                    if (!GJ) piv[k] = p;
+                    const int r = lp[k];
+                    s_r = r;
+                    s_piv = cb[r];
+                    if (cb[r] == 0.0) {
+                        *status = k;
+                        s_stop = 1;
+                    }
+                    if (GJ) cb[r] = 0.0;  // f = 0: the update leaves the pivot row alone
+                }
+            }
+            __syncthreads();
+            if (s_stop) {
+                stop = true;
+                break;
+            }
+            const int r = s_r;
+            const double pivot = s_piv;
+            // 3. pivot row -> smem (owner warp: ty == r % 16, register row r / 16)
+            if (ty == (r & 15)) {
+                const int qr = r >> 4;
+                const double ip = GJ ? 1.0 / pivot : 0.0;
+#pragma unroll
+                for (int m = 0; m < DR_COLS; ++m) {
+                    double v = a[0][m];
+#pragma unroll
+                    for (int q = 1; q < DR_ROWS; ++q) v = dr_sel(q == qr, a[q][m], v);
+                    const int j = tx + 32 * m;
+                    if (GJ) {
+                        v = (m == mb && tx == kl) ? ip : v * ip;
+#pragma unroll
+                        for (int q = 0; q < DR_ROWS; ++q) a[q][m] = dr_sel(q == qr, v, a[q][m]);
+                    }
+                    if (j < n) {
+                        rowbuf[j] = v;
+                        if (!GJ && j >= k) Ls[r * n + j] = v;  // final U row of r
+                    }
+                }
+            }
+            if (!GJ)
+                for (int li = k + 1 + tid; li < n; li += DR_THREADS) {
+                    const int ph = lp[li];
+                    const double l = __ddiv_rn(cb[ph], pivot);
+                    lbuf[ph] = l;
+                    Ls[ph * n + k] = l;
+                }
+            __syncthreads();
+            // 4. rank-1 update of the register tile
+            double rb[DR_COLS];
+#pragma unroll
+            for (int m = 0; m < DR_COLS; ++m) rb[m] = rowbuf[tx + 32 * m];
+            // row loads first (independent), then predicated updates: no
+            // per-row branches, so the 10 rows' DMUL/DADD chains overlap
+            // unpredicated updates: rows that must not change either have
+            // f = 0 (GJ pivot row, padding) or are finished and already saved
+            // in the Ls history (LU); padding rows/columns hold garbage
+            if (GJ) {
+#pragma unroll
+                for (int q = 0; q < DR_ROWS; ++q) {
+                    const double f = cb[ty + 16 * q];
+                    if (tx == kl) a[q][mb] = dr_sel(ty + 16 * q != r, 0.0, a[q][mb]);
+#pragma unroll
+                    for (int m = 0; m < DR_COLS; ++m) a[q][m] = __fma_rn(-f, rb[m], a[q][m]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < DR_ROWS; ++q) {
+                    const double l = lbuf[ty + 16 * q];
+#pragma unroll
+                    for (int m = mb; m < DR_COLS; ++m) a[q][m] = dsub(a[q][m], dmul(l, rb[m]));
+                }
+            }
+        }
+        if (stop) break;
+    }
+    __syncthreads();
+    // write back: LU rows in logical (swapped) order, L part from the history;
+    // inverse un-permuted: inv[posof[p]][lp[j]] = a[p][j]
+#pragma unroll
+    for (int q = 0; q < DR_ROWS; ++q) {
+        const int i = ty + 16 * q;
+        if (i < n) {
+            const int rl = posof[i];
+            const int64_t row = static_cast<int64_t>(rl) * n;
+#pragma unroll
+            for (int m = 0; m < DR_COLS; ++m) {
+                const int j = tx + 32 * m;
+                if (j < n) gout[GJ ? row + lp[j] : row + j] = GJ ? a[q][m] : Ls[i * n + j];
+            }
+        }
+    }
+}
+
 constexpr int LS_THREADS = 64;
 
 __device__ __forceinline__ void named_bar(int id, int count) {
@@ -1012,6 +1216,14 @@ void lu_densify(Ctx& c, const CsrView& A, double* dense) {
 
 void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
     if (n == 0) return;
+    if (n <= DR_MAXN) {
+        const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_dense_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(double) * DR_MAXN * DR_MAXN)));
+        LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status);
+        return;
+    }
     if (n > 2048) invalid("coarse_factorize: coarse system larger than 2048 unknowns is not supported on device");
     const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
     const int use_smem = sm <= 180 * 1024 ? 1 : 0;
@@ -1027,6 +1239,12 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
+}
+
+bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {
+    if (n == 0 || n > DR_MAXN) return false;
+    LAUNCH(c, "coarse", 0.0, k_dense_reg<true>, 1, DR_THREADS, 0, static_cast<int>(n), a, inv, piv, status);
+    return true;
 }
 
 void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv) {

@@ -22,7 +22,7 @@ def _bits(a):
     return np.asarray(a, np.float64).view(np.int64)
 
 
-def assert_same_hierarchy(g, r, values=True):
+def assert_same_hierarchy(g, r, values=True, lu=True):
     assert g.num_levels() == len(r.levels), (g.num_levels(), len(r.levels))
     for l, RL in enumerate(r.levels):
         rp, ci, v = g.level_A(l)
@@ -38,7 +38,7 @@ def assert_same_hierarchy(g, r, values=True):
         if RL.inv_diag is not None and values:
             np.testing.assert_array_equal(_bits(g.level_smoother(l)), _bits(RL.inv_diag),
                                           err_msg=f"level {l} inv_diag")
-    if values:
+    if values and lu:
         lu, piv = g.coarse_lu()
         np.testing.assert_array_equal(piv, r.piv)
         np.testing.assert_array_equal(_bits(lu), _bits(r.lu))
@@ -190,7 +190,10 @@ def test_inverse_coarse_mode_solve_parity(ctx, name):
     he = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
     hi = amg.setup(A, amg.AmgParams(coarse_solve="inverse", **kw), ctx=ctx)
     r = ref.setup(A, ref.params(**kw))
-    assert_same_hierarchy(hi, r)
+    assert_same_hierarchy(hi, r, lu=hi.coarse_n() > 160)  # small coarse systems: direct inverse, no LU
+    if hi.coarse_n() <= 160:
+        with pytest.raises(amg.InvalidArgument, match="inverse"):
+            hi.coarse_lu()
     f = np.random.default_rng(3).uniform(-1, 1, len(A[0]) - 1)
     ue, ui = amg.vcycle(he, f), amg.vcycle(hi, f)
     assert np.linalg.norm(ue - ui) <= 1e-12 * np.linalg.norm(ue)

@@ -69,7 +69,36 @@ def main():
         cnt, ms, by = ctx.probe_read()
         if cnt:
             print(f"  {fam:14s} launches={cnt:6d} ms={ms:9.3f} GB/s={by/ms/1e6 if ms>0 else 0:8.1f}")
+    # per-level device time (family@level) for the V-cycle and rebuild kernels
+    lf = ["vcycle_down", "vcycle_smooth", "restrict", "prolong", "vcycle_premul", "rap", "smoother"]
+    print("  level " + " ".join(f"{x[:13]:>22s}" for x in lf))
+    for l in range(h.num_levels()):
+        cells = []
+        for fam in lf:
+            ctx.probe(f"{fam}@{l}")
+            h.rebuild_values(vals[1].data_ptr(), adopt=True)
+            u.zero_()
+            torch.cuda.synchronize()
+            amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()))
+            cnt, ms, by = ctx.probe_read()
+            cells.append(f"{ms:8.3f}ms/{by/ms/1e6 if ms>0 else 0:6.0f}({cnt:4d})")
+        print(f"  {l:5d} " + " ".join(f"{c:>22s}" for c in cells))
     ctx.probe(None)
+    # one V-cycle, device time
+    fz = f.clone()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(3):
+        amg.vcycle_device(h, fz.data_ptr(), u.data_ptr())
+    ctx.synchronize()
+    if s is not None:
+        with torch.cuda.stream(s):
+            ev0.record()
+            for _ in range(20):
+                amg.vcycle_device(h, fz.data_ptr(), u.data_ptr())
+            ev1.record()
+        ctx.synchronize()
+        print(f"  vcycle: {ev0.elapsed_time(ev1)/20:.3f} ms")
 
 
 if __name__ == "__main__":
