@@ -249,7 +249,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         }
         rap_numeric(c, A.pat->n, B.pat->n, B.pat->rp.get(), B.pat->diag.get(), A.rap->nnz_c, A.rap->cptr.get(),
                     A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz, fuse ? B.w.get() : nullptr,
-                    W.err.get() + i + 1);
+                    W.err.get() + i + 1, A.rap->max_chunk);
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
@@ -281,6 +281,7 @@ void symbolic_pass(Hier& h) {
         plan->nnz_c = s.nnz_c;
         plan->cptr = std::move(s.cptr);
         plan->contrib = std::move(s.contrib);
+        plan->max_chunk = rap_chunk_max(c, plan->nnz_c, plan->cptr.get());
         A.rap = plan;
         auto P = std::make_shared<Pattern>();
         P->n = A.T->nc;
@@ -405,6 +406,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             plan->nnz_c = s.nnz_c;
             plan->cptr = std::move(s.cptr);
             plan->contrib = std::move(s.contrib);
+            plan->max_chunk = rap_chunk_max(c, plan->nnz_c, plan->cptr.get());
             auto P = std::make_shared<Pattern>();
             P->n = nc;
             P->ncols = nc;
@@ -417,7 +419,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             CsrView nv = next.view();
             find_diag(c, nv, P->diag.get());
             rap_numeric(c, Av.n, nc, P->rp.get(), P->diag.get(), s.nnz_c, plan->cptr.get(), plan->contrib.get(),
-                        Av.val, next.val.get(), Av.nnz, nullptr, nullptr);
+                        Av.val, next.val.get(), Av.nnz, nullptr, nullptr, plan->max_chunk);
             P->max_span = max_group_span(c, P->rp.get(), P->n);
             cur.rap = plan;
         }

@@ -38,6 +38,7 @@ struct Transfer {
 // Cached Galerkin plan A_i -> A_{i+1}.
 struct RapPlan {
     int64_t nnz_f = 0, nnz_c = 0;
+    int max_chunk = -1;  // largest contrib count of a k_rap_tma chunk (-1: not computed)
     DevArray<int> cptr, contrib;
 };
 

@@ -67,8 +67,11 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
 // Numeric Galerkin product on the cached plan (two-level bracket of
 // spmm(R, spmm(A, P)), csr.cpp:145-194).  crp/cdiag/wc/bad are reserved for
 // a fused coarse-level smoother rebuild (currently a separate kernel).
+// largest contrib count of any RT_CH-entry chunk of a plan (TMA stage size; host sync)
+int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr);
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
-                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad);
+                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad,
+                 int max_chunk = -1);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);

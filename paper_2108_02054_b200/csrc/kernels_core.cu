@@ -529,36 +529,197 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 // use the default policy so sectors shared by neighbouring aggregates can hit
 // in L2.  (Variants measured slower in round 1 — row-group warps, shared-memory
 // staging, 4 entries per thread: see DESIGN.md §3.3.)
-__global__ void k_rap(int64_t nnz_c, const int* __restrict__ cptr, const int* __restrict__ contrib,
-                      const double* __restrict__ af, double* __restrict__ ac) {
-    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nnz_c;
-         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int p0 = __ldcs(cptr + c), p1 = __ldcs(cptr + c + 1);
-        double acc = 0.0, part = 0.0;
-        int p = p0;
-        for (; p + 2 <= p1; p += 2) {
-            const int e0 = __ldcs(contrib + p), e1 = __ldcs(contrib + p + 1);
-            const double v0 = __ldg(af + (e0 & 0x7fffffff)), v1 = __ldg(af + (e1 & 0x7fffffff));
-            part = dadd(part, v0);
-            if (e0 < 0) {
-                acc = dadd(acc, part);
-                part = 0.0;
-            }
-            part = dadd(part, v1);
-            if (e1 < 0) {
-                acc = dadd(acc, part);
-                part = 0.0;
-            }
-        }
-        if (p < p1) {
-            const int e0 = __ldcs(contrib + p);
-            part = dadd(part, __ldg(af + (e0 & 0x7fffffff)));
-            if (e0 < 0) acc = dadd(acc, part);
-        }
-        __stcs(ac + c, acc);
+// Numeric Galerkin product: coarse entry c sums its fine
+// nonzeros contrib[cptr[c]..cptr[c+1]) in the reference's two-level bracket
+// order (bit 31 of a contrib marks the end of one fine row's partial sum).
+// Persistent blocks sweep the coarse entries in chunks of 256 x RAP_ILP,
+// all blocks advancing together, so the fine values touched by a chunk (the
+// rows of a few neighbouring aggregates) are still in L2 when the next chunk
+// reuses their sectors.  Each thread runs RAP_ILP independent entries with
+// the first two contributions loaded speculatively (avg 1.3 per entry at
+// L0), so the cptr -> contrib -> value chains overlap.
+constexpr int RAP_ILP = 4, RAP_BLOCK = 256;
+
+__device__ __forceinline__ void rap_acc(double v, int e, double& acc, double& part) {
+    part = dadd(part, v);
+    if (e < 0) {
+        acc = dadd(acc, part);
+        part = 0.0;
     }
 }
 
+__global__ void __launch_bounds__(RAP_BLOCK) k_rap(int64_t nnz_c, const int* __restrict__ cptr,
+                                                   const int* __restrict__ contrib, const double* __restrict__ af,
+                                                   double* __restrict__ ac) {
+    constexpr int64_t CHUNK = static_cast<int64_t>(RAP_BLOCK) * RAP_ILP;
+    for (int64_t base = blockIdx.x * CHUNK; base < nnz_c; base += static_cast<int64_t>(gridDim.x) * CHUNK) {
+        int p0[RAP_ILP], p1[RAP_ILP], e0[RAP_ILP], e1[RAP_ILP];
+        double v0[RAP_ILP], v1[RAP_ILP];
+#pragma unroll
+        for (int k = 0; k < RAP_ILP; ++k) {
+            const int64_t c = base + k * RAP_BLOCK + threadIdx.x;
+            p0[k] = c < nnz_c ? __ldcs(cptr + c) : 0;
+            p1[k] = c < nnz_c ? __ldcs(cptr + c + 1) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < RAP_ILP; ++k) {
+            e0[k] = p0[k] < p1[k] ? __ldcs(contrib + p0[k]) : 0;
+            e1[k] = p0[k] + 1 < p1[k] ? __ldcs(contrib + p0[k] + 1) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < RAP_ILP; ++k) {
+            v0[k] = p0[k] < p1[k] ? __ldg(af + (e0[k] & 0x7fffffff)) : 0.0;
+            v1[k] = p0[k] + 1 < p1[k] ? __ldg(af + (e1[k] & 0x7fffffff)) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < RAP_ILP; ++k) {
+            const int64_t c = base + k * RAP_BLOCK + threadIdx.x;
+            if (c >= nnz_c) continue;
+            double acc = 0.0, part = 0.0;
+            if (p0[k] < p1[k]) rap_acc(v0[k], e0[k], acc, part);
+            if (p0[k] + 1 < p1[k]) rap_acc(v1[k], e1[k], acc, part);
+            for (int q = p0[k] + 2; q < p1[k]; ++q) {
+                const int e = __ldcs(contrib + q);
+                rap_acc(__ldg(af + (e & 0x7fffffff)), e, acc, part);
+            }
+            __stcs(ac + c, acc);
+        }
+    }
+}
+
+// TMA-staged variant: the streamed plan arrays (cptr and the chunk's
+// contrib range) arrive by 1-D bulk copies into a double-buffered shared
+// stage one chunk ahead, so the only global latency left per entry is the
+// fine-value gather.  Chunks of RT_CH coarse entries, persistent blocks.
+constexpr int RT_CH = 1024, RT_BLOCK = 256;
+
+// PER entries per thread (strided by RT_BLOCK inside the chunk), the first B
+// contributions of each loaded speculatively, the rest in batches of B; the
+// accumulation is always the strict per-entry sequence of rap_acc.
+template <int PER, int B>
+__global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const int* __restrict__ cptr,
+                                                         const int* __restrict__ contrib,
+                                                         const double* __restrict__ af, double* __restrict__ ac,
+                                                         int cstage) {
+    static_assert(PER * RT_BLOCK <= RT_CH && RT_CH % (PER * RT_BLOCK) == 0, "chunk split");
+    extern __shared__ __align__(128) unsigned char rt_smem[];
+    int* s_cp = reinterpret_cast<int*>(rt_smem);  // [2][RT_CH + 4]
+    int* s_cn = s_cp + 2 * (RT_CH + 4);            // [2][cstage]
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int s_ab[2];
+    const int tid = threadIdx.x;
+    const int64_t nchunks = (nnz_c + RT_CH - 1) / RT_CH;
+    const int64_t G = gridDim.x;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // thread 0: stage chunk j whose contrib range [a, b) is known
+    auto issue = [&](int64_t j, int st, int a, int b) {
+        const int64_t c0 = j * RT_CH;
+        const int64_t c1 = c0 + RT_CH < nnz_c ? c0 + RT_CH : nnz_c;
+        const int ab = a & ~3, be = (b + 3) & ~3;
+        s_ab[st] = ab;
+        const uint32_t bc = static_cast<uint32_t>((c1 - c0 + 1 + 3) & ~3) * 4u;
+        const uint32_t bn = static_cast<uint32_t>(be - ab) * 4u;
+        fence_proxy_async();
+        mbar_expect_tx(&bar[st], bc + bn);
+        tma_load_1d(s_cp + st * (RT_CH + 4), cptr + c0, bc, &bar[st]);
+        if (bn) tma_load_1d(s_cn + st * cstage, contrib + ab, bn, &bar[st]);
+    };
+    auto range = [&](int64_t j, int& a, int& b) {
+        const int64_t c0 = j * RT_CH;
+        a = __ldg(cptr + c0);
+        b = __ldg(cptr + (c0 + RT_CH < nnz_c ? c0 + RT_CH : nnz_c));
+    };
+    int64_t j = blockIdx.x;
+    if (tid == 0) {
+        int a, b;
+        if (j < nchunks) {
+            range(j, a, b);
+            issue(j, 0, a, b);
+        }
+        if (j + G < nchunks) {
+            range(j + G, a, b);
+            issue(j + G, 1, a, b);
+        }
+    }
+    int st = 0;
+    uint32_t phase = 0;
+    for (; j < nchunks; j += G) {
+        // contrib range of the chunk two ahead (used after this chunk)
+        int na = 0, nb = 0;
+        const bool more = tid == 0 && j + 2 * G < nchunks;
+        if (more) range(j + 2 * G, na, nb);
+        mbar_wait(&bar[st], (phase >> st) & 1u);
+        phase ^= (1u << st);
+        const int64_t c0 = j * RT_CH;
+        const int* cp = s_cp + st * (RT_CH + 4);
+        const int* cn = s_cn + st * cstage;
+        const int ab = s_ab[st];
+        for (int sub = 0; sub < RT_CH; sub += PER * RT_BLOCK) {
+            int p0[PER], p1[PER], e[PER][B];
+            double v[PER][B];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int x = sub + k * RT_BLOCK + tid;
+                const bool ok = c0 + x < nnz_c;
+                p0[k] = ok ? cp[x] - ab : 0;
+                p1[k] = ok ? cp[x + 1] - ab : 0;
+#pragma unroll
+                for (int t = 0; t < B; ++t) e[k][t] = p0[k] + t < p1[k] ? cn[p0[k] + t] : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k)
+#pragma unroll
+                for (int t = 0; t < B; ++t) v[k][t] = p0[k] + t < p1[k] ? __ldg(af + (e[k][t] & 0x7fffffff)) : 0.0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int64_t c = c0 + sub + k * RT_BLOCK + tid;
+                if (c >= nnz_c) continue;
+                double acc = 0.0, part = 0.0;
+#pragma unroll
+                for (int t = 0; t < B; ++t)
+                    if (p0[k] + t < p1[k]) rap_acc(v[k][t], e[k][t], acc, part);
+                for (int q = p0[k] + B; q < p1[k]; q += B) {
+                    int ee[B];
+                    double vv[B];
+#pragma unroll
+                    for (int t = 0; t < B; ++t) ee[t] = q + t < p1[k] ? cn[q + t] : 0;
+#pragma unroll
+                    for (int t = 0; t < B; ++t) vv[t] = q + t < p1[k] ? __ldg(af + (ee[t] & 0x7fffffff)) : 0.0;
+#pragma unroll
+                    for (int t = 0; t < B; ++t)
+                        if (q + t < p1[k]) rap_acc(vv[t], ee[t], acc, part);
+                }
+                __stcs(ac + c, acc);
+            }
+        }
+        __syncthreads();  // stage st consumed
+        if (more) issue(j + 2 * G, st, na, nb);
+        st ^= 1;
+    }
+}
+
+template <int PER, int B>
+void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                    double* ac, int cstage, size_t sm) {
+    static bool attr = false;
+    if (sm > 48 * 1024 && !attr) {
+        CK(cudaFuncSetAttribute(k_rap_tma<PER, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr = true;
+    }
+    int res = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_rap_tma<PER, B>, RT_BLOCK, sm));
+    const int64_t chunks = (nnz_c + RT_CH - 1) / RT_CH;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * std::max(res, 1)));
+    LAUNCH(c, "rap", bytes, (k_rap_tma<PER, B>), grid, RT_BLOCK, sm, nnz_c, cptr, contrib, af, ac, cstage);
+}
+
+// ---- end k_rap_tma
 __global__ void k_jacobi(int n, const double* __restrict__ val, const int* __restrict__ dpos,
                          double* __restrict__ w, int* bad) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -1186,8 +1347,32 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
     launch_rowpass(c, "resid_norm", spmv_bytes(A), A, OpResidNorm{f, x, r, r2}, g, s, true);
 }
 
+__global__ void k_rap_chunk_max(int64_t nnz_c, const int* __restrict__ cptr, int* out) {
+    const int64_t nchunks = (nnz_c + RT_CH - 1) / RT_CH;
+    int m = 0;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nchunks;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c1 = (j + 1) * RT_CH < nnz_c ? (j + 1) * RT_CH : nnz_c;
+        m = max(m, cptr[c1] - cptr[j * RT_CH]);
+    }
+    atomicMax(out, m);
+}
+
+int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr) {
+    if (nnz_c == 0) return 0;
+    DevArray<int> d(1, c.stream);
+    CK(cudaMemsetAsync(d.get(), 0, sizeof(int), c.stream));
+    LAUNCH(c, "setup", 0.0, k_rap_chunk_max, grid_for((nnz_c + RT_CH - 1) / RT_CH, 256, c.num_sms * 4), 256, 0,
+           nnz_c, cptr, d.get());
+    int h = 0;
+    d2h(&h, d.get(), 1, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    return h;
+}
+
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
-                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad) {
+                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad,
+                 int max_chunk) {
     if (nnz_c == 0) return;
     (void)crp;
     (void)cdiag;
@@ -1195,7 +1380,24 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdia
     (void)bad;
     // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1)
     const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
-    LAUNCH(c, "rap", bytes, k_rap, grid_for(nnz_c, 256, c.num_sms * 32), 256, 0, nnz_c, cptr, contrib, af, ac);
+    if (max_chunk >= 0) {
+        const int cstage = (max_chunk + 8 + 3) & ~3;
+        const size_t sm = sizeof(int) * (2 * (RT_CH + 4) + 2 * static_cast<size_t>(cstage));
+        if (sm <= 96 * 1024) {
+            // contributions per coarse entry: 1.3 (C3 L0), 2.4 (L1), 3-6 below
+            if (2 * nnz_f <= 5 * nnz_c)
+                launch_rap_tma<4, 2>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm);
+            else
+                launch_rap_tma<2, 4>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm);
+            return;
+        }
+    }
+    // persistent grid: exactly the resident blocks, so the sweep stays in order
+    static int resident = 0;
+    if (!resident) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_rap, RAP_BLOCK, 0));
+    const int64_t chunks = (nnz_c + RAP_BLOCK * RAP_ILP - 1) / (RAP_BLOCK * RAP_ILP);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * resident));
+    LAUNCH(c, "rap", bytes, k_rap, grid, RAP_BLOCK, 0, nnz_c, cptr, contrib, af, ac);
 }
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
