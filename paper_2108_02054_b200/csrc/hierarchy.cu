@@ -606,6 +606,24 @@ static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
 // V-cycle over levels s..L-1 (s = 0: the whole hierarchy); f and u live on
 // level s.  The partitioned multi-GPU solve runs the replicated coarse levels
 // through this with s = T+1.
+// First level of the persistent V-cycle tail (kernels_tail.cu): the first
+// level at or below s from which every operator has at most AMGR_TAIL_NNZ
+// nonzeros; -1 = no tail.  Off by default: measured on B200 the grid-barrier
+// version is slower than the per-level launches (each phase still pays ~3
+// dependent L2 round trips plus a ~1.5 us grid barrier), see DESIGN.md.
+static int tail_start(const Hier& h, size_t s) {
+    const char* e = std::getenv("AMGR_TAIL_NNZ");
+    const long thr = e ? std::atol(e) : 0L;
+    const size_t L = h.lv.size();
+    if (thr <= 0 || h.prm.pre != 1 || h.prm.post != 1 || h.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV) return -1;
+    for (size_t i = s; i + 1 < L; ++i) {
+        bool small = true;
+        for (size_t k = i; k + 1 < L; ++k) small = small && h.lv[k].pat->nnz <= thr;
+        if (small) return (L - 1 - i) <= static_cast<size_t>(TAIL_MAX) ? static_cast<int>(i) : -1;
+    }
+    return -1;
+}
+
 void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
@@ -626,8 +644,10 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     std::vector<double*> cur(L);
     const int pre = h.prm.pre, post = h.prm.post;
     if (pre >= 1) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
+    const int ts = tail_start(h, s);
+    const size_t top = ts >= 0 ? static_cast<size_t>(ts) : L - 1;  // levels >= top: tail kernels
     // down leg
-    for (size_t i = s; i + 1 < L; ++i) {
+    for (size_t i = s; i < top; ++i) {
         c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();
@@ -656,12 +676,44 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
         restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, W.f[i + 1].get(),
                      next_smoothed ? h.lv[i + 1].w.get() : nullptr, om, next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
+    TailDesc td;
+    if (ts >= 0) {
+        for (size_t l = top; l + 1 < L; ++l) {
+            const Level& Li = h.lv[l];
+            const CsrView A = Li.view();
+            TailLevel& t = td.lv[td.count++];
+            t.n = static_cast<int>(A.n);
+            t.nc = static_cast<int>(Li.T->nc);
+            t.rp = A.rp;
+            t.col = A.col;
+            t.val = A.val;
+            t.w = Li.w.get();
+            t.agg = Li.T->agg.get();
+            t.mptr = Li.T->mptr.get();
+            t.midx = Li.T->midx.get();
+            t.f = fin[l];
+            t.u0 = W.u[l].get();
+            t.r = W.r[l].get();
+            t.fc = W.f[l + 1].get();
+            t.u0c = l + 2 < L ? W.u[l + 1].get() : nullptr;
+            t.wc = l + 2 < L ? h.lv[l + 1].w.get() : nullptr;
+            t.uout = l == s ? u : W.t[l].get();
+            t.ec = l + 2 < L ? W.t[l + 1].get() : W.u[L - 1].get();
+            ufinal[l] = t.uout;
+        }
+        c.cur_level = static_cast<int>(top);
+        tail_down(c, td, om, g);
+    }
     // coarsest: direct solve (hierarchy.cpp:175)
     c.cur_level = static_cast<int>(L - 1);
     coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
     ufinal[L - 1] = W.u[L - 1].get();
+    if (ts >= 0) {
+        c.cur_level = static_cast<int>(top);
+        tail_up(c, td, om, g);
+    }
     // up leg
-    for (size_t i = L - 1; i-- > s;) {
+    for (size_t i = top; i-- > s;) {
         c.cur_level = static_cast<int>(i);
         const Level& Li = h.lv[i];
         const CsrView A = Li.view();

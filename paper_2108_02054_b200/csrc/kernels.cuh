@@ -67,6 +67,33 @@ void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, doub
 // Numeric Galerkin product on the cached plan (two-level bracket of
 // spmm(R, spmm(A, P)), csr.cpp:145-194).  crp/cdiag/wc/bad are reserved for
 // a fused coarse-level smoother rebuild (currently a separate kernel).
+// ---- V-cycle tail (kernels_tail.cu) ----
+struct TailLevel {
+    int n = 0, nc = 0;
+    const int* rp = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+    const double* w = nullptr;     // smoother weights of level l
+    const int* agg = nullptr;      // level l -> l+1
+    const int* mptr = nullptr;     // members of the level-(l+1) rows
+    const int* midx = nullptr;
+    const double* f = nullptr;     // rhs of level l
+    double* u0 = nullptr;          // first iterate (premul / restriction)
+    double* r = nullptr;           // residual scratch
+    double* fc = nullptr;          // rhs of level l+1
+    double* u0c = nullptr;         // first iterate of level l+1 (null: l+1 is the coarsest)
+    const double* wc = nullptr;    // smoother weights of level l+1
+    double* uout = nullptr;        // up-leg result of level l
+    const double* ec = nullptr;    // final iterate of level l+1
+};
+constexpr int TAIL_MAX = 16;
+struct TailDesc {
+    int count = 0;                 // levels first .. first+count-1 (all above the coarsest)
+    TailLevel lv[TAIL_MAX];
+};
+void tail_down(Ctx& c, const TailDesc& d, double om, Gate g);
+void tail_up(Ctx& c, const TailDesc& d, double om, Gate g);
+
 // largest contrib count of any RT_CH-entry chunk of a plan (TMA stage size; host sync)
 int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr);
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,

@@ -264,6 +264,28 @@ def test_many_levels_and_launch_count(ctx):
     assert ctx.launches() > l0 + 3 * (h.num_levels() - 1)
 
 
+@pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "random_300"])
+def test_vcycle_tail_kernels_bit_exact(ctx, name, monkeypatch):
+    """The cooperative V-cycle tail (AMGR_TAIL_NNZ, off by default) runs every
+    level in two grid-barrier kernels with prolongation fused into smoothing:
+    same bits as the reference's (fixed) V-cycle and the same solve."""
+    make, kw = CASES[name]
+    A = make()
+    r = ref.setup(A, ref.params(**kw))
+    f = np.random.default_rng(7).uniform(-1, 1, len(A[0]) - 1)
+    uref = ref.vcycle(r, f, fixed=True, prm=ref.params(**kw))
+    monkeypatch.setenv("AMGR_TAIL_NNZ", "100000000")
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    l0 = ctx.launches()
+    u = amg.vcycle(h, f)
+    assert ctx.launches() - l0 <= 6  # premul, tail down, coarse, tail up (+ copies)
+    np.testing.assert_array_equal(_bits(u), _bits(uref))
+    fr = P.rhs(len(A[0]) - 1)
+    _, st = amg.bicgstab(h, fr)
+    rs = ref.bicgstab(r, fr, fixed=True, prm=ref.params(**kw))
+    assert st.converged and abs(st.iterations - rs.iterations) <= 1
+
+
 # ---------------------------------------------------------------- extensions vs the restated oracle
 @pytest.mark.parametrize("problem", ["poisson", "convdiff"])
 def test_chebyshev_smoother_vs_oracle(ctx, problem):
