@@ -1,6 +1,7 @@
 // extern "C" boundary of libamgr_b200.so (include/amgr.h).  Thin: validates
 // arguments, converts exceptions into amgr_status + last-error text, and
 // forwards to the C++ orchestration in hierarchy.cu.
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <random>
@@ -104,6 +105,10 @@ amgr_status amgr_ctx_create(int device, void* stream, amgr_ctx** out) {
         if (major != 10 || minor != 0)
             amgr::fail(AMGR_E_CUDA, "libamgr_b200 is built for sm_100a (B200); device reports sm_" +
                                         std::to_string(major) + std::to_string(minor));
+        {
+            const char* e = std::getenv("AMGR_PDL");
+            ctx->c.pdl = !(e && std::string(e) == "0");
+        }
         if (stream) {
             ctx->c.stream = static_cast<cudaStream_t>(stream);
         } else {

@@ -60,6 +60,7 @@ struct Ctx {
     int cur_level = -1;  // hierarchy level the orchestration is currently launching for
     // auxiliary stream for independent work inside one call (created lazily,
     // joined back into `stream` before the call returns)
+    bool pdl = true;  // AMGR_PDL=0 disables programmatic dependent launch
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
@@ -92,6 +93,32 @@ inline void join_side(Ctx& c) {
     CK(cudaEventRecord(c.join_ev, c.side));
     CK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
 }
+
+// Programmatic dependent launch for the solve-path kernels: the next kernel
+// of the stream may be scheduled while this one drains; every kernel
+// launched this way starts with pdl_enter() (griddepcontrol.wait: full
+// completion + visibility of the predecessor, then launch_dependents).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+#define LAUNCH_PDL(ctx, family, bytes, kernel, grid, block, smem, ...)                                  \
+    do {                                                                                               \
+        ::amgr::probe_begin((ctx), (family), (bytes));                                                 \
+        cudaLaunchConfig_t cfg_{};                                                                     \
+        cfg_.gridDim = dim3(grid);                                                                     \
+        cfg_.blockDim = dim3(block);                                                                   \
+        cfg_.dynamicSmemBytes = (smem);                                                                \
+        cfg_.stream = (ctx).stream;                                                                    \
+        cudaLaunchAttribute at_[1];                                                                    \
+        at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                \
+        at_[0].val.programmaticStreamSerializationAllowed = 1;                                         \
+        cfg_.attrs = at_;                                                                              \
+        cfg_.numAttrs = (ctx).pdl ? 1 : 0;                                                             \
+        CK(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__));                                           \
+        ::amgr::probe_end((ctx), (family));                                                            \
+        ++(ctx).launches;                                                                              \
+    } while (0)
 
 #define LAUNCH(ctx, family, bytes, kernel, grid, block, smem, ...)                  \
     do {                                                                              \

@@ -69,6 +69,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // (csr.cpp:79-84), gathering up to RP_BATCH operands at a time.
 template <class Op, int CH>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
+    pdl_enter();
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
     extern __shared__ __align__(128) unsigned char rp_smem[];
@@ -211,6 +212,7 @@ constexpr int RS_MINB = 5;
 
 template <class Op>
 __global__ void __launch_bounds__(RS_BLOCK, RS_MINB) k_rowpass_simple(CsrView A, Op op, Gate g, DotSink sink) {
+    pdl_enter();
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
     __shared__ double s_val[RS_WARPS][RS_CH];
@@ -452,7 +454,7 @@ void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const O
                                 static_cast<int>(smem)));
         configured = true;
     }
-    LAUNCH(c, fam, bytes, (k_rowpass<Op, CH>), grid, RP_BLOCK, smem, A, op, g, s);
+    LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH>), grid, RP_BLOCK, smem, A, op, g, s);
 }
 
 template <class Op>
@@ -463,7 +465,7 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     if (rowpass_variant() == 1) {
         unsigned grid = grid_for(groups, RS_WARPS);
         if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
-        LAUNCH(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
+        LAUNCH_PDL(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
         return;
     }
     int64_t want = (groups + RP_WARPS - 1) / RP_WARPS;
@@ -485,6 +487,7 @@ double spmv_bytes(const CsrView& A) {
 __global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __restrict__ midx,
                            const double* __restrict__ r, double* __restrict__ fc, const double* __restrict__ wc,
                            double om, double* __restrict__ u0c, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
         int p = __ldg(mptr + I);
@@ -508,6 +511,7 @@ __global__ void k_restrict(int nc, const int* __restrict__ mptr, const int* __re
 // u0 = 0 + (om*w)*f : first pre-smoothing iterate from a zero guess
 __global__ void k_premul(int n, const double* __restrict__ f, const double* __restrict__ w, double om,
                          double* __restrict__ u0, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         u0[i] = dadd(0.0, dmul(dmul(om, w[i]), f[i]));
@@ -515,6 +519,7 @@ __global__ void k_premul(int n, const double* __restrict__ f, const double* __re
 
 __global__ void k_prolong(int n, const double* __restrict__ u, const int* __restrict__ agg,
                           const double* __restrict__ uc, double* __restrict__ out, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         out[i] = dadd(u[i], dadd(0.0, uc[agg[i]]));
@@ -1062,6 +1067,7 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __restrict__ m,
                                                          const int64_t* __restrict__ piv,
                                                          const double* b, double* x, int use_smem, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bar;
@@ -1175,6 +1181,7 @@ __global__ void __launch_bounds__(1024) k_lu_inverse(int n, const double* __rest
 // x = inv * b, warp per row, fixed-order lane partials + shuffle tree
 __global__ void __launch_bounds__(1024) k_inv_apply(int n, const double* __restrict__ inv, const double* b,
                                                     double* x, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     extern __shared__ double bs[];
     for (int i = threadIdx.x; i < n; i += blockDim.x) bs[i] = b[i];
@@ -1239,12 +1246,14 @@ __global__ void k_cheb_zero(int n, const double* __restrict__ f, const double* _
 
 // ---- misc ---------------------------------------------------------------------
 __global__ void k_fill(double* x, int64_t n, double v, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         x[i] = v;
 }
 __global__ void k_copy(double* d, const double* s, int64_t n, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1310,7 +1319,7 @@ void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double
 }
 void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, double* u0, Gate g) {
     if (n == 0) return;
-    LAUNCH(c, "vcycle_premul", 24.0 * n, k_premul, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f,
+    LAUNCH_PDL(c, "vcycle_premul", 24.0 * n, k_premul, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f,
            w, om, u0, g);
 }
 void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g) {
@@ -1326,13 +1335,13 @@ void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, doubl
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
                 Gate g) {
     if (n == 0) return;
-    LAUNCH(c, "prolong", 20.0 * n, k_prolong, grid_for(n, 256, c.num_sms * 16), 256, 0,
+    LAUNCH_PDL(c, "prolong", 20.0 * n, k_prolong, grid_for(n, 256, c.num_sms * 16), 256, 0,
            static_cast<int>(n), u, agg, uc, out, g);
 }
 void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const double* r, double* fc,
                   const double* wc, double om, double* u0c, Gate g) {
     if (nc == 0) return;
-    LAUNCH(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc), mptr,
+    LAUNCH_PDL(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc), mptr,
            midx, r, fc, wc, om, u0c, g);
 }
 void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double* a, DotSink s, Gate g) {
@@ -1440,7 +1449,7 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    LAUNCH(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
+    LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }
 
 bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {
@@ -1460,7 +1469,7 @@ void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x,
     if (n == 0) return;
     const size_t sm = sizeof(double) * static_cast<size_t>(n);
     if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    LAUNCH(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
+    LAUNCH_PDL(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
 }
 
 void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s) {
@@ -1493,11 +1502,11 @@ void axpy1(Ctx& c, int64_t n, double* x, const double* d, Gate g) {
 
 void fill(Ctx& c, double* x, int64_t n, double v, Gate g) {
     if (n == 0) return;
-    LAUNCH(c, "vec", 8.0 * n, k_fill, grid_for(n, 256, c.num_sms * 16), 256, 0, x, n, v, g);
+    LAUNCH_PDL(c, "vec", 8.0 * n, k_fill, grid_for(n, 256, c.num_sms * 16), 256, 0, x, n, v, g);
 }
 void copy(Ctx& c, double* d, const double* s, int64_t n, Gate g) {
     if (n == 0) return;
-    LAUNCH(c, "vec", 16.0 * n, k_copy, grid_for(n, 256, c.num_sms * 16), 256, 0, d, s, n, g);
+    LAUNCH_PDL(c, "vec", 16.0 * n, k_copy, grid_for(n, 256, c.num_sms * 16), 256, 0, d, s, n, g);
 }
 void find_diag(Ctx& c, const CsrView& A, int* dpos) {
     if (A.n == 0) return;

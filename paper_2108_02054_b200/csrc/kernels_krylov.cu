@@ -17,6 +17,7 @@ __device__ __forceinline__ double rel(const KState* s, double sq) { return sqrt(
 
 // ---- BiCGStab scalar kernels ------------------------------------------------
 __global__ void k_bicg_begin(KState* s) {
+    pdl_enter();
     int f = s->flags;
     if (f & KF_DONE) return;
     if (s->it >= s->max_iter) {
@@ -36,6 +37,7 @@ __global__ void k_bicg_begin(KState* s) {
 }
 
 __global__ void k_bicg_alpha(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     const double rtv = s->d_rtv;
@@ -47,12 +49,14 @@ __global__ void k_bicg_alpha(KState* s) {
 }
 
 __global__ void k_bicg_half_test(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     if (rel(s, s->d_ss) <= s->tol) s->flags = f | KF_HALF;
 }
 
 __global__ void k_bicg_half_check(KState* s) {
+    pdl_enter();
     int f = s->flags;
     if ((f & KF_DONE) || !(f & KF_HALF)) return;
     const double res = rel(s, s->d_true);
@@ -67,6 +71,7 @@ __global__ void k_bicg_half_check(KState* s) {
 }
 
 __global__ void k_bicg_omega(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & (KF_DONE | KF_HALF)) return;
     const double tt = s->d_tt;
@@ -78,6 +83,7 @@ __global__ void k_bicg_omega(KState* s) {
 }
 
 __global__ void k_bicg_end_test(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & (KF_DONE | KF_HALF)) return;
     s->rho_old = s->rho;
@@ -85,6 +91,7 @@ __global__ void k_bicg_end_test(KState* s) {
 }
 
 __global__ void k_bicg_end_check(KState* s) {
+    pdl_enter();
     int f = s->flags;
     if (f & (KF_DONE | KF_HALF)) return;
     if (f & KF_CHECK) {
@@ -103,6 +110,7 @@ __global__ void k_bicg_end_check(KState* s) {
 // ---- BiCGStab vector kernels --------------------------------------------------
 __global__ void k_bicg_p(const KState* s, int n, const double* __restrict__ r, double* __restrict__ p,
                          const double* __restrict__ v) {
+    pdl_enter();
     if (s->flags & KF_DONE) return;
     const bool first = s->it == 1;
     const double beta = s->beta, om = s->omega;
@@ -113,6 +121,7 @@ __global__ void k_bicg_p(const KState* s, int n, const double* __restrict__ r, d
 __global__ void __launch_bounds__(VB) k_bicg_s(const KState* s, int n, const double* __restrict__ r,
                                                const double* __restrict__ v, double* __restrict__ sv,
                                                DotSink ds) {
+    pdl_enter();
     if (s->flags & KF_DONE) return;
     const double alpha = s->alpha;
     double d[1] = {0.0};
@@ -125,6 +134,7 @@ __global__ void __launch_bounds__(VB) k_bicg_s(const KState* s, int n, const dou
 }
 
 __global__ void k_bicg_half_u(const KState* s, int n, double* __restrict__ u, const double* __restrict__ ph) {
+    pdl_enter();
     const int f = s->flags;
     if ((f & KF_DONE) || !(f & KF_HALF)) return;
     const double alpha = s->alpha;
@@ -133,6 +143,7 @@ __global__ void k_bicg_half_u(const KState* s, int n, double* __restrict__ u, co
 }
 
 __global__ void k_bicg_half_r(const KState* s, int n, double* __restrict__ r, const double* __restrict__ sv) {
+    pdl_enter();
     const int f = s->flags;
     if ((f & KF_DONE) || !(f & KF_HALF)) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) r[i] = sv[i];
@@ -144,6 +155,7 @@ __global__ void __launch_bounds__(VB) k_bicg_update(const KState* s, int n, doub
                                                     const double* __restrict__ sv,
                                                     const double* __restrict__ t,
                                                     const double* __restrict__ rt, DotSink ds) {
+    pdl_enter();
     if (s->flags & (KF_DONE | KF_HALF)) return;
     const double alpha = s->alpha, om = s->omega;
     double d[2] = {0.0, 0.0};
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(VB) k_bicg_update(const KState* s, int n, doub
 
 // ---- CG ------------------------------------------------------------------------
 __global__ void k_cg_begin(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     if (s->it >= s->max_iter) {
@@ -169,6 +182,7 @@ __global__ void k_cg_begin(KState* s) {
     s->flags = f & ~KF_CHECK;
 }
 __global__ void k_cg_alpha(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     const double pq = s->d_pq;
@@ -181,6 +195,7 @@ __global__ void k_cg_alpha(KState* s) {
 __global__ void __launch_bounds__(VB) k_cg_update(const KState* s, int n, double* __restrict__ u,
                                                   double* __restrict__ r, const double* __restrict__ p,
                                                   const double* __restrict__ q, DotSink ds) {
+    pdl_enter();
     if (s->flags & KF_DONE) return;
     const double a = s->alpha;
     double d[1] = {0.0};
@@ -193,11 +208,13 @@ __global__ void __launch_bounds__(VB) k_cg_update(const KState* s, int n, double
     block_dots<1>(d, ds);
 }
 __global__ void k_cg_test(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     if (rel(s, s->d_rr) <= s->tol) s->flags = f | KF_CHECK;
 }
 __global__ void k_cg_check(KState* s) {
+    pdl_enter();
     int f = s->flags;
     if (f & KF_DONE) return;
     if (f & KF_CHECK) {
@@ -212,6 +229,7 @@ __global__ void k_cg_check(KState* s) {
     s->flags = f;
 }
 __global__ void k_cg_beta(KState* s) {
+    pdl_enter();
     const int f = s->flags;
     if (f & KF_DONE) return;
     const double rz = s->d_rz;
@@ -219,6 +237,7 @@ __global__ void k_cg_beta(KState* s) {
     s->rho = rz;
 }
 __global__ void k_cg_p(const KState* s, int n, const double* __restrict__ z, double* __restrict__ p) {
+    pdl_enter();
     if (s->flags & KF_DONE) return;
     const double b = s->beta;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -227,6 +246,7 @@ __global__ void k_cg_p(const KState* s, int n, const double* __restrict__ z, dou
 
 __global__ void __launch_bounds__(VB) k_dot(int n, const double* __restrict__ a, const double* __restrict__ b,
                                             DotSink ds, Gate g) {
+    pdl_enter();
     if (gated_off(g)) return;
     double d[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -238,7 +258,7 @@ __global__ void __launch_bounds__(VB) k_dot(int n, const double* __restrict__ a,
 
 Gate gate_of(const KState* st, int skip, int need) { return Gate{&st->flags, skip, need}; }
 
-#define SCALAR(c, k, st) LAUNCH(c, "krylov_scalar", 0.0, k, 1, 1, 0, st)
+#define SCALAR(c, k, st) LAUNCH_PDL(c, "krylov_scalar", 0.0, k, 1, 1, 0, st)
 
 void bicg_begin(Ctx& c, KState* st) { SCALAR(c, k_bicg_begin, st); }
 void bicg_alpha(Ctx& c, KState* st) { SCALAR(c, k_bicg_alpha, st); }
@@ -249,23 +269,23 @@ void bicg_end_test(Ctx& c, KState* st) { SCALAR(c, k_bicg_end_test, st); }
 void bicg_end_check(Ctx& c, KState* st) { SCALAR(c, k_bicg_end_check, st); }
 
 void bicg_p(Ctx& c, KState* st, int64_t n, const double* r, double* p, const double* v) {
-    LAUNCH(c, "krylov_vec", 32.0 * n, k_bicg_p, grid_for(n, VB, c.num_sms * 8), VB, 0, st, static_cast<int>(n), r,
+    LAUNCH_PDL(c, "krylov_vec", 32.0 * n, k_bicg_p, grid_for(n, VB, c.num_sms * 8), VB, 0, st, static_cast<int>(n), r,
            p, v);
 }
 void bicg_s(Ctx& c, KState* st, int64_t n, const double* r, const double* v, double* s, DotSink ds) {
-    LAUNCH(c, "krylov_vec", 24.0 * n, k_bicg_s, dot_grid(c), VB, 0, st, static_cast<int>(n), r, v, s, ds);
+    LAUNCH_PDL(c, "krylov_vec", 24.0 * n, k_bicg_s, dot_grid(c), VB, 0, st, static_cast<int>(n), r, v, s, ds);
 }
 void bicg_half_u(Ctx& c, KState* st, int64_t n, double* u, const double* phat) {
-    LAUNCH(c, "krylov_vec", 24.0 * n, k_bicg_half_u, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
+    LAUNCH_PDL(c, "krylov_vec", 24.0 * n, k_bicg_half_u, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
            static_cast<int>(n), u, phat);
 }
 void bicg_half_r(Ctx& c, KState* st, int64_t n, double* r, const double* s) {
-    LAUNCH(c, "krylov_vec", 16.0 * n, k_bicg_half_r, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
+    LAUNCH_PDL(c, "krylov_vec", 16.0 * n, k_bicg_half_r, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
            static_cast<int>(n), r, s);
 }
 void bicg_update(Ctx& c, KState* st, int64_t n, double* u, const double* phat, const double* shat, double* r,
                  const double* s, const double* t, const double* rt, DotSink ds) {
-    LAUNCH(c, "krylov_vec", 64.0 * n, k_bicg_update, dot_grid(c), VB, 0, st, static_cast<int>(n), u, phat, shat,
+    LAUNCH_PDL(c, "krylov_vec", 64.0 * n, k_bicg_update, dot_grid(c), VB, 0, st, static_cast<int>(n), u, phat, shat,
            r, s, t, rt, ds);
 }
 
@@ -276,15 +296,15 @@ void cg_check(Ctx& c, KState* st) { SCALAR(c, k_cg_check, st); }
 void cg_beta(Ctx& c, KState* st) { SCALAR(c, k_cg_beta, st); }
 void cg_update(Ctx& c, KState* st, int64_t n, double* u, double* r, const double* p, const double* q,
                DotSink ds) {
-    LAUNCH(c, "krylov_vec", 48.0 * n, k_cg_update, dot_grid(c), VB, 0, st, static_cast<int>(n), u, r, p, q, ds);
+    LAUNCH_PDL(c, "krylov_vec", 48.0 * n, k_cg_update, dot_grid(c), VB, 0, st, static_cast<int>(n), u, r, p, q, ds);
 }
 void cg_p(Ctx& c, KState* st, int64_t n, const double* z, double* p) {
-    LAUNCH(c, "krylov_vec", 24.0 * n, k_cg_p, grid_for(n, VB, c.num_sms * 8), VB, 0, st, static_cast<int>(n), z,
+    LAUNCH_PDL(c, "krylov_vec", 24.0 * n, k_cg_p, grid_for(n, VB, c.num_sms * 8), VB, 0, st, static_cast<int>(n), z,
            p);
 }
 
 void dot(Ctx& c, int64_t n, const double* a, const double* b, DotSink ds, Gate g) {
-    LAUNCH(c, "krylov_vec", 16.0 * n, k_dot, dot_grid(c), VB, 0, static_cast<int>(n), a, b, ds, g);
+    LAUNCH_PDL(c, "krylov_vec", 16.0 * n, k_dot, dot_grid(c), VB, 0, static_cast<int>(n), a, b, ds, g);
 }
 
 }  // namespace amgr
