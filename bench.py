@@ -23,8 +23,13 @@ cpu_baseline = the unmodified reference (oracle/_ref, single-threaded as
                shipped) on a bounded sample of the same workload
 --impl reference runs that reference arm alone (rank 0).
 
+strategies   = none / full / partial reuse through the library's run_sequence
+               (rebuild, solve and total ms per step; not part of `value`)
+
 Multi-GPU (torchrun, N>1): each rank runs an independent 256^3 system
-(replicas; the row-partitioned NCCL path is not built yet) — see DESIGN.md.
+(replicas).  The row-partitioned NCCL solve (amgr_dist_*) exists and is
+tested at world size 1 on the device and world size 2 on CPU, but is not
+driven from here until it has run on more than one GPU — see DESIGN.md §5.
 """
 from __future__ import annotations
 
@@ -60,6 +65,8 @@ def args_parse():
                    help="coarsest solve: exact replay of dense_lu.cpp (bit-exact V-cycle) or the explicit inverse")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-strategies", action="store_true",
+                   help="skip the none/full/partial reuse comparison (run_sequence over 4 steps each)")
     return p.parse_args()
 
 
@@ -355,6 +362,27 @@ def main():
         e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": 8 * nnz + 16 * n,
                "d2h_bytes_per_step": 8 * n, "timer": "host wall clock around the C-ABI calls (sync both sides)"}
 
+    # ---- reuse strategies (north star: rebuild / solve / total ms per step for
+    # no-reuse, full-reuse and partial-reuse), through the library's own
+    # run_sequence driver (reuse.cpp:46-136 semantics) on the same sequence ----
+    strategies = None
+    if not a.no_strategies:
+        from paper_2108_02054_b200 import reuse as R
+
+        strategies = {}
+        seq = R.DeviceGridSequence(a.problem, g, 4, ctx=ctx)
+        for kind in ("none", "full", "partial"):
+            res = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind[kind]), prm, sp, ctx=ctx, keep_solutions=False)
+            st = res.report.steps[1:]  # step 0 is the initial full setup for every strategy
+            rb = 1e3 * sum(s.setup_time for s in st) / len(st)
+            so = 1e3 * sum(s.solve_time for s in st) / len(st)
+            strategies[kind] = {"rebuild_ms_per_step": rb, "solve_ms_per_step": so, "total_ms_per_step": rb + so,
+                                "iterations": [s.iterations for s in st], "converged": all(s.converged for s in st)}
+        strategies["note"] = (f"{a.problem} {g}^3 sequence steps 1..3 of a 4-step run_sequence per strategy; "
+                              "times from the driver's own per-step device clocks; 'full' solves with the "
+                              "step-0 hierarchy operator, as the reference does (reuse.cpp:104)")
+        del seq
+
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
     avg_it = float(np.mean(iters))
@@ -395,6 +423,7 @@ def main():
                "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
                "converged": all(conv), "setup_s": setup_s, "step0_iterations": st0.iterations,
                "clocks": clk.summary(), "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
+               "strategies": strategies,
                "cpu_baseline": cpu}
         print(json.dumps(out), flush=True)
     if world > 1:
