@@ -18,6 +18,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "reduce.cuh"
 
@@ -27,7 +29,7 @@ namespace amgr {
 
 namespace {
 
-constexpr int TL_BLOCK = 256;
+constexpr int TL_BLOCK = 1024;  // one block per SM: a finished block's barrier spin (L1 invalidate per poll) cannot thrash a co-resident working block's L1
 constexpr int TL_BATCH = 8;
 
 __device__ __forceinline__ double dsub_(double a, double b) { return __dsub_rn(a, b); }
@@ -55,19 +57,34 @@ __device__ __forceinline__ double row_sum(const TailLevel& L, int i, X x) {
     return s;
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(k) if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) d.trace[k] = gtime();
 __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, Gate g) {
     if (gated_off(g)) return;
+    int tk = 0;
+    TRACE(tk++);
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int l = 0; l < d.count; ++l) {
-        const TailLevel& L = d.lv[l];
+    // unrolled: every descriptor access has a compile-time offset (a dynamic
+    // index into the parameter bank costs a slow indexed constant load per
+    // warp per level — 60% of this kernel's time when measured)
+#pragma unroll
+    for (int l = 0; l < TAIL_MAX; ++l) {
+        if (l >= d.count) break;
+        const TailLevel L = d.lv[l];
         const double* u0 = L.u0;
         for (int64_t i = tid; i < L.n; i += nt) {
             const double s = row_sum(L, static_cast<int>(i), [&](int j) { return __ldcg(u0 + j); });
             L.r[i] = dsub_(__ldcg(L.f + i), s);  // f of level > first was written by this kernel
         }
+        TRACE(tk++);
         grid.sync();
+        TRACE(tk++);
         for (int64_t I = tid; I < L.nc; I += nt) {
             int p = __ldg(L.mptr + I);
             const int p1 = __ldg(L.mptr + I + 1);
@@ -85,7 +102,9 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, G
             L.fc[I] = s;
             if (L.u0c) L.u0c[I] = dadd(0.0, dmul_(dmul_(om, __ldg(L.wc + I)), s));
         }
+        TRACE(tk++);
         if (l + 1 < d.count) grid.sync();
+        TRACE(tk++);
     }
 }
 
@@ -94,8 +113,11 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_up(TailDesc d, double om, Gat
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int l = d.count - 1; l >= 0; --l) {
-        const TailLevel& L = d.lv[l];
+#pragma unroll
+    for (int k = 0; k < TAIL_MAX; ++k) {
+        const int l = TAIL_MAX - 1 - k;
+        if (l >= d.count) continue;
+        const TailLevel L = d.lv[l];
         const double* u0 = L.u0;
         const int* agg = L.agg;
         const double* ec = L.ec;
@@ -117,7 +139,8 @@ void launch_coop(Ctx& c, const char* fam, K kernel, int& per_sm, const TailDesc&
     int64_t nmax = 0;
     for (int l = 0; l < d.count; ++l) nmax = d.lv[l].n > nmax ? d.lv[l].n : nmax;
     int64_t blocks = (nmax + TL_BLOCK - 1) / TL_BLOCK;
-    const int64_t cap = static_cast<int64_t>(c.num_sms) * (per_sm > 0 ? per_sm : 1);
+    int64_t cap = static_cast<int64_t>(c.num_sms);  // one block per SM (see TL_BLOCK)
+    if (const char* e = std::getenv("AMGR_TAIL_BLOCKS")) cap = std::atol(e);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     TailDesc dd = d;
