@@ -607,6 +607,13 @@ static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
 // V-cycle over levels s..L-1 (s = 0: the whole hierarchy); f and u live on
 // level s.  The partitioned multi-GPU solve runs the replicated coarse levels
 // through this with s = T+1.
+// Fold the first pre-smoothing iterate into the top level's down pass and
+// prolongation (default on; AMGR_FOLD_PREMUL=0 materialises it with k_premul).
+static bool fold_premul() {
+    const char* e = std::getenv("AMGR_FOLD_PREMUL");
+    return !(e && std::string(e) == "0");
+}
+
 // First level of the persistent V-cycle tail (kernels_tail.cu): the first
 // level at or below s from which every operator has at most AMGR_TAIL_NNZ
 // nonzeros; -1 = no tail.  Off by default: measured on B200 the grid-barrier
@@ -644,9 +651,12 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     for (size_t i = s + 1; i < L; ++i) fin[i] = W.f[i].get();
     std::vector<double*> cur(L);
     const int pre = h.prm.pre, post = h.prm.post;
-    if (pre >= 1) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
     const int ts = tail_start(h, s);
     const size_t top = ts >= 0 ? static_cast<size_t>(ts) : L - 1;  // levels >= top: tail kernels
+    // one pre-sweep from zero: its iterate u0 = (om w) f is folded into the
+    // top level's down pass and prolongation instead of being materialised
+    const bool fold = pre == 1 && top > s && fold_premul();
+    if (pre >= 1 && !fold) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
     // down leg
     for (size_t i = s; i < top; ++i) {
         c.cur_level = static_cast<int>(i);
@@ -662,7 +672,10 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
         } else {
             double* src = a;
             if (pre == 1) {
-                vc_down(c, A, fin[i], a, r, g);
+                if (fold && i == s)
+                    vc_down_premul(c, A, fin[i], Li.w.get(), om, r, g);
+                else
+                    vc_down(c, A, fin[i], a, r, g);
             } else {
                 double* dst = b;
                 for (int s = 1; s < pre; ++s) {
@@ -735,14 +748,20 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
         const CsrView A = Li.view();
         double* a = cur[i];
         double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
+        auto prolong = [&](double* dst) {
+            if (fold && i == s)
+                vc_prolong_premul(c, A.n, fin[i], Li.w.get(), om, Li.T->agg.get(), ufinal[i + 1], dst, g);
+            else
+                vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], dst, g);
+        };
         if (post <= 0) {
             double* t = (i == s) ? u : b;
-            vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], t, g);
+            prolong(t);
             ufinal[i] = t;
             continue;
         }
         // x = u + P u_c into b, then the post-smoothing sweeps
-        vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
+        prolong(b);
         double* src = b;
         for (int k = 1; k <= post; ++k) {
             double* dst = (i == s && k == post) ? u : (src == b ? a : b);

@@ -45,6 +45,10 @@ void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
                const double* u, double* out, Gate g = {});
 // prolongation (hierarchy.cpp:179-182): out = u + (0 + uc[agg])
+// premul folded into the top level's down leg and prolongation (pre == 1)
+void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g);
+void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,
+                       const double* uc, double* out, Gate g);
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
                 Gate g = {});
 // restriction fc[I] = sum over members ascending of r[m] (R spmv, csr.cpp:79-84);

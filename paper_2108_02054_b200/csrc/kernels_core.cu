@@ -373,6 +373,22 @@ struct OpDown {
     __device__ void finish(int i, double s, const Row& q, double*) const { r[i] = dsub(q.a, s); }
 };
 
+// down leg at the V-cycle's top level with the first pre-smoothing iterate
+// folded in: u0_j = 0 + (om*w_j)*f_j is formed per gathered column (the same
+// operations as k_premul), so the premul pass disappears; the DRAM bytes are
+// OpDown's (w replaces u0 as the gathered vector).
+struct OpDownP {
+    static constexpr int NDOT = 0;
+    using Row = Row1;
+    const double* f;
+    const double* w;
+    double om;
+    double* r;
+    __device__ double x(int j) const { return dadd(0.0, dmul(dmul(om, __ldg(w + j)), __ldg(f + j))); }
+    __device__ Row load(int i) const { return {__ldg(f + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const { r[i] = dsub(q.a, s); }
+};
+
 // one damped sweep (smoother.cpp:42-47): out_i = x_i + (om*w_i)*(f_i - (A x)_i)
 struct OpSmooth {
     static constexpr int NDOT = 0;
@@ -592,6 +608,16 @@ __global__ void k_premul(int n, const double* __restrict__ f, const double* __re
     if (gated_off(g)) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         u0[i] = dadd(0.0, dmul(dmul(om, w[i]), f[i]));
+}
+
+// prolongation onto the implicit first iterate u0 = 0 + (om*w)*f (see OpDownP)
+__global__ void k_prolong_p(int n, const double* __restrict__ f, const double* __restrict__ w, double om,
+                            const int* __restrict__ agg, const double* __restrict__ uc, double* __restrict__ out,
+                            Gate g) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = dadd(dadd(0.0, dmul(dmul(om, w[i]), f[i])), dadd(0.0, uc[agg[i]]));
 }
 
 __global__ void k_prolong(int n, const double* __restrict__ u, const int* __restrict__ agg,
@@ -1403,6 +1429,16 @@ void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double
     // A + f read once, u0 gathered (read once), r written once
     const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, u0, r}, g, {}, false);
+}
+void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    launch_rowpass(c, "vcycle_down", bytes, A, OpDownP{f, w, om, r}, g, {}, false);
+}
+void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,
+                       const double* uc, double* out, Gate g) {
+    if (n == 0) return;
+    LAUNCH_PDL(c, "prolong", 28.0 * n, k_prolong_p, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f,
+               w, om, agg, uc, out, g);
 }
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
                double* out, Gate g) {
