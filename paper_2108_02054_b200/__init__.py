@@ -28,6 +28,8 @@ __all__ = [
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libamgr_b200.so")
+# development A/B of kernel variants: AMGR_LIB=<path to another build>
+LIB_PATH = os.environ.get("AMGR_LIB", LIB_PATH)
 
 HOST, DEVICE, DEVICE_ADOPT = 0, 1, 2
 SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}

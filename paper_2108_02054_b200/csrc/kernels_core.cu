@@ -795,10 +795,12 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
 #pragma unroll
                 for (int t = 0; t < B; ++t) e[k][t] = p0[k] + t < p1[k] ? cn[p0[k] + t] : 0;
             }
+            // unpredicated gathers (missing contributions re-read af[0], a cache
+            // hit) so all PER*B loads are in flight before the first use
 #pragma unroll
             for (int k = 0; k < PER; ++k)
 #pragma unroll
-                for (int t = 0; t < B; ++t) v[k][t] = p0[k] + t < p1[k] ? __ldg(af + (e[k][t] & 0x7fffffff)) : 0.0;
+                for (int t = 0; t < B; ++t) v[k][t] = __ldg(af + (e[k][t] & 0x7fffffff));
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int64_t c = c0 + sub + k * RT_BLOCK + tid;
