@@ -67,7 +67,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // group).  Row pointers and epilogue operands of the next group are prefetched
 // into registers.  Threads own rows and accumulate strictly in column order
 // (csr.cpp:79-84), gathering up to RP_BATCH operands at a time.
-template <class Op, int CH, bool SPEC>
+// GATHER: 0 = RP_BATCH predicated gathers (level 0's 7-entry rows);
+//         8 / 12 = that many unpredicated gathers (coarser levels: 8 for
+//         > 12 nnz/row, 12 for 8..12 nnz/row; measured per level)
+template <class Op, int CH, int GATHER>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     pdl_enter();
     if (gated_off(g)) return;
@@ -158,27 +161,28 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                 {
                     int a = max(rs, cb);
                     const int b = min(re, cb + CH);
+                    constexpr bool SPEC = GATHER > 0;
+                    constexpr int NB = SPEC ? GATHER : RP_BATCH;
                     while (a < b) {
-                        const int cnt = min(RP_BATCH, b - a);
+                        const int cnt = min(NB, b - a);
                         const int k = a - cb;
-                        double xv[RP_BATCH];
+                        double xv[NB];
                         if constexpr (SPEC) {
                             // unpredicated gathers (lanes past the row end re-read the
                             // first entry's operand, a cache hit): with predicated loads
                             // the scheduler interleaves them with the DMULs and only ~2
-                            // are outstanding (measured on levels >= 1; level 0's 7-entry
-                            // rows are better served by the predicated form)
-                            int cj[RP_BATCH];
+                            // are outstanding (measured on levels >= 1)
+                            int cj[NB];
 #pragma unroll
-                            for (int t = 0; t < RP_BATCH; ++t) cj[t] = s_col[w][st][k + (t < cnt ? t : 0)];
+                            for (int t = 0; t < NB; ++t) cj[t] = s_col[w][st][k + (t < cnt ? t : 0)];
 #pragma unroll
-                            for (int t = 0; t < RP_BATCH; ++t) xv[t] = op.x(cj[t]);
+                            for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
                         } else {
 #pragma unroll
-                            for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
+                            for (int t = 0; t < NB; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
                         }
 #pragma unroll
-                        for (int t = 0; t < RP_BATCH; ++t)
+                        for (int t = 0; t < NB; ++t)
                             if (t < cnt) sum = dadd(sum, dmul(s_val[w][st][k + t], xv[t]));
                         a += cnt;
                     }
@@ -543,17 +547,17 @@ int rowpass_variant() {
     return v;
 }
 
-template <class Op, int CH, bool SPEC>
+template <class Op, int CH, int GATHER>
 void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
                 unsigned grid) {
     constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * CH * 12 + RP_WARPS * 2 * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {
-        CK(cudaFuncSetAttribute(k_rowpass<Op, CH, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_rowpass<Op, CH, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
         configured = true;
     }
-    LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, SPEC>), grid, RP_BLOCK, smem, A, op, g, s);
+    LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, GATHER>), grid, RP_BLOCK, smem, A, op, g, s);
 }
 
 template <class Op>
@@ -578,10 +582,12 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
     if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
-    if (A.nnz > 8 * A.n)
-        launch_tma<Op, RP_CH, true>(c, fam, bytes, A, op, g, s, grid);
+    if (A.nnz > 12 * A.n)
+        launch_tma<Op, RP_CH, 8>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.nnz > 8 * A.n)
+        launch_tma<Op, RP_CH, 12>(c, fam, bytes, A, op, g, s, grid);
     else
-        launch_tma<Op, RP_CH, false>(c, fam, bytes, A, op, g, s, grid);
+        launch_tma<Op, RP_CH, 0>(c, fam, bytes, A, op, g, s, grid);
 }
 
 double spmv_bytes(const CsrView& A) {
