@@ -1,18 +1,27 @@
 #!/bin/bash
-# Round profiling recipe (run under gpurun): launch list of one V-cycle region
-# and full captures of the dominant level-0 kernels at 256^3.
-set -x
+# Round profiling recipe (run under gpurun, one GPU): the launch list of one
+# region (rebuild + 2 V-cycles + 2 solve iterations) and --set full captures
+# of the dominant kernels at 256^3; tools/ncu_summarize.py turns them into
+# profiles/<round>_ncu_full_summary.json and <round>_traffic.json.
+# Each ncu command runs only after the same command exited 0 without ncu.
+R=${1:-r01}
 mkdir -p gpurun_out
+full() {  # full <name> <what> <regex> <skip>
+  ncu --set full --clock-control none --import-source on --profile-from-start off \
+      -k regex:"$3" -s $4 -c 1 -o gpurun_out/$1 python tools/region_driver.py 256 $2 > gpurun_out/ncu_$1.log 2>&1
+}
 python tools/region_driver.py 256 all > gpurun_out/plain_all.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
-      --log-file gpurun_out/launches_all.csv python tools/region_driver.py 256 all > gpurun_out/ncu_list.log 2>&1
-# rowpass launches in the region (rebuild has none): V-cycle 1 = 14 down + 14 smooth
-python tools/region_driver.py 256 vcycle > gpurun_out/plain_v.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on --profile-from-start off \
-      -k regex:k_rowpass -s 27 -c 1 -o gpurun_out/smooth_L0 python tools/region_driver.py 256 vcycle > gpurun_out/ncu_s.log 2>&1
-ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:k_rowpass -s 0 -c 1 -o gpurun_out/down_L0 python tools/region_driver.py 256 vcycle > gpurun_out/ncu_d.log 2>&1
-python tools/region_driver.py 256 rebuild > gpurun_out/plain_r.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on --profile-from-start off \
-      -k regex:k_rap -s 0 -c 1 -o gpurun_out/rap_L0 python tools/region_driver.py 256 rebuild > gpurun_out/ncu_r.log 2>&1
-tail -2 gpurun_out/ncu_*.log
+      --log-file gpurun_out/${R}_launches.csv python tools/region_driver.py 256 all > gpurun_out/ncu_list.log 2>&1
+python tools/region_driver.py 256 vcycle > gpurun_out/plain_v.log 2>&1 && {
+  # V-cycle launch order of ^k_rowpass$: down L0..L13 (14), up L4..L0 (5; L5+ use k_rowpass_ep)
+  full smooth_L0 vcycle '^k_rowpass$' 18
+  full down_L0 vcycle '^k_rowpass$' 0
+  full down_L1 vcycle '^k_rowpass$' 1
+}
+python tools/region_driver.py 256 rebuild > gpurun_out/plain_r.log 2>&1 && {
+  full rap_L0 rebuild '^k_rap_tma$' 0
+  full rap_L1 rebuild '^k_rap_tma$' 1
+}
+python tools/ncu_summarize.py $R
+tail -n 2 gpurun_out/ncu_*.log
