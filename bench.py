@@ -65,6 +65,9 @@ def args_parse():
                    help="coarsest solve: exact replay of dense_lu.cpp (bit-exact V-cycle) or the explicit inverse")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--partitioned", action="store_true",
+                   help="row-partitioned NCCL solve of ONE global system over all ranks (strong scaling; "
+                        "opt-in until it has run on more than one GPU, see DESIGN.md 5)")
     p.add_argument("--no-strategies", action="store_true",
                    help="skip the none/full/partial reuse comparison (run_sequence over 4 steps each)")
     return p.parse_args()
@@ -207,12 +210,125 @@ def run_reference_arm(a):
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
+def run_partitioned(a, rank, world, local):
+    """One global C3 system, rows partitioned over the ranks (amgr_dist_*):
+    per step the distributed rebuild (global numeric rebuild + local value
+    gathers) and the partitioned BiCGStab (NCCL halo exchange, transition
+    allgather, replicated coarse levels, rank-ordered dots)."""
+    import torch
+
+    import paper_2108_02054_b200 as amg
+    from paper_2108_02054_b200 import distributed as D
+
+    L = amg.lib()
+    ctx = amg.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    g, kind = a.size, amg.PROBLEM[a.problem]
+    n, nnz = g ** 3, int(L.amgr_problem_nnz(g))
+    W, K = max(a.warmup, 0), max(a.steps, 1)
+    ksteps = list(range(0, 1 + W + K))
+    rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(nnz + 8, dtype=torch.int32, device="cuda")
+    vals = [torch.empty(nnz + 8, dtype=torch.float64, device="cuda") for _ in ksteps]
+    torch.cuda.synchronize()
+    amg._check(L.amgr_problem_pattern(ctx.ptr, g, rp.data_ptr(), ci.data_ptr()), ctx.ptr)
+    for k, v in zip(ksteps, vals):
+        amg._check(L.amgr_problem_values(ctx.ptr, kind, g, k % a.nsteps, a.nsteps, v.data_ptr()), ctx.ptr)
+    f = torch.empty(n, dtype=torch.float64, device="cuda")
+    amg._check(L.amgr_problem_rhs(ctx.ptr, n, 42, f.data_ptr(), amg.DEVICE), ctx.ptr)
+    ctx.synchronize()
+    prm = amg.AmgParams(coarse_solve=a.coarse)
+    t0 = time.perf_counter()
+    h = amg.setup(amg.DeviceCsr(n, n, nnz, rp.data_ptr(), ci.data_ptr(), vals[0].data_ptr()), prm, ctx=ctx)
+    ctx.synchronize()
+    setup_s = time.perf_counter() - t0
+    ids = [D.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.broadcast_object_list(ids, src=0)
+    t0 = time.perf_counter()
+    ds = D.DistSolver(h, rank, world, ids[0], replicate_below=20000)
+    plan_s = time.perf_counter() - t0
+    own = torch.from_numpy(ds.owned0).cuda()
+    fl = f[own].contiguous()
+    ul = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    sp = amg.SolveParams()
+    ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
+    for k in range(1, 1 + W):
+        ds.rebuild_values(vals[k].data_ptr())
+        ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
+    ctx.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 1)]
+    iters = []
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for j, k in enumerate(range(1 + W, 1 + W + K)):
+            ds.rebuild_values(vals[k].data_ptr())
+            ev[2 * j + 1].record(stream)
+            st = ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
+            ev[2 * j + 2].record(stream)
+            iters.append(st.iterations)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launches() - launches0
+    total_ms = ev[0].elapsed_time(ev[2 * K])
+    rebuild_ms = sum(ev[2 * j].elapsed_time(ev[2 * j + 1]) for j in range(K)) / K
+    solve_ms = sum(ev[2 * j + 1].elapsed_time(ev[2 * j + 2]) for j in range(K)) / K
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    if rank == 0:
+        out = {"metric": METRIC, "value": total_ms / K, "unit": "ms/step", "n_gpus": world, "steps": K, "warmup": W,
+               "ms_per_step": total_ms / K, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic (device-generated dam-break sequence)",
+               "config": {"workload": f"C3 dam-break {g}^3, partial reuse, row-partitioned over {world} GPU(s)",
+                          "problem": a.problem, "grid": g, "n": n, "nnz": nnz, "coarse_solve": a.coarse,
+                          "parallelism": f"rows{world}", "partitioned_levels": ds.plan.top + 1,
+                          "local_rows_rank0": ds.n_local},
+               "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
+               "setup_s": setup_s, "plan_s": plan_s, "clocks": clk.summary(), "gpu_launches": launches,
+               "e2e": None, "roofline": None, "cpu_baseline": None}
+        print(json.dumps(out), flush=True)
+    ds.close()
+
+
 def main():
     a = args_parse()
     if a.impl == "reference":
         run_reference_arm(a)
         return
     rank, world, local = dist_env()
+    if a.partitioned:
+        import torch
+
+        torch.cuda.set_device(local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_partitioned(a, rank, world, local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
     import torch
 
     torch.cuda.set_device(local)
