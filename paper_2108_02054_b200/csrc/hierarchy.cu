@@ -716,22 +716,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
             ufinal[l] = t.uout;
         }
         c.cur_level = static_cast<int>(top);
-        static unsigned long long* tr = nullptr;
-        if (std::getenv("AMGR_TAIL_TRACE")) {
-            if (!tr) cudaMalloc(&tr, 8 * 256);
-            cudaMemsetAsync(tr, 0, 8 * 256, c.stream);
-            td.trace = tr;
-        }
         tail_down(c, td, om, g);
-        if (td.trace) {
-            unsigned long long hbuf[256];
-            cudaMemcpyAsync(hbuf, tr, 8 * 256, cudaMemcpyDeviceToHost, c.stream);
-            cudaStreamSynchronize(c.stream);
-            fprintf(stderr, "tail trace (ns from start):");
-            for (int k = 1; k < 4 * td.count + 1; ++k) fprintf(stderr, " %llu", hbuf[k] - hbuf[0]);
-            fprintf(stderr, "\n");
-            td.trace = nullptr;
-        }
     }
     // coarsest: direct solve (hierarchy.cpp:175)
     c.cur_level = static_cast<int>(L - 1);

@@ -92,7 +92,6 @@ struct TailLevel {
 };
 constexpr int TAIL_MAX = 16;
 struct TailDesc {
-    unsigned long long* trace = nullptr;
     int count = 0;                 // levels first .. first+count-1 (all above the coarsest)
     TailLevel lv[TAIL_MAX];
 };

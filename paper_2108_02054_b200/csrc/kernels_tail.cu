@@ -57,16 +57,8 @@ __device__ __forceinline__ double row_sum(const TailLevel& L, int i, X x) {
     return s;
 }
 
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define TRACE(k) if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) d.trace[k] = gtime();
 __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, Gate g) {
     if (gated_off(g)) return;
-    int tk = 0;
-    TRACE(tk++);
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -82,9 +74,7 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, G
             const double s = row_sum(L, static_cast<int>(i), [&](int j) { return __ldcg(u0 + j); });
             L.r[i] = dsub_(__ldcg(L.f + i), s);  // f of level > first was written by this kernel
         }
-        TRACE(tk++);
         grid.sync();
-        TRACE(tk++);
         for (int64_t I = tid; I < L.nc; I += nt) {
             int p = __ldg(L.mptr + I);
             const int p1 = __ldg(L.mptr + I + 1);
@@ -102,9 +92,7 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, G
             L.fc[I] = s;
             if (L.u0c) L.u0c[I] = dadd(0.0, dmul_(dmul_(om, __ldg(L.wc + I)), s));
         }
-        TRACE(tk++);
         if (l + 1 < d.count) grid.sync();
-        TRACE(tk++);
     }
 }
 
@@ -140,7 +128,6 @@ void launch_coop(Ctx& c, const char* fam, K kernel, int& per_sm, const TailDesc&
     for (int l = 0; l < d.count; ++l) nmax = d.lv[l].n > nmax ? d.lv[l].n : nmax;
     int64_t blocks = (nmax + TL_BLOCK - 1) / TL_BLOCK;
     int64_t cap = static_cast<int64_t>(c.num_sms);  // one block per SM (see TL_BLOCK)
-    if (const char* e = std::getenv("AMGR_TAIL_BLOCKS")) cap = std::atol(e);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     TailDesc dd = d;
