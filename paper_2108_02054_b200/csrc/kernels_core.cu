@@ -284,67 +284,6 @@ __global__ void __launch_bounds__(RS_BLOCK, RS_MINB) k_rowpass_simple(CsrView A,
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
 
-// Entry-parallel gather variant for the small coarse levels, whose rows are
-// few but long and uneven (C3: levels >= 8 have rows of 60-147 nonzeros):
-// per 256-entry chunk of a warp's 32-row group the lanes load columns and
-// values and gather ALL operands x_col in parallel into shared memory, then
-// each lane accumulates its own row serially from shared memory (same
-// column order, bit-identical).  A long row then costs ~2 memory round trips
-// plus its serial DADD chain, instead of one round trip per 8 entries.
-constexpr int EP_WARPS = 8, EP_BLOCK = EP_WARPS * 32, EP_CH = 256;
-
-template <class Op>
-__global__ void __launch_bounds__(EP_BLOCK) k_rowpass_ep(CsrView A, Op op, Gate g, DotSink sink) {
-    pdl_enter();
-    if (gated_off(g)) return;
-    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
-    __shared__ double s_val[EP_WARPS][EP_CH];
-    __shared__ double s_x[EP_WARPS][EP_CH];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int n = static_cast<int>(A.n);
-    double dots[ND];
-#pragma unroll
-    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
-    const int64_t wstride = static_cast<int64_t>(gridDim.x) * EP_WARPS;
-    for (int64_t wid = static_cast<int64_t>(blockIdx.x) * EP_WARPS + w; wid * 32 < n; wid += wstride) {
-        const int r0 = static_cast<int>(wid * 32);
-        const int r1 = min(r0 + 32, n);
-        const int row = r0 + lane;
-        const bool valid = row < n;
-        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + r1);
-        const int rs = valid ? __ldg(A.rp + row) : e1;
-        const int re = valid ? __ldg(A.rp + row + 1) : e1;
-        double sum = 0.0;
-        typename Op::Row rw;
-        if (valid) rw = op.load(row);
-        for (int c0 = e0; c0 < e1; c0 += EP_CH) {
-            const int c1 = min(c0 + EP_CH, e1);
-            int cl[EP_CH / 32];
-            double vl[EP_CH / 32];
-#pragma unroll
-            for (int t = 0; t < EP_CH / 32; ++t) {
-                const int e = c0 + lane + 32 * t;
-                cl[t] = e < c1 ? __ldg(A.col + e) : 0;
-                vl[t] = e < c1 ? __ldg(A.val + e) : 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < EP_CH / 32; ++t) {
-                const int e = c0 + lane + 32 * t;
-                if (e < c1) {
-                    s_x[w][e - c0] = op.x(cl[t]);
-                    s_val[w][e - c0] = vl[t];
-                }
-            }
-            __syncwarp();
-            const int a = max(rs, c0), b = min(re, c1);
-            for (int k = a; k < b; ++k) sum = dadd(sum, dmul(s_val[w][k - c0], s_x[w][k - c0]));
-            __syncwarp();
-        }
-        if (valid) op.finish(row, sum, rw, dots);
-    }
-    if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
-}
-
 // ---- row-pass operators ----------------------------------------------------
 struct NoRow {};
 struct Row1 {
@@ -530,15 +469,6 @@ struct OpChebStep {
 
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
-// levels with at most this many rows use the entry-parallel row pass
-int64_t ep_rows() {
-    static const int64_t v = [] {
-        const char* e = getenv("AMGR_EP_ROWS");
-        return e ? static_cast<int64_t>(atol(e)) : static_cast<int64_t>(131072);
-    }();
-    return v;
-}
-
 int rowpass_variant() {
     static int v = [] {
         const char* e = getenv("AMGR_ROWPASS");
@@ -562,20 +492,13 @@ void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const O
 
 template <class Op>
 void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g,
-                    DotSink s, bool fixed_grid, bool allow_ep = false) {
+                    DotSink s, bool fixed_grid) {
     if (A.n == 0) return;
     const int64_t groups = (A.n + 31) / 32;
     if (rowpass_variant() == 1) {
         unsigned grid = grid_for(groups, RS_WARPS);
         if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
         LAUNCH_PDL(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
-        return;
-    }
-    // entry-parallel variant: measured faster on the small levels' up-leg
-    // sweeps (operands and A L2-resident after the down leg), slower on the
-    // down leg (A comes back from DRAM) — so only where the caller allows it
-    if (allow_ep && !fixed_grid && A.n <= ep_rows()) {
-        LAUNCH_PDL(c, fam, bytes, k_rowpass_ep<Op>, grid_for(groups, EP_WARPS), EP_BLOCK, 0, A, op, g, s);
         return;
     }
     int64_t want = (groups + RP_WARPS - 1) / RP_WARPS;
@@ -1467,7 +1390,7 @@ void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, doub
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
                double* out, Gate g) {
     const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;
-    launch_rowpass(c, "vcycle_smooth", bytes, A, OpSmooth{f, w, om, u, out}, g, {}, false, true);
+    launch_rowpass(c, "vcycle_smooth", bytes, A, OpSmooth{f, w, om, u, out}, g, {}, false);
 }
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
                 Gate g) {
