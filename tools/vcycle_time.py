@@ -1,6 +1,7 @@
-"""Development probe: device time of one V-cycle (stream-launched) at g^3
-dam-break while varying environment knobs read per call (AMGR_BOTTOM_ROWS,
-AMGR_TAIL_NNZ, ...).  usage: python tools/vcycle_time.py g VAR v1 v2 ..."""
+"""Development probe: device time of one V-cycle (stream-launched) and of
+one BiCGStab iteration (CUDA-graph path, 30 iterations from a zero guess) at
+g^3 dam-break while varying an environment knob read per call
+(AMGR_TAIL_NNZ, AMGR_FOLD_PREMUL, ...).  usage: python tools/vcycle_time.py g VAR v1 v2 ..."""
 import os
 import sys
 
@@ -41,4 +42,16 @@ for rep in range(2):
                 amg.vcycle_device(h, f.data_ptr(), u.data_ptr())
             e1.record()
         ctx.synchronize()
-        print(f"{var}={val}: vcycle {e0.elapsed_time(e1) / 20:.3f} ms", flush=True)
+        vc = e0.elapsed_time(e1) / 20
+        it = []
+        for _ in range(3):
+            u.zero_()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):
+                e0.record()
+            _, st = amg.bicgstab(h, f.data_ptr(), (u.data_ptr(), u.data_ptr()), amg.SolveParams(max_iter=30))
+            with torch.cuda.stream(s):
+                e1.record()
+            ctx.synchronize()
+            it.append(e0.elapsed_time(e1) / max(st.iterations, 1))
+        print(f"{var}={val}: vcycle {vc:.3f} ms, bicgstab {min(it):.3f} ms/iteration ({st.iterations} its)", flush=True)
