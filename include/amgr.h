@@ -292,6 +292,12 @@ amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, i
  * coarsening.cpp:122-132) and R = P^T as CSR (row_ptr n_coarse+1, col n). */
 amgr_status amgr_hier_level_P(const amgr_hier* h, int level, int64_t* agg);
 amgr_status amgr_hier_level_R(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col);
+/* P (which = 0, nrows x n_coarse) or R = P^T (which = 1) of a level as a
+ * general CSR with values: the tentative P (one 1.0 per row) or the smoothed
+ * prolongator of the smoothed-aggregation extension.  Call with
+ * row_ptr == NULL to query *nnz, then with buffers of nrows+1 / nnz / nnz. */
+amgr_status amgr_hier_level_transfer(const amgr_hier* h, int level, int which, int64_t* nnz, int64_t* row_ptr,
+                                     int64_t* col, double* values);
 /* Smoother state: inv_diag (JacobiSmoother::inv_diag, smoother.hpp:11-16). */
 amgr_status amgr_hier_level_smoother(const amgr_hier* h, int level, double* inv_diag);
 /* Chebyshev extension: power-iteration estimate of lambda_max(D^-1 A) of a

@@ -132,6 +132,7 @@ PROTOTYPES = {
     "amgr_copy_to_host": (_I, [_V, _V, _V, C.c_size_t]),
     "amgr_run_sequence": (_I, [_V, _L, _V, _V, _V, _V, _V, _V, _V, _V]),
     "amgr_speedup_percent": (_D, [_D, _D]),
+    "amgr_hier_level_transfer": (_I, [_V, _I, _I, _P(_L), _V, _V, _V]),
     "amgr_nccl_unique_id": (_I, [_V]),
     "amgr_dist_create": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
     "amgr_dist_rebuild_values": (_I, [_V, _V, _I]),
@@ -362,6 +363,21 @@ class Hierarchy:
         ci = np.zeros(d["nrows"], np.int64)
         _check(lib().amgr_hier_level_R(self._p, lvl, rp.ctypes.data, ci.ctypes.data), self.ctx.ptr)
         return rp, ci
+
+    def level_transfer(self, lvl: int, which: str = "P"):
+        """General CSR (row_ptr, col, values) of P or R = P^T (tentative or, under
+        smoothed aggregation, the smoothed prolongator)."""
+        w = {"P": 0, "R": 1}[which]
+        d = self.level_dims(lvl)
+        nnz = C.c_int64()
+        _check(lib().amgr_hier_level_transfer(self._p, lvl, w, C.byref(nnz), None, None, None), self.ctx.ptr)
+        rows = d["nrows"] if w == 0 else d["n_coarse"]
+        rp = np.zeros(rows + 1, np.int64)
+        ci = np.zeros(max(nnz.value, 1), np.int64)
+        v = np.zeros(max(nnz.value, 1))
+        _check(lib().amgr_hier_level_transfer(self._p, lvl, w, C.byref(nnz), rp.ctypes.data, ci.ctypes.data,
+                                              v.ctypes.data), self.ctx.ptr)
+        return rp, ci[:nnz.value], v[:nnz.value]
 
     def level_smoother(self, lvl: int) -> np.ndarray:
         d = self.level_dims(lvl)

@@ -339,6 +339,7 @@ amgr_status amgr_hier_level_R(const amgr_hier* h, int level, int64_t* row_ptr, i
         if (level < 0 || level >= static_cast<int>(H.lv.size()) || !H.lv[level].T)
             amgr::invalid("level has no transfer operator");
         const amgr::Transfer& T = *H.lv[level].T;
+        if (T.smoothed) amgr::invalid("smoothed aggregation level: use amgr_hier_level_transfer");
         amgr::DevArray<int64_t> t(std::max(T.nf, T.nc + 1), c.stream);
         amgr::i32_to_i64(c, T.mptr.get(), t.get(), T.nc + 1);
         amgr::d2h(row_ptr, t.get(), T.nc + 1, c.stream);
@@ -346,6 +347,53 @@ amgr_status amgr_hier_level_R(const amgr_hier* h, int level, int64_t* row_ptr, i
         amgr::i32_to_i64(c, T.midx.get(), t.get(), T.nf);
         amgr::d2h(col, t.get(), T.nf, c.stream);
         CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+amgr_status amgr_hier_level_transfer(const amgr_hier* h, int level, int which, int64_t* nnz, int64_t* row_ptr,
+                                     int64_t* col, double* values) {
+    if (!h || !nnz || (which != 0 && which != 1)) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] {
+        amgr::Hier& H = *h->h;
+        amgr::Ctx& c = *H.ctx;
+        if (level < 0 || level >= static_cast<int>(H.lv.size()) || !H.lv[level].T)
+            amgr::invalid("level has no transfer operator");
+        const amgr::Transfer& T = *H.lv[level].T;
+        const int64_t rows = which == 0 ? T.nf : T.nc;
+        if (T.smoothed) {
+            const amgr::Pattern& M = which == 0 ? *T.P : *T.R;
+            *nnz = M.nnz;
+            if (!row_ptr) return;
+            if (!col || !values) amgr::invalid("amgr_hier_level_transfer: null output buffer");
+            amgr::DevArray<int64_t> t(std::max(M.nnz, rows + 1), c.stream);
+            amgr::i32_to_i64(c, M.rp.get(), t.get(), rows + 1);
+            amgr::d2h(row_ptr, t.get(), rows + 1, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            amgr::i32_to_i64(c, M.col.get(), t.get(), M.nnz);
+            amgr::d2h(col, t.get(), M.nnz, c.stream);
+            amgr::d2h(values, (which == 0 ? T.Pv : T.Rv).get(), M.nnz, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            return;
+        }
+        // tentative: P row i = (agg_i, 1.0); R = member lists with 1.0
+        *nnz = T.nf;
+        if (!row_ptr) return;
+        if (!col || !values) amgr::invalid("amgr_hier_level_transfer: null output buffer");
+        amgr::DevArray<int64_t> t(T.nf + 1, c.stream);
+        if (which == 0) {
+            std::vector<int64_t> rp(static_cast<size_t>(T.nf + 1));
+            for (int64_t i = 0; i <= T.nf; ++i) rp[i] = i;
+            std::copy(rp.begin(), rp.end(), row_ptr);
+            amgr::i32_to_i64(c, T.agg.get(), t.get(), T.nf);
+        } else {
+            amgr::i32_to_i64(c, T.mptr.get(), t.get(), T.nc + 1);
+            amgr::d2h(row_ptr, t.get(), T.nc + 1, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            amgr::i32_to_i64(c, T.midx.get(), t.get(), T.nf);
+        }
+        amgr::d2h(col, t.get(), T.nf, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        for (int64_t k = 0; k < T.nf; ++k) values[k] = 1.0;
     });
 }
 

@@ -273,6 +273,9 @@ amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, in
             amgr::invalid("amgr_dist_create: need 0 <= top < num_levels - 1");
         if (H.prm.pre != 1 || H.prm.post != 1 || H.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV)
             amgr::invalid("amgr_dist_create: the partitioned solve supports 1+1 Jacobi/SPAI0 sweeps");
+        for (const auto& l : H.lv)
+            if (l.T && l.T->smoothed)
+                amgr::invalid("amgr_dist_create: the partitioned solve supports plain (tentative) aggregation only");
         auto d = std::make_unique<amgr::DistHier>();
         d->g = &H;
         d->ctx = &c;

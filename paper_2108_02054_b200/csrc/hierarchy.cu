@@ -224,6 +224,101 @@ void reset_err(Hier& h) {
     h2d(W.err.get(), e.data(), static_cast<int64_t>(e.size()), h.ctx->stream);
 }
 
+// ---- smoothed aggregation (extension; oracle/amg_oracle.c) -------------------
+// P = P_tent - (w D^-1) A P_tent on the pattern of A P_tent, R = P^T.
+static void build_sa_transfer(Ctx& c, Level& cur, Transfer& T, double w, size_t l) {
+    const CsrView Av = cur.view();
+    DevArray<int> trp, tcol;
+    DevArray<double> tval;
+    tentative_csr(c, Av.n, T.agg.get(), trp, tcol, tval);
+    SpgPlan ap0;
+    spgemm_symbolic(c, Av, trp.get(), tcol.get(), T.nc, ap0, "smoothed_prolongator");
+    DevArray<double> pv(ap0.nnz, c.stream);
+    spgemm_numeric(c, ap0, Av.val, tval.get(), pv.get());
+    DevArray<int> bad(1, c.stream);
+    const int big = 0x7fffffff;
+    h2d(bad.get(), &big, 1, c.stream);
+    sa_prolongator_values(c, Av.n, ap0.rp.get(), ap0.col.get(), pv.get(), T.agg.get(), cur.pat->diag.get(), Av.val,
+                          w, bad.get());
+    const int b = d2h_scalar(bad.get(), c.stream);
+    if (b != big) {
+        std::ostringstream os;
+        os << level_prefix(l) << "smoothed_prolongator: zero diagonal at row " << b;
+        invalid(os.str());
+    }
+    auto P = std::make_shared<Pattern>();
+    P->n = Av.n;
+    P->ncols = T.nc;
+    P->nnz = ap0.nnz;
+    P->rp = std::move(ap0.rp);
+    P->col = std::move(ap0.col);
+    P->max_span = max_group_span(c, P->rp.get(), P->n);
+    DevArray<int> rrp, rcol;
+    DevArray<double> rv;
+    transpose_csr(c, Av.n, T.nc, P->nnz, P->rp.get(), P->col.get(), pv.get(), rrp, rcol, rv);
+    auto R = std::make_shared<Pattern>();
+    R->n = T.nc;
+    R->ncols = Av.n;
+    R->nnz = P->nnz;
+    R->rp = std::move(rrp);
+    R->col = std::move(rcol);
+    R->max_span = max_group_span(c, R->rp.get(), R->n);
+    T.P = P;
+    T.Pv = std::move(pv);
+    T.R = R;
+    T.Rv = std::move(rv);
+    T.smoothed = true;
+}
+
+// Galerkin plan of a smoothed level: A P (pattern + plan) then R (A P); the
+// coarse pattern is the structural pattern of R A P (o_galerkin).
+static std::shared_ptr<Pattern> sa_galerkin_plan(Ctx& c, const CsrView& Av, const Transfer& T, RapPlan& plan) {
+    plan.ap = std::make_shared<SpgPlan>();
+    spgemm_symbolic(c, Av, T.P->rp.get(), T.P->col.get(), T.nc, *plan.ap, "galerkin");
+    plan.ap_val.alloc(plan.ap->nnz, c.stream);
+    CsrView rv = csr_view(*T.R, T.Rv.get());
+    plan.rap = std::make_shared<SpgPlan>();
+    spgemm_symbolic(c, rv, plan.ap->rp.get(), plan.ap->col.get(), T.nc, *plan.rap, "galerkin");
+    plan.nnz_f = Av.nnz;
+    plan.nnz_c = plan.rap->nnz;
+    auto P = std::make_shared<Pattern>();
+    P->n = T.nc;
+    P->ncols = T.nc;
+    P->nnz = plan.rap->nnz;
+    P->rp = std::move(plan.rap->rp);
+    P->col = std::move(plan.rap->col);
+    P->diag.alloc(P->n, c.stream);
+    P->max_span = max_group_span(c, P->rp.get(), P->n);
+    return P;
+}
+
+static void sa_galerkin_numeric(Ctx& c, const RapPlan& plan, const double* af, const Transfer& T, double* ac) {
+    spgemm_numeric(c, *plan.ap, af, T.Pv.get(), const_cast<double*>(plan.ap_val.get()));
+    spgemm_numeric(c, *plan.rap, T.Rv.get(), plan.ap_val.get(), ac);
+}
+
+static bool any_smoothed(const Hier& h) {
+    for (const auto& l : h.lv)
+        if (l.T && l.T->smoothed) return true;
+    return false;
+}
+
+// restriction / prolongation of level i (tentative: member sums and k_prolong;
+// smoothed: row passes over R and P)
+static void restrict_level(Ctx& c, const Level& Li, const double* r, double* fc, const double* wc, double om,
+                           double* u0c, Gate g) {
+    if (Li.T->smoothed)
+        vc_restrict_general(c, csr_view(*Li.T->R, Li.T->Rv.get()), r, fc, wc, om, u0c, g);
+    else
+        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, fc, wc, om, u0c, g);
+}
+static void prolong_level(Ctx& c, const Level& Li, const double* u, const double* e, double* out, Gate g) {
+    if (Li.T->smoothed)
+        vc_prolong_general(c, csr_view(*Li.T->P, Li.T->Pv.get()), u, e, out, g);
+    else
+        vc_prolong(c, Li.pat->n, u, Li.T->agg.get(), e, out, g);
+}
+
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans.
 // Level 0's smoother is rebuilt by its own kernel; for every coarser smoothed
 // level the Jacobi rebuild is fused into the Galerkin kernel that produces it
@@ -248,9 +343,12 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
             if (B.w.size() != B.pat->n) B.w.alloc(B.pat->n, c.stream);
             B.has_smoother = true;
         }
-        rap_numeric(c, A.pat->n, B.pat->n, B.pat->rp.get(), B.pat->diag.get(), A.rap->nnz_c, A.rap->cptr.get(),
-                    A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz, fuse ? B.w.get() : nullptr,
-                    W.err.get() + i + 1, A.rap->max_chunk);
+        if (A.T->smoothed)
+            sa_galerkin_numeric(c, *A.rap, A.view().val, *A.T, B.val.get());
+        else
+            rap_numeric(c, A.pat->n, B.pat->n, B.pat->rp.get(), B.pat->diag.get(), A.rap->nnz_c, A.rap->cptr.get(),
+                        A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz, fuse ? B.w.get() : nullptr,
+                        W.err.get() + i + 1, A.rap->max_chunk);
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
@@ -275,6 +373,16 @@ void symbolic_pass(Hier& h) {
     Ctx& c = *h.ctx;
     for (size_t i = 0; i + 1 < h.lv.size(); ++i) {
         Level& A = h.lv[i];
+        if (A.T->smoothed) {
+            auto plan = std::make_shared<RapPlan>();
+            auto P = sa_galerkin_plan(c, A.view(), *A.T, *plan);
+            A.rap = plan;
+            Level& B = h.lv[i + 1];
+            B.pat = P;
+            CsrView v = B.view();
+            find_diag(c, v, P->diag.get());
+            continue;
+        }
         RapSymbolic s;
         rap_symbolic(c, A.view(), A.T->agg.get(), A.T->nc, s);
         auto plan = std::make_shared<RapPlan>();
@@ -382,6 +490,11 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
                << " unknowns (> max_direct_size " << p.max_direct << ")";
             fail(AMGR_E_RUNTIME, os.str());
         }
+        if (p.coarsening == AMGR_COARSENING_SMOOTHED) {
+            clk.begin(PH_TRANSFER);
+            build_sa_transfer(c, cur, *T, p.sa_omega, l);
+            clk.end(PH_TRANSFER);
+        }
         // smoother (hierarchy.cpp:79-87)
         {
             const int big = 0x7fffffff;
@@ -399,7 +512,16 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
         // Galerkin product (hierarchy.cpp:89-93): symbolic plan + numeric values
         Level next;
         clk.begin(PH_GALERKIN);
-        {
+        if (T->smoothed) {
+            auto plan = std::make_shared<RapPlan>();
+            auto P = sa_galerkin_plan(c, Av, *T, *plan);
+            next.pat = P;
+            next.val.alloc(P->nnz, c.stream);
+            CsrView nv = next.view();
+            find_diag(c, nv, P->diag.get());
+            sa_galerkin_numeric(c, *plan, Av.val, *T, next.val.get());
+            cur.rap = plan;
+        } else {
             RapSymbolic s;
             rap_symbolic(c, Av, T->agg.get(), nc, s);
             auto plan = std::make_shared<RapPlan>();
@@ -576,8 +698,7 @@ static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
         }
         cur[i] = x;
         residual(c, A, fin[i], x, W.r[i].get(), g);
-        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), W.r[i].get(), W.f[i + 1].get(), nullptr, 0.0,
-                     nullptr, g);
+        restrict_level(c, Li, W.r[i].get(), W.f[i + 1].get(), nullptr, 0.0, nullptr, g);
     }
     c.cur_level = static_cast<int>(L - 1);
     coarse_solve(h, W.f[L - 1].get(), W.u[L - 1].get(), g);
@@ -588,7 +709,7 @@ static void vcycle_cheb(Hier& h, const double* f, double* u, Gate g) {
         const CsrView A = Li.view();
         double* a = cur[i];
         double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
-        vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], b, g);
+        prolong_level(c, Li, a, ufinal[i + 1], b, g);
         double* x = b;
         for (int s = 0; s < h.prm.post; ++s) {
             double* other = (x == a) ? b : a;
@@ -623,7 +744,9 @@ static int tail_start(const Hier& h, size_t s) {
     const char* e = std::getenv("AMGR_TAIL_NNZ");
     const long thr = e ? std::atol(e) : 0L;
     const size_t L = h.lv.size();
-    if (thr <= 0 || h.prm.pre != 1 || h.prm.post != 1 || h.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV) return -1;
+    if (thr <= 0 || h.prm.pre != 1 || h.prm.post != 1 || h.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV ||
+        any_smoothed(h))
+        return -1;
     for (size_t i = s; i + 1 < L; ++i) {
         bool small = true;
         for (size_t k = i; k + 1 < L; ++k) small = small && h.lv[k].pat->nnz <= thr;
@@ -655,7 +778,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     const size_t top = ts >= 0 ? static_cast<size_t>(ts) : L - 1;  // levels >= top: tail kernels
     // one pre-sweep from zero: its iterate u0 = (om w) f is folded into the
     // top level's down pass and prolongation instead of being materialised
-    const bool fold = pre == 1 && top > s && fold_premul();
+    const bool fold = pre == 1 && top > s && fold_premul() && !h.lv[s].T->smoothed;
     if (pre >= 1 && !fold) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
     // down leg
     for (size_t i = s; i < top; ++i) {
@@ -687,8 +810,8 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
             cur[i] = src;
         }
         const bool next_smoothed = pre >= 1 && i + 2 < L;
-        restrict_sum(c, Li.T->nc, Li.T->mptr.get(), Li.T->midx.get(), r, W.f[i + 1].get(),
-                     next_smoothed ? h.lv[i + 1].w.get() : nullptr, om, next_smoothed ? W.u[i + 1].get() : nullptr, g);
+        restrict_level(c, Li, r, W.f[i + 1].get(), next_smoothed ? h.lv[i + 1].w.get() : nullptr, om,
+                       next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
     TailDesc td;
     if (ts >= 0) {
@@ -737,7 +860,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
             if (fold && i == s)
                 vc_prolong_premul(c, A.n, fin[i], Li.w.get(), om, Li.T->agg.get(), ufinal[i + 1], dst, g);
             else
-                vc_prolong(c, A.n, a, Li.T->agg.get(), ufinal[i + 1], dst, g);
+                prolong_level(c, Li, a, ufinal[i + 1], dst, g);
         };
         if (post <= 0) {
             double* t = (i == s) ? u : b;

@@ -31,16 +31,35 @@ struct Pattern {
     DevArray<int> rp, col, diag;
 };
 // Frozen transfer operators of one level: P (agg) and R = P^T (mptr/midx).
+// Smoothed aggregation (extension) additionally keeps the general P and R.
 struct Transfer {
     int64_t nf = 0, nc = 0;
     DevArray<int> agg, mptr, midx;
+    bool smoothed = false;
+    std::shared_ptr<struct Pattern> P, R;  // P: nf x nc, R = P^T: nc x nf
+    DevArray<double> Pv, Rv;
 };
 // Cached Galerkin plan A_i -> A_{i+1}.
 struct RapPlan {
     int64_t nnz_f = 0, nnz_c = 0;
+    // smoothed aggregation: A_{i+1} = R (A P) as two plan-based numeric SpGEMMs
+    std::shared_ptr<SpgPlan> ap, rap;
+    DevArray<double> ap_val;
     int max_chunk = -1;  // largest contrib count of a k_rap_tma chunk (-1: not computed)
     DevArray<int> cptr, contrib;
 };
+
+inline CsrView csr_view(const Pattern& p, const double* val) {
+    CsrView v;
+    v.n = p.n;
+    v.ncols = p.ncols;
+    v.nnz = p.nnz;
+    v.rp = p.rp.get();
+    v.col = p.col.get();
+    v.val = val;
+    v.max_span = p.max_span;
+    return v;
+}
 
 struct Level {
     std::shared_ptr<Pattern> pat;

@@ -45,6 +45,11 @@ void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
                const double* u, double* out, Gate g = {});
 // prolongation (hierarchy.cpp:179-182): out = u + (0 + uc[agg])
+// smoothed aggregation (extension): restriction / prolongation with general
+// R and P (row passes over their CSR)
+void vc_restrict_general(Ctx& c, const CsrView& R, const double* r, double* fc, const double* wc, double om,
+                         double* u0c, Gate g);
+void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double* e, double* out, Gate g);
 // premul folded into the top level's down leg and prolongation (pre == 1)
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g);
 void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,

@@ -361,6 +361,36 @@ struct OpSmooth {
     }
 };
 
+// smoothed aggregation (extension): restriction f_c = R r as a row pass over
+// R (o_vcycle: spmv(R, r)), with the coarse level's first iterate
+// u0_c = 0 + (om*w_c)*f_c in the epilogue as k_restrict does
+struct OpRestrictG {
+    static constexpr int NDOT = 0;
+    using Row = NoRow;
+    const double* r;
+    double* fc;
+    const double* wc;
+    double om;
+    double* u0c;
+    __device__ double x(int j) const { return __ldg(r + j); }
+    __device__ Row load(int) const { return {}; }
+    __device__ void finish(int i, double s, const Row&, double*) const {
+        fc[i] = s;
+        if (u0c) u0c[i] = dadd(0.0, dmul(dmul(om, wc[i]), s));
+    }
+};
+// ... and prolongation out = u + P e (o_vcycle: r = spmv(P, e); u += r)
+struct OpProlongG {
+    static constexpr int NDOT = 0;
+    using Row = Row1;
+    const double* e;
+    const double* u;
+    double* out;
+    __device__ double x(int j) const { return __ldg(e + j); }
+    __device__ Row load(int i) const { return {__ldg(u + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double*) const { out[i] = dadd(q.a, s); }
+};
+
 struct OpSpmvDot {
     static constexpr int NDOT = 1;
     using Row = Row1;
@@ -1376,6 +1406,15 @@ void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double
     // A + f read once, u0 gathered (read once), r written once
     const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, u0, r}, g, {}, false);
+}
+void vc_restrict_general(Ctx& c, const CsrView& R, const double* r, double* fc, const double* wc, double om,
+                         double* u0c, Gate g) {
+    const double bytes = 12.0 * R.nnz + 4.0 * (R.n + 1) + 8.0 * R.ncols + 8.0 * R.n * (u0c ? 3 : 1);
+    launch_rowpass(c, "restrict", bytes, R, OpRestrictG{r, fc, wc, om, u0c}, g, {}, false);
+}
+void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double* e, double* out, Gate g) {
+    const double bytes = 12.0 * P.nnz + 4.0 * (P.n + 1) + 8.0 * P.ncols + 16.0 * P.n;
+    launch_rowpass(c, "prolong", bytes, P, OpProlongG{e, u, out}, g, {}, false);
 }
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
     const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;

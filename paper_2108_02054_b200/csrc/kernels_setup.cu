@@ -5,6 +5,9 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <sstream>
+
+#include "reduce.cuh"
 #include "setup.cuh"
 
 namespace amgr {
@@ -422,6 +425,246 @@ void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbo
     out.rp.alloc(nc + 1, c.stream);
     LAUNCH(c, "setup", 0.0, k_graph_ptr, grid_for(nc + 1, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, nc, b,
            out.rp.get());
+}
+
+
+// ---- smoothed aggregation ----------------------------------------------------
+// Smoothed aggregation (extension, north star "tentative and
+// smoothed prolongator"; the reference ships only the tentative P).  Parity
+// is against the restated oracle (oracle/amg_oracle.c:smoothed_prolongator,
+// o_spmm, o_transpose, o_galerkin), bit for bit.
+//
+//  * spgemm_symbolic: C = A B on the device.  Every product a_ik b_kj becomes
+//    a triple keyed (i, j); triples are generated in (i, k, B-row) order and
+//    stable-radix-sorted by key, so each output entry's products stay in the
+//    reference spmm's accumulation order (k ascending, csr.cpp:145-184).  The
+//    unique keys are C's structural pattern (sorted columns, cancellation
+//    zeros kept); the sorted (a-index, b-index) pairs are the numeric plan.
+//  * spgemm_numeric: c_e = sum over the plan of a*b, from 0.0, in plan order
+//    (thread per output entry).  With the plan cached, a partial rebuild of a
+//    smoothed level is two numeric SpGEMMs: A P (P frozen) then R (A P).
+//  * sa_prolongator_values: P = P_tent - (w D^-1) A P_tent on the pattern of
+//    A P_tent: v = (J == agg_i ? 1 : 0) - (w * (1/a_ii)) * (A P_tent)_iJ.
+//  * transpose: R = P^T with sorted columns (stable sort of P's entries by
+//    column keeps the row order), values carried along.
+namespace {
+
+constexpr int SA_B = 256;
+
+#define SA_STRIDE(i, n)                                                                    \
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (n); \
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+__global__ void k_sp_count(CsrView A, const int* __restrict__ brp, int64_t* cnt) {
+    SA_STRIDE(e, A.nnz) {
+        const int k = A.col[e];
+        cnt[e] = brp[k + 1] - brp[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[A.nnz] = 0;
+}
+
+__global__ void k_sp_triples(CsrView A, const int* __restrict__ brp, const int* __restrict__ bcol, int bj,
+                             const int64_t* __restrict__ off, uint64_t* __restrict__ key, int* __restrict__ ia,
+                             int* __restrict__ ib, int* __restrict__ id) {
+    SA_STRIDE(i, A.n) {
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const int k = A.col[e];
+            int64_t t = off[e];
+            for (int q = brp[k]; q < brp[k + 1]; ++q, ++t) {
+                key[t] = (static_cast<uint64_t>(i) << bj) | static_cast<uint64_t>(bcol[q]);
+                ia[t] = e;
+                ib[t] = q;
+                id[t] = static_cast<int>(t);
+            }
+        }
+    }
+}
+
+__global__ void k_sp_heads(const uint64_t* keys, int64_t m, int64_t* head) {
+    SA_STRIDE(p, m) head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+}
+
+// unique keys, plan pointer, gathered pairs
+__global__ void k_sp_plan(const uint64_t* __restrict__ ks, const int* __restrict__ perm, const int64_t* head,
+                          const int64_t* pos, int64_t m, const int* __restrict__ ia, const int* __restrict__ ib,
+                          uint64_t* __restrict__ ukeys, int* __restrict__ optr, int* __restrict__ pa,
+                          int* __restrict__ pb) {
+    SA_STRIDE(p, m) {
+        if (head[p]) {
+            ukeys[pos[p]] = ks[p];
+            optr[pos[p]] = static_cast<int>(p);
+        }
+        const int t = perm[p];
+        pa[p] = ia[t];
+        pb[p] = ib[t];
+    }
+}
+
+__global__ void k_sp_rowptr(const uint64_t* ukeys, int64_t m, int64_t n, int b, int* ptr) {
+    SA_STRIDE(i, n + 1) {
+        const uint64_t target = static_cast<uint64_t>(i) << b;
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (ukeys[mid] < target)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        ptr[i] = static_cast<int>(lo);
+    }
+}
+
+__global__ void k_sp_col(const uint64_t* ukeys, int64_t m, uint64_t mask, int* col) {
+    SA_STRIDE(p, m) col[p] = static_cast<int>(ukeys[p] & mask);
+}
+
+__global__ void k_sp_set(int* p, int v) { *p = v; }
+
+__global__ void k_spgemm_num(int64_t nnz, const int* __restrict__ optr, const int* __restrict__ pa,
+                             const int* __restrict__ pb, const double* __restrict__ a, const double* __restrict__ b,
+                             double* __restrict__ c) {
+    SA_STRIDE(e, nnz) {
+        double s = 0.0;
+        for (int t = optr[e]; t < optr[e + 1]; ++t) s = dadd(s, dmul(a[pa[t]], b[pb[t]]));
+        c[e] = s;
+    }
+}
+
+__global__ void k_tentative(int64_t n, const int* __restrict__ agg, int* rp, int* col, double* val) {
+    SA_STRIDE(i, n) {
+        rp[i] = static_cast<int>(i);
+        col[i] = agg[i];
+        val[i] = 1.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rp[n] = static_cast<int>(n);
+}
+
+__global__ void k_sa_values(int64_t n, const int* __restrict__ rp, const int* __restrict__ col, double* v,
+                            const int* __restrict__ agg, const int* __restrict__ dpos, const double* __restrict__ aval,
+                            double w, int* bad) {
+    SA_STRIDE(i, n) {
+        const int k = dpos[i];
+        const double d = k >= 0 ? aval[k] : 0.0;
+        if (k < 0 || d == 0.0) {
+            atomicMin(bad, static_cast<int>(i));
+            continue;
+        }
+        const double s = dmul(w, __ddiv_rn(1.0, d));
+        const int J = agg[i];
+        for (int q = rp[i]; q < rp[i + 1]; ++q) v[q] = dsub(col[q] == J ? 1.0 : 0.0, dmul(s, v[q]));
+    }
+}
+
+__global__ void k_row_of(int64_t n, const int* __restrict__ rp, int* rowof) {
+    SA_STRIDE(i, n) for (int e = rp[i]; e < rp[i + 1]; ++e) rowof[e] = static_cast<int>(i);
+}
+
+__global__ void k_tr_keys(int64_t m, const int* __restrict__ col, uint64_t* key, int* id) {
+    SA_STRIDE(e, m) {
+        key[e] = static_cast<uint64_t>(col[e]);
+        id[e] = static_cast<int>(e);
+    }
+}
+
+__global__ void k_tr_fill(int64_t m, const int* __restrict__ perm, const int* __restrict__ rowof,
+                          const double* __restrict__ val, int* tcol, double* tval) {
+    SA_STRIDE(p, m) {
+        const int e = perm[p];
+        tcol[p] = rowof[e];
+        tval[p] = val[e];
+    }
+}
+
+}  // namespace
+
+void spgemm_symbolic(Ctx& c, const CsrView& A, const int* brp, const int* bcol, int64_t bcols, SpgPlan& out,
+                     const char* what) {
+    const int64_t m = A.nnz;
+    DevArray<int64_t> cnt(m + 1, c.stream), off(m + 1, c.stream);
+    LAUNCH(c, "setup", 0.0, k_sp_count, grid_for(m > 0 ? m : 1, SA_B, c.num_sms * 16), SA_B, 0, A, brp, cnt.get());
+    exclusive_sum(c, cnt.get(), off.get(), m + 1);
+    const int64_t T = d2h_scalar(off.get() + m, c.stream);
+    if (T >= (int64_t{1} << 31) - 1) {
+        std::ostringstream os;
+        os << what << ": " << T << " products exceed the 2^31 plan limit of the device SpGEMM";
+        fail(AMGR_E_RUNTIME, os.str());
+    }
+    const int bi = bits_for(A.n), bj = bits_for(bcols);
+    DevArray<uint64_t> k0(T, c.stream), k1(T, c.stream);
+    DevArray<int> ia(T, c.stream), ib(T, c.stream), v0(T, c.stream), v1(T, c.stream);
+    if (T > 0)
+        LAUNCH(c, "setup", 0.0, k_sp_triples, grid_for(A.n, SA_B, c.num_sms * 16), SA_B, 0, A, brp, bcol, bj,
+               off.get(), k0.get(), ia.get(), ib.get(), v0.get());
+    uint64_t* ks = k0.get();
+    int* vs = v0.get();
+    if (T > 1) sort_pairs(c, k0.get(), k1.get(), v0.get(), v1.get(), T, bi + bj, &ks, &vs);
+    DevArray<int64_t> head(T, c.stream), pos(T, c.stream);
+    int64_t nnz = 0;
+    if (T > 0) {
+        LAUNCH(c, "setup", 0.0, k_sp_heads, grid_for(T, SA_B, c.num_sms * 16), SA_B, 0, ks, T, head.get());
+        exclusive_sum(c, head.get(), pos.get(), T);
+        nnz = d2h_scalar(pos.get() + T - 1, c.stream) + d2h_scalar(head.get() + T - 1, c.stream);
+    }
+    out.nnz = nnz;
+    out.products = T;
+    out.optr.alloc(nnz + 1, c.stream);
+    out.pa.alloc(T, c.stream);
+    out.pb.alloc(T, c.stream);
+    DevArray<uint64_t> ukeys(nnz, c.stream);
+    if (T > 0)
+        LAUNCH(c, "setup", 0.0, k_sp_plan, grid_for(T, SA_B, c.num_sms * 16), SA_B, 0, ks, vs, head.get(), pos.get(),
+               T, ia.get(), ib.get(), ukeys.get(), out.optr.get(), out.pa.get(), out.pb.get());
+    LAUNCH(c, "setup", 0.0, k_sp_set, 1, 1, 0, out.optr.get() + nnz, static_cast<int>(T));
+    out.rp.alloc(A.n + 1, c.stream);
+    LAUNCH(c, "setup", 0.0, k_sp_rowptr, grid_for(A.n + 1, SA_B, c.num_sms * 16), SA_B, 0, ukeys.get(), nnz, A.n,
+           bj, out.rp.get());
+    out.col.alloc(nnz, c.stream);
+    if (nnz > 0)
+        LAUNCH(c, "setup", 0.0, k_sp_col, grid_for(nnz, SA_B, c.num_sms * 16), SA_B, 0, ukeys.get(), nnz,
+               (uint64_t{1} << bj) - 1, out.col.get());
+}
+
+void spgemm_numeric(Ctx& c, const SpgPlan& p, const double* a, const double* b, double* out) {
+    if (p.nnz == 0) return;
+    LAUNCH(c, "rap", 8.0 * p.nnz + 12.0 * p.products, k_spgemm_num, grid_for(p.nnz, SA_B, c.num_sms * 16), SA_B, 0,
+           p.nnz, p.optr.get(), p.pa.get(), p.pb.get(), a, b, out);
+}
+
+void tentative_csr(Ctx& c, int64_t n, const int* agg, DevArray<int>& rp, DevArray<int>& col, DevArray<double>& val) {
+    rp.alloc(n + 1, c.stream);
+    col.alloc(n, c.stream);
+    val.alloc(n, c.stream);
+    LAUNCH(c, "setup", 0.0, k_tentative, grid_for(n, SA_B, c.num_sms * 16), SA_B, 0, n, agg, rp.get(), col.get(),
+           val.get());
+}
+
+void sa_prolongator_values(Ctx& c, int64_t n, const int* rp, const int* col, double* v, const int* agg,
+                           const int* dpos, const double* aval, double w, int* bad) {
+    LAUNCH(c, "setup", 0.0, k_sa_values, grid_for(n, SA_B, c.num_sms * 16), SA_B, 0, n, rp, col, v, agg, dpos, aval,
+           w, bad);
+}
+
+void transpose_csr(Ctx& c, int64_t nrows, int64_t ncols, int64_t nnz, const int* rp, const int* col,
+                   const double* val, DevArray<int>& trp, DevArray<int>& tcol, DevArray<double>& tval) {
+    DevArray<int> rowof(nnz, c.stream), v0(nnz, c.stream), v1(nnz, c.stream);
+    DevArray<uint64_t> k0(nnz, c.stream), k1(nnz, c.stream);
+    if (nnz > 0) {
+        LAUNCH(c, "setup", 0.0, k_row_of, grid_for(nrows, SA_B, c.num_sms * 16), SA_B, 0, nrows, rp, rowof.get());
+        LAUNCH(c, "setup", 0.0, k_tr_keys, grid_for(nnz, SA_B, c.num_sms * 16), SA_B, 0, nnz, col, k0.get(),
+               v0.get());
+    }
+    uint64_t* ks = k0.get();
+    int* vs = v0.get();
+    if (nnz > 1) sort_pairs(c, k0.get(), k1.get(), v0.get(), v1.get(), nnz, bits_for(ncols), &ks, &vs);
+    trp.alloc(ncols + 1, c.stream);
+    LAUNCH(c, "setup", 0.0, k_sp_rowptr, grid_for(ncols + 1, SA_B, c.num_sms * 16), SA_B, 0, ks, nnz, ncols, 0,
+           trp.get());
+    tcol.alloc(nnz, c.stream);
+    tval.alloc(nnz, c.stream);
+    if (nnz > 0)
+        LAUNCH(c, "setup", 0.0, k_tr_fill, grid_for(nnz, SA_B, c.num_sms * 16), SA_B, 0, nnz, vs, rowof.get(), val,
+               tcol.get(), tval.get());
 }
 
 }  // namespace amgr

@@ -37,4 +37,25 @@ struct RapSymbolic {
 };
 void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbolic& out);
 
+// ---- smoothed aggregation (extension) ----
+// Device SpGEMM C = A B: structural pattern of C (sorted columns) and the
+// numeric plan (per output entry, its (a index, b index) products in the
+// reference spmm's accumulation order).
+struct SpgPlan {
+    int64_t nnz = 0, products = 0;
+    DevArray<int> rp, col;          // pattern of C (rows = A's rows)
+    DevArray<int> optr, pa, pb;     // plan
+};
+void spgemm_symbolic(Ctx& c, const CsrView& A, const int* brp, const int* bcol, int64_t bcols, SpgPlan& out,
+                     const char* what);
+void spgemm_numeric(Ctx& c, const SpgPlan& p, const double* a, const double* b, double* out);
+// P_tent as CSR (row i: column agg_i, value 1.0; coarsening.cpp:122-132)
+void tentative_csr(Ctx& c, int64_t n, const int* agg, DevArray<int>& rp, DevArray<int>& col, DevArray<double>& val);
+// in place on the values of A P_tent: v = (J == agg_i) - (w * (1/a_ii)) * v; first bad row -> *bad
+void sa_prolongator_values(Ctx& c, int64_t n, const int* rp, const int* col, double* v, const int* agg,
+                           const int* dpos, const double* aval, double w, int* bad);
+// T = M^T (sorted columns, values carried)
+void transpose_csr(Ctx& c, int64_t nrows, int64_t ncols, int64_t nnz, const int* rp, const int* col,
+                   const double* val, DevArray<int>& trp, DevArray<int>& tcol, DevArray<double>& tval);
+
 }  // namespace amgr

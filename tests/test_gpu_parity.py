@@ -287,6 +287,55 @@ def test_vcycle_tail_kernels_bit_exact(ctx, name, monkeypatch):
 
 
 # ---------------------------------------------------------------- extensions vs the restated oracle
+@pytest.mark.parametrize("name,sa_omega", [("poisson2d_40", 2.0 / 3.0), ("poisson3d_12", 2.0 / 3.0),
+                                           ("dambreak_16", 0.5), ("random_300", 2.0 / 3.0)])
+def test_smoothed_aggregation_vs_oracle(ctx, name, sa_omega):
+    """Smoothed aggregation (extension, parity pinned to the restated oracle):
+    the device-built smoothed prolongator P, R = P^T, every A_i (two device
+    SpGEMMs), the V-cycle with general R/P, a partial update and the solves."""
+    from oracle import oracle as O
+
+    make, kw = CASES[name]
+    A = make()
+    kw = dict(kw, coarsening="smoothed", sa_omega=sa_omega)
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    o = O.setup(A, O.params(**kw))
+    assert h.num_levels() == len(o.levels)
+    for l, L in enumerate(o.levels):
+        rp, ci, v = h.level_A(l)
+        np.testing.assert_array_equal(rp, L.A[0], err_msg=f"level {l} row_ptr")
+        np.testing.assert_array_equal(ci, L.A[1], err_msg=f"level {l} col")
+        np.testing.assert_array_equal(_bits(v), _bits(L.A[2]), err_msg=f"level {l} values")
+        if L.P is not None:
+            for which, ref_m in (("P", L.P), ("R", L.R)):
+                mrp, mci, mv = h.level_transfer(l, which)
+                np.testing.assert_array_equal(mrp, ref_m[0], err_msg=f"level {l} {which} row_ptr")
+                np.testing.assert_array_equal(mci, ref_m[1], err_msg=f"level {l} {which} col")
+                np.testing.assert_array_equal(_bits(mv), _bits(ref_m[2]), err_msg=f"level {l} {which} values")
+            np.testing.assert_array_equal(_bits(h.level_smoother(l)), _bits(L.w))
+    lu, piv = h.coarse_lu()
+    np.testing.assert_array_equal(piv, o.piv)
+    np.testing.assert_array_equal(_bits(lu), _bits(o.lu))
+    n = len(A[0]) - 1
+    f = np.random.default_rng(4).uniform(-1, 1, n)
+    np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(O.vcycle(o, f)))
+    fr = P.rhs(n)
+    _, st = amg.bicgstab(h, fr)
+    so = O.bicgstab(o, fr)
+    assert st.converged and abs(st.iterations - so.iterations) <= 1
+    _, sc = amg.cg(h, fr)
+    oc = O.cg(o, fr)
+    assert sc.converged == oc.converged and abs(sc.iterations - oc.iterations) <= 1
+    # partial update: frozen P/R values, new Galerkin products
+    A2 = (A[0], A[1], A[2] * np.linspace(1.0, 1.5, len(A[2])))
+    h2 = amg.partial_update(h, A2, amg.AmgParams(**kw))
+    o2 = O.partial_update(o, A2, O.params(**kw))
+    for l, L in enumerate(o2.levels):
+        np.testing.assert_array_equal(_bits(h2.level_A(l)[2]), _bits(L.A[2]), err_msg=f"update level {l}")
+    np.testing.assert_array_equal(_bits(amg.vcycle(h2, f)), _bits(O.vcycle(o2, f)))
+
+
+
 @pytest.mark.parametrize("problem", ["poisson", "convdiff"])
 def test_chebyshev_smoother_vs_oracle(ctx, problem):
     """Chebyshev + power iteration (extension, parity unpinned by the
