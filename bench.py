@@ -448,6 +448,43 @@ def main():
                 "bytes_formula": "12*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads)",
                 "nnz": lvl0["nnz"], "n": lvl0["nrows"], "peak_source": peak_kind, "kernels": extra}
 
+    # ---- whole-phase rooflines (SURVEY.md 8(d) algorithmic bytes from this
+    # hierarchy's level shapes): rebuild, one V-cycle, one BiCGStab iteration ----
+    dims = [h.level_dims(l) for l in range(h.num_levels())]
+    nl = [d["nrows"] for d in dims]
+    zl = [d["nnz"] for d in dims]
+    Lh = len(dims)
+    rap_b = sum(12 * zl[i] + 8 * zl[i + 1] + 4 * nl[i] + 4 * (nl[i + 1] + 1) for i in range(Lh - 1))
+    jac_b = sum(20 * nl[i] for i in range(Lh - 1))
+    spmv = [12 * zl[i] + 4 * (nl[i] + 1) + 16 * nl[i] for i in range(Lh)]
+    vc_b = sum(2 * spmv[i] + 64 * nl[i] for i in range(Lh - 1))
+    it_b = 2 * vc_b + 2 * spmv[0] + 192 * nl[0]
+    # one V-cycle, device time (stream-launched, 10 repetitions)
+    vz = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        amg.vcycle_device(h, f.data_ptr(), vz.data_ptr())
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record()
+        for _ in range(10):
+            amg.vcycle_device(h, f.data_ptr(), vz.data_ptr())
+        e1.record()
+    ctx.synchronize()
+    vc_ms = e0.elapsed_time(e1) / 10
+    it_ms = solve_ms / max(float(np.mean(iters)), 1.0)
+
+    def phase(bytes_, ms):
+        gbs = bytes_ / ms / 1e6
+        return {"algorithmic_GB": bytes_ / 1e9, "ms": ms, "GB_s": gbs, "frac_measured_peak": gbs / peak,
+                "frac_8TBs_nominal": gbs / 8000.0}
+
+    phases = {"rebuild": phase(rap_b + jac_b, rebuild_ms), "vcycle": phase(vc_b, vc_ms),
+              "bicgstab_iteration": phase(it_b, it_ms),
+              "bytes_formulas": "SURVEY.md 8(d): RAP 12nnz_i+8nnz_i+1+4n_i+4(n_i+1 +1), Jacobi 20n_i, "
+                                "V-cycle sum(2 SpMV_i + 64 n_i), iteration 2 V + 2 SpMV_0 + 192 n_0"}
+    del vz
+
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None
     if not a.no_e2e:
@@ -539,7 +576,7 @@ def main():
                "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
                "converged": all(conv), "setup_s": setup_s, "step0_iterations": st0.iterations,
                "clocks": clk.summary(), "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
-               "strategies": strategies,
+               "strategies": strategies, "phase_rooflines": phases,
                "cpu_baseline": cpu}
         print(json.dumps(out), flush=True)
     if world > 1:
