@@ -71,7 +71,11 @@ struct Ctx {
 template <class F>
 void on_side(Ctx& c, F&& fn) {
     if (!c.side) {
-        CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        // highest priority: the side stream carries the one-CTA coarse
+        // factorization, which must not queue behind wide smoother grids
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi));
         CK(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
     }

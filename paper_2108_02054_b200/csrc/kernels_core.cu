@@ -805,16 +805,30 @@ void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const 
 }
 
 // ---- end k_rap_tma
+// w = 1/a_ii (smoother.cpp:8-32).  Each thread handles JB rows strided by the
+// grid so the JB diagonal gathers (one 32-byte sector each) are in flight
+// together.
+constexpr int JB = 4;
 __global__ void k_jacobi(int n, const double* __restrict__ val, const int* __restrict__ dpos,
                          double* __restrict__ w, int* bad) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int k = dpos[i];
-        const double d = k >= 0 ? val[k] : 0.0;
-        if (d == 0.0) {
-            atomicMin(bad, i);
-            w[i] = 0.0;
-        } else {
-            w[i] = __ddiv_rn(1.0, d);
+    const int stride = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += JB * stride) {
+        int k[JB];
+        double d[JB];
+#pragma unroll
+        for (int t = 0; t < JB; ++t) k[t] = i0 + t * stride < n ? __ldg(dpos + i0 + t * stride) : -1;
+#pragma unroll
+        for (int t = 0; t < JB; ++t) d[t] = k[t] >= 0 ? __ldg(val + k[t]) : 0.0;
+#pragma unroll
+        for (int t = 0; t < JB; ++t) {
+            const int i = i0 + t * stride;
+            if (i >= n) continue;
+            if (d[t] == 0.0) {
+                atomicMin(bad, i);
+                w[i] = 0.0;
+            } else {
+                w[i] = __ddiv_rn(1.0, d[t]);
+            }
         }
     }
 }
