@@ -319,15 +319,13 @@ static void prolong_level(Ctx& c, const Level& Li, const double* u, const double
         vc_prolong(c, Li.pat->n, u, Li.T->agg.get(), e, out, g);
 }
 
-// Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans.
-// Level 0's smoother is rebuilt by its own kernel; for every coarser smoothed
-// level the Jacobi rebuild is fused into the Galerkin kernel that produces it
-// (its time is therefore booked under `galerkin`).
+// Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans:
+// the Galerkin chain, then the per-level smoother rebuilds (main stream)
+// concurrently with the coarsest factorization (side stream).
 void numeric_pass(Hier& h, PhaseClock& clk) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
-    const bool jacobi = false;  // fused coarse-level Jacobi disabled: separate smoother kernel per level
     // Galerkin chain first; then the coarsest dense factorization (one CTA)
     // runs on the side stream concurrently with the per-level smoother
     // rebuilds, which do not depend on it.  Errors are still reported in the
@@ -338,17 +336,11 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         clk.begin(PH_GALERKIN);
         Level& B = h.lv[i + 1];
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
-        const bool fuse = jacobi && i + 2 < L;
-        if (fuse) {
-            if (B.w.size() != B.pat->n) B.w.alloc(B.pat->n, c.stream);
-            B.has_smoother = true;
-        }
         if (A.T->smoothed)
             sa_galerkin_numeric(c, *A.rap, A.view().val, *A.T, B.val.get());
         else
-            rap_numeric(c, A.pat->n, B.pat->n, B.pat->rp.get(), B.pat->diag.get(), A.rap->nnz_c, A.rap->cptr.get(),
-                        A.rap->contrib.get(), A.view().val, B.val.get(), A.pat->nnz, fuse ? B.w.get() : nullptr,
-                        W.err.get() + i + 1, A.rap->max_chunk);
+            rap_numeric(c, A.pat->n, B.pat->n, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val,
+                        B.val.get(), A.pat->nnz, A.rap->max_chunk);
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
@@ -358,7 +350,6 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         clk.end(PH_COARSE);
     });
     for (size_t i = 0; i + 1 < L; ++i) {
-        if (i > 0 && jacobi) continue;
         c.cur_level = static_cast<int>(i);
         clk.begin(PH_SMOOTHER);
         build_smoother(c, h.lv[i], h.prm, W.err.get() + i);
@@ -541,8 +532,8 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             next.val.alloc(s.nnz_c, c.stream);
             CsrView nv = next.view();
             find_diag(c, nv, P->diag.get());
-            rap_numeric(c, Av.n, nc, P->rp.get(), P->diag.get(), s.nnz_c, plan->cptr.get(), plan->contrib.get(),
-                        Av.val, next.val.get(), Av.nnz, nullptr, nullptr, plan->max_chunk);
+            rap_numeric(c, Av.n, nc, s.nnz_c, plan->cptr.get(), plan->contrib.get(), Av.val, next.val.get(), Av.nnz,
+                        plan->max_chunk);
             P->max_span = max_group_span(c, P->rp.get(), P->n);
             cur.rap = plan;
         }

@@ -105,9 +105,8 @@ void tail_up(Ctx& c, const TailDesc& d, double om, Gate g);
 
 // largest contrib count of any RT_CH-entry chunk of a plan (TMA stage size; host sync)
 int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr);
-void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
-                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad,
-                 int max_chunk = -1);
+void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f, int max_chunk = -1);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);

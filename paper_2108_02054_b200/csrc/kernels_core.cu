@@ -222,68 +222,6 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
 
-constexpr int RS_BLOCK = 256;  // simple variant: one 32-row group per warp, synchronous staging
-constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_CH = 256;
-constexpr int RS_MINB = 5;
-
-template <class Op>
-__global__ void __launch_bounds__(RS_BLOCK, RS_MINB) k_rowpass_simple(CsrView A, Op op, Gate g, DotSink sink) {
-    pdl_enter();
-    if (gated_off(g)) return;
-    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
-    __shared__ double s_val[RS_WARPS][RS_CH];
-    __shared__ int s_col[RS_WARPS][RS_CH];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int n = static_cast<int>(A.n);
-    double dots[ND];
-#pragma unroll
-    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
-    const int64_t wstride = static_cast<int64_t>(gridDim.x) * RS_WARPS;
-    for (int64_t wid = static_cast<int64_t>(blockIdx.x) * RS_WARPS + w; wid * 32 < n; wid += wstride) {
-        const int r0 = static_cast<int>(wid * 32);
-        const int r1 = min(r0 + 32, n);
-        const int row = r0 + lane;
-        const bool valid = row < n;
-        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + r1);
-        const int rs = valid ? __ldg(A.rp + row) : e1;
-        const int re = valid ? __ldg(A.rp + row + 1) : e1;
-        double sum = 0.0, xdiag = 0.0;
-        typename Op::Row rw;
-        if (valid) rw = op.load(row);
-        for (int c0 = e0; c0 < e1; c0 += RS_CH) {
-            const int c1 = min(c0 + RS_CH, e1);
-#pragma unroll 4
-            for (int e = c0 + lane; e < c1; e += 32) {
-                s_val[w][e - c0] = __ldg(A.val + e);
-                s_col[w][e - c0] = __ldg(A.col + e);
-            }
-            __syncwarp();
-            int a = max(rs, c0);
-            const int b = min(re, c1);
-            // issue up to RP_BATCH independent operand gathers, then accumulate
-            // them strictly in column order
-            while (a < b) {
-                const int cnt = min(RP_BATCH, b - a);
-                const int k = a - c0;
-                double xv[RP_BATCH];
-#pragma unroll
-                for (int t = 0; t < RP_BATCH; ++t) xv[t] = t < cnt ? op.x(s_col[w][k + t]) : 0.0;
-#pragma unroll
-                for (int t = 0; t < RP_BATCH; ++t)
-                    if (t < cnt) {
-                        sum = dadd(sum, dmul(s_val[w][k + t], xv[t]));
-                        if (s_col[w][k + t] == row) xdiag = xv[t];
-                    }
-                a += cnt;
-            }
-            __syncwarp();
-        }
-        if (valid) op.finish(row, sum, rw, dots);
-    }
-    if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
-}
-
 // ---- row-pass operators ----------------------------------------------------
 struct NoRow {};
 struct Row1 {
@@ -499,13 +437,6 @@ struct OpChebStep {
 
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
-int rowpass_variant() {
-    static int v = [] {
-        const char* e = getenv("AMGR_ROWPASS");
-        return (e && std::string(e) == "simple") ? 1 : 0;
-    }();
-    return v;
-}
 
 template <class Op, int CH, int GATHER>
 void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
@@ -525,12 +456,6 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
                     DotSink s, bool fixed_grid) {
     if (A.n == 0) return;
     const int64_t groups = (A.n + 31) / 32;
-    if (rowpass_variant() == 1) {
-        unsigned grid = grid_for(groups, RS_WARPS);
-        if (fixed_grid) grid = static_cast<unsigned>(dot_grid(c));
-        LAUNCH_PDL(c, fam, bytes, k_rowpass_simple<Op>, grid, RS_BLOCK, 0, A, op, g, s);
-        return;
-    }
     int64_t want = (groups + RP_WARPS - 1) / RP_WARPS;
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
@@ -1492,14 +1417,9 @@ int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr) {
     return h;
 }
 
-void rap_numeric(Ctx& c, int64_t nf, int64_t nc, const int* crp, const int* cdiag, int64_t nnz_c, const int* cptr,
-                 const int* contrib, const double* af, double* ac, int64_t nnz_f, double* wc, int* bad,
-                 int max_chunk) {
+void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f, int max_chunk) {
     if (nnz_c == 0) return;
-    (void)crp;
-    (void)cdiag;
-    (void)wc;
-    (void)bad;
     // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1)
     const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
     if (max_chunk >= 0) {
