@@ -272,6 +272,16 @@ amgr_status amgr_dist_create(amgr_hier* global, const void* nccl_id128, int rank
                              const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
                              amgr_dist** out);
 /* Global rebuild on every rank + gather of the local values (round 1). */
+/* Test transport: W ranks of ONE process (one host thread and one context
+ * each, same device) exchange through stream-ordered device copies and host
+ * barriers instead of NCCL, so the multi-rank device path can be checked on
+ * a single GPU.  Same plan arguments as amgr_dist_create. */
+typedef struct amgr_loopback amgr_loopback;
+amgr_status amgr_dist_loopback_create(int world, amgr_loopback** out);
+void amgr_dist_loopback_destroy(amgr_loopback* lb);
+amgr_status amgr_dist_create_loopback(amgr_hier* global, amgr_loopback* lb, int rank, int world, int top,
+                                      const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
+                                      amgr_dist** out);
 amgr_status amgr_dist_rebuild_values(amgr_dist* d, const double* global_values, int location);
 /* f/u: device vectors over the owned level-0 rows. */
 amgr_status amgr_dist_vcycle(amgr_dist* d, const double* f_local, double* u_local);

@@ -135,6 +135,9 @@ PROTOTYPES = {
     "amgr_hier_level_transfer": (_I, [_V, _I, _I, _P(_L), _V, _V, _V]),
     "amgr_nccl_unique_id": (_I, [_V]),
     "amgr_dist_create": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
+    "amgr_dist_loopback_create": (_I, [_I, _P(_V)]),
+    "amgr_dist_loopback_destroy": (None, [_V]),
+    "amgr_dist_create_loopback": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
     "amgr_dist_rebuild_values": (_I, [_V, _V, _I]),
     "amgr_dist_vcycle": (_I, [_V, _V, _V]),
     "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),

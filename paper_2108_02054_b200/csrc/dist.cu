@@ -20,8 +20,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <sstream>
 
 #include "hierarchy.cuh"
@@ -135,10 +137,52 @@ struct DistLevel {
     }
 };
 
+// In-process transport for testing the multi-rank device path on ONE GPU:
+// W ranks live in one process (one host thread and one context/stream each).
+// Every exchange is stream-ordered like its NCCL counterpart: a rank posts
+// its send pointers plus an event recorded after the producing kernel, all
+// ranks meet at a host barrier, each rank makes its stream wait on the
+// producers' events and pulls the data with device-to-device copies, records
+// a "consumed" event, and after a second barrier waits on its consumers'
+// events before its send buffers may be reused.  No kernel ever waits on
+// another rank's kernel.
+struct Loopback {
+    int world = 1;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t generation = 0;
+    struct Post {
+        std::vector<const double*> ptr;  // by destination rank (halo) or [0] (allgather)
+        std::vector<int64_t> cnt;
+        cudaEvent_t ready = nullptr, consumed = nullptr;
+    };
+    std::vector<Post> post;
+    explicit Loopback(int w) : world(w), post(static_cast<size_t>(w)) {
+        for (auto& p : post) {
+            p.ptr.assign(static_cast<size_t>(w), nullptr);
+            p.cnt.assign(static_cast<size_t>(w), 0);
+        }
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const int64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct DistHier {
     Hier* g = nullptr;
     Ctx* ctx = nullptr;
     ncclComm_t comm = nullptr;
+    Loopback* lb = nullptr;  // test transport instead of NCCL
+    cudaEvent_t ev_ready = nullptr, ev_consumed = nullptr;
     int rank = 0, world = 1, T = -1;
     std::vector<DistLevel> lv;
     // transition (level T -> T+1)
@@ -157,6 +201,35 @@ static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
     if (L.send_idx.size() > 0)
         LAUNCH(c, "halo_pack", 16.0 * L.send_idx.size(), k_gather_d, grid_for(L.send_idx.size(), 256, c.num_sms * 8),
                256, 0, L.send_idx.size(), x, L.send_idx.get(), L.send_buf.get(), g);
+    if (d.lb) {  // every rank enters both barriers, peers or not
+        Loopback& lb = *d.lb;
+        Loopback::Post& me = lb.post[d.rank];
+        CK(cudaEventRecord(d.ev_ready, c.stream));
+        for (int q = 0; q < d.world; ++q) {
+            me.ptr[q] = nullptr;
+            me.cnt[q] = 0;
+        }
+        for (size_t k = 0; k < L.send_peer.size(); ++k) {
+            me.ptr[L.send_peer[k]] = L.send_buf.get() + L.send_off[k];
+            me.cnt[L.send_peer[k]] = L.send_cnt[k];
+        }
+        me.ready = d.ev_ready;
+        me.consumed = d.ev_consumed;
+        lb.barrier();
+        for (size_t k = 0; k < L.recv_peer.size(); ++k) {
+            const Loopback::Post& src = lb.post[L.recv_peer[k]];
+            if (src.cnt[d.rank] != L.recv_cnt[k]) fail(AMGR_E_RUNTIME, "loopback halo: send/recv counts differ");
+            CK(cudaStreamWaitEvent(c.stream, src.ready, 0));
+            CK(cudaMemcpyAsync(x + L.n_own + L.recv_off[k], src.ptr[d.rank], sizeof(double) * L.recv_cnt[k],
+                               cudaMemcpyDeviceToDevice, c.stream));
+        }
+        CK(cudaEventRecord(d.ev_consumed, c.stream));
+        lb.barrier();
+        for (size_t k = 0; k < L.send_peer.size(); ++k)
+            CK(cudaStreamWaitEvent(c.stream, lb.post[L.send_peer[k]].consumed, 0));
+        lb.barrier();  // posts may be rewritten only after every rank has read them
+        return;
+    }
     if (d.world == 1 || (L.send_peer.empty() && L.recv_peer.empty())) return;
     NK(N().GroupStart());
     for (size_t k = 0; k < L.send_peer.size(); ++k)
@@ -168,15 +241,41 @@ static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
     NK(N().GroupEnd());
 }
 
+// allgather of count doubles per rank (rank r's block at recv + r*count)
+static void allgather(DistHier& d, const double* send, double* recv, int64_t count) {
+    Ctx& c = *d.ctx;
+    if (d.lb) {
+        Loopback& lb = *d.lb;
+        Loopback::Post& me = lb.post[d.rank];
+        CK(cudaEventRecord(d.ev_ready, c.stream));
+        me.ptr[0] = send;
+        me.cnt[0] = count;
+        me.ready = d.ev_ready;
+        me.consumed = d.ev_consumed;
+        lb.barrier();
+        for (int q = 0; q < d.world; ++q) {
+            CK(cudaStreamWaitEvent(c.stream, lb.post[q].ready, 0));
+            CK(cudaMemcpyAsync(recv + q * count, lb.post[q].ptr[0], sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                               c.stream));
+        }
+        CK(cudaEventRecord(d.ev_consumed, c.stream));
+        lb.barrier();
+        for (int q = 0; q < d.world; ++q) CK(cudaStreamWaitEvent(c.stream, lb.post[q].consumed, 0));
+        lb.barrier();
+        return;
+    }
+    if (d.world > 1)
+        NK(N().AllGather(send, recv, static_cast<size_t>(count), ncclDouble, d.comm, c.stream));
+    else
+        d2d(recv, send, count, c.stream);
+}
+
 // deterministic cross-rank sum of k local dots (d.dloc[0..k)) into outs
 static void allsum(DistHier& d, int k, std::initializer_list<double*> outs) {
     Ctx& c = *d.ctx;
     std::vector<double*> o(outs);
     h2d(d.douts.get(), o.data(), static_cast<int64_t>(o.size()), c.stream);
-    if (d.world > 1)
-        NK(N().AllGather(d.dloc.get(), d.dall.get(), static_cast<size_t>(k), ncclDouble, d.comm, c.stream));
-    else
-        d2d(d.dall.get(), d.dloc.get(), k, c.stream);
+    allgather(d, d.dloc.get(), d.dall.get(), k);
     LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), d.douts.get());
 }
 
@@ -208,10 +307,7 @@ static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
         }
     }
     // transition: replicate f_{T+1}, then the coarse levels on every rank
-    if (d.world > 1)
-        NK(N().AllGather(d.tsend.get(), d.tgather.get(), static_cast<size_t>(d.tpad), ncclDouble, d.comm, c.stream));
-    else
-        d2d(d.tgather.get(), d.tsend.get(), d.tpad, c.stream);
+    allgather(d, d.tsend.get(), d.tgather.get(), d.tpad);
     LAUNCH(c, "dist", 0.0, k_unpad, grid_for(d.tpad, 256, 64), 256, 0, d.world, d.tpad, d.tgather.get(),
            d.tdispl_d.get(), d.tcnt_d.get(), d.fT.get());
     vcycle_from(h, static_cast<size_t>(T + 1), d.fT.get(), d.uT.get(), g);
@@ -260,10 +356,11 @@ amgr_status amgr_nccl_unique_id(void* out128) {
     return AMGR_OK;
 }
 
-amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, int world, int top,
-                             const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
-                             amgr_dist** out) {
-    if (!hg || !nccl_id128 || !out || (top >= 0 && !levels) || world < 1) return AMGR_E_INVALID_ARGUMENT;
+static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top, const amgr_dist_level* levels,
+                                    int64_t t_count_total, const int64_t* t_counts, amgr_dist** out,
+                                    const std::function<void(amgr::DistHier&)>& connect) {
+    if (!hg || !out || (top >= 0 && !levels) || world < 1 || rank < 0 || rank >= world)
+        return AMGR_E_INVALID_ARGUMENT;
     *out = nullptr;
     amgr::Hier& H = *hg->h;
     amgr::Ctx& c = *H.ctx;
@@ -282,9 +379,7 @@ amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, in
         d->rank = rank;
         d->world = world;
         d->T = top;
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_id128, sizeof(id));
-        NK(::amgr::N().CommInitRank(&d->comm, world, id, rank));
+        connect(*d);
         auto up32 = [&](amgr::DevArray<int>& dst, const int64_t* src, int64_t n) {
             std::vector<int> tmp(static_cast<size_t>(n));
             for (int64_t k = 0; k < n; ++k) tmp[k] = static_cast<int>(src[k]);
@@ -369,9 +464,42 @@ amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, in
     }
 }
 
+amgr_status amgr_dist_create(amgr_hier* hg, const void* nccl_id128, int rank, int world, int top,
+                             const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
+                             amgr_dist** out) {
+    if (!nccl_id128) return AMGR_E_INVALID_ARGUMENT;
+    return dist_create_impl(hg, rank, world, top, levels, t_count_total, t_counts, out, [&](amgr::DistHier& d) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof(id));
+        NK(::amgr::N().CommInitRank(&d.comm, world, id, rank));
+    });
+}
+
+amgr_status amgr_dist_loopback_create(int world, amgr_loopback** out) {
+    if (!out || world < 1) return AMGR_E_INVALID_ARGUMENT;
+    *out = reinterpret_cast<amgr_loopback*>(new amgr::Loopback(world));
+    return AMGR_OK;
+}
+
+void amgr_dist_loopback_destroy(amgr_loopback* lb) { delete reinterpret_cast<amgr::Loopback*>(lb); }
+
+amgr_status amgr_dist_create_loopback(amgr_hier* hg, amgr_loopback* lbh, int rank, int world, int top,
+                                      const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
+                                      amgr_dist** out) {
+    auto* lb = reinterpret_cast<amgr::Loopback*>(lbh);
+    if (!lb || lb->world != world) return AMGR_E_INVALID_ARGUMENT;
+    return dist_create_impl(hg, rank, world, top, levels, t_count_total, t_counts, out, [&](amgr::DistHier& d) {
+        d.lb = lb;
+        CK(cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&d.ev_consumed, cudaEventDisableTiming));
+    });
+}
+
 void amgr_dist_destroy(amgr_dist* d) {
     if (!d) return;
     if (d->d && d->d->comm) amgr::nccl_api()->CommDestroy(d->d->comm);
+    if (d->d && d->d->ev_ready) cudaEventDestroy(d->d->ev_ready);
+    if (d->d && d->d->ev_consumed) cudaEventDestroy(d->d->ev_consumed);
     delete d;
 }
 

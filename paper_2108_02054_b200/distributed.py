@@ -34,6 +34,22 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class Loopback:
+    """In-process test transport (amgr_dist_loopback_create): all ranks of the
+    job live in one process, one host thread and one Context each, on the
+    same GPU; exchanges are stream-ordered device copies + host barriers."""
+
+    def __init__(self, world: int):
+        self._p = C.c_void_p()
+        _check(lib().amgr_dist_loopback_create(world, C.byref(self._p)), None)
+        self.world = world
+
+    def close(self):
+        if self._p:
+            lib().amgr_dist_loopback_destroy(self._p)
+            self._p = None
+
+
 def hierarchy_structure(h: Hierarchy):
     """Download the structure build_plan needs (patterns and aggregates)."""
     out = []
@@ -45,8 +61,8 @@ def hierarchy_structure(h: Hierarchy):
 
 
 class DistSolver:
-    def __init__(self, h: Hierarchy, rank: int, world: int, nccl_id: bytes, replicate_below: int = 20000,
-                 plan: PT.Plan | None = None):
+    def __init__(self, h: Hierarchy, rank: int, world: int, nccl_id: bytes | None = None,
+                 replicate_below: int = 20000, plan: PT.Plan | None = None, loopback: Loopback | None = None):
         self.h, self.rank, self.world = h, rank, world
         struct = hierarchy_structure(h)
         self.plan = plan or PT.build_plan(struct, rank, world, replicate_below)
@@ -74,9 +90,13 @@ class DistSolver:
         t_counts = np.bincount(own_t, minlength=world).astype(np.int64)
         self._keep.append(t_counts)
         self._p = C.c_void_p()
-        idb = C.create_string_buffer(nccl_id, 128)
-        _check(lib().amgr_dist_create(h._p, idb, rank, world, T, levels, int(t_counts.sum()), t_counts.ctypes.data,
-                                      C.byref(self._p)), h.ctx.ptr)
+        if loopback is not None:
+            _check(lib().amgr_dist_create_loopback(h._p, loopback._p, rank, world, T, levels, int(t_counts.sum()),
+                                                   t_counts.ctypes.data, C.byref(self._p)), h.ctx.ptr)
+        else:
+            idb = C.create_string_buffer(nccl_id, 128)
+            _check(lib().amgr_dist_create(h._p, idb, rank, world, T, levels, int(t_counts.sum()),
+                                          t_counts.ctypes.data, C.byref(self._p)), h.ctx.ptr)
         self.owned0 = self.plan.levels[0].owned
 
     @property
