@@ -26,10 +26,12 @@ cpu_baseline = the unmodified reference (oracle/_ref, single-threaded as
 strategies   = none / full / partial reuse through the library's run_sequence
                (rebuild, solve and total ms per step; not part of `value`)
 
-Multi-GPU (torchrun, N>1): each rank runs an independent 256^3 system
-(replicas).  The row-partitioned NCCL solve (amgr_dist_*) exists and is
-tested at world size 1 on the device and world size 2 on CPU, but is not
-driven from here until it has run on more than one GPU — see DESIGN.md §5.
+Multi-GPU (torchrun, N>1): ONE global 256^3 system row-partitioned over
+the ranks (amgr_dist_*: NCCL halo send/recv, transition allgather,
+rank-ordered dots; levels below --replicate-below rows replicated), strong
+scaling.  `--replicas` runs N independent systems instead.  The multi-rank
+device path is verified on one GPU through the loopback transport
+(tests/test_gpu_dist.py) — see DESIGN.md §5.
 """
 from __future__ import annotations
 
@@ -66,8 +68,12 @@ def args_parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--partitioned", action="store_true",
-                   help="row-partitioned NCCL solve of ONE global system over all ranks (strong scaling; "
-                        "opt-in until it has run on more than one GPU, see DESIGN.md 5)")
+                   help="row-partitioned NCCL solve of ONE global system over all ranks (strong scaling); the "
+                        "default when launched with more than one rank")
+    p.add_argument("--replicas", action="store_true",
+                   help="with N ranks, run N independent systems instead of partitioning one")
+    p.add_argument("--replicate-below", type=int, default=1000000,
+                   help="partitioned mode: levels with fewer rows are replicated on every rank")
     p.add_argument("--no-strategies", action="store_true",
                    help="skip the none/full/partial reuse comparison (run_sequence over 4 steps each)")
     return p.parse_args()
@@ -248,7 +254,7 @@ def run_partitioned(a, rank, world, local):
 
         dist.broadcast_object_list(ids, src=0)
     t0 = time.perf_counter()
-    ds = D.DistSolver(h, rank, world, ids[0], replicate_below=20000)
+    ds = D.DistSolver(h, rank, world, ids[0], replicate_below=a.replicate_below)
     plan_s = time.perf_counter() - t0
     own = torch.from_numpy(ds.owned0).cuda()
     fl = f[own].contiguous()
@@ -294,6 +300,52 @@ def run_partitioned(a, rank, world, local):
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    # roofline probe (every rank runs the probed solve; rank 0 reports its
+    # local level-0 post-smoothing sweep)
+    peak, peak_kind = hbm_peak()
+    ctx.probe("vcycle_smooth@0")
+    ul.zero_()
+    torch.cuda.synchronize()
+    ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
+    cnt, pms, pbytes = ctx.probe_read()
+    ctx.probe(None)
+    achieved = (pbytes / cnt) / (pms / cnt) / 1e6 if cnt else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "kernel": "k_rowpass<OpSmooth> level 0, rank-local rows", "peak_source": peak_kind}
+    # e2e: per step the global A_k values and the local f go host -> device,
+    # the local solution comes back
+    e2e = None
+    if not a.no_e2e:
+        hv = []
+        for k in range(1 + W, 1 + W + K):
+            tt = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
+            tt.copy_(vals[k][:nnz])
+            hv.append(tt)
+        dv = torch.empty(nnz + 8, dtype=torch.float64, device="cuda")
+        fh = torch.empty(ds.n_local, dtype=torch.float64, pin_memory=True)
+        fh.copy_(fl)
+        uh = torch.empty(ds.n_local, dtype=torch.float64, pin_memory=True)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = time.perf_counter()
+        for tt in hv:
+            dv[:nnz].copy_(tt, non_blocking=True)
+            fl.copy_(fh, non_blocking=True)
+            torch.cuda.synchronize()
+            ds.rebuild_values(dv.data_ptr())
+            ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
+            uh.copy_(ul)
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - e0) * 1e3 / K
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": 8 * nnz + 8 * ds.n_local,
+               "d2h_bytes_per_step": 8 * ds.n_local, "timer": "host wall clock, max over ranks"}
     if rank == 0:
         out = {"metric": METRIC, "value": total_ms / K, "unit": "ms/step", "n_gpus": world, "steps": K, "warmup": W,
                "ms_per_step": total_ms / K, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
@@ -304,7 +356,10 @@ def run_partitioned(a, rank, world, local):
                           "local_rows_rank0": ds.n_local},
                "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
                "setup_s": setup_s, "plan_s": plan_s, "clocks": clk.summary(), "gpu_launches": launches,
-               "e2e": None, "roofline": None, "cpu_baseline": None}
+               "e2e": e2e, "roofline": roofline, "cpu_baseline": None,
+               "note": ("one global system row-partitioned over the ranks (amgr_dist_*: NCCL halo send/recv, "
+                        "transition allgather, rank-ordered dots); levels below replicate_below rows replicated; "
+                        f"replicate_below={a.replicate_below}")}
         print(json.dumps(out), flush=True)
     ds.close()
 
@@ -315,7 +370,7 @@ def main():
         run_reference_arm(a)
         return
     rank, world, local = dist_env()
-    if a.partitioned:
+    if a.partitioned or (world > 1 and not a.replicas):
         import torch
 
         torch.cuda.set_device(local)
