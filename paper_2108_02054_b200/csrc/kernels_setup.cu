@@ -138,10 +138,15 @@ __device__ __forceinline__ int ld_state(const int* s, int i) {
     return *reinterpret_cast<const volatile int*>(s + i);
 }
 
-__global__ void __launch_bounds__(SB) k_agg_round(int n, const int* __restrict__ ptr, const int* __restrict__ adj,
+// One round over the current list of undecided nodes (compacted between
+// batches of rounds, so late rounds touch only the few nodes still open).
+__global__ void __launch_bounds__(SB) k_agg_round(const int* __restrict__ nact, const int* __restrict__ act,
+                                                  const int* __restrict__ ptr, const int* __restrict__ adj,
                                                   int* state, int* undecided) {
     int local = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int na = *nact;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < na; t += gridDim.x * blockDim.x) {
+        const int i = act[t];
         if (ld_state(state, i) != 0) continue;
         const int p0 = ptr[i], p1 = ptr[i + 1];
         if (p0 == p1) {  // isolated: never a pass-1 root
@@ -192,6 +197,22 @@ __global__ void __launch_bounds__(SB) k_agg_round(int n, const int* __restrict__
     if (local) atomicAdd(&s_cnt, local);
     __syncthreads();
     if (threadIdx.x == 0 && s_cnt) atomicAdd(undecided, s_cnt);
+}
+
+__global__ void k_iota_list(int n, int* act, int* nact) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) act[i] = i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nact = n;
+}
+
+// keep the still-undecided nodes (order irrelevant: decisions are final and
+// depend only on neighbour states)
+__global__ void k_compact_list(const int* __restrict__ nact, const int* __restrict__ act, const int* state,
+                               int* nact2, int* act2) {
+    const int na = *nact;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < na; t += gridDim.x * blockDim.x) {
+        const int i = act[t];
+        if (ld_state(state, i) == 0) act2[atomicAdd(nact2, 1)] = i;
+    }
 }
 
 __global__ void k_root_flags(const int* state, int64_t n, int64_t* rf) {
@@ -336,13 +357,16 @@ int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds
     CK(cudaMemsetAsync(state.get(), 0, sizeof(int) * n, c.stream));
     constexpr int BATCH = 16;
     DevArray<int> cnt(BATCH, c.stream);
+    DevArray<int> list0(n, c.stream), list1(n, c.stream), nl(2, c.stream);
+    int *act = list0.get(), *act2 = list1.get(), *nact = nl.get(), *nact2 = nl.get() + 1;
     int64_t r = 0;
     const unsigned grid = grid_for(n, SB, c.num_sms * 8);
+    LAUNCH(c, "setup", 0.0, k_iota_list, grid, SB, 0, static_cast<int>(n), act, nact);
     for (;;) {
         CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int) * BATCH, c.stream));
         for (int k = 0; k < BATCH; ++k)
-            LAUNCH(c, "setup", 0.0, k_agg_round, grid, SB, 0, static_cast<int>(n), g.ptr.get(), g.adj.get(),
-                   state.get(), cnt.get() + k);
+            LAUNCH(c, "setup", 0.0, k_agg_round, grid, SB, 0, nact, act, g.ptr.get(), g.adj.get(), state.get(),
+                   cnt.get() + k);
         r += BATCH;
         int h[BATCH];
         d2h(h, cnt.get(), BATCH, c.stream);
@@ -357,6 +381,10 @@ int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds
             r = r - BATCH + done_at + 1;
             break;
         }
+        CK(cudaMemsetAsync(nact2, 0, sizeof(int), c.stream));
+        LAUNCH(c, "setup", 0.0, k_compact_list, grid, SB, 0, nact, act, state.get(), nact2, act2);
+        std::swap(act, act2);
+        std::swap(nact, nact2);
     }
     if (rounds) *rounds = r;
 
