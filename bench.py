@@ -28,7 +28,7 @@ strategies   = none / full / partial reuse through the library's run_sequence
 
 Multi-GPU (torchrun, N>1): ONE global 256^3 system row-partitioned over
 the ranks (amgr_dist_*: NCCL halo send/recv, transition allgather,
-rank-ordered dots; levels below --replicate-below rows replicated), strong
+rank-ordered dots; levels below --replicate-below (150K) rows replicated), strong
 scaling.  `--replicas` runs N independent systems instead.  The multi-rank
 device path is verified on one GPU through the loopback transport
 (tests/test_gpu_dist.py) — see DESIGN.md §5.
@@ -72,7 +72,7 @@ def args_parse():
                         "default when launched with more than one rank")
     p.add_argument("--replicas", action="store_true",
                    help="with N ranks, run N independent systems instead of partitioning one")
-    p.add_argument("--replicate-below", type=int, default=1000000,
+    p.add_argument("--replicate-below", type=int, default=150000,
                    help="partitioned mode: levels with fewer rows are replicated on every rank")
     p.add_argument("--no-strategies", action="store_true",
                    help="skip the none/full/partial reuse comparison (run_sequence over 4 steps each)")
