@@ -289,6 +289,21 @@ amgr_status amgr_dist_bicgstab(amgr_dist* d, const double* f_local, double* u_lo
                                const amgr_solve_params* prm, amgr_solve_stats* stats);
 void amgr_dist_destroy(amgr_dist* d);
 
+/* ---- Matrix Market ingestion (matrix_market.hpp:12-27) -------------------- */
+/* A device CSR owned by the library (int32 indices, fp64 values). */
+typedef struct amgr_matrix amgr_matrix;
+/* mm_read (matrix_market.cpp:104-140): coordinate real/integer, general or
+ * symmetric (expanded); parsed on the host (multi-threaded), assembled on the
+ * device exactly as csr_from_triplets (csr.cpp:24-75).  Errors: AMGR_E_RUNTIME
+ * with the reference's "path:line: message" text. */
+amgr_status amgr_mm_read(amgr_ctx* ctx, const char* path, amgr_matrix** out);
+/* Device view for amgr_setup / amgr_rebuild (location AMGR_DEVICE). */
+amgr_status amgr_matrix_csr(const amgr_matrix* m, amgr_csr* view);
+void amgr_matrix_free(amgr_matrix* m);
+/* mm_read_vector (matrix_market.cpp:176-203) into a host buffer: *n in =
+ * capacity (values may be NULL to query), out = length. */
+amgr_status amgr_mm_read_vector(amgr_ctx* ctx, const char* path, int64_t* n, double* values);
+
 /* ---- introspection / download (parity dumps) ----------------------------- */
 /* Number of levels, finest first (Hierarchy::num_levels, hierarchy.hpp:54). */
 int amgr_hier_num_levels(const amgr_hier* h);

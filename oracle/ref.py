@@ -59,6 +59,10 @@ def lib():
         L.ref_partial_update.argtypes = [vp, i64, i64, _i64p, _i64p, _f64p,
                                          C.POINTER(RefParams), C.POINTER(vp), C.POINTER(f64),
                                          cp, C.c_int]
+        L.ref_mm_read.argtypes = [cp, _i64p, vp, vp, vp, cp, C.c_int]
+        L.ref_mm_read.restype = C.c_int
+        L.ref_mm_read_vector.argtypes = [cp, C.POINTER(i64), vp, cp, C.c_int]
+        L.ref_mm_read_vector.restype = C.c_int
         L.ref_free.argtypes = [vp]
         L.ref_num_levels.argtypes = [vp]
         L.ref_num_levels.restype = i64
@@ -276,3 +280,32 @@ def galerkin(A, agg, nc):
     crp, cci, cv = np.zeros(nc + 1, np.int64), np.zeros(nnz, np.int64), np.zeros(nnz)
     lib().ref_galerkin(n, nc, rp, ci, v, agg, crp.ctypes.data, cci.ctypes.data, cv.ctypes.data)
     return crp, cci, cv
+
+
+def mm_read(path):
+    """amgreuse::mm_read through the unmodified reference -> (rp, ci, v, ncols)."""
+    dims = np.zeros(3, np.int64)
+    err = C.create_string_buffer(1024)
+    rc = lib().ref_mm_read(str(path).encode(), dims, None, None, None, err, 1024)
+    if rc:
+        raise RefError(rc, err.value.decode())
+    rp = np.zeros(dims[0] + 1, np.int64)
+    ci = np.zeros(max(dims[2], 1), np.int64)
+    v = np.zeros(max(dims[2], 1))
+    rc = lib().ref_mm_read(str(path).encode(), dims, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, err, 1024)
+    if rc:
+        raise RefError(rc, err.value.decode())
+    return rp, ci[:dims[2]], v[:dims[2]], int(dims[1])
+
+
+def mm_read_vector(path):
+    n = C.c_int64()
+    err = C.create_string_buffer(1024)
+    rc = lib().ref_mm_read_vector(str(path).encode(), C.byref(n), None, err, 1024)
+    if rc:
+        raise RefError(rc, err.value.decode())
+    v = np.zeros(max(n.value, 1))
+    rc = lib().ref_mm_read_vector(str(path).encode(), C.byref(n), v.ctypes.data, err, 1024)
+    if rc:
+        raise RefError(rc, err.value.decode())
+    return v[:n.value]

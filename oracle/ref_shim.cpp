@@ -29,6 +29,7 @@
 #include "amgreuse/csr.hpp"
 #include "amgreuse/dense_lu.hpp"
 #include "amgreuse/hierarchy.hpp"
+#include "amgreuse/matrix_market.hpp"
 #include "amgreuse/smoother.hpp"
 
 using namespace amgreuse;
@@ -359,6 +360,41 @@ int ref_coarse_factorize(int64_t n, const int64_t* rp, const int64_t* ci, const 
         DenseFactorization f = coarse_factorize(A);
         std::memcpy(lu, f.lu.data(), sizeof(double) * f.lu.size());
         std::memcpy(piv, f.piv.data(), sizeof(int64_t) * f.piv.size());
+        return 0;
+    } catch (const std::runtime_error& e) {
+        return report(e, 2, err, errlen);
+    } catch (const std::exception& e) {
+        return report(e, 1, err, errlen);
+    }
+}
+
+// mm_read (matrix_market.cpp:104-140): first call with rp == nullptr returns
+// the dimensions; the second fills the CSR.  Re-reads the file each call.
+int ref_mm_read(const char* path, int64_t* dims, int64_t* rp, int64_t* ci, double* v, char* err, int errlen) {
+    try {
+        CsrMatrix A = mm_read(path);
+        dims[0] = A.nrows;
+        dims[1] = A.ncols;
+        dims[2] = A.nnz();
+        if (rp) {
+            std::memcpy(rp, A.row_ptr.data(), sizeof(int64_t) * A.row_ptr.size());
+            std::memcpy(ci, A.col_idx.data(), sizeof(int64_t) * A.col_idx.size());
+            std::memcpy(v, A.values.data(), sizeof(double) * A.values.size());
+        }
+        return 0;
+    } catch (const std::runtime_error& e) {
+        return report(e, 2, err, errlen);
+    } catch (const std::exception& e) {
+        return report(e, 1, err, errlen);
+    }
+}
+
+// mm_read_vector (matrix_market.cpp:176-203)
+int ref_mm_read_vector(const char* path, int64_t* n, double* v, char* err, int errlen) {
+    try {
+        std::vector<double> x = mm_read_vector(path);
+        *n = static_cast<int64_t>(x.size());
+        if (v) std::memcpy(v, x.data(), sizeof(double) * x.size());
         return 0;
     } catch (const std::runtime_error& e) {
         return report(e, 2, err, errlen);

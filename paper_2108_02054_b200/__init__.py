@@ -133,6 +133,10 @@ PROTOTYPES = {
     "amgr_run_sequence": (_I, [_V, _L, _V, _V, _V, _V, _V, _V, _V, _V]),
     "amgr_speedup_percent": (_D, [_D, _D]),
     "amgr_hier_level_transfer": (_I, [_V, _I, _I, _P(_L), _V, _V, _V]),
+    "amgr_mm_read": (_I, [_V, C.c_char_p, _P(_V)]),
+    "amgr_matrix_csr": (_I, [_V, _P(_Csr)]),
+    "amgr_matrix_free": (None, [_V]),
+    "amgr_mm_read_vector": (_I, [_V, C.c_char_p, _P(_L), _V]),
     "amgr_nccl_unique_id": (_I, [_V]),
     "amgr_dist_create": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
     "amgr_dist_loopback_create": (_I, [_I, _P(_V)]),
@@ -529,3 +533,64 @@ def run_sequence(*args, **kwargs):
     """RunResult run_sequence(systems, StrategyConfig, AmgParams, SolveParams) — reuse.hpp:70-71."""
     from .reuse import run_sequence as _rs
     return _rs(*args, **kwargs)
+
+
+# ---- Matrix Market ingestion (matrix_market.hpp) -------------------------------------
+class Matrix:
+    """A device CSR owned by the library (amgr_matrix), e.g. from mm_read."""
+
+    def __init__(self, ptr, ctx: Context):
+        self._p = ptr
+        self.ctx = ctx
+        c = _Csr()
+        _check(lib().amgr_matrix_csr(self._p, C.byref(c)), ctx.ptr)
+        self.nrows, self.ncols, self.nnz = int(c.nrows), int(c.ncols), int(c.nnz)
+        self._view = DeviceCsr(self.nrows, self.ncols, self.nnz, c.row_ptr, c.col_idx, c.values, 32)
+
+    def device_csr(self) -> DeviceCsr:
+        """Device view (setup / partial_update / rebuild accept it directly)."""
+        return self._view
+
+    def to_host(self):
+        """(row_ptr int64, col int64, values) host copies."""
+        v = self._view
+        rp = np.zeros(self.nrows + 1, np.int32)
+        ci = np.zeros(max(self.nnz, 1), np.int32)
+        val = np.zeros(max(self.nnz, 1))
+        L = lib()
+        _check(L.amgr_copy_to_host(self.ctx.ptr, rp.ctypes.data, v.row_ptr, 4 * (self.nrows + 1)), self.ctx.ptr)
+        if self.nnz:
+            _check(L.amgr_copy_to_host(self.ctx.ptr, ci.ctypes.data, v.col_idx, 4 * self.nnz), self.ctx.ptr)
+            _check(L.amgr_copy_to_host(self.ctx.ptr, val.ctypes.data, v.values, 8 * self.nnz), self.ctx.ptr)
+        return rp.astype(np.int64), ci[:self.nnz].astype(np.int64), val[:self.nnz]
+
+    def close(self):
+        if self._p:
+            lib().amgr_matrix_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mm_read(path, ctx: Context | None = None) -> Matrix:
+    """CsrMatrix mm_read(path) (matrix_market.hpp:17): parsed on the host,
+    assembled on the device; raises RuntimeFailure with the reference's text."""
+    ctx = ctx or default_context()
+    p = C.c_void_p()
+    _check(lib().amgr_mm_read(ctx.ptr, os.fspath(path).encode(), C.byref(p)), ctx.ptr)
+    return Matrix(p, ctx)
+
+
+def mm_read_vector(path, ctx: Context | None = None) -> np.ndarray:
+    """std::vector<double> mm_read_vector(path) (matrix_market.hpp:25)."""
+    ctx = ctx or default_context()
+    n = C.c_int64(0)
+    _check(lib().amgr_mm_read_vector(ctx.ptr, os.fspath(path).encode(), C.byref(n), None), ctx.ptr)
+    v = np.zeros(max(n.value, 1))
+    n2 = C.c_int64(n.value)
+    _check(lib().amgr_mm_read_vector(ctx.ptr, os.fspath(path).encode(), C.byref(n2), v.ctypes.data), ctx.ptr)
+    return v[:n.value]

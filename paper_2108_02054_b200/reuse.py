@@ -223,3 +223,66 @@ class DeviceGridSequence:
         self.ctx.synchronize()
         return DeviceCsr(self.n, self.n, self.nnz, self.rp.data_ptr(), self.ci.data_ptr(), self.v.data_ptr()), \
             self.f.data_ptr()
+
+
+class FileSequence:
+    """FileSequence / read_sequence (matrix_market.hpp:29-47,
+    matrix_market.cpp:205-256): `step_NNNN.mtx` (+ optional `step_NNNN.rhs.mtx`,
+    else an RHS of ones) in one directory, read lazily in index order; the
+    matrices are assembled on the device (mm_read)."""
+
+    def __init__(self, directory, ctx: Context | None = None):
+        import os
+        import re
+
+        from . import RuntimeFailure
+
+        self.ctx = ctx  # resolved lazily: the directory scan needs no device
+        d = os.fspath(directory)
+        if not os.path.isdir(d):
+            raise RuntimeFailure("read_sequence: not a directory: " + d)
+        mats, rhs = {}, {}
+        for name in os.listdir(d):
+            path = os.path.join(d, name)
+            if not os.path.isfile(path):
+                continue
+            m = re.match(r"^step_(\d{1,4})(.{1,15})$", name)  # sscanf("step_%4ld%15s")
+            if not m:
+                continue
+            idx, tail = int(m.group(1)), m.group(2)
+            if tail == ".mtx":
+                mats[idx] = path
+            elif tail == ".rhs.mtx":
+                rhs[idx] = path
+        if not mats:
+            raise RuntimeFailure("read_sequence: no step_NNNN.mtx files in " + d)
+        self.mats, self.rhs = [], []
+        expected = min(mats)
+        for idx in sorted(mats):
+            if idx != expected:
+                raise RuntimeFailure(f"read_sequence: gap in step numbering, expected step {expected} but found "
+                                     f"step {idx}")
+            expected += 1
+            self.mats.append(mats[idx])
+            self.rhs.append(rhs.get(idx))
+        self._keep = None
+
+    def size(self) -> int:
+        return len(self.mats)
+
+    def step(self, k: int):
+        from . import RuntimeFailure, mm_read, mm_read_vector
+
+        if k >= self.size():
+            raise IndexError("FileSequence::step: index out of range")
+        ctx = self.ctx or default_context()
+        M = mm_read(self.mats[k], ctx)
+        if self.rhs[k] is None:
+            f = np.ones(M.nrows)
+        else:
+            f = mm_read_vector(self.rhs[k], ctx)
+            if len(f) != M.nrows:
+                raise RuntimeFailure(f"step {k}: RHS length {len(f)} does not match matrix size {M.nrows} "
+                                     f"({self.rhs[k]})")
+        self._keep = M  # the device CSR must outlive the driver's use of this step
+        return M.device_csr(), f

@@ -117,3 +117,24 @@ def test_device_generated_sequence(ctx):
     base = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.none), ctx=ctx, keep_solutions=False)
     assert base.report.full_rebuilds == 4
     assert R.speedup_percent(base.report, res.report, R.SpeedupBasis.setup) > 0.0
+
+
+def test_file_sequence_directory_rules(tmp_path):
+    """read_sequence (matrix_market.cpp:225-256): directory scan, gaps, missing
+    files — host logic, no device needed."""
+    from paper_2108_02054_b200 import RuntimeFailure
+    from paper_2108_02054_b200 import reuse as R
+
+    with pytest.raises(RuntimeFailure, match="not a directory"):
+        R.FileSequence(tmp_path / "nope")
+    with pytest.raises(RuntimeFailure, match="no step_NNNN.mtx files"):
+        R.FileSequence(tmp_path)
+    for k in (3, 4, 6):
+        (tmp_path / f"step_{k:04d}.mtx").write_text("x")
+    with pytest.raises(RuntimeFailure, match="gap in step numbering, expected step 5 but found step 6"):
+        R.FileSequence(tmp_path)
+    (tmp_path / "step_0006.mtx").unlink()
+    (tmp_path / "step_0004.rhs.mtx").write_text("x")
+    (tmp_path / "notes.txt").write_text("x")
+    s = R.FileSequence(tmp_path)
+    assert s.size() == 2 and s.rhs[0] is None and s.rhs[1].endswith("step_0004.rhs.mtx")
