@@ -63,6 +63,7 @@ def lib():
         L.ref_mm_read.restype = C.c_int
         L.ref_mm_read_vector.argtypes = [cp, C.POINTER(i64), vp, cp, C.c_int]
         L.ref_mm_read_vector.restype = C.c_int
+        L.ref_render.restype = C.c_int
         L.ref_free.argtypes = [vp]
         L.ref_num_levels.argtypes = [vp]
         L.ref_num_levels.restype = i64
@@ -309,3 +310,29 @@ def mm_read_vector(path):
     if rc:
         raise RefError(rc, err.value.decode())
     return v[:n.value]
+
+
+def render(which, fmt, seqdir, amg, solve, reuse_iter_limit, rebuild_every, kinds, steps):
+    """tools/bench_app.cpp render_report (which 0) / write_per_step_csv (which 1)
+    of the unmodified reference over given run data.  steps[s][k] =
+    (action, setup, solve, iterations, converged, (4 phase times))."""
+    ns = len(steps[0])
+    act = np.array([[x[0] for x in row] for row in steps], np.int32).ravel()
+    se = np.array([[x[1] for x in row] for row in steps], np.float64).ravel()
+    so = np.array([[x[2] for x in row] for row in steps], np.float64).ravel()
+    it = np.array([[x[3] for x in row] for row in steps], np.int64).ravel()
+    cv = np.array([[x[4] for x in row] for row in steps], np.int32).ravel()
+    ph = np.array([[x[5] for x in row] for row in steps], np.float64).ravel()
+    kk = np.array(kinds, np.int32)
+    buf = C.create_string_buffer(1 << 20)
+    f64, i64 = C.c_double, C.c_int64
+    rc = lib().ref_render(C.c_int(which), C.c_int(fmt), str(seqdir).encode(), f64(amg[0]), f64(amg[1]),
+                          C.c_int(amg[2]), C.c_int(amg[3]), i64(amg[4]), f64(solve[0]), i64(solve[1]),
+                          i64(reuse_iter_limit), i64(rebuild_every or 0), C.c_int(len(kinds)),
+                          kk.ctypes.data_as(C.c_void_p), i64(ns), act.ctypes.data_as(C.c_void_p),
+                          se.ctypes.data_as(C.c_void_p), so.ctypes.data_as(C.c_void_p),
+                          it.ctypes.data_as(C.c_void_p), cv.ctypes.data_as(C.c_void_p),
+                          ph.ctypes.data_as(C.c_void_p), buf, C.c_int(1 << 20))
+    if rc:
+        raise RefError(1, buf.value.decode())
+    return buf.value.decode()

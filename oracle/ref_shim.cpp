@@ -31,6 +31,9 @@
 #include "amgreuse/hierarchy.hpp"
 #include "amgreuse/matrix_market.hpp"
 #include "amgreuse/smoother.hpp"
+#include "bench_app.hpp"
+
+#include <sstream>
 
 using namespace amgreuse;
 
@@ -400,6 +403,75 @@ int ref_mm_read_vector(const char* path, int64_t* n, double* v, char* err, int e
         return report(e, 2, err, errlen);
     } catch (const std::exception& e) {
         return report(e, 1, err, errlen);
+    }
+}
+
+// Report renderers of the reference's bench tool (tools/bench_app.cpp:129-266)
+// over caller-supplied run data: one run per strategy (repeat = 1), steps
+// given as flat arrays.  which: 0 = render_report, 1 = write_per_step_csv.
+int ref_render(int which, int format, const char* seqdir, double eps, double omega, int pre, int post,
+               int64_t coarse_enough, double tol, int64_t max_iter, int64_t reuse_iter_limit, int64_t rebuild_every,
+               int nstrat, const int* kinds, int64_t nsteps, const int* actions, const double* setup,
+               const double* solve, const int64_t* iters, const int* conv, const double* phases, char* out,
+               int outlen) {
+    try {
+        bench::BenchConfig cfg;
+        cfg.sequence_dir = seqdir;
+        cfg.amg.eps = eps;
+        cfg.amg.omega = omega;
+        cfg.amg.pre_sweeps = pre;
+        cfg.amg.post_sweeps = post;
+        cfg.amg.coarse_enough = coarse_enough;
+        cfg.solve.tol = tol;
+        cfg.solve.max_iter = max_iter;
+        cfg.reuse_iter_limit = reuse_iter_limit;
+        if (rebuild_every > 0) cfg.rebuild_every = rebuild_every;
+        cfg.format = format == 0 ? bench::OutputFormat::markdown : bench::OutputFormat::csv;
+        std::vector<bench::StrategyOutcome> outcomes;
+        for (int s = 0; s < nstrat; ++s) {
+            RunReport r;
+            r.strategy.kind = static_cast<StrategyKind>(kinds[s]);
+            double ts = 0.0, tv = 0.0, it = 0.0;
+            for (int64_t k = 0; k < nsteps; ++k) {
+                const int64_t x = s * nsteps + k;
+                StepMetrics m;
+                m.step = k;
+                m.setup_time = setup[x];
+                m.solve_time = solve[x];
+                m.iterations = iters[x];
+                m.converged = conv[x] != 0;
+                m.action = static_cast<StepAction>(actions[x]);
+                m.phase_timings.transfer_ops = phases[4 * x + 0];
+                m.phase_timings.galerkin = phases[4 * x + 1];
+                m.phase_timings.smoother = phases[4 * x + 2];
+                m.phase_timings.coarse_solver = phases[4 * x + 3];
+                if (m.action == StepAction::full_build) ++r.full_rebuilds;
+                ts += m.setup_time;
+                tv += m.solve_time;
+                it += static_cast<double>(m.iterations);
+                r.steps.push_back(m);
+            }
+            r.total_setup = ts;
+            r.total_solve = tv;
+            r.avg_iterations = it / static_cast<double>(nsteps);
+            bench::StrategyOutcome o;
+            o.kind = r.strategy.kind;
+            o.runs.push_back(r);
+            o.median = r;
+            outcomes.push_back(o);
+        }
+        std::ostringstream os;
+        if (which == 0)
+            bench::render_report(os, cfg, outcomes);
+        else
+            bench::write_per_step_csv(os, outcomes);
+        const std::string t = os.str();
+        if (static_cast<int>(t.size()) >= outlen) return -static_cast<int>(t.size()) - 1;
+        std::memcpy(out, t.data(), t.size());
+        out[t.size()] = '\0';
+        return 0;
+    } catch (const std::exception& e) {
+        return report(e, 1, out, outlen);
     }
 }
 

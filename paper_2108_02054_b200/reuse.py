@@ -286,3 +286,170 @@ class FileSequence:
                                      f"({self.rhs[k]})")
         self._keep = M  # the device CSR must outlive the driver's use of this step
         return M.device_csr(), f
+
+
+# ---- benchmark driver and report (tools/bench_app.cpp) -----------------------------
+@dataclass
+class StrategyOutcome:
+    """bench_app.hpp:36-41: all runs of one strategy and the per-cell median."""
+    kind: StrategyKind
+    runs: list
+    median: RunReport
+
+
+def _median(v):
+    v = sorted(v)
+    n = len(v)
+    return v[n // 2] if n % 2 == 1 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+
+
+def median_report(runs) -> RunReport:
+    """bench_app.cpp:24-40"""
+    import copy
+
+    out = copy.deepcopy(runs[0])
+    if len(runs) == 1:
+        return out
+    for s in range(len(out.steps)):
+        out.steps[s].setup_time = _median([r.steps[s].setup_time for r in runs])
+        out.steps[s].solve_time = _median([r.steps[s].solve_time for r in runs])
+    out.total_setup = _median([r.total_setup for r in runs])
+    out.total_solve = _median([r.total_solve for r in runs])
+    return out
+
+
+def effective_strategies(kinds) -> list:
+    """bench_app.cpp:83-93: `none` is the implicit speedup baseline."""
+    out = []
+    if any(k != StrategyKind.none for k in kinds):
+        out.append(StrategyKind.none)
+    for k in kinds:
+        if k not in out:
+            out.append(k)
+    return out
+
+
+def run_benchmark(systems, kinds=(StrategyKind.none, StrategyKind.full, StrategyKind.partial),
+                  amg: AmgParams | None = None, solve: SolveParams | None = None, reuse_iter_limit: int = 0,
+                  rebuild_every: int | None = None, repeat: int = 1, ctx: Context | None = None) -> list:
+    """run_benchmark (bench_app.cpp:223-246): every strategy `repeat` times over
+    the same sequence on the device; rebuild_every applies to `partial`."""
+    if not kinds:
+        raise InvalidArgument("at least one strategy is required")
+    if repeat < 1:
+        raise InvalidArgument("--repeat must be >= 1")
+    outcomes = []
+    for k in effective_strategies(list(kinds)):
+        cfg = StrategyConfig(k, reuse_iter_limit, rebuild_every if k == StrategyKind.partial else None)
+        runs = [run_sequence(systems, cfg, amg, solve, ctx=ctx, keep_solutions=False).report for _ in range(repeat)]
+        outcomes.append(StrategyOutcome(k, runs, median_report(runs)))
+    return outcomes
+
+
+_DISPLAY = {StrategyKind.none: "No reuse", StrategyKind.full: "Full reuse", StrategyKind.partial: "Partial reuse"}
+_ACTION = {StepAction.full_build: "full_build", StepAction.partial_update: "partial_update",
+           StepAction.reused_unchanged: "reused_unchanged"}
+
+
+def _fmt_speedup(p: float) -> str:
+    if math.isinf(p):
+        return "inf" if p > 0 else "-inf"
+    return f"{p:.0f}"
+
+
+def _header(p: str, amg: AmgParams, solve: SolveParams, source: str, reuse_iter_limit: int,
+            rebuild_every: int | None, repeat: int, parallel: bool) -> str:
+    """render_header (bench_app.cpp:98-126)"""
+    s = f"{p}source: {source}\n"
+    s += (f"{p}amg: eps {amg.eps:g}, omega {amg.omega:g}, sweeps {amg.pre_sweeps}+{amg.post_sweeps}, "
+          f"coarse_enough {amg.coarse_enough}\n")
+    s += f"{p}solver: bicgstab, tol {solve.tol:g}, max_iter {solve.max_iter}"
+    if reuse_iter_limit > 0:
+        s += f", reuse_iter_limit {reuse_iter_limit}"
+    if rebuild_every:
+        s += f", rebuild_every {rebuild_every}"
+    s += "\n"
+    if repeat > 1:
+        s += f"{p}repeat: {repeat} (per-cell medians)\n"
+    if parallel:
+        s += f"{p}timings: contended (strategies ran in parallel)\n"
+    return s
+
+
+def render_report(outcomes, fmt: str = "markdown", source: str = "", amg: AmgParams | None = None,
+                  solve: SolveParams | None = None, reuse_iter_limit: int = 0, rebuild_every: int | None = None,
+                  repeat: int = 1, parallel: bool = False) -> str:
+    """render_report (bench_app.cpp:248-266): Table-1-style strategy comparison
+    (setup, solve, rebuilds, iterations, speedups vs `none`) and the Table-2-style
+    setup-phase breakdown of the full builds; markdown or csv.  `source` is the
+    header's source description, e.g. "sequence directory <dir>"."""
+    amg = amg or AmgParams()
+    solve = solve or SolveParams()
+    base = next((o.median for o in outcomes if o.kind == StrategyKind.none), None)
+    speedups = base is not None and len(outcomes) > 1
+    # breakdown (bench_app.cpp:176-206): the last `none` outcome, else the first
+    pick = outcomes[0]
+    for o in outcomes:
+        if o.kind == StrategyKind.none:
+            pick = o
+    t = full_build_phase_totals(pick.median)
+    rows = [("Transfer operators", t.transfer_ops), ("Galerkin operator", t.galerkin), ("Smoother", t.smoother),
+            ("Direct solver for the coarsest system", t.coarse_solver)]
+    total = sum(x for _, x in rows) or 1.0
+    s = ""
+    if fmt == "markdown":
+        s += "# AMG setup reuse benchmark\n\n"
+        s += _header("- ", amg, solve, source, reuse_iter_limit, rebuild_every, repeat, parallel)
+        s += "\n## Strategy comparison\n\n"
+        s += "| Strategy | Setup (s) | Solve (s) | Rebuilds | Average iterations |"
+        if speedups:
+            s += " Total speedup (%) | Setup speedup (%) |"
+        s += "\n|---|---|---|---|---|" + ("---|---|" if speedups else "") + "\n"
+        for o in outcomes:
+            r = o.median
+            s += (f"| {_DISPLAY[o.kind]} | {r.total_setup:.3f} | {r.total_solve:.3f} | {r.full_rebuilds} | "
+                  f"{r.avg_iterations:.1f} |")
+            if speedups:
+                if o.kind == StrategyKind.none:
+                    s += "  |  |"
+                else:
+                    s += (f" {_fmt_speedup(speedup_percent(base, r, SpeedupBasis.total))} | "
+                          f"{_fmt_speedup(speedup_percent(base, r, SpeedupBasis.setup))} |")
+            s += "\n"
+        s += "\n## Setup phase breakdown (full builds)\n\n"
+        s += "| Setup phase | Share (%) |\n|---|---|\n"
+        for label, x in rows:
+            s += f"| {label} | {100.0 * x / total:.1f} |\n"
+    else:
+        s += _header("# ", amg, solve, source, reuse_iter_limit, rebuild_every, repeat, parallel)
+        s += "strategy,setup_s,solve_s,rebuilds,avg_iterations"
+        if speedups:
+            s += ",total_speedup_pct,setup_speedup_pct"
+        s += "\n"
+        for o in outcomes:
+            r = o.median
+            s += f"{o.kind.name},{r.total_setup:.3f},{r.total_solve:.3f},{r.full_rebuilds},{r.avg_iterations:.1f}"
+            if speedups:
+                if o.kind == StrategyKind.none:
+                    s += ",,"
+                else:
+                    s += (f",{_fmt_speedup(speedup_percent(base, r, SpeedupBasis.total))},"
+                          f"{_fmt_speedup(speedup_percent(base, r, SpeedupBasis.setup))}")
+            s += "\n"
+        s += "\nsetup_phase,share_pct\n"
+        for label, x in rows:
+            s += f'"{label}",{100.0 * x / total:.1f}\n'
+    return s
+
+
+def per_step_csv(outcomes) -> str:
+    """write_per_step_csv (bench_app.cpp:268-281)"""
+    s = ("strategy,step,action,setup_s,solve_s,iterations,converged,"
+         "transfer_ops_s,galerkin_s,smoother_s,coarse_solver_s\n")
+    for o in outcomes:
+        for m in o.median.steps:
+            p = m.phase_timings
+            s += (f"{o.kind.name},{m.step},{_ACTION[m.action]},{m.setup_time:.9g},{m.solve_time:.9g},"
+                  f"{m.iterations},{1 if m.converged else 0},{p.transfer_ops:.9g},{p.galerkin:.9g},"
+                  f"{p.smoother:.9g},{p.coarse_solver:.9g}\n")
+    return s

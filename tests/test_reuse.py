@@ -138,3 +138,72 @@ def test_file_sequence_directory_rules(tmp_path):
     (tmp_path / "notes.txt").write_text("x")
     s = R.FileSequence(tmp_path)
     assert s.size() == 2 and s.rhs[0] is None and s.rhs[1].endswith("step_0004.rhs.mtx")
+
+
+def _synthetic_outcomes():
+    """Three strategies x 4 steps of made-up timings (inf speedup for the
+    setup-free full reuse, sub-microsecond and large values)."""
+    from paper_2108_02054_b200 import PhaseTimings
+    from paper_2108_02054_b200 import reuse as R
+
+    rng = np.random.default_rng(5)
+    spec = {R.StrategyKind.none: [0, 0, 0, 0], R.StrategyKind.full: [0, 2, 2, 2],
+            R.StrategyKind.partial: [0, 1, 1, 0]}
+    outcomes, raw = [], []
+    for kind, acts in spec.items():
+        steps, rrow = [], []
+        for k, a in enumerate(acts):
+            setup = 0.0 if a == 2 else float(rng.uniform(1e-4, 3.0))
+            solve = float(rng.uniform(1e-7, 40.0))
+            it = int(rng.integers(1, 101))
+            conv = bool(rng.integers(0, 2))
+            ph = [float(x) for x in rng.uniform(0, 1.0, 4)] if a == 0 else [0.0, float(rng.uniform(0, 1)),
+                                                                              float(rng.uniform(0, 1)), 1e-6]
+            steps.append(R.StepMetrics(k, setup, solve, it, conv, R.StepAction(a), PhaseTimings(*ph)))
+            rrow.append((a, setup, solve, it, int(conv), ph))
+        rep = R.RunReport(strategy=R.StrategyConfig(kind), steps=steps)
+        rep.total_setup = sum(s.setup_time for s in steps)
+        rep.total_solve = sum(s.solve_time for s in steps)
+        rep.full_rebuilds = sum(1 for s in steps if s.action == R.StepAction.full_build)
+        rep.avg_iterations = sum(s.iterations for s in steps) / len(steps)
+        outcomes.append(R.StrategyOutcome(kind, [rep], rep))
+        raw.append(rrow)
+    return outcomes, raw
+
+
+@pytest.mark.parametrize("fmt", ["markdown", "csv"])
+def test_report_renderer_matches_reference_bench_app(fmt):
+    """Table-1/Table-2-style report and per-step CSV (tools/bench_app.cpp:129-281)
+    are byte-identical to the unmodified reference's renderers on the same run data."""
+    from oracle import ref
+    from paper_2108_02054_b200 import AmgParams, SolveParams
+    from paper_2108_02054_b200 import reuse as R
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    outcomes, raw = _synthetic_outcomes()
+    amg = AmgParams(eps=0.08, omega=0.72, coarse_enough=100)
+    sp = SolveParams(tol=1e-8, max_iter=100)
+    for rie, rbe in ((0, None), (25, 3)):
+        mine = R.render_report(outcomes, fmt, source="sequence directory /data/seq", amg=amg, solve=sp,
+                               reuse_iter_limit=rie, rebuild_every=rbe)
+        theirs = ref.render(0, 0 if fmt == "markdown" else 1, "/data/seq",
+                            (0.08, 0.72, 1, 1, 100), (1e-8, 100), rie, rbe, [int(o.kind) for o in outcomes], raw)
+        assert mine == theirs
+    assert R.per_step_csv(outcomes) == ref.render(1, 0, "/data/seq", (0.08, 0.72, 1, 1, 100), (1e-8, 100), 0, None,
+                                                  [int(o.kind) for o in outcomes], raw)
+    assert R.effective_strategies([R.StrategyKind.partial, R.StrategyKind.partial]) == [R.StrategyKind.none,
+                                                                                       R.StrategyKind.partial]
+
+
+@pytest.mark.gpu
+def test_bench_app_cli_on_device(tmp_path, capsys):
+    """The reuse benchmark CLI end to end on the device (3 strategies over a
+    generated sequence): report + per-step CSV with one row per step."""
+    from paper_2108_02054_b200 import bench_app
+
+    per = tmp_path / "steps.csv"
+    assert bench_app.main(["--generate", "dambreak", "--grid", "16", "--steps", "3", "--per-step", str(per)]) == 0
+    out = capsys.readouterr().out
+    assert out.startswith("# AMG setup reuse benchmark") and "| Partial reuse |" in out
+    assert len(per.read_text().strip().splitlines()) == 1 + 3 * 3
