@@ -202,10 +202,16 @@ enum { AMGR_REUSE_NONE = 0, AMGR_REUSE_FULL = 1, AMGR_REUSE_PARTIAL = 2 };
 /* StepAction (reuse.hpp:31) */
 enum { AMGR_ACTION_FULL_BUILD = 0, AMGR_ACTION_PARTIAL_UPDATE = 1, AMGR_ACTION_REUSED_UNCHANGED = 2 };
 
-/* StrategyConfig (reuse.hpp:20-28).  rebuild_every <= 0 means "absent". */
+/* StrategyConfig (reuse.hpp:20-28).  rebuild_every <= 0 means "absent".
+ * flags (extension, SPEC.md:444-447 leaves it unspecified):
+ * AMGR_STRATEGY_ESCALATE makes partial reuse convergence-triggered — after a
+ * solve that did not converge or used >= reuse_iter_limit iterations (max_iter
+ * when 0) the next step is a full build, the rule the reference applies to
+ * full reuse (reuse.cpp:116-117). */
+enum { AMGR_STRATEGY_ESCALATE = 1 };
 typedef struct amgr_strategy {
     int32_t kind;
-    int32_t pad;
+    int32_t flags;
     int64_t reuse_iter_limit;
     int64_t rebuild_every;
 } amgr_strategy;

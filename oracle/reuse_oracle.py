@@ -8,7 +8,8 @@ from oracle import oracle as O
 FULL_BUILD, PARTIAL_UPDATE, REUSED_UNCHANGED = 0, 1, 2
 
 
-def run_sequence(systems, kind, reuse_iter_limit=0, rebuild_every=None, prm=None, tol=1e-8, max_iter=100):
+def run_sequence(systems, kind, reuse_iter_limit=0, rebuild_every=None, prm=None, tol=1e-8, max_iter=100,
+                 escalate=False):
     prm = prm or O.params()
     iter_limit = reuse_iter_limit if reuse_iter_limit > 0 else max_iter
     if iter_limit > max_iter:
@@ -27,14 +28,16 @@ def run_sequence(systems, kind, reuse_iter_limit=0, rebuild_every=None, prm=None
             act = FULL_BUILD if (h is None or dims_changed or rebuild_flag) else REUSED_UNCHANGED
         else:
             periodic = rebuild_every is not None and k > 0 and k % rebuild_every == 0
-            act = FULL_BUILD if (h is None or dims_changed or periodic) else PARTIAL_UPDATE
+            # extension (AMGR_STRATEGY_ESCALATE): the full-reuse rule applied to partial reuse
+            act = FULL_BUILD if (h is None or dims_changed or periodic or (escalate and rebuild_flag)) \
+                else PARTIAL_UPDATE
         if act == FULL_BUILD:
             h = O.setup(A, prm)
         elif act == PARTIAL_UPDATE:
             h = O.partial_update(h, A, prm)
         u0 = prev if prev is not None and len(prev) == n else None
         s = O.bicgstab(h, rhs, u0, tol, max_iter)
-        if kind == "full":
+        if kind == "full" or (kind == "partial" and escalate):
             rebuild_flag = (not s.converged) or s.iterations >= iter_limit
         prev = s.u
         out.append((act, s.iterations, s.converged, s.u))

@@ -49,8 +49,9 @@ void run_sequence(Ctx& c, int64_t nsteps, amgr_step_fn step, void* user, const a
                 break;
             default: {
                 const bool periodic = st.rebuild_every > 0 && k > 0 && k % st.rebuild_every == 0;
-                m.action = (!have || dims_changed || periodic) ? AMGR_ACTION_FULL_BUILD
-                                                               : AMGR_ACTION_PARTIAL_UPDATE;
+                const bool escalate = (st.flags & AMGR_STRATEGY_ESCALATE) && rebuild_flag;
+                m.action = (!have || dims_changed || periodic || escalate) ? AMGR_ACTION_FULL_BUILD
+                                                                           : AMGR_ACTION_PARTIAL_UPDATE;
             }
         }
         CK(cudaStreamSynchronize(c.stream));
@@ -84,7 +85,8 @@ void run_sequence(Ctx& c, int64_t nsteps, amgr_step_fn step, void* user, const a
         m.solve_time = since(t1);
         m.iterations = ss.iterations;
         m.converged = ss.converged;
-        if (st.kind == AMGR_REUSE_FULL) rebuild_flag = !ss.converged || ss.iterations >= iter_limit;
+        if (st.kind == AMGR_REUSE_FULL || (st.kind == AMGR_REUSE_PARTIAL && (st.flags & AMGR_STRATEGY_ESCALATE)))
+            rebuild_flag = !ss.converged || ss.iterations >= iter_limit;
         if (prev.size() != n) prev.alloc(n, c.stream);
         copy(c, prev.get(), u.get(), n);
         if (sink) {

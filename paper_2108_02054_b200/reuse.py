@@ -41,10 +41,13 @@ class StepAction(enum.IntEnum):
 
 @dataclass
 class StrategyConfig:
-    """reuse.hpp:20-28"""
+    """reuse.hpp:20-28.  escalate (extension): partial reuse
+    falls back to a full build after a solve that did not converge or used
+    >= reuse_iter_limit iterations (the reference's full-reuse rule)."""
     kind: StrategyKind = StrategyKind.none
     reuse_iter_limit: int = 0
     rebuild_every: int | None = None
+    escalate: bool = False
 
 
 @dataclass
@@ -77,7 +80,7 @@ class RunResult:
 
 
 class _Strategy(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("reuse_iter_limit", C.c_int64),
+    _fields_ = [("kind", C.c_int32), ("flags", C.c_int32), ("reuse_iter_limit", C.c_int64),
                 ("rebuild_every", C.c_int64)]
 
 
@@ -135,7 +138,7 @@ def run_sequence(systems, strategy: StrategyConfig, amg: AmgParams | None = None
 
     step_fn = STEP_FN(step_cb)
     sink_fn = SINK_FN(sink_cb) if keep_solutions else SINK_FN()
-    st = _Strategy(int(strategy.kind), 0, strategy.reuse_iter_limit,
+    st = _Strategy(int(strategy.kind), 1 if strategy.escalate else 0, strategy.reuse_iter_limit,
                    strategy.rebuild_every if strategy.rebuild_every is not None else 0)
     metrics = (_StepMetrics * n_steps)()
     p = amg._c()

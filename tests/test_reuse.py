@@ -207,3 +207,22 @@ def test_bench_app_cli_on_device(tmp_path, capsys):
     out = capsys.readouterr().out
     assert out.startswith("# AMG setup reuse benchmark") and "| Partial reuse |" in out
     assert len(per.read_text().strip().splitlines()) == 1 + 3 * 3
+
+
+@pytest.mark.gpu
+def test_partial_reuse_escalation_matches_restated_rule(ctx):
+    """Extension: partial reuse with convergence-triggered
+    escalation — a solve that needed >= reuse_iter_limit iterations makes the
+    next step a full build (the reference's full-reuse rule, reuse.cpp:116-117,
+    applied to partial reuse); actions match the restated driver."""
+    from oracle import reuse_oracle as RO
+    from paper_2108_02054_b200 import reuse as R
+
+    seq = dambreak_seq(14, [0, 1, 49, 0, 1, 49])
+    st = R.StrategyConfig(R.StrategyKind.partial, reuse_iter_limit=1, escalate=True)
+    res = R.run_sequence(seq, st, ctx=ctx)
+    ref = RO.run_sequence(seq, "partial", 1, escalate=True)
+    assert [int(s.action) for s in res.report.steps] == [r[0] for r in ref]
+    assert 1 < res.report.full_rebuilds < len(ref)  # escalated, but not every step
+    plain = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind.partial), ctx=ctx)
+    assert plain.report.full_rebuilds == 1
