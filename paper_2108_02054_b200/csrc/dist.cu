@@ -586,7 +586,9 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
     const Gate GH = gate_of(st, KF_DONE, KF_HALF);
     const Gate GF = gate_of(st, KF_DONE | KF_HALF);
     const Gate GC = gate_of(st, KF_DONE | KF_HALF, KF_CHECK);
-    for (;;) {
+    // one iteration of look-ahead, no per-iteration host sync; no CUDA graph
+    // (the loopback test transport synchronises host threads while enqueuing)
+    auto iter = [&]() {
         bicg_begin(c, st);
         bicg_p(c, st, n, d.kr.get(), d.kp.get(), d.kv.get());
         dist_vcycle(d, d.kp.get(), d.kph.get(), G);
@@ -616,9 +618,8 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
         resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GC);
         allsum(d, 1, {&st->d_true});
         bicg_end_check(c, st);
-        s = rd();
-        if (s.flags & KF_DONE) break;
-    }
+    };
+    run_iterations(h, iter, s, false);
     out.iterations = s.it;
     if (s.flags & KF_CONVERGED) {
         out.converged = 1;

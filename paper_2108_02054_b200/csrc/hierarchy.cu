@@ -924,7 +924,7 @@ void write_state(Hier& h, const KState& s) {
 // flight ahead of the host's convergence check (flags copied to pinned memory
 // and signalled by an event).  Falls back to direct launches while a kernel
 // probe is active (probe events must bracket individual launches).
-static void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& out) {
+void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& out, bool allow_graph) {
     Ctx& c = *h.ctx;
     KState* st = work(h).st.get();
     static thread_local KState* pinned = nullptr;
@@ -934,7 +934,7 @@ static void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, K
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     cudaGraphExec_t exec = nullptr;
     int64_t per_iter = 0;
-    const bool use_graph = c.probe.family.empty() && !getenv("AMGR_NO_GRAPH");
+    const bool use_graph = allow_graph && c.probe.family.empty() && !getenv("AMGR_NO_GRAPH");
     if (use_graph) {
         cudaGraph_t graph;
         const int64_t l0 = c.launches;

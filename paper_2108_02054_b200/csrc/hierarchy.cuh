@@ -3,6 +3,7 @@
 // (proj/include/amgreuse/hierarchy.hpp, bicgstab.hpp) with device storage.
 #pragma once
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -128,6 +129,10 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
 void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
         amgr_solve_stats& st);
 Work& work(Hier& h);
+// Enqueue Krylov iterations with one iteration of look-ahead (gated kernels
+// no-op once KF_DONE is set), as one CUDA graph when allowed; returns the
+// final device state.
+void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& out, bool allow_graph = true);
 
 // device generators (kernels_gen.cu)
 int64_t problem_nnz(int64_t g);
