@@ -604,7 +604,8 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
         resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GH);
         allsum(d, 1, {&st->d_true});
         bicg_half_check(c, st);
-        bicg_half_r(c, st, n, d.kr.get(), d.ks.get());
+        bicg_half_r(c, st, n, d.kr.get(), d.ks.get(), d.krt.get(), local_sink(d, 0));
+        allsum(d, 1, {&st->d_rtr});  // stale when gated off; bicg_update rewrites d_rtr then
         dist_vcycle(d, d.ks.get(), d.ksh.get(), GF);
         halo(d, L0, d.ksh.get(), GF);
         spmv_dot2(c, A, d.ksh.get(), d.kt.get(), d.ks.get(), local_sink(d, 0), GF);

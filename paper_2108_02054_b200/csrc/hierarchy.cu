@@ -1033,7 +1033,7 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
         bicg_half_u(c, st, n, u, B.ph);
         resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GH);
         bicg_half_check(c, st);
-        bicg_half_r(c, st, n, B.r, B.s);
+        bicg_half_r(c, st, n, B.r, B.s, B.rt, sink(h, ST_FIELD(st, d_rtr)));
         vcycle(h, B.s, B.sh, GF);
         spmv_dot2(c, A, B.sh, B.t, B.s, sink(h, ST_FIELD(st, d_ts)), GF);
         bicg_omega(c, st);

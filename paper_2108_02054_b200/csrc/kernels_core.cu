@@ -339,7 +339,7 @@ struct OpSpmvDot {
     __device__ Row load(int i) const { return {__ldg(a + i)}; }
     __device__ void finish(int i, double s, const Row& q, double* d) const {
         y[i] = s;
-        d[0] = __fma_rn(q.a, s, d[0]);
+        d[0] = dadd(d[0], dmul(q.a, s));
     }
 };
 
@@ -353,8 +353,8 @@ struct OpSpmvDot2 {
     __device__ Row load(int i) const { return {__ldg(b + i)}; }
     __device__ void finish(int i, double s, const Row& q, double* d) const {
         y[i] = s;
-        d[0] = __fma_rn(s, q.a, d[0]);
-        d[1] = __fma_rn(s, s, d[1]);
+        d[0] = dadd(d[0], dmul(s, q.a));
+        d[1] = dadd(d[1], dmul(s, s));
     }
 };
 
@@ -371,7 +371,7 @@ struct OpResidNorm {
         const double t = dsub(q.a, s);
         if (r) r[i] = t;
         if (r2) r2[i] = t;
-        d[0] = __fma_rn(t, t, d[0]);
+        d[0] = dadd(d[0], dmul(t, t));
     }
 };
 
@@ -388,7 +388,7 @@ struct OpPower {
     __device__ void finish(int i, double s, const Row& q, double* d) const {
         const double t = dmul(q.a, s);
         y[i] = t;
-        d[0] = __fma_rn(t, t, d[0]);
+        d[0] = dadd(d[0], dmul(t, t));
     }
 };
 
@@ -716,8 +716,8 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
 template <int PER, int B>
 void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
                     double* ac, int cstage, size_t sm) {
-    static bool attr = false;
-    if (sm > 48 * 1024 && !attr) {
+    static bool attr = false;  // opt in once (dynamic + static may exceed 48 KB)
+    if (!attr) {
         CK(cudaFuncSetAttribute(k_rap_tma<PER, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr = true;
     }
@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(256) k_power_norm(int n, const double* __restr
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const double t = y[i] * sc;
         x[i] = t;
-        d[0] = __fma_rn(t, t, d[0]);
+        d[0] = dadd(d[0], dmul(t, t));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) st[2] = sqrt(yy) / sqrt(st[1]);
     block_dots<1>(d, ds);
@@ -1462,9 +1462,14 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
     if (n == 0) return;
     if (n <= DR_MAXN) {
         const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
-        if (sm > 48 * 1024)
+        // always opt in: dynamic + static shared memory above 48 KB needs the
+        // attribute even when the dynamic part alone is below it (n = 72..78)
+        static bool attr = false;
+        if (!attr) {
             CK(cudaFuncSetAttribute(k_dense_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sizeof(double) * DR_MAXN * DR_MAXN)));
+            attr = true;
+        }
         LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status);
         return;
     }
@@ -1481,7 +1486,11 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     const size_t full = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + 3 * n);
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
-    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    static bool attr = false;  // opt in once (dynamic + static may exceed 48 KB)
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
     LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }
 
@@ -1501,7 +1510,11 @@ void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* 
 void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g) {
     if (n == 0) return;
     const size_t sm = sizeof(double) * static_cast<size_t>(n);
-    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
     LAUNCH_PDL(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
 }
 

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(VB) k_bicg_s(const KState* s, int n, const dou
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const double t = dsub(r[i], dmul(alpha, v[i]));
         sv[i] = t;
-        d[0] = __fma_rn(t, t, d[0]);
+        d[0] = dadd(d[0], dmul(t, t));
     }
     block_dots<1>(d, ds);
 }
@@ -142,11 +142,21 @@ __global__ void k_bicg_half_u(const KState* s, int n, double* __restrict__ u, co
         u[i] = dadd(u[i], dmul(alpha, ph[i]));
 }
 
-__global__ void k_bicg_half_r(const KState* s, int n, double* __restrict__ r, const double* __restrict__ sv) {
+// half-step continue (bicgstab.cpp:98-99): r = s, and the next iteration's
+// rho = dot(rtilde, r) (bicgstab.cpp:68) from the new r
+__global__ void __launch_bounds__(VB) k_bicg_half_r(const KState* s, int n, double* __restrict__ r,
+                                                    const double* __restrict__ sv, const double* __restrict__ rt,
+                                                    DotSink ds) {
     pdl_enter();
     const int f = s->flags;
     if ((f & KF_DONE) || !(f & KF_HALF)) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) r[i] = sv[i];
+    double d[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double si = sv[i];
+        r[i] = si;
+        d[0] = dadd(d[0], dmul(rt[i], si));
+    }
+    block_dots<1>(d, ds);
 }
 
 __global__ void __launch_bounds__(VB) k_bicg_update(const KState* s, int n, double* __restrict__ u,
@@ -163,8 +173,8 @@ __global__ void __launch_bounds__(VB) k_bicg_update(const KState* s, int n, doub
         u[i] = dadd(u[i], dadd(dmul(alpha, ph[i]), dmul(om, sh[i])));
         const double ri = dsub(sv[i], dmul(om, t[i]));
         r[i] = ri;
-        d[0] = __fma_rn(ri, ri, d[0]);
-        d[1] = __fma_rn(rt[i], ri, d[1]);
+        d[0] = dadd(d[0], dmul(ri, ri));
+        d[1] = dadd(d[1], dmul(rt[i], ri));
     }
     block_dots<2>(d, ds);
 }
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(VB) k_cg_update(const KState* s, int n, double
         u[i] = dadd(u[i], dmul(a, p[i]));
         const double ri = dsub(r[i], dmul(a, q[i]));
         r[i] = ri;
-        d[0] = __fma_rn(ri, ri, d[0]);
+        d[0] = dadd(d[0], dmul(ri, ri));
     }
     block_dots<1>(d, ds);
 }
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(VB) k_dot(int n, const double* __restrict__ a,
     if (gated_off(g)) return;
     double d[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        d[0] = __fma_rn(a[i], b[i], d[0]);
+        d[0] = dadd(d[0], dmul(a[i], b[i]));
     block_dots<1>(d, ds);
 }
 
@@ -279,9 +289,8 @@ void bicg_half_u(Ctx& c, KState* st, int64_t n, double* u, const double* phat) {
     LAUNCH_PDL(c, "krylov_vec", 24.0 * n, k_bicg_half_u, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
            static_cast<int>(n), u, phat);
 }
-void bicg_half_r(Ctx& c, KState* st, int64_t n, double* r, const double* s) {
-    LAUNCH_PDL(c, "krylov_vec", 16.0 * n, k_bicg_half_r, grid_for(n, VB, c.num_sms * 8), VB, 0, st,
-           static_cast<int>(n), r, s);
+void bicg_half_r(Ctx& c, KState* st, int64_t n, double* r, const double* s, const double* rt, DotSink ds) {
+    LAUNCH_PDL(c, "krylov_vec", 24.0 * n, k_bicg_half_r, dot_grid(c), VB, 0, st, static_cast<int>(n), r, s, rt, ds);
 }
 void bicg_update(Ctx& c, KState* st, int64_t n, double* u, const double* phat, const double* shat, double* r,
                  const double* s, const double* t, const double* rt, DotSink ds) {

@@ -33,7 +33,8 @@ void bicg_s(Ctx& c, KState* st, int64_t n, const double* r, const double* v, dou
 void bicg_half_test(Ctx& c, KState* st);                               // :91
 void bicg_half_u(Ctx& c, KState* st, int64_t n, double* u, const double* phat);  // :92
 void bicg_half_check(Ctx& c, KState* st);                              // :93-100
-void bicg_half_r(Ctx& c, KState* st, int64_t n, double* r, const double* s);  // :98
+// r = s and rho_next = dot(rtilde, r) into ds (bicgstab.cpp:98, :68)
+void bicg_half_r(Ctx& c, KState* st, int64_t n, double* r, const double* s, const double* rt, DotSink ds);
 void bicg_omega(Ctx& c, KState* st);                                   // :106-111
 void bicg_update(Ctx& c, KState* st, int64_t n, double* u, const double* phat, const double* shat,
                  double* r, const double* s, const double* t, const double* rt,
