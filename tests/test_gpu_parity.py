@@ -376,3 +376,20 @@ def test_spai0_smoother_vs_oracle(ctx):
     _, st = amg.bicgstab(h, fr)
     so = O.bicgstab(o, fr)
     assert st.converged and abs(st.iterations - so.iterations) <= 1
+
+
+@pytest.mark.parametrize("n", [72, 75, 78, 150])
+def test_direct_solve_sizes_around_the_smem_opt_in(ctx, n):
+    """Stalled coarsening (no strong couplings) -> the whole matrix is the
+    coarsest system; n = 72..78 is where dynamic + static shared memory of the
+    register LU kernel first exceeds 48 KB (regression: missing opt-in)."""
+    A = P.random_csr(n, n, 0.05, 3, diag=4.0)
+    kw = dict(eps=0.99)
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    assert h.num_levels() == 1 and h.coarse_n() == n
+    lu, piv = h.coarse_lu()
+    np.testing.assert_array_equal(piv, r.piv)
+    np.testing.assert_array_equal(_bits(lu), _bits(r.lu))
+    f = np.random.default_rng(2).uniform(-1, 1, n)
+    np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r, f, fixed=True, prm=ref.params(**kw))))
