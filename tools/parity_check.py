@@ -40,6 +40,13 @@ def main():
     fr = P.rhs(n)
     _, st = amg.bicgstab(h, fr)
     rs = ref.bicgstab(r, fr, fixed=True)
+    # partial update to a later step: frozen transfers, new Galerkin values
+    A2 = P.grid3d_values(kind, g, k + 9)
+    r2 = ref.partial_update(r, A2, ref.params())
+    h2 = amg.partial_update(h, A2)
+    pok = all(np.array_equal(bits(h2.level_A(l)[2]), bits(L.A[2])) for l, L in enumerate(r2.levels))
+    pvok = np.array_equal(bits(amg.vcycle(h2, f)), bits(ref.vcycle(r2, f, fixed=True)))
+    print(f"  partial update to k={k + 9}: level values bit-exact {pok}, V-cycle bit-exact {pvok}", flush=True)
     print(f"{kind} {g}^3 k={k}: levels {h.num_levels()}, hierarchy bit-exact {ok}, V-cycle bit-exact {vok}, "
           f"BiCGStab {st.iterations} vs reference {rs.iterations} (converged {st.converged}/{rs.converged}); "
           f"reference setup {t_ref:.1f} s", flush=True)
