@@ -58,7 +58,10 @@ enum { AMGR_HOST = 0, AMGR_DEVICE = 1,
         * (zero copy) until the next rebuild; it must stay valid and
         * unmodified, be 16-byte aligned and have >= 32 bytes of slack past
         * the last value (read by 16-byte TMA bulk copies). */
-       AMGR_DEVICE_ADOPT = 2 };
+       AMGR_DEVICE_ADOPT = 2,
+       /* amgr_rebuild_values only (values = NULL): use the values staged by
+        * the last amgr_stage_values (swapped in, no copy). */
+       AMGR_STAGED = 3 };
 
 /* Smoother kinds.  JACOBI is the reference's (smoother.hpp:11-16); SPAI0 and
  * CHEBYSHEV are north-star extensions with restated oracles (parity unpinned
@@ -171,6 +174,12 @@ amgr_status amgr_rebuild(amgr_hier* h, const amgr_csr* A_new);
 /* Values-only rebuild: `values` are the new A_0 entries in the CSR order of
  * the hierarchy's finest pattern (nnz of level 0 entries).  The caller
  * asserts the pattern is unchanged. */
+/* Pipelining (extension): copy the NEXT step's A_0 values (host or device)
+ * into a per-hierarchy staging buffer on the context's copy stream, ordered
+ * after the work already queued on the context stream, so the transfer runs
+ * on the copy engines while the current step's solve computes.  Consume with
+ * amgr_rebuild_values(h, NULL, AMGR_STAGED). */
+amgr_status amgr_stage_values(amgr_hier* h, const double* values, int location);
 amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location);
 
 /* Replaces `std::vector<double> vcycle(const Hierarchy&, span f, const AmgParams&)`

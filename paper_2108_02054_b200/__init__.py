@@ -31,7 +31,7 @@ LIB_PATH = os.path.join(_HERE, "libamgr_b200.so")
 # development A/B of kernel variants: AMGR_LIB=<path to another build>
 LIB_PATH = os.environ.get("AMGR_LIB", LIB_PATH)
 
-HOST, DEVICE, DEVICE_ADOPT = 0, 1, 2
+HOST, DEVICE, DEVICE_ADOPT, STAGED = 0, 1, 2, 3
 SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}
 COARSENING = {"plain": 0, "smoothed": 1}
 COARSE_SOLVE = {"exact": 0, "inverse": 1}
@@ -133,6 +133,7 @@ PROTOTYPES = {
     "amgr_run_sequence": (_I, [_V, _L, _V, _V, _V, _V, _V, _V, _V, _V]),
     "amgr_speedup_percent": (_D, [_D, _D]),
     "amgr_hier_level_transfer": (_I, [_V, _I, _I, _P(_L), _V, _V, _V]),
+    "amgr_stage_values": (_I, [_V, _V, _I]),
     "amgr_mm_read": (_I, [_V, C.c_char_p, _P(_V)]),
     "amgr_matrix_csr": (_I, [_V, _P(_Csr)]),
     "amgr_matrix_free": (None, [_V]),
@@ -435,6 +436,22 @@ class Hierarchy:
         else:
             v = _f64(values)
             _check(lib().amgr_rebuild_values(self._p, v.ctypes.data, HOST), self.ctx.ptr)
+
+    def stage_values(self, values, host: bool | None = None):
+        """Pipelining (amgr_stage_values): copy the next step's values on the
+        context's copy stream while the current work runs.  `values` is a
+        device pointer (int; host=True for a pinned host pointer) or a numpy
+        array (kept alive until the copy completed: call rebuild_staged)."""
+        if isinstance(values, int):
+            _check(lib().amgr_stage_values(self._p, values, HOST if host else DEVICE), self.ctx.ptr)
+        else:
+            self._staged_keep = _f64(values)
+            _check(lib().amgr_stage_values(self._p, self._staged_keep.ctypes.data, HOST), self.ctx.ptr)
+
+    def rebuild_staged(self):
+        """amgr_rebuild_values(h, NULL, AMGR_STAGED): swap the staged values in."""
+        _check(lib().amgr_rebuild_values(self._p, None, STAGED), self.ctx.ptr)
+        self._staged_keep = None
 
     def spmv(self, lvl: int, x):
         d = self.level_dims(lvl)

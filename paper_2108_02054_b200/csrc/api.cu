@@ -137,6 +137,10 @@ void amgr_ctx_destroy(amgr_ctx* ctx) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    if (ctx->c.copy) {
+        cudaStreamSynchronize(ctx->c.copy);
+        cudaStreamDestroy(ctx->c.copy);
+    }
     if (ctx->c.side) {
         cudaStreamSynchronize(ctx->c.side);
         cudaStreamDestroy(ctx->c.side);
@@ -182,8 +186,13 @@ amgr_status amgr_rebuild(amgr_hier* h, const amgr_csr* A) {
     return guard_c(ctx_of(h), [&] { amgr::rebuild(*h->h, *A); });
 }
 
-amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location) {
+amgr_status amgr_stage_values(amgr_hier* h, const double* values, int location) {
     if (!h || !values) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] { amgr::stage_values(*h->h, values, location); });
+}
+
+amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location) {
+    if (!h || (!values && location != AMGR_STAGED)) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] { amgr::rebuild_values(*h->h, values, location); });
 }
 

@@ -63,6 +63,7 @@ struct Ctx {
     bool pdl = true;  // AMGR_PDL=0 disables programmatic dependent launch
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaStream_t copy = nullptr;  // staged H2D of the next step's values (lazily created)
 };
 
 // Run fn with c.stream temporarily redirected to the side stream, ordered

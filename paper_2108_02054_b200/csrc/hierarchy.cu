@@ -608,9 +608,42 @@ void rebuild(Hier& h, const amgr_csr& A) {
     rebuild_into(h, A);
 }
 
+Hier::~Hier() {
+    if (staged_ev) cudaEventDestroy(staged_ev);
+    if (main_ev) cudaEventDestroy(main_ev);
+}
+
+void stage_values(Hier& h, const double* values, int location) {
+    Ctx& c = *h.ctx;
+    if (location != AMGR_HOST && location != AMGR_DEVICE) invalid("stage_values: location must be HOST or DEVICE");
+    if (!c.copy) CK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    if (!h.staged_ev) {
+        CK(cudaEventCreateWithFlags(&h.staged_ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h.main_ev, cudaEventDisableTiming));
+    }
+    const int64_t nnz = h.lv.front().pat->nnz;
+    if (h.staged.size() != nnz) h.staged.alloc(nnz, c.stream);
+    // the staging buffer may still be read by work queued on the main stream
+    CK(cudaEventRecord(h.main_ev, c.stream));
+    CK(cudaStreamWaitEvent(c.copy, h.main_ev, 0));
+    if (nnz > 0)
+        CK(cudaMemcpyAsync(h.staged.get(), values, sizeof(double) * nnz,
+                           location == AMGR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.copy));
+    CK(cudaEventRecord(h.staged_ev, c.copy));
+    h.staged_ready = true;
+}
+
 void rebuild_values(Hier& h, const double* values, int location) {
     Ctx& c = *h.ctx;
-    if (location == AMGR_DEVICE_ADOPT) {
+    if (location == AMGR_STAGED) {
+        if (!h.staged_ready) invalid("rebuild_values: no staged values (call amgr_stage_values first)");
+        CK(cudaStreamWaitEvent(c.stream, h.staged_ev, 0));
+        Level& L0 = h.lv.front();
+        L0.ext_val = nullptr;
+        if (L0.val.size() != L0.pat->nnz) L0.val.alloc(L0.pat->nnz, c.stream);
+        L0.val.swap(h.staged);  // the previous values become the next staging buffer
+        h.staged_ready = false;
+    } else if (location == AMGR_DEVICE_ADOPT) {
         if (reinterpret_cast<uintptr_t>(values) % 16 != 0) invalid("rebuild_values: adopted buffer must be 16-byte aligned");
         h.lv.front().ext_val = values;
     } else {

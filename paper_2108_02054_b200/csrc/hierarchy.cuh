@@ -110,6 +110,10 @@ struct Hier {
     bool lu_formed = false;   // false in the inverse mode when the direct Gauss-Jordan kernel ran
     DevArray<int64_t> piv;
     DevArray<double> inv;  // AMGR_COARSE_INVERSE
+    DevArray<double> staged;  // next step's A_0 values (amgr_stage_values)
+    cudaEvent_t staged_ev = nullptr, main_ev = nullptr;
+    bool staged_ready = false;
+    ~Hier();
     int64_t nL = 0;
     amgr_phase_timings tm{};
     std::shared_ptr<Work> ws;
@@ -122,6 +126,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p);
 std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const AmgP& p);
 void rebuild(Hier& h, const amgr_csr& A);
 void rebuild_values(Hier& h, const double* values, int location);
+void stage_values(Hier& h, const double* values, int location);
 void vcycle(Hier& h, const double* f, double* u, Gate g = {});
 void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g = {});
 void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,

@@ -393,3 +393,23 @@ def test_direct_solve_sizes_around_the_smem_opt_in(ctx, n):
     np.testing.assert_array_equal(_bits(lu), _bits(r.lu))
     f = np.random.default_rng(2).uniform(-1, 1, n)
     np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r, f, fixed=True, prm=ref.params(**kw))))
+
+
+def test_staged_values_rebuild_matches_plain_rebuild(ctx):
+    """amgr_stage_values + AMGR_STAGED (copy-stream pipelining) gives the same
+    hierarchy as a plain values rebuild, over two consecutive steps (the
+    staging buffer is recycled)."""
+    A0 = P.grid3d_values("dambreak", 16, 0)
+    h = amg.setup(A0, ctx=ctx)
+    g = amg.setup(A0, ctx=ctx)
+    for k in (11, 23):
+        Ak = P.grid3d_values("dambreak", 16, k)
+        h.stage_values(Ak[2])
+        h.rebuild_staged()
+        g.rebuild_values(Ak[2])
+        for l in range(h.num_levels()):
+            np.testing.assert_array_equal(_bits(h.level_A(l)[2]), _bits(g.level_A(l)[2]))
+        f = np.random.default_rng(k).uniform(-1, 1, 16 ** 3)
+        np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(amg.vcycle(g, f)))
+    with pytest.raises(amg.InvalidArgument, match="no staged values"):
+        h.rebuild_staged()
