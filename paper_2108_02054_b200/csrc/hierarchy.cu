@@ -154,7 +154,7 @@ void build_smoother(Ctx& c, Level& L, const AmgP& p, int* bad) {
         CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), c.stream));
         if (L.pst.size() != 3) L.pst.alloc(3, c.stream);
         if (L.cheb.size() != 2 * p.cheb_degree + 1) L.cheb.alloc(2 * p.cheb_degree + 1, c.stream);
-        fill(c, x.get(), n, 1.0);
+        power_start(c, n, x.get());
         const double init[3] = {0.0, static_cast<double>(n), 0.0};
         h2d(L.pst.get(), init, 3, c.stream);
         for (int it = 0; it < p.power_iters; ++it) {
@@ -473,6 +473,10 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             if (nc < Av.n) members(c, Av.n, nc, T->agg.get(), T->mptr, T->midx);
         }
         clk.end(PH_TRANSFER);
+        if (std::getenv("AMGR_TRACE_SETUP"))
+            std::fprintf(stderr, "[amgr setup] level %zu: n=%lld nnz=%lld -> nc=%lld (agg rounds %lld)\n", l,
+                         static_cast<long long>(Av.n), static_cast<long long>(Av.nnz), static_cast<long long>(nc),
+                         static_cast<long long>(h->agg_rounds));
         if (nc == Av.n) {
             // coarsening stalled (hierarchy.cpp:70-77)
             if (Av.n <= p.max_direct) break;

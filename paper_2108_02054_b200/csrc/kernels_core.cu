@@ -1232,6 +1232,19 @@ __global__ void __launch_bounds__(256) k_power_norm(int n, const double* __restr
     block_dots<1>(d, ds);
 }
 
+// power-iteration start vector: pseudo-random signs, x.x = n exactly
+// (oracle/amg_oracle.c power_start_sign, same hash)
+__global__ void k_power_start(int64_t n, double* x) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = (static_cast<uint64_t>(i) + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        x[i] = (z >> 63) ? -1.0 : 1.0;
+    }
+}
+
 // Chebyshev coefficients from lam (oracle smooth_cheb): hi = lam*safety,
 // lo = hi*lower, theta, delta, sigma; rho recursion for the degree-1 steps.
 __global__ void k_cheb_coef(const double* st, double safety, double lower, int degree, double* coef) {
@@ -1520,6 +1533,9 @@ void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x,
 
 void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s) {
     launch_rowpass(c, "power", spmv_bytes(A) + 8.0 * A.n, A, OpPower{x, w, y}, Gate{}, s, true);
+}
+void power_start(Ctx& c, int64_t n, double* x) {
+    LAUNCH(c, "power", 8.0 * n, k_power_start, grid_for(n, 256, c.num_sms * 16), 256, 0, n, x);
 }
 void power_norm(Ctx& c, int64_t n, const double* y, double* x, double* st, DotSink s) {
     LAUNCH(c, "power", 16.0 * n, k_power_norm, dot_grid(c), 256, 0, static_cast<int>(n), y, x, st, s);

@@ -358,6 +358,22 @@ def test_chebyshev_smoother_and_power_bound():
     assert s.converged and s.iterations < 30
 
 
+def test_power_iteration_estimate_covers_lambda_max():
+    """The random-sign start puts weight on the top mode of D^-1 A, so ten
+    power iterations times the 1.1 safety factor bound lambda_max from above
+    (a constant start, the smoothest mode, left the estimate ~40% low)."""
+    for kind in ("poisson", "dambreak"):
+        rp, ci, v = A = P.grid3d_values(kind, 8, 3)
+        n = len(rp) - 1
+        D = np.zeros((n, n))
+        for i in range(n):
+            D[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+        lam = np.max(np.abs(np.linalg.eigvals(D / np.diag(D)[:, None])))
+        h = O.setup(A, O.params(smoother="chebyshev", power_iters=10))
+        assert 0.9 * lam < h.levels[0].lam_max / 1.1 <= lam * (1 + 1e-12)
+        assert h.levels[0].lam_max >= lam
+
+
 def test_cg_extension_converges_on_spd():
     A = P.grid3d_values("poisson", 12, 1)
     h = O.setup(A)
