@@ -496,11 +496,15 @@ def main():
     except Exception:
         pass
     lvl0 = h.level_dims(0)
+    cb0 = h.level_layout(0)["col_bytes"]
+    csr_bytes = 12 * lvl0["nnz"] + 4 * (lvl0["nrows"] + 1) + 32 * lvl0["nrows"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": "k_rowpass<OpSmooth> level 0 (post-smoothing sweep)",
                 "bytes_per_launch": pbytes / cnt if cnt else None,
-                "bytes_formula": "12*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads)",
+                "bytes_formula": f"(8+{cb0})*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads; "
+                                 f"{cb0}-byte column codes, DESIGN.md 2)",
+                "csr_equivalent_GB_s": (csr_bytes / (pms / cnt) / 1e6) if cnt else None,
                 "nnz": lvl0["nnz"], "n": lvl0["nrows"], "peak_source": peak_kind, "kernels": extra}
 
     # ---- whole-phase rooflines (SURVEY.md 8(d) algorithmic bytes from this
@@ -511,7 +515,8 @@ def main():
     Lh = len(dims)
     rap_b = sum(12 * zl[i] + 8 * zl[i + 1] + 4 * nl[i] + 4 * (nl[i + 1] + 1) for i in range(Lh - 1))
     jac_b = sum(20 * nl[i] for i in range(Lh - 1))
-    spmv = [12 * zl[i] + 4 * (nl[i] + 1) + 16 * nl[i] for i in range(Lh)]
+    cbl = [h.level_layout(l)["col_bytes"] for l in range(Lh)]
+    spmv = [(8 + cbl[i]) * zl[i] + 4 * (nl[i] + 1) + 16 * nl[i] for i in range(Lh)]
     vc_b = sum(2 * spmv[i] + 64 * nl[i] for i in range(Lh - 1))
     it_b = 2 * vc_b + 2 * spmv[0] + 192 * nl[0]
     # one V-cycle, device time (stream-launched, 10 repetitions)
@@ -537,7 +542,9 @@ def main():
     phases = {"rebuild": phase(rap_b + jac_b, rebuild_ms), "vcycle": phase(vc_b, vc_ms),
               "bicgstab_iteration": phase(it_b, it_ms),
               "bytes_formulas": "SURVEY.md 8(d): RAP 12nnz_i+8nnz_i+1+4n_i+4(n_i+1 +1), Jacobi 20n_i, "
-                                "V-cycle sum(2 SpMV_i + 64 n_i), iteration 2 V + 2 SpMV_0 + 192 n_0"}
+                                "V-cycle sum(2 SpMV_i + 64 n_i), iteration 2 V + 2 SpMV_0 + 192 n_0; "
+                                "SpMV_i with (8 + column bytes) per entry",
+              "column_bytes_per_level": cbl}
     del vz
 
     # ---- e2e through the C-ABI with host buffers ----

@@ -325,6 +325,11 @@ int amgr_hier_num_levels(const amgr_hier* h);
 /* dims[0]=nrows, dims[1]=nnz, dims[2]=n_coarse (0 on the coarsest level),
  * dims[3]=has_smoother. */
 amgr_status amgr_hier_level_dims(const amgr_hier* h, int level, int64_t* dims);
+/* Row-pass layout of A_level (no reference counterpart):
+ * *col_bytes = bytes per stored column in the row passes (4 = int32 columns,
+ * 1 / 2 = coded column stream col = row + dict[code]), *ndict = dictionary
+ * size (0 when uncoded).  Either pointer may be NULL. */
+amgr_status amgr_hier_level_layout(const amgr_hier* h, int level, int32_t* col_bytes, int32_t* ndict);
 /* A_level as int64 CSR (row_ptr nrows+1, col nnz, values nnz) into host buffers. */
 amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col,
                               double* values);

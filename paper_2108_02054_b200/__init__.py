@@ -112,6 +112,7 @@ PROTOTYPES = {
     "amgr_spmv": (_I, [_V, _I, _V, _V, _I]),
     "amgr_hier_num_levels": (_I, [_V]),
     "amgr_hier_level_dims": (_I, [_V, _I, _V]),
+    "amgr_hier_level_layout": (_I, [_V, _I, _V, _V]),
     "amgr_hier_level_A": (_I, [_V, _I, _V, _V, _V]),
     "amgr_hier_level_P": (_I, [_V, _I, _V]),
     "amgr_hier_level_R": (_I, [_V, _I, _V, _V]),
@@ -347,6 +348,13 @@ class Hierarchy:
         d = np.zeros(4, np.int64)
         _check(lib().amgr_hier_level_dims(self._p, lvl, d.ctypes.data), self.ctx.ptr)
         return {"nrows": int(d[0]), "nnz": int(d[1]), "n_coarse": int(d[2]), "has_smoother": bool(d[3])}
+
+    def level_layout(self, lvl: int):
+        """Row-pass layout of A_lvl: bytes per stored column (4 raw, 1/2
+        coded) and the offset-dictionary size (amgr_hier_level_layout)."""
+        cb, nd = C.c_int32(), C.c_int32()
+        _check(lib().amgr_hier_level_layout(self._p, lvl, C.byref(cb), C.byref(nd)), self.ctx.ptr)
+        return {"col_bytes": int(cb.value), "ndict": int(nd.value)}
 
     def finest_size(self) -> int:
         return self.level_dims(0)["nrows"]

@@ -302,6 +302,17 @@ amgr_status amgr_hier_level_dims(const amgr_hier* h, int level, int64_t* dims) {
     });
 }
 
+amgr_status amgr_hier_level_layout(const amgr_hier* h, int level, int32_t* col_bytes, int32_t* ndict) {
+    if (!h) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] {
+        const amgr::Hier& H = *h->h;
+        if (level < 0 || level >= static_cast<int>(H.lv.size())) amgr::invalid("level out of range");
+        const amgr::ColCode& cc = H.lv[level].pat->cc;
+        if (col_bytes) *col_bytes = cc.mode == 1 ? 1 : cc.mode == 2 ? 2 : 4;
+        if (ndict) *ndict = cc.ndict;
+    });
+}
+
 amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col, double* values) {
     if (!h) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] {

@@ -545,6 +545,14 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
         cur.T = T;
         h->lv.push_back(std::move(next));
     }
+    // coded column streams for the row passes (all levels but the coarsest,
+    // which is solved densely)
+    clk.begin(PH_GALERKIN);
+    for (size_t l = 0; l + 1 < h->lv.size(); ++l) {
+        Pattern& P = *h->lv[l].pat;
+        encode_columns(c, P.n, P.nnz, P.rp.get(), P.col.get(), P.cc);
+    }
+    clk.end(PH_GALERKIN);
     clk.begin(PH_COARSE);
     coarse_factorize(*h, lu_status.get());
     clk.end(PH_COARSE);

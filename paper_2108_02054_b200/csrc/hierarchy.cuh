@@ -30,7 +30,15 @@ struct Pattern {
     int64_t n = 0, ncols = 0, nnz = 0;
     int max_span = 0;
     DevArray<int> rp, col, diag;
+    ColCode cc;  // coded column stream for the row passes (mode 0: none)
 };
+inline void set_code(CsrView& v, const ColCode& cc) {
+    v.cmode = cc.mode;
+    v.ndict = cc.ndict;
+    v.code = cc.mode == 1 ? static_cast<const void*>(cc.c8.get())
+                          : cc.mode == 2 ? static_cast<const void*>(cc.c16.get()) : nullptr;
+    v.dict = cc.mode ? cc.dict.get() : nullptr;
+}
 // Frozen transfer operators of one level: P (agg) and R = P^T (mptr/midx).
 // Smoothed aggregation (extension) additionally keeps the general P and R.
 struct Transfer {
@@ -59,6 +67,7 @@ inline CsrView csr_view(const Pattern& p, const double* val) {
     v.col = p.col.get();
     v.val = val;
     v.max_span = p.max_span;
+    set_code(v, p.cc);
     return v;
 }
 
@@ -81,6 +90,7 @@ struct Level {
         v.col = pat->col.get();
         v.val = ext_val ? ext_val : val.get();
         v.max_span = pat->max_span;
+        set_code(v, pat->cc);
         return v;
     }
 };

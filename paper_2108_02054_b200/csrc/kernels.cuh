@@ -19,6 +19,12 @@ struct CsrView {
     const int* col = nullptr;
     const double* val = nullptr;
     int max_span = 0;  // widest 16-byte-aligned nnz span of a 32-row group (row-pass chunk sizing)
+    // coded column stream (encode_columns): col_k = row + dict[code_k]
+    // cmode 0 = raw int32 columns, 1 = uint8 codes, 2 = uint16 codes
+    int cmode = 0;
+    int ndict = 0;
+    const void* code = nullptr;
+    const int* dict = nullptr;
 };
 
 // Deterministic multi-block dot products: per-block partials + last-block

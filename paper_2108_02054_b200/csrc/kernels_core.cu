@@ -14,6 +14,7 @@
 
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "reduce.cuh"
@@ -70,16 +71,31 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // GATHER: 0 = RP_BATCH predicated gathers (level 0's 7-entry rows);
 //         8 / 12 = that many unpredicated gathers (coarser levels: 8 for
 //         > 12 nnz/row, 12 for 8..12 nnz/row; measured per level)
-template <class Op, int CH, int GATHER>
+// CT: column stream element.  int = raw columns; uint8_t / uint16_t = coded
+// columns (encode_columns), col = row + dict[code], the uint8 dictionary
+// staged in shared memory.  Chunk ranges are aligned to 16 bytes of CT.
+template <class Op, int CH, int GATHER, class CT>
 __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, DotSink sink) {
     pdl_enter();
     if (gated_off(g)) return;
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    constexpr bool CODED = sizeof(CT) < 4;
+    constexpr int ALN = 16 / static_cast<int>(sizeof(CT));  // entries per 16 bytes of column stream
     extern __shared__ __align__(128) unsigned char rp_smem[];
     auto s_val = reinterpret_cast<double(*)[2][CH]>(rp_smem);
-    auto s_col = reinterpret_cast<int(*)[2][CH]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH);
+    auto s_col = reinterpret_cast<CT(*)[2][CH]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH);
     auto s_bar = reinterpret_cast<uint64_t(*)[2]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH +
-                                                  sizeof(int) * RP_WARPS * 2 * CH);
+                                                  sizeof(CT) * RP_WARPS * 2 * CH);
+    int* s_dict = reinterpret_cast<int*>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH +
+                                         sizeof(CT) * RP_WARPS * 2 * CH + sizeof(uint64_t) * RP_WARPS * 2);
+    const CT* colstream = CODED ? static_cast<const CT*>(A.code) : reinterpret_cast<const CT*>(A.col);
+    if constexpr (sizeof(CT) == 1) {
+        for (int t = threadIdx.x; t < A.ndict; t += blockDim.x) s_dict[t] = __ldg(A.dict + t);
+        __syncthreads();
+    }
+    // value ranges are clamped to the 4-aligned end of the value array (a
+    // caller's adopted buffer has no more slack than that)
+    const int nnz4 = static_cast<int>((A.nnz + 3) & ~int64_t{3});
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = static_cast<int>(A.n);
     const int ngroups = (n + 31) >> 5;
@@ -97,15 +113,22 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             mbar_fence_init();
         }
         __syncwarp();
-        auto issue = [&](int base, int end, int st) {  // [base, min(base+CH, end)), base/end 4-aligned
+        auto issue = [&](int base, int end, int st) {  // [base, min(base+CH, end)), base/end ALN-aligned
             const int cnt = min(CH, end - base);
             if (lane == 0) {
                 fence_proxy_async();
-                const uint32_t bv = static_cast<uint32_t>(cnt) * 8u, bc = static_cast<uint32_t>(cnt) * 4u;
+                const int vcnt = CODED ? min(cnt, nnz4 - base) : cnt;
+                const uint32_t bv = static_cast<uint32_t>(vcnt) * 8u,
+                               bc = static_cast<uint32_t>(cnt) * static_cast<uint32_t>(sizeof(CT));
                 mbar_expect_tx(&bar[st], bv + bc);
                 tma_load_1d(&s_val[w][st][0], A.val + base, bv, &bar[st]);
-                tma_load_1d(&s_col[w][st][0], A.col + base, bc, &bar[st]);
+                tma_load_1d(&s_col[w][st][0], colstream + base, bc, &bar[st]);
             }
+        };
+        auto colof = [&](int row, CT code) -> int {
+            if constexpr (sizeof(CT) == 1) return row + s_dict[code];
+            else if constexpr (sizeof(CT) == 2) return row + __ldg(A.dict + code);
+            else return code;
         };
         auto rows_of = [&](int grp, int& rs, int& re) {
             const int row = grp * 32 + lane;
@@ -124,7 +147,7 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
         }
         // group range (aligned) of the current group
         int gs = __shfl_sync(0xffffffffu, rs, 0), ge = __shfl_sync(0xffffffffu, re, 31);
-        int ab = gs & ~3, ae = (ge + 3) & ~3;
+        int ab = gs & ~(ALN - 1), ae = (ge + ALN - 1) & ~(ALN - 1);
         int st = 0;
         uint32_t phase = 0;
         int cb = ab;                     // base of the chunk to consume next
@@ -148,8 +171,8 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                 } else if (NG < ngroups) {
                     const int ngs = __shfl_sync(0xffffffffu, nrs, 0), nge = __shfl_sync(0xffffffffu, nre, 31);
                     if (nge > ngs) {
-                        pb = ngs & ~3;
-                        pe = (nge + 3) & ~3;
+                        pb = ngs & ~(ALN - 1);
+                        pe = (nge + ALN - 1) & ~(ALN - 1);
                     }
                 }
                 if (pb >= 0) issue(pb, pe, st ^ 1);
@@ -174,7 +197,15 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                             // are outstanding (measured on levels >= 1)
                             int cj[NB];
 #pragma unroll
-                            for (int t = 0; t < NB; ++t) cj[t] = s_col[w][st][k + (t < cnt ? t : 0)];
+                            for (int t = 0; t < NB; ++t) cj[t] = colof(row, s_col[w][st][k + (t < cnt ? t : 0)]);
+#pragma unroll
+                            for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
+                        } else if constexpr (CODED) {
+                            // decode the batch first (unpredicated shared-memory reads),
+                            // then the predicated gathers
+                            int cj[NB];
+#pragma unroll
+                            for (int t = 0; t < NB; ++t) cj[t] = colof(row, s_col[w][st][k + (t < cnt ? t : 0)]);
 #pragma unroll
                             for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
                         } else {
@@ -206,8 +237,8 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
             if (G >= ngroups) break;
             gs = __shfl_sync(0xffffffffu, rs, 0);
             ge = __shfl_sync(0xffffffffu, re, 31);
-            ab = gs & ~3;
-            ae = (ge + 3) & ~3;
+            ab = gs & ~(ALN - 1);
+            ae = (ge + ALN - 1) & ~(ALN - 1);
             if (!ready || cb != ab) {  // first chunk of the new group not prefetched
                 cb = ab;
                 ready = false;
@@ -273,6 +304,7 @@ struct OpDown {
 // OpDown's (w replaces u0 as the gathered vector).
 struct OpDownP {
     static constexpr int NDOT = 0;
+    static constexpr int GATHERS = 2;  // w_j and f_j per entry
     using Row = Row1;
     const double* f;
     const double* w;
@@ -416,6 +448,7 @@ struct OpChebStart {
 // Chebyshev step k (>= 1): x' = x + d; r = w*(f - A x'); d' = c1*d + c2*r
 struct OpChebStep {
     static constexpr int NDOT = 0;
+    static constexpr int GATHERS = 2;  // x_j and d_j per entry
     using Row = Row4;
     const double* f;
     const double* w;
@@ -438,17 +471,28 @@ struct OpChebStep {
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
 
-template <class Op, int CH, int GATHER>
+// operand gathers per stored entry of a row-pass Op (default 1)
+template <class Op, class = void>
+struct gathers_of {
+    static constexpr int v = 1;
+};
+template <class Op>
+struct gathers_of<Op, std::void_t<decltype(Op::GATHERS)>> {
+    static constexpr int v = Op::GATHERS;
+};
+
+template <class Op, int CH, int GATHER, class CT>
 void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
                 unsigned grid) {
-    constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * CH * 12 + RP_WARPS * 2 * sizeof(uint64_t);
+    constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * CH * (8 + sizeof(CT)) +
+                            RP_WARPS * 2 * sizeof(uint64_t) + (sizeof(CT) == 1 ? 256 * sizeof(int) : 0);
     static bool configured = false;
     if (!configured) {
-        CK(cudaFuncSetAttribute(k_rowpass<Op, CH, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_rowpass<Op, CH, GATHER, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
         configured = true;
     }
-    LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, GATHER>), grid, RP_BLOCK, smem, A, op, g, s);
+    LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, GATHER, CT>), grid, RP_BLOCK, smem, A, op, g, s);
 }
 
 template <class Op>
@@ -460,17 +504,30 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
     if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
-    if (A.nnz > 12 * A.n)
-        launch_tma<Op, RP_CH, 8>(c, fam, bytes, A, op, g, s, grid);
+    // coded columns: uint8 only on <= 8 nnz/row, uint16 only above (encode_columns).
+    // Ops that gather two operands per entry (OpDownP) read the raw columns:
+    // with the extra dictionary lookup per entry they ran 9% slower coded.
+    if (A.cmode == 1 && !(gathers_of<Op>::v > 1))
+        launch_tma<Op, RP_CH, 0, uint8_t>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.cmode == 2 && !(gathers_of<Op>::v > 1) && A.nnz > 12 * A.n)
+        launch_tma<Op, RP_CH, 8, uint16_t>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.cmode == 2 && !(gathers_of<Op>::v > 1))
+        launch_tma<Op, RP_CH, 12, uint16_t>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.nnz > 12 * A.n)
+        launch_tma<Op, RP_CH, 8, int>(c, fam, bytes, A, op, g, s, grid);
     else if (A.nnz > 8 * A.n)
-        launch_tma<Op, RP_CH, 12>(c, fam, bytes, A, op, g, s, grid);
+        launch_tma<Op, RP_CH, 12, int>(c, fam, bytes, A, op, g, s, grid);
     else
-        launch_tma<Op, RP_CH, 0>(c, fam, bytes, A, op, g, s, grid);
+        launch_tma<Op, RP_CH, 0, int>(c, fam, bytes, A, op, g, s, grid);
 }
 
+// bytes per stored entry of a row pass: fp64 value + column (int32, or the
+// 1-/2-byte code of a coded column stream)
+double entry_bytes(const CsrView& A) { return A.cmode == 1 ? 9.0 : A.cmode == 2 ? 10.0 : 12.0; }
+
 double spmv_bytes(const CsrView& A) {
-    // 12 B/nnz (value + int32 column) + row_ptr + x read once + y written once
-    return 12.0 * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
+    // value + column per entry + row_ptr + x read once + y written once
+    return entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
 }
 
 // ---- restriction / prolongation ------------------------------------------
@@ -1356,7 +1413,7 @@ void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, d
 }
 void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g) {
     // A + f read once, u0 gathered (read once), r written once
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, u0, r}, g, {}, false);
 }
 void vc_restrict_general(Ctx& c, const CsrView& R, const double* r, double* fc, const double* wc, double om,
@@ -1369,7 +1426,7 @@ void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double*
     launch_rowpass(c, "prolong", bytes, P, OpProlongG{e, u, out}, g, {}, false);
 }
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDownP{f, w, om, r}, g, {}, false);
 }
 void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,
@@ -1380,7 +1437,7 @@ void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, doub
 }
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
                double* out, Gate g) {
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;
+    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;
     launch_rowpass(c, "vcycle_smooth", bytes, A, OpSmooth{f, w, om, u, out}, g, {}, false);
 }
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,

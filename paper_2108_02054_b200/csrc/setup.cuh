@@ -12,6 +12,20 @@ struct GraphDev {
     DevArray<int> ptr, adj;
 };
 
+// Coded column stream of a pattern (row-pass layout): when the
+// pattern's column offsets j - i take few distinct values (a stencil: 7 on the
+// 7-point level 0, ~2K on its first aggregation level), the row passes read a
+// 1- or 2-byte code per entry instead of the int32 column, col = i + dict[code].
+// Columns, their order and the arithmetic are unchanged.
+struct ColCode {
+    int mode = 0;  // 0 raw, 1 uint8, 2 uint16
+    int ndict = 0;
+    DevArray<uint8_t> c8;
+    DevArray<uint16_t> c16;
+    DevArray<int> dict;
+};
+void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out);
+
 // First row (ascending) whose diagonal is missing or zero, or -1.
 // (strength_graph, coarsening.cpp:19-32; build_smoother, smoother.cpp:12-28)
 int64_t first_bad_diag(Ctx& c, const CsrView& A, const int* dpos);

@@ -413,3 +413,57 @@ def test_staged_values_rebuild_matches_plain_rebuild(ctx):
         np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(amg.vcycle(g, f)))
     with pytest.raises(amg.InvalidArgument, match="no staged values"):
         h.rebuild_staged()
+
+
+@pytest.mark.parametrize("kind,g", [("dambreak", 20), ("blob", 24)])
+def test_coded_columns_match_raw_columns(ctx, kind, g, monkeypatch):
+    """Coded column stream (encode_columns: col = row + dict[code], uint8 on the
+    7-point level, uint16 on the wider levels) against the raw int32 layout
+    (AMGR_COLCODE=0): identical hierarchy, V-cycle and solve, bit for bit; and
+    against the oracle."""
+    from oracle import oracle as O
+
+    A = P.grid3d_values(kind, g, 9)
+    n = g ** 3
+    h = amg.setup(A, ctx=ctx)  # default: uint8 codes on the 7-point level only
+    lay = [h.level_layout(l) for l in range(h.num_levels())]
+    assert lay[0] == {"col_bytes": 1, "ndict": 7}
+    assert all(x["col_bytes"] == 4 for x in lay[1:])
+    monkeypatch.setenv("AMGR_COLCODE", "16")
+    hw = amg.setup(A, ctx=ctx)
+    assert all(hw.level_layout(l)["col_bytes"] == 2 for l in range(1, hw.num_levels() - 1))
+    monkeypatch.setenv("AMGR_COLCODE", "0")
+    hr = amg.setup(A, ctx=ctx)
+    assert all(hr.level_layout(l)["col_bytes"] == 4 for l in range(hr.num_levels()))
+    f = np.random.default_rng(11).uniform(-1, 1, n)
+    ref_v = _bits(O.vcycle(O.setup(A), f))
+    for x in (h, hw, hr):
+        np.testing.assert_array_equal(_bits(amg.vcycle(x, f)), ref_v)
+    fr = P.rhs(n)
+    u2, s2 = amg.bicgstab(hr, fr)
+    for x in (h, hw):
+        u1, s1 = amg.bicgstab(x, fr)
+        assert s1.iterations == s2.iterations
+        np.testing.assert_array_equal(_bits(u1), _bits(u2))
+    # partial reuse keeps the coded pattern
+    A2 = P.grid3d_values(kind, g, 10)
+    h2 = amg.partial_update(h, A2)
+    assert h2.level_layout(0)["col_bytes"] == 1
+    np.testing.assert_array_equal(_bits(amg.vcycle(h2, f)), _bits(O.vcycle(O.partial_update(O.setup(A), A2), f)))
+
+
+def test_coded_columns_fallback_many_offsets(ctx):
+    """A pattern whose offsets exceed the code dictionary keeps int32 columns."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    rows = []
+    for i in range(n):
+        cols = set(rng.choice(n, 5, replace=False).tolist()) | {i}
+        rows.append([(c, (4.0 if c == i else -0.5)) for c in cols])
+    A = P.csr_from_dense_rows(rows, n)
+    h = amg.setup(A, amg.AmgParams(coarse_enough=50), ctx=ctx)
+    assert h.level_layout(0)["col_bytes"] == 4
+    from oracle import oracle as O
+
+    f = rng.uniform(-1, 1, n)
+    np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(O.vcycle(O.setup(A, O.params(coarse_enough=50)), f)))
