@@ -59,8 +59,12 @@ enum { AMGR_HOST = 0, AMGR_DEVICE = 1,
         * unmodified, be 16-byte aligned and have >= 32 bytes of slack past
         * the last value (read by 16-byte TMA bulk copies). */
        AMGR_DEVICE_ADOPT = 2,
-       /* amgr_rebuild_values only (values = NULL): use the values staged by
-        * the last amgr_stage_values (swapped in, no copy). */
+       /* amgr_rebuild_values (values = NULL): use the values staged by the
+        * last amgr_stage_values (swapped in, no copy); a pending
+        * amgr_stage_rhs is committed with them.  amgr_bicgstab / amgr_cg
+        * (f = NULL): f = the RHS committed by the last STAGED rebuild
+        * (staging the next step's RHS meanwhile does not change it), u0 and
+        * u are device pointers. */
        AMGR_STAGED = 3 };
 
 /* Smoother kinds.  JACOBI is the reference's (smoother.hpp:11-16); SPAI0 and
@@ -141,7 +145,13 @@ amgr_status amgr_ctx_create(int device, void* stream, amgr_ctx** out);
 void amgr_ctx_destroy(amgr_ctx* ctx);
 const char* amgr_last_error(const amgr_ctx* ctx);
 void* amgr_ctx_stream(const amgr_ctx* ctx);
+/* Waits for the context stream and the copy / download streams. */
 amgr_status amgr_ctx_synchronize(amgr_ctx* ctx);
+/* Pipelining (extension): snapshot n doubles of device memory on the context
+ * stream (after the work queued so far) and copy them to host_dst on a
+ * download stream, so the transfer overlaps the next calls' device work.
+ * host_dst is complete after amgr_ctx_synchronize (pinned memory for overlap). */
+amgr_status amgr_download_async(amgr_ctx* ctx, const double* device_src, double* host_dst, int64_t n);
 /* Library version string and the compiled architecture ("sm_100a"). */
 const char* amgr_version(void);
 
@@ -180,6 +190,10 @@ amgr_status amgr_rebuild(amgr_hier* h, const amgr_csr* A_new);
  * on the copy engines while the current step's solve computes.  Consume with
  * amgr_rebuild_values(h, NULL, AMGR_STAGED). */
 amgr_status amgr_stage_values(amgr_hier* h, const double* values, int location);
+/* Pipelining (extension): the same for the next step's right-hand side
+ * (finest_size entries); committed by the next STAGED rebuild, then read by
+ * the STAGED solves until the following one. */
+amgr_status amgr_stage_rhs(amgr_hier* h, const double* f, int location);
 amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location);
 
 /* Replaces `std::vector<double> vcycle(const Hierarchy&, span f, const AmgParams&)`

@@ -32,6 +32,14 @@ LIB_PATH = os.path.join(_HERE, "libamgr_b200.so")
 LIB_PATH = os.environ.get("AMGR_LIB", LIB_PATH)
 
 HOST, DEVICE, DEVICE_ADOPT, STAGED = 0, 1, 2, 3
+
+
+class _StagedRhs:
+    def __repr__(self):
+        return "STAGED_RHS"
+
+
+STAGED_RHS = _StagedRhs()  # bicgstab(h, STAGED_RHS, (u0_ptr, u_ptr)): f = the staged RHS
 SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}
 COARSENING = {"plain": 0, "smoothed": 1}
 COARSE_SOLVE = {"exact": 0, "inverse": 1}
@@ -135,6 +143,8 @@ PROTOTYPES = {
     "amgr_speedup_percent": (_D, [_D, _D]),
     "amgr_hier_level_transfer": (_I, [_V, _I, _I, _P(_L), _V, _V, _V]),
     "amgr_stage_values": (_I, [_V, _V, _I]),
+    "amgr_stage_rhs": (_I, [_V, _V, _I]),
+    "amgr_download_async": (_I, [_V, _V, _V, _L]),
     "amgr_mm_read": (_I, [_V, C.c_char_p, _P(_V)]),
     "amgr_matrix_csr": (_I, [_V, _P(_Csr)]),
     "amgr_matrix_free": (None, [_V]),
@@ -293,7 +303,14 @@ class Context:
         return lib().amgr_ctx_stream(self._p) or 0
 
     def synchronize(self):
+        """amgr_ctx_synchronize: the context stream and the copy / download streams."""
         _check(lib().amgr_ctx_synchronize(self._p), self._p)
+
+    def download_async(self, device_ptr: int, host_ptr: int, n: int):
+        """amgr_download_async: snapshot n doubles at device_ptr (stream-ordered)
+        and copy them to host_ptr on the download stream; complete after
+        synchronize()."""
+        _check(lib().amgr_download_async(self._p, device_ptr, host_ptr, n), self._p)
 
     def launches(self) -> int:
         return int(lib().amgr_launch_count(self._p))
@@ -456,6 +473,16 @@ class Hierarchy:
             self._staged_keep = _f64(values)
             _check(lib().amgr_stage_values(self._p, self._staged_keep.ctypes.data, HOST), self.ctx.ptr)
 
+    def stage_rhs(self, f, host: bool | None = None):
+        """Pipelining (amgr_stage_rhs): the next step's right-hand side, like
+        stage_values; committed by the next rebuild_staged, then read by
+        bicgstab(h, STAGED_RHS, ...)."""
+        if isinstance(f, int):
+            _check(lib().amgr_stage_rhs(self._p, f, HOST if host else DEVICE), self.ctx.ptr)
+        else:
+            self._rhs_keep = _f64(f)
+            _check(lib().amgr_stage_rhs(self._p, self._rhs_keep.ctypes.data, HOST), self.ctx.ptr)
+
     def rebuild_staged(self):
         """amgr_rebuild_values(h, NULL, AMGR_STAGED): swap the staged values in."""
         _check(lib().amgr_rebuild_values(self._p, None, STAGED), self.ctx.ptr)
@@ -524,6 +551,13 @@ def vcycle_device(h: Hierarchy, f_ptr: int, u_ptr: int) -> None:
 
 def _solve(fn, h, f, u0, prm):
     prm = prm or SolveParams()
+    if f is STAGED_RHS:  # staged RHS (amgr_stage_rhs); u0 = (u0_ptr, u_ptr) device addresses
+        u0_ptr, u_ptr = u0
+        sp = _SolveParams(prm.tol, prm.max_iter)
+        st = _SolveStats()
+        _check(fn(h._p, None, u0_ptr, u_ptr, C.byref(sp), C.byref(st), STAGED), h.ctx.ptr)
+        return None, SolveStats(int(st.iterations), float(st.relative_residual), bool(st.converged),
+                                bool(st.breakdown))
     if isinstance(f, int):  # device pointers: (f, u0, u) all device addresses
         u0_ptr, u_ptr = u0
         sp = _SolveParams(prm.tol, prm.max_iter)

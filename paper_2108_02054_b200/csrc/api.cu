@@ -141,6 +141,13 @@ void amgr_ctx_destroy(amgr_ctx* ctx) {
         cudaStreamSynchronize(ctx->c.copy);
         cudaStreamDestroy(ctx->c.copy);
     }
+    if (ctx->c.d2h) {
+        cudaStreamSynchronize(ctx->c.d2h);
+        if (ctx->c.snap) cudaFree(ctx->c.snap);
+        cudaStreamDestroy(ctx->c.d2h);
+        cudaEventDestroy(ctx->c.snap_ev);
+        cudaEventDestroy(ctx->c.d2h_done_ev);
+    }
     if (ctx->c.side) {
         cudaStreamSynchronize(ctx->c.side);
         cudaStreamDestroy(ctx->c.side);
@@ -155,7 +162,37 @@ const char* amgr_last_error(const amgr_ctx* ctx) { return ctx ? ctx->c.last_erro
 void* amgr_ctx_stream(const amgr_ctx* ctx) { return ctx ? ctx->c.stream : nullptr; }
 
 amgr_status amgr_ctx_synchronize(amgr_ctx* ctx) {
-    return guard(ctx, [&] { CK(cudaStreamSynchronize(ctx->c.stream)); });
+    return guard(ctx, [&] {
+        CK(cudaStreamSynchronize(ctx->c.stream));
+        if (ctx->c.copy) CK(cudaStreamSynchronize(ctx->c.copy));
+        if (ctx->c.d2h) CK(cudaStreamSynchronize(ctx->c.d2h));
+    });
+}
+
+amgr_status amgr_download_async(amgr_ctx* ctx, const double* device_src, double* host_dst, int64_t n) {
+    if (!ctx || n < 0 || (n > 0 && (!device_src || !host_dst))) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] {
+        amgr::Ctx& c = ctx->c;
+        if (n == 0) return;
+        if (!c.d2h) {
+            CK(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c.snap_ev, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c.d2h_done_ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(c.d2h_done_ev, c.d2h));
+        }
+        // the snapshot buffer is reused: the previous download must have drained it
+        CK(cudaStreamWaitEvent(c.stream, c.d2h_done_ev, 0));
+        if (c.snap_n < n) {
+            if (c.snap) CK(cudaFreeAsync(c.snap, c.stream));
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&c.snap), sizeof(double) * static_cast<size_t>(n), c.stream));
+            c.snap_n = n;
+        }
+        amgr::d2d(c.snap, device_src, n, c.stream);
+        CK(cudaEventRecord(c.snap_ev, c.stream));
+        CK(cudaStreamWaitEvent(c.d2h, c.snap_ev, 0));
+        amgr::d2h(host_dst, c.snap, n, c.d2h);
+        CK(cudaEventRecord(c.d2h_done_ev, c.d2h));
+    });
 }
 
 amgr_status amgr_setup(amgr_ctx* ctx, const amgr_csr* A, const amgr_amg_params* prm, amgr_hier** out) {
@@ -189,6 +226,11 @@ amgr_status amgr_rebuild(amgr_hier* h, const amgr_csr* A) {
 amgr_status amgr_stage_values(amgr_hier* h, const double* values, int location) {
     if (!h || !values) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] { amgr::stage_values(*h->h, values, location); });
+}
+
+amgr_status amgr_stage_rhs(amgr_hier* h, const double* f, int location) {
+    if (!h || !f) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] { amgr::stage_rhs(*h->h, f, location); });
 }
 
 amgr_status amgr_rebuild_values(amgr_hier* h, const double* values, int location) {
@@ -244,17 +286,21 @@ amgr_status amgr_vcycle(amgr_hier* h, const double* f, double* u, int location) 
 
 static amgr_status solve(amgr_hier* h, const double* f, const double* u0, double* u, const amgr_solve_params* prm,
                          amgr_solve_stats* stats, int location, bool use_cg) {
-    if (!h || !f || !u0 || !u || !stats) return AMGR_E_INVALID_ARGUMENT;
+    if (!h || (!f && location != AMGR_STAGED) || !u0 || !u || !stats) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] {
         amgr::Hier& H = *h->h;
         const int64_t n = H.lv.front().pat->n;
         amgr_solve_params sp;
         amgr_solve_params_default(&sp);
         if (prm) sp = *prm;
-        VecIO io(*H.ctx, location);
-        const double* fd = io.in(f, n);
-        const double* u0d = (u0 == u && location == AMGR_DEVICE) ? u0 : io.in(u0, n);
-        double* ud = (location == AMGR_DEVICE) ? u : io.out(u, n);
+        // AMGR_STAGED: f is the RHS staged by amgr_stage_rhs (committed by the
+        // STAGED rebuild, or here), u0 / u are device pointers
+        const bool staged = location == AMGR_STAGED;
+        VecIO io(*H.ctx, staged ? AMGR_DEVICE : location);
+        const double* fd = staged ? amgr::committed_rhs(H) : io.in(f, n);
+        const bool dev = staged || location == AMGR_DEVICE;
+        const double* u0d = (u0 == u && dev) ? u0 : io.in(u0, n);
+        double* ud = dev ? u : io.out(u, n);
         if (use_cg)
             amgr::cg(H, fd, u0d, ud, sp, *stats);
         else

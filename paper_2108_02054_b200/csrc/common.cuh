@@ -64,6 +64,11 @@ struct Ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaStream_t copy = nullptr;  // staged H2D of the next step's values (lazily created)
+    // amgr_download_async: device snapshot + D2H on its own stream (lazily created)
+    cudaStream_t d2h = nullptr;
+    cudaEvent_t snap_ev = nullptr, d2h_done_ev = nullptr;
+    double* snap = nullptr;
+    int64_t snap_n = 0;
 };
 
 // Run fn with c.stream temporarily redirected to the side stream, ordered

@@ -623,16 +623,53 @@ void rebuild(Hier& h, const amgr_csr& A) {
 Hier::~Hier() {
     if (staged_ev) cudaEventDestroy(staged_ev);
     if (main_ev) cudaEventDestroy(main_ev);
+    if (rhs_ev) cudaEventDestroy(rhs_ev);
+}
+
+static void ensure_copy_stream(Hier& h) {
+    Ctx& c = *h.ctx;
+    if (!c.copy) CK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    if (!h.staged_ev) {
+        CK(cudaEventCreateWithFlags(&h.staged_ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h.main_ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h.rhs_ev, cudaEventDisableTiming));
+    }
+}
+
+void stage_rhs(Hier& h, const double* f, int location) {
+    Ctx& c = *h.ctx;
+    if (location != AMGR_HOST && location != AMGR_DEVICE) invalid("stage_rhs: location must be HOST or DEVICE");
+    if (!f) invalid("stage_rhs: f is null");
+    ensure_copy_stream(h);
+    const int64_t n = h.lv.front().pat->n;
+    if (h.staged_rhs.size() != n) h.staged_rhs.alloc(n, c.stream);
+    // the staging buffer may still be read by work queued on the main stream
+    CK(cudaEventRecord(h.main_ev, c.stream));
+    CK(cudaStreamWaitEvent(c.copy, h.main_ev, 0));
+    CK(cudaMemcpyAsync(h.staged_rhs.get(), f, sizeof(double) * n,
+                       location == AMGR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.copy));
+    CK(cudaEventRecord(h.rhs_ev, c.copy));
+    h.rhs_staged = true;
+}
+
+void commit_rhs(Hier& h) {
+    Ctx& c = *h.ctx;
+    CK(cudaStreamWaitEvent(c.stream, h.rhs_ev, 0));
+    h.rhs.swap(h.staged_rhs);  // the previous RHS becomes the next staging buffer
+    h.rhs_staged = false;
+    h.rhs_ready = true;
+}
+
+const double* committed_rhs(Hier& h) {
+    if (!h.rhs_ready)
+        invalid("staged solve: no staged right-hand side (amgr_stage_rhs, then a STAGED rebuild commits it)");
+    return h.rhs.get();
 }
 
 void stage_values(Hier& h, const double* values, int location) {
     Ctx& c = *h.ctx;
     if (location != AMGR_HOST && location != AMGR_DEVICE) invalid("stage_values: location must be HOST or DEVICE");
-    if (!c.copy) CK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
-    if (!h.staged_ev) {
-        CK(cudaEventCreateWithFlags(&h.staged_ev, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&h.main_ev, cudaEventDisableTiming));
-    }
+    ensure_copy_stream(h);
     const int64_t nnz = h.lv.front().pat->nnz;
     if (h.staged.size() != nnz) h.staged.alloc(nnz, c.stream);
     // the staging buffer may still be read by work queued on the main stream
@@ -655,6 +692,7 @@ void rebuild_values(Hier& h, const double* values, int location) {
         if (L0.val.size() != L0.pat->nnz) L0.val.alloc(L0.pat->nnz, c.stream);
         L0.val.swap(h.staged);  // the previous values become the next staging buffer
         h.staged_ready = false;
+        if (h.rhs_staged) commit_rhs(h);  // the step's RHS, staged with its values
     } else if (location == AMGR_DEVICE_ADOPT) {
         if (reinterpret_cast<uintptr_t>(values) % 16 != 0) invalid("rebuild_values: adopted buffer must be 16-byte aligned");
         h.lv.front().ext_val = values;

@@ -123,6 +123,11 @@ struct Hier {
     DevArray<double> staged;  // next step's A_0 values (amgr_stage_values)
     cudaEvent_t staged_ev = nullptr, main_ev = nullptr;
     bool staged_ready = false;
+    // staged right-hand side (amgr_stage_rhs): committed into rhs by the next
+    // STAGED rebuild (or STAGED solve), read by amgr_bicgstab/amgr_cg(AMGR_STAGED)
+    DevArray<double> staged_rhs, rhs;
+    cudaEvent_t rhs_ev = nullptr;
+    bool rhs_staged = false, rhs_ready = false;
     ~Hier();
     int64_t nL = 0;
     amgr_phase_timings tm{};
@@ -137,6 +142,10 @@ std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const Amg
 void rebuild(Hier& h, const amgr_csr& A);
 void rebuild_values(Hier& h, const double* values, int location);
 void stage_values(Hier& h, const double* values, int location);
+void stage_rhs(Hier& h, const double* f, int location);
+// the RHS committed by the last STAGED rebuild (amgr_stage_rhs staged it)
+const double* committed_rhs(Hier& h);
+void commit_rhs(Hier& h);
 void vcycle(Hier& h, const double* f, double* u, Gate g = {});
 void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g = {});
 void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,

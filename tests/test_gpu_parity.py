@@ -415,6 +415,55 @@ def test_staged_values_rebuild_matches_plain_rebuild(ctx):
         h.rebuild_staged()
 
 
+def test_pipelined_steps_match_plain_steps(ctx):
+    """The fully pipelined step sequence (amgr_stage_values + amgr_stage_rhs
+    one step ahead, STAGED rebuild, STAGED solve on device-resident u,
+    amgr_download_async of each solution) gives the plain host-path results
+    bit for bit: per-step solutions, iteration counts, and the staged RHS is
+    the step's own (a different RHS per step)."""
+    import torch
+
+    g = 16
+    n = g ** 3
+    mats = [P.grid3d_values("dambreak", g, k) for k in (0, 7, 15, 22)]
+    rhs = [np.random.default_rng(k).uniform(0.1, 1, n) for k in range(4)]
+    # plain path: host buffers, u0 = previous solution
+    h = amg.setup(mats[0], ctx=ctx)
+    u = np.zeros(n)
+    plain = []
+    for k in range(1, 4):
+        h.rebuild_values(mats[k][2])
+        u, st = amg.bicgstab(h, rhs[k], u)
+        plain.append((u.copy(), st.iterations))
+    # pipelined path
+    hp = amg.setup(mats[0], ctx=ctx)
+    dev = torch.device("cuda", ctx.device)
+    ub = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    hv = [torch.from_numpy(mats[k][2]).pin_memory() for k in range(4)]
+    hf = [torch.from_numpy(rhs[k]).pin_memory() for k in range(4)]
+    out = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(3)]
+    torch.cuda.synchronize()
+    hp.stage_values(hv[1].data_ptr(), host=True)
+    hp.stage_rhs(hf[1].data_ptr(), host=True)
+    its = []
+    for j, k in enumerate(range(1, 4)):
+        hp.rebuild_staged()
+        if k + 1 < 4:
+            hp.stage_values(hv[k + 1].data_ptr(), host=True)
+            hp.stage_rhs(hf[k + 1].data_ptr(), host=True)
+        _, st = amg.bicgstab(hp, amg.STAGED_RHS, (ub[(j + 1) % 2].data_ptr(), ub[j % 2].data_ptr()))
+        its.append(st.iterations)
+        ctx.download_async(ub[j % 2].data_ptr(), out[j].data_ptr(), n)
+    ctx.synchronize()
+    for j in range(3):
+        assert its[j] == plain[j][1]
+        np.testing.assert_array_equal(_bits(out[j].numpy()), _bits(plain[j][0]))
+    # a staged solve with no staged RHS ever is an error
+    h2 = amg.setup(mats[0], ctx=ctx)
+    with pytest.raises(amg.InvalidArgument, match="no staged right-hand side"):
+        amg.bicgstab(h2, amg.STAGED_RHS, (ub[0].data_ptr(), ub[1].data_ptr()))
+
+
 @pytest.mark.parametrize("kind,g", [("dambreak", 20), ("blob", 24)])
 def test_coded_columns_match_raw_columns(ctx, kind, g, monkeypatch):
     """Coded column stream (encode_columns: col = row + dict[code], uint8 on the
