@@ -1,6 +1,7 @@
 // Host orchestration of the device AMG hierarchy.  Each function cites the
 // reference function whose semantics (order of phases, error texts, timing
 // buckets) it reproduces.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -439,6 +440,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     h->ctx = &c;
     h->prm = p;
     PhaseClock clk(c);
+    const auto t_setup = std::chrono::steady_clock::now();
 
     Level L0;
     L0.pat = make_pattern(c, A);
@@ -474,9 +476,10 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
         }
         clk.end(PH_TRANSFER);
         if (std::getenv("AMGR_TRACE_SETUP"))
-            std::fprintf(stderr, "[amgr setup] level %zu: n=%lld nnz=%lld -> nc=%lld (agg rounds %lld)\n", l,
+            std::fprintf(stderr, "[amgr setup] level %zu: n=%lld nnz=%lld -> nc=%lld (agg rounds %lld) t=%.1f ms\n", l,
                          static_cast<long long>(Av.n), static_cast<long long>(Av.nnz), static_cast<long long>(nc),
-                         static_cast<long long>(h->agg_rounds));
+                         static_cast<long long>(h->agg_rounds),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count());
         if (nc == Av.n) {
             // coarsening stalled (hierarchy.cpp:70-77)
             if (Av.n <= p.max_direct) break;
