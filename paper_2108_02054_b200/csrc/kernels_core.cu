@@ -1426,7 +1426,8 @@ void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double*
     launch_rowpass(c, "prolong", bytes, P, OpProlongG{e, u, out}, g, {}, false);
 }
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
-    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    // OpDownP always reads int32 columns (gathers_of<OpDownP> = 2, launch_rowpass)
+    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDownP{f, w, om, r}, g, {}, false);
 }
 void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,
@@ -1611,7 +1612,9 @@ void cheb_zero(Ctx& c, int64_t n, const double* f, const double* w, const double
 }
 void cheb_step(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* d,
                const double* coef, int k, double* xout, double* dout, Gate g) {
-    launch_rowpass(c, "cheb", spmv_bytes(A) + 40.0 * A.n, A, OpChebStep{f, w, x, d, coef, k, xout, dout}, g, {},
+    // OpChebStep reads int32 columns (two gathers per entry, launch_rowpass)
+    const double raw = 12.0 * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
+    launch_rowpass(c, "cheb", raw + 40.0 * A.n, A, OpChebStep{f, w, x, d, coef, k, xout, dout}, g, {},
                    false);
 }
 void axpy1(Ctx& c, int64_t n, double* x, const double* d, Gate g) {

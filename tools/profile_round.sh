@@ -24,4 +24,5 @@ python tools/region_driver.py 256 rebuild > gpurun_out/plain_r.log 2>&1 && {
   full rap_L1 rebuild '^k_rap_tma$' 1
 }
 python tools/ncu_summarize.py $R
+# (copy gpurun_out/${R}_launches.csv to profiles/${R}_launches_256_rebuild_vcycle_solve.csv)
 tail -n 2 gpurun_out/ncu_*.log
