@@ -107,7 +107,7 @@ typedef struct amgr_amg_params {
     double sa_omega;         /* smoothed-aggregation damping (extension)    */
     int32_t cheb_degree;     /* Chebyshev degree (extension)                */
     int32_t power_iters;     /* power iterations for lambda_max (extension) */
-    double cheb_lower;       /* lambda_min = cheb_lower * lambda_max        */
+    double cheb_lower;       /* lambda_min = cheb_lower * lambda_max (0.3)  */
     double cheb_safety;      /* lambda_max safety factor                    */
     int32_t coarse_solve;    /* AMGR_COARSE_*          (extension)          */
     int32_t reserved;

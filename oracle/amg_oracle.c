@@ -361,6 +361,7 @@ typedef struct {
     int has_smoother;
     double* w;       /* inv_diag (jacobi, chebyshev) or m (spai0) */
     double lam_max;  /* chebyshev upper bound (after safety factor) */
+    double omega;    /* Jacobi weight of this level (sa_jacobi_omega; = prm.omega otherwise) */
 } olevel;
 
 struct ohier {
@@ -416,7 +417,29 @@ static void smooth_level(const ohier* h, const olevel* L, const double* f, doubl
     if (h->prm.smoother == 2)
         smooth_cheb(L, &h->prm, f, u, sweeps, r);
     else
-        smooth_jacobi(L, h->prm.smoother == 1 ? 1.0 : h->prm.omega, f, u, sweeps, r);
+        smooth_jacobi(L, h->prm.smoother == 1 ? 1.0 : L->omega, f, u, sweeps, r);
+}
+
+/* Smoothed aggregation (extension): the Galerkin operators of a smoothed P
+ * are not diagonally dominant, and lambda_max(D^-1 A_l) grows to 4-15 on the
+ * coarse levels (C1 at 32^3), where the fixed weight 0.72 diverges.  Each
+ * level of an SA hierarchy therefore damps with
+ *   omega_l = min(omega, (4/3) / g_l),  g_l = max_i sum_j |a_ij| / |a_ii|
+ * (Gershgorin bound of D^-1 A_l: order-independent, so device and oracle
+ * agree bit for bit).  Plain aggregation keeps omega. */
+static double sa_jacobi_omega(const ocsr* A, double omega) {
+    double g = 0.0;
+    for (idx_t i = 0; i < A->nrows; ++i) {
+        double s = 0.0, d = 0.0;
+        for (idx_t k = A->rp[i]; k < A->rp[i + 1]; ++k) {
+            s += fabs(A->v[k]);
+            if (A->ci[k] == i) d = A->v[k];
+        }
+        const double q = s / fabs(d);
+        if (q > g) g = q;
+    }
+    const double cap = (4.0 / 3.0) / g;
+    return cap < omega ? cap : omega;
 }
 
 static int build_level_smoother(olevel* L, const oparams* p, char* err, int errlen) {
@@ -424,6 +447,7 @@ static int build_level_smoother(olevel* L, const oparams* p, char* err, int errl
     L->has_smoother = 1;
     int rc = p->smoother == 1 ? spai0_build(&L->A, L->w, err, errlen) : jacobi_build(&L->A, L->w, err, errlen);
     if (rc) return rc;
+    L->omega = (p->coarsening == 1 && p->smoother == 0) ? sa_jacobi_omega(&L->A, p->omega) : p->omega;
     if (p->smoother == 2) L->lam_max = power_lambda(&L->A, L->w, p->power_iters) * p->cheb_safety;
     return 0;
 }

@@ -35,7 +35,7 @@ SMOOTHER = {"jacobi": 0, "spai0": 1, "chebyshev": 2}
 
 def params(eps=0.08, omega=0.72, pre_sweeps=1, post_sweeps=1, coarse_enough=100, max_direct_size=2000,
            smoother="jacobi", coarsening="plain", sa_omega=2.0 / 3.0, cheb_degree=3, power_iters=10,
-           cheb_lower=1.0 / 30.0, cheb_safety=1.1) -> OParams:
+           cheb_lower=0.3, cheb_safety=1.1) -> OParams:
     return OParams(eps, omega, pre_sweeps, post_sweeps, coarse_enough, max_direct_size, SMOOTHER[smoother],
                    {"plain": 0, "smoothed": 1}[coarsening], sa_omega, cheb_degree, power_iters, cheb_lower,
                    cheb_safety)

@@ -193,7 +193,7 @@ class AmgParams:
     sa_omega: float = 2.0 / 3.0
     cheb_degree: int = 3
     power_iters: int = 10
-    cheb_lower: float = 1.0 / 30.0
+    cheb_lower: float = 0.3
     cheb_safety: float = 1.1
     coarse_solve: str = "exact"
 

@@ -77,7 +77,7 @@ void amgr_amg_params_default(amgr_amg_params* p) {
     p->sa_omega = 2.0 / 3.0;
     p->cheb_degree = 3;
     p->power_iters = 10;
-    p->cheb_lower = 1.0 / 30.0;
+    p->cheb_lower = 0.3;  // interval [0.3, 1] x lambda_max: robust on the nonsymmetric C5 operators
     p->cheb_safety = 1.1;
     p->coarse_solve = AMGR_COARSE_EXACT;
     p->reserved = 0;

@@ -320,6 +320,29 @@ static void prolong_level(Ctx& c, const Level& Li, const double* u, const double
         vc_prolong(c, Li.pat->n, u, Li.T->agg.get(), e, out, g);
 }
 
+// Smoothed aggregation + Jacobi (extension): per-level weight
+// om_l = min(omega, (4/3) / g_l), g_l = max_i sum_j |a_ij| / |a_ii| — the
+// Galerkin operators of a smoothed P have lambda_max(D^-1 A_l) up to 4-15,
+// where the fixed weight diverges (oracle/amg_oracle.c sa_jacobi_omega).
+static void sa_jacobi_weights(Hier& h) {
+    if (h.prm.coarsening != AMGR_COARSENING_SMOOTHED || h.prm.smoother != AMGR_SMOOTHER_JACOBI) return;
+    Ctx& c = *h.ctx;
+    const size_t L = h.lv.size();
+    if (L < 2) return;
+    DevArray<unsigned long long> gb(static_cast<int64_t>(L), c.stream);
+    CK(cudaMemsetAsync(gb.get(), 0, sizeof(unsigned long long) * L, c.stream));
+    for (size_t l = 0; l + 1 < L; ++l) gershgorin_bound(c, h.lv[l].view(), h.lv[l].pat->diag.get(), gb.get() + l);
+    std::vector<unsigned long long> hb(L);
+    d2h(hb.data(), gb.get(), static_cast<int64_t>(L), c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    for (size_t l = 0; l + 1 < L; ++l) {
+        double g;
+        std::memcpy(&g, &hb[l], sizeof(double));
+        const double cap = (4.0 / 3.0) / g;
+        h.lv[l].om = cap < h.prm.omega ? cap : h.prm.omega;
+    }
+}
+
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans:
 // the Galerkin chain, then the per-level smoother rebuilds (main stream)
 // concurrently with the coarsest factorization (side stream).
@@ -358,6 +381,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     }
     join_side(c);
     c.cur_level = -1;
+    sa_jacobi_weights(h);
 }
 
 // Symbolic pass with frozen transfers (pattern change under partial reuse).
@@ -556,6 +580,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
         encode_columns(c, P.n, P.nnz, P.rp.get(), P.col.get(), P.cc);
     }
     clk.end(PH_GALERKIN);
+    sa_jacobi_weights(*h);
     clk.begin(PH_COARSE);
     coarse_factorize(*h, lu_status.get());
     clk.end(PH_COARSE);
@@ -717,6 +742,24 @@ void rebuild_values(Hier& h, const double* values, int location) {
 // prolongation x = u + P u_c (coalesced pass) -> post-smoothing sweeps.
 // One Chebyshev sweep (oracle smooth_cheb) on level i from x (zero when
 // from_zero) into *out; returns the buffer holding the result.
+// Chebyshev direction vectors of every smoothed level (allocated lazily by
+// the first sweep otherwise)
+static void ensure_cheb_work(Hier& h) {
+    if (h.prm.smoother != AMGR_SMOOTHER_CHEBYSHEV) return;
+    Ctx& c = *h.ctx;
+    Work& W = work(h);
+    const size_t L = h.lv.size();
+    if (W.d0.size() != L) {
+        W.d0.resize(L);
+        W.d1.resize(L);
+    }
+    for (size_t i = 0; i + 1 < L; ++i) {
+        const int64_t n = h.lv[i].pat->n;
+        if (W.d0[i].size() != n) W.d0[i].alloc(n, c.stream);
+        if (W.d1[i].size() != n) W.d1[i].alloc(n, c.stream);
+    }
+}
+
 static double* cheb_sweep(Hier& h, size_t i, const double* f, double* x, double* other, bool from_zero, Gate g) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
@@ -856,7 +899,8 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
     // one pre-sweep from zero: its iterate u0 = (om w) f is folded into the
     // top level's down pass and prolongation instead of being materialised
     const bool fold = pre == 1 && top > s && fold_premul() && !h.lv[s].T->smoothed;
-    if (pre >= 1 && !fold) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), om, W.u[s].get(), g);
+    auto oml = [&](size_t l) { return h.om_level(l); };
+    if (pre >= 1 && !fold) vc_premul(c, h.lv[s].pat->n, f, h.lv[s].w.get(), oml(s), W.u[s].get(), g);
     // down leg
     for (size_t i = s; i < top; ++i) {
         c.cur_level = static_cast<int>(i);
@@ -873,13 +917,13 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
             double* src = a;
             if (pre == 1) {
                 if (fold && i == s)
-                    vc_down_premul(c, A, fin[i], Li.w.get(), om, r, g);
+                    vc_down_premul(c, A, fin[i], Li.w.get(), oml(i), r, g);
                 else
                     vc_down(c, A, fin[i], a, r, g);
             } else {
                 double* dst = b;
                 for (int s = 1; s < pre; ++s) {
-                    vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+                    vc_smooth(c, A, fin[i], Li.w.get(), oml(i), src, dst, g);
                     std::swap(src, dst);
                 }
                 residual(c, A, fin[i], src, r, g);
@@ -887,7 +931,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
             cur[i] = src;
         }
         const bool next_smoothed = pre >= 1 && i + 2 < L;
-        restrict_level(c, Li, r, W.f[i + 1].get(), next_smoothed ? h.lv[i + 1].w.get() : nullptr, om,
+        restrict_level(c, Li, r, W.f[i + 1].get(), next_smoothed ? h.lv[i + 1].w.get() : nullptr, oml(i + 1),
                        next_smoothed ? W.u[i + 1].get() : nullptr, g);
     }
     TailDesc td;
@@ -935,7 +979,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
         double* b = (a == W.u[i].get()) ? W.t[i].get() : W.u[i].get();
         auto prolong = [&](double* dst) {
             if (fold && i == s)
-                vc_prolong_premul(c, A.n, fin[i], Li.w.get(), om, Li.T->agg.get(), ufinal[i + 1], dst, g);
+                vc_prolong_premul(c, A.n, fin[i], Li.w.get(), oml(i), Li.T->agg.get(), ufinal[i + 1], dst, g);
             else
                 prolong_level(c, Li, a, ufinal[i + 1], dst, g);
         };
@@ -950,7 +994,7 @@ void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g) {
         double* src = b;
         for (int k = 1; k <= post; ++k) {
             double* dst = (i == s && k == post) ? u : (src == b ? a : b);
-            vc_smooth(c, A, fin[i], Li.w.get(), om, src, dst, g);
+            vc_smooth(c, A, fin[i], Li.w.get(), oml(i), src, dst, g);
             src = dst;
         }
         ufinal[i] = src;
@@ -1022,6 +1066,9 @@ void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& 
     int64_t per_iter = 0;
     const bool use_graph = allow_graph && c.probe.family.empty() && !getenv("AMGR_NO_GRAPH");
     if (use_graph) {
+        // no stream-ordered allocation may happen inside the capture (it would
+        // become a graph-owned allocation that blocks relaunching the graph)
+        ensure_cheb_work(h);
         cudaGraph_t graph;
         const int64_t l0 = c.launches;
         CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));

@@ -20,7 +20,7 @@ struct AmgP {
     int coarsening = AMGR_COARSENING_PLAIN;
     double sa_omega = 2.0 / 3.0;
     int cheb_degree = 3, power_iters = 10;
-    double cheb_lower = 1.0 / 30.0, cheb_safety = 1.1;
+    double cheb_lower = 0.3, cheb_safety = 1.1;
     int coarse_solve = AMGR_COARSE_EXACT;
 };
 AmgP to_amgp(const amgr_amg_params* p);
@@ -79,6 +79,7 @@ struct Level {
     DevArray<double> cheb; // Chebyshev coefficients (extension): theta, c1/c2 per step, hi
     DevArray<double> pst;  // power-iteration state {yy, xx, lam}
     bool has_smoother = false;
+    double om = -1.0;  // per-level Jacobi weight of an SA hierarchy (sa_jacobi_weights); < 0: prm's
     std::shared_ptr<Transfer> T;   // null on the coarsest level
     std::shared_ptr<RapPlan> rap;  // null on the coarsest level
     CsrView view() const {
@@ -135,6 +136,7 @@ struct Hier {
     int64_t agg_rounds = 0;
 
     double om_eff() const { return prm.smoother == AMGR_SMOOTHER_SPAI0 ? 1.0 : prm.omega; }
+    double om_level(size_t l) const { return l < lv.size() && lv[l].om > 0.0 ? lv[l].om : om_eff(); }
 };
 
 std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p);

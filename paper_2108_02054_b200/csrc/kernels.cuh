@@ -139,6 +139,8 @@ void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x,
 // st = {yy, xx, lam} (lam = |y|/|x_prev|), x.x -> s.out (= st[1])
 void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s);
 void power_start(Ctx& c, int64_t n, double* x);
+// atomicMax of max_i sum_j |a_ij| / |a_ii| into *out (double bits; zero it first)
+void gershgorin_bound(Ctx& c, const CsrView& A, const int* dpos, unsigned long long* out);
 void power_norm(Ctx& c, int64_t n, const double* y, double* x, double* st, DotSink s);
 // coef[0] = theta, coef[2k-1], coef[2k] = c1, c2 of step k, coef[2*degree] = hi
 void cheb_coef(Ctx& c, const double* st, double safety, double lower, int degree, double* coef);

@@ -1289,6 +1289,25 @@ __global__ void __launch_bounds__(256) k_power_norm(int n, const double* __restr
     block_dots<1>(d, ds);
 }
 
+// Gershgorin bound of D^-1 A: g = max_i sum_j |a_ij| / |a_ii| (row sums in
+// column order; max is order-independent), as a non-negative double whose bit
+// pattern orders like the value (atomicMax on the bits)
+__global__ void k_gershgorin(CsrView A, const int* __restrict__ dpos, unsigned long long* out) {
+    double g = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < A.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) s = dadd(s, fabs(A.val[k]));
+        const double q = __ddiv_rn(s, fabs(A.val[dpos[i]]));
+        g = q > g ? q : g;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double h = __shfl_xor_sync(0xffffffffu, g, o);
+        g = h > g ? h : g;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(g)));
+}
+
 // power-iteration start vector: pseudo-random signs, x.x = n exactly
 // (oracle/amg_oracle.c power_start_sign, same hash)
 __global__ void k_power_start(int64_t n, double* x) {
@@ -1591,6 +1610,11 @@ void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x,
 
 void power_step(Ctx& c, const CsrView& A, const double* w, const double* x, double* y, DotSink s) {
     launch_rowpass(c, "power", spmv_bytes(A) + 8.0 * A.n, A, OpPower{x, w, y}, Gate{}, s, true);
+}
+void gershgorin_bound(Ctx& c, const CsrView& A, const int* dpos, unsigned long long* out) {
+    if (A.n == 0) return;
+    LAUNCH(c, "smoother", 12.0 * A.nnz + 8.0 * A.n, k_gershgorin, grid_for(A.n, 256, c.num_sms * 8), 256, 0, A, dpos,
+           out);
 }
 void power_start(Ctx& c, int64_t n, double* x) {
     LAUNCH(c, "power", 8.0 * n, k_power_start, grid_for(n, 256, c.num_sms * 16), 256, 0, n, x);

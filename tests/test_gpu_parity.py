@@ -516,3 +516,20 @@ def test_coded_columns_fallback_many_offsets(ctx):
 
     f = rng.uniform(-1, 1, n)
     np.testing.assert_array_equal(_bits(amg.vcycle(h, f)), _bits(O.vcycle(O.setup(A, O.params(coarse_enough=50)), f)))
+
+
+def test_chebyshev_solve_without_prior_vcycle(ctx):
+    """The first Chebyshev sweep used to allocate its direction vectors lazily;
+    when that happened inside the solver's CUDA-graph capture the allocation
+    became graph-owned and relaunching the graph failed (cudaGraphLaunch:
+    invalid argument).  A solve as the very first call must work."""
+    from oracle import oracle as O
+
+    g = 20
+    A = O.grid3d("convdiff", g, 4)
+    kw = dict(smoother="chebyshev")
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    fr = P.rhs(g ** 3)
+    _, st = amg.bicgstab(h, fr)
+    so = O.bicgstab(O.setup(A, O.params(**kw)), fr)
+    assert st.converged and so.converged and abs(st.iterations - so.iterations) <= 1

@@ -396,3 +396,21 @@ def test_smoothed_aggregation_omega0_equals_tentative():
     sa = O.setup(A, O.params(coarsening="smoothed"))
     s = O.cg(sa, P.rhs(256))
     assert s.converged
+
+
+def test_sa_jacobi_per_level_weight_keeps_cg_converging():
+    """C1 (shifted Laplacian, SA + Jacobi, CG, partial reuse): with the fixed
+    weight 0.72 the SA coarse levels (lambda_max(D^-1 A_l) up to 4-15) made
+    the V-cycle indefinite and CG stalled at max_iter from step 3 on; the
+    per-level weight min(omega, (4/3)/g_l) keeps every step converging."""
+    g, steps = 16, 10
+    f = P.rhs(g ** 3)
+    prm = O.params(coarsening="smoothed")
+    h = O.setup(P.grid3d_values("poisson", g, 0, steps), prm)
+    u = np.zeros(g ** 3)
+    for k in range(steps):
+        if k:
+            h = O.partial_update(h, P.grid3d_values("poisson", g, k, steps), prm)
+        s = O.cg(h, f, u)
+        assert s.converged and s.iterations <= 20, (k, s.iterations)
+        u = s.u
