@@ -3,6 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstdint>
 #include <memory>
 #include <sstream>
@@ -170,7 +174,15 @@ class DevArray {
         stream_ = s;
         n_ = n;
         // +8 elements of slack: TMA bulk copies read 16-byte-rounded ranges
-        if (n > 0) CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), sizeof(T) * static_cast<size_t>(n + 8), s));
+        if (n > 0) {
+            static const bool tr = std::getenv("AMGR_TRACE_ALLOC") != nullptr;
+            const auto t0 = std::chrono::steady_clock::now();
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), sizeof(T) * static_cast<size_t>(n + 8), s));
+            if (tr) {
+                const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                if (ms > 2.0) std::fprintf(stderr, "[amgr alloc] %.1f MB took %.1f ms\n", sizeof(T) * n / 1e6, ms);
+            }
+        }
     }
     void release() {
         if (p_) cudaFreeAsync(p_, stream_);

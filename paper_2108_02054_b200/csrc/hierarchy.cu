@@ -456,6 +456,34 @@ Work& work(Hier& h) {
     return *h.ws;
 }
 
+// Setup allocates and frees many large temporaries of varying sizes (sort
+// buffers, plans).  When no free block of the stream-ordered pool fits, the
+// pool maps new physical memory, which measured 0.1-0.5 s per GB-sized
+// request and made setup times swing 0.3 -> 1.4 s at 256^3.  One large
+// allocation up front (freed immediately; the context keeps the pool's
+// memory, release threshold = max) leaves a single mapped region that the
+// setup's temporaries are carved from.
+static void reserve_pool(Ctx& c, int64_t nnz) {
+    const char* e = std::getenv("AMGR_POOL_RESERVE_BYTES_PER_NNZ");
+    const double per = e ? std::atof(e) : 128.0;
+    const size_t want = static_cast<size_t>(per * static_cast<double>(nnz));
+    if (want == 0) return;
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetMemPool(&pool, c.device));
+    uint64_t reserved = 0;
+    CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    if (reserved >= want) return;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (want - reserved > free_b / 2) return;  // never take more than half of what is free
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, want - reserved, c.stream) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    CK(cudaFreeAsync(p, c.stream));
+}
+
 // ---- setup (hierarchy.cpp:45-105) ------------------------------------------------
 std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     if (A.nrows != A.ncols) invalid("setup: matrix is not square");
@@ -465,7 +493,9 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     h->prm = p;
     PhaseClock clk(c);
     const auto t_setup = std::chrono::steady_clock::now();
+    const bool trace = std::getenv("AMGR_TRACE_SETUP") != nullptr;
 
+    reserve_pool(c, A.nnz);
     Level L0;
     L0.pat = make_pattern(c, A);
     upload_values(c, L0.val, A.values, A.nnz, A.location);
@@ -491,6 +521,13 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             }
             GraphDev g;
             strength_graph(c, Av, cur.pat->diag.get(), p.eps * p.eps, g);
+            if (trace) {
+                CK(cudaStreamSynchronize(c.stream));
+                std::fprintf(stderr, "[amgr setup] level %zu: strength graph (%lld edges) t=%.1f ms\n", l,
+                             static_cast<long long>(g.m),
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup)
+                                 .count());
+            }
             int64_t rounds = 0;
             nc = aggregate(c, g, T->agg, &rounds);
             h->agg_rounds += rounds;
@@ -499,7 +536,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             if (nc < Av.n) members(c, Av.n, nc, T->agg.get(), T->mptr, T->midx);
         }
         clk.end(PH_TRANSFER);
-        if (std::getenv("AMGR_TRACE_SETUP"))
+        if (trace)
             std::fprintf(stderr, "[amgr setup] level %zu: n=%lld nnz=%lld -> nc=%lld (agg rounds %lld) t=%.1f ms\n", l,
                          static_cast<long long>(Av.n), static_cast<long long>(Av.nnz), static_cast<long long>(nc),
                          static_cast<long long>(h->agg_rounds),
@@ -569,6 +606,11 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
             cur.rap = plan;
         }
         clk.end(PH_GALERKIN);
+        if (trace) {
+            CK(cudaStreamSynchronize(c.stream));
+            std::fprintf(stderr, "[amgr setup] level %zu: smoother + Galerkin done t=%.1f ms\n", l,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count());
+        }
         cur.T = T;
         h->lv.push_back(std::move(next));
     }
