@@ -470,14 +470,17 @@ static void reserve_pool(Ctx& c, int64_t nnz) {
     if (want == 0) return;
     cudaMemPool_t pool;
     CK(cudaDeviceGetMemPool(&pool, c.device));
-    uint64_t reserved = 0;
+    // the pool's idle part (reserved - used) must hold the setup's temporaries;
+    // a live hierarchy (e.g. the previous step's under no-reuse) is "used"
+    uint64_t reserved = 0, used = 0;
     CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-    if (reserved >= want) return;
+    CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    if (reserved - used >= want) return;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    if (want - reserved > free_b / 2) return;  // never take more than half of what is free
+    if (want > free_b / 2) return;  // never take more than half of what is free
     void* p = nullptr;
-    if (cudaMallocAsync(&p, want - reserved, c.stream) != cudaSuccess) {
+    if (cudaMallocAsync(&p, want, c.stream) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
