@@ -202,6 +202,69 @@ __global__ void __launch_bounds__(SB) k_agg_round(const int* __restrict__ nact, 
     if (threadIdx.x == 0 && s_cnt) atomicAdd(undecided, s_cnt);
 }
 
+// Decision of one undecided node from the current states (0: not yet
+// determinable).  Same rule as k_agg_round.
+__device__ __forceinline__ int agg_decide(int i, const int* __restrict__ ptr, const int* __restrict__ adj,
+                                          const int* state) {
+    const int p0 = ptr[i], p1 = ptr[i + 1];
+    if (p0 == p1) return 2;  // isolated: never a pass-1 root
+    bool blocked = false;
+    int p = p0;
+    for (; p < p1; ++p) {
+        const int j = adj[p];
+        if (j > i) break;
+        const int s = ld_state(state, j);
+        if (s == 1) return 2;
+        if (s == 0) blocked = true;
+    }
+    if (blocked) return 0;
+    bool unknown = false;
+    for (int q = p; q < p1; ++q) {
+        const int j = adj[q];
+        bool taken = false, junk = false;
+        for (int t = ptr[j]; t < ptr[j + 1]; ++t) {
+            const int x = adj[t];
+            if (x >= i) break;
+            const int s = ld_state(state, x);
+            if (s == 1) {
+                taken = true;
+                break;
+            }
+            if (s == 0) junk = true;
+        }
+        if (!taken && !junk) return 1;
+        if (!taken) unknown = true;
+    }
+    return unknown ? 0 : 2;
+}
+
+// Persistent replay: every thread walks its nodes i = t, t+T, ... in
+// ascending order and waits on each until it is determinable.  The lowest
+// undecided node of the graph only depends on decided nodes, and its owner
+// is waiting on exactly that node (its earlier nodes are lower, hence
+// decided), so the sweep always progresses provided all threads are resident
+// (cooperative launch).  Decisions are final, so the states reached are the
+// rounds' fixed point; the chain of dependent decisions costs one L2 round
+// trip per link instead of one kernel launch per round.
+__global__ void k_agg_persistent(int n, const int* __restrict__ ptr, const int* __restrict__ adj, int* state,
+                                 int* stuck) {
+    const int T = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
+        int d;
+        unsigned spins = 0;
+        while ((d = agg_decide(i, ptr, adj, state)) == 0) {
+            // the chain can be ~3g links long; a node that stays undetermined
+            // for ~seconds means a broken invariant: report instead of hanging
+            if (++spins > (1u << 24) || *reinterpret_cast<volatile int*>(stuck)) {
+                atomicExch(stuck, 1);
+                return;
+            }
+            __nanosleep(64);
+        }
+        reinterpret_cast<volatile int*>(state)[i] = d;
+    }
+}
+
 __global__ void k_iota_list(int n, int* act, int* nact) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) act[i] = i;
     if (blockIdx.x == 0 && threadIdx.x == 0) *nact = n;
@@ -364,8 +427,30 @@ int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds
     int *act = list0.get(), *act2 = list1.get(), *nact = nl.get(), *nact2 = nl.get() + 1;
     int64_t r = 0;
     const unsigned grid = grid_for(n, SB, c.num_sms * 8);
-    LAUNCH(c, "setup", 0.0, k_iota_list, grid, SB, 0, static_cast<int>(n), act, nact);
-    for (;;) {
+    const char* pe = std::getenv("AMGR_AGG_PERSISTENT");
+    const bool persistent = !(pe && pe[0] == '0');
+    if (persistent) {
+        static int per_sm = -1;
+        if (per_sm < 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_persistent, SB, 0));
+        int64_t blocks = (n + SB - 1) / SB;
+        const int64_t cap = static_cast<int64_t>(c.num_sms) * per_sm;
+        if (blocks > cap) blocks = cap;
+        int nn = static_cast<int>(n);
+        const int* pp = g.ptr.get();
+        const int* aa = g.adj.get();
+        int* ss = state.get();
+        DevArray<int> stuck(1, c.stream);
+        CK(cudaMemsetAsync(stuck.get(), 0, sizeof(int), c.stream));
+        int* st = stuck.get();
+        void* args[] = {&nn, &pp, &aa, &ss, &st};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_agg_persistent),
+                                       dim3(static_cast<unsigned>(blocks)), dim3(SB), args, 0, c.stream));
+        ++c.launches;
+        if (d2h_scalar(stuck.get(), c.stream)) fail(AMGR_E_RUNTIME, "aggregate: persistent replay made no progress");
+        r = 1;
+    }
+    if (!persistent) LAUNCH(c, "setup", 0.0, k_iota_list, grid, SB, 0, static_cast<int>(n), act, nact);
+    while (!persistent) {
         CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int) * BATCH, c.stream));
         for (int k = 0; k < BATCH; ++k)
             LAUNCH(c, "setup", 0.0, k_agg_round, grid, SB, 0, nact, act, g.ptr.get(), g.adj.get(), state.get(),
