@@ -12,6 +12,7 @@
 //  * jacobi/spai0 rebuild, restriction, dense LU factor/solve.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -25,7 +26,8 @@ namespace {
 
 constexpr int RP_WARPS = 4;                 // warps per block
 constexpr int RP_BLOCK = RP_WARPS * 32;
-constexpr int RP_CH = 256;                  // entries per TMA chunk (multiple of 4)
+constexpr int RP_CH = 256;                  // entries per TMA chunk (multiple of 16)
+constexpr int RP_CH_W12 = 384;              // chunk of the 8..12-entries-per-row variant
 constexpr int RP_BATCH = 8;                 // operand gathers in flight per thread
 constexpr int RP_BLOCKS_PER_SM = 8;         // persistent grid: 32 warps per SM
 
@@ -471,6 +473,22 @@ struct OpChebStep {
 int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
 
+// resident blocks per SM of the 384-entry-chunk variant (persistent grid)
+template <class Op>
+int rp_blocks_w12() {
+    static int blocks = -1;
+    if (blocks < 0) {
+        constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * RP_CH_W12 * 12 + RP_WARPS * 2 * sizeof(uint64_t);
+        CK(cudaFuncSetAttribute(k_rowpass<Op, RP_CH_W12, 12, int>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_rowpass<Op, RP_CH_W12, 12, int>, RP_BLOCK,
+                                                         smem));
+        if (blocks < 1) blocks = 1;
+        if (blocks > RP_BLOCKS_PER_SM) blocks = RP_BLOCKS_PER_SM;
+    }
+    return blocks;
+}
+
 // operand gathers per stored entry of a row-pass Op (default 1)
 template <class Op, class = void>
 struct gathers_of {
@@ -513,7 +531,16 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
         launch_tma<Op, RP_CH, 8, uint16_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.cmode == 2 && !(gathers_of<Op>::v > 1))
         launch_tma<Op, RP_CH, 12, uint16_t>(c, fam, bytes, A, op, g, s, grid);
-    else if (A.nnz > 12 * A.n)
+    else if (A.nnz > 8 * A.n && A.nnz <= 12 * A.n && !fixed_grid) {
+        // 8..12 entries per row (C3 level 1): a 32-row group (~350 entries)
+        // fits one 384-entry chunk, so lanes do not split their rows across
+        // chunk boundaries; 6 resident blocks per SM instead of 8.
+        // Level-1 passes 238/251 -> 211/228 us at 256^3 (512: no gain; the
+        // > 12 nnz/row levels were slower with larger chunks).
+        launch_tma<Op, RP_CH_W12, 12, int>(c, fam, bytes, A, op, g, s,
+                                            static_cast<unsigned>(std::min<int64_t>(
+                                                want, static_cast<int64_t>(c.num_sms) * rp_blocks_w12<Op>())));
+    } else if (A.nnz > 12 * A.n)
         launch_tma<Op, RP_CH, 8, int>(c, fam, bytes, A, op, g, s, grid);
     else if (A.nnz > 8 * A.n)
         launch_tma<Op, RP_CH, 12, int>(c, fam, bytes, A, op, g, s, grid);
