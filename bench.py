@@ -608,6 +608,10 @@ def main():
 
         strategies = {}
         seq = R.DeviceGridSequence(a.problem, g, 4, ctx=ctx)
+        # warm-up (untimed): a 2-step no-reuse run grows the stream-ordered
+        # pool to the setup's peak once, as the main loop's warm-up steps do
+        R.run_sequence(R.DeviceGridSequence(a.problem, g, 2, ctx=ctx), R.StrategyConfig(R.StrategyKind.none), prm,
+                       sp, ctx=ctx, keep_solutions=False)
         for kind in ("none", "full", "partial"):
             res = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind[kind]), prm, sp, ctx=ctx, keep_solutions=False)
             st = res.report.steps[1:]  # step 0 is the initial full setup for every strategy

@@ -465,7 +465,7 @@ Work& work(Hier& h) {
 // setup's temporaries are carved from.
 static void reserve_pool(Ctx& c, int64_t nnz) {
     const char* e = std::getenv("AMGR_POOL_RESERVE_BYTES_PER_NNZ");
-    const double per = e ? std::atof(e) : 128.0;
+    const double per = e ? std::atof(e) : 96.0;  // setup peak measured 82 B/nnz at 256^3 (AMGR_TRACE_SETUP)
     const size_t want = static_cast<size_t>(per * static_cast<double>(nnz));
     if (want == 0) return;
     cudaMemPool_t pool;
@@ -499,6 +499,14 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     const bool trace = std::getenv("AMGR_TRACE_SETUP") != nullptr;
 
     reserve_pool(c, A.nnz);
+    uint64_t used0 = 0;
+    if (trace) {
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetMemPool(&pool, c.device));
+        CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used0));
+        uint64_t zero = 0;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero));
+    }
     Level L0;
     L0.pat = make_pattern(c, A);
     upload_values(c, L0.val, A.values, A.nnz, A.location);
@@ -633,6 +641,16 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     if (st >= 0) throw_lu(st);
     h->tm = clk.collect();
     work(*h);
+    if (trace) {
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetMemPool(&pool, c.device));
+        uint64_t high = 0, now = 0;
+        CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high));
+        CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &now));
+        std::fprintf(stderr, "[amgr setup] pool: peak +%.2f GB during setup (%.1f B/nnz), hierarchy +%.2f GB\n",
+                     (high - used0) / 1e9, static_cast<double>(high - used0) / static_cast<double>(A.nnz),
+                     (now - used0) / 1e9);
+    }
     return h;
 }
 
