@@ -1134,6 +1134,7 @@ void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& 
         ensure_cheb_work(h);
         cudaGraph_t graph;
         const int64_t l0 = c.launches;
+        const auto t0 = std::chrono::steady_clock::now();
         CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
         enqueue_iter();
         CK(cudaStreamEndCapture(c.stream, &graph));
@@ -1141,6 +1142,10 @@ void run_iterations(Hier& h, const std::function<void()>& enqueue_iter, KState& 
         c.launches = l0;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         CK(cudaGraphDestroy(graph));
+        if (std::getenv("AMGR_TRACE_SOLVE"))
+            std::fprintf(stderr, "[amgr solve] capture + instantiate of one iteration (%lld kernels): %.2f ms\n",
+                         static_cast<long long>(per_iter),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
     auto launch = [&](int slot) {
         if (use_graph) {
