@@ -31,6 +31,34 @@ constexpr int RP_CH_W12 = 384;              // chunk of the 8..12-entries-per-ro
 constexpr int RP_BATCH = 8;                 // operand gathers in flight per thread
 constexpr int RP_BLOCKS_PER_SM = 8;         // persistent grid: 32 warps per SM
 
+// operand gathers per stored entry of a row-pass Op (default 1)
+template <class Op, class = void>
+struct gathers_of {
+    static constexpr int v = 1;
+};
+template <class Op>
+struct gathers_of<Op, std::void_t<decltype(Op::GATHERS)>> {
+    static constexpr int v = Op::GATHERS;
+};
+
+// x_j of a batch of columns.  Ops with several operands per entry (GATHERS
+// > 1) split x into gather + combine so every load of the batch is issued
+// before the first arithmetic use: left fused, ptxas interleaved them and
+// kept only ~2 entries' loads in flight (coded level-0 OpDownP 346 -> 275 us).
+template <int NB, class Op>
+__device__ __forceinline__ void gather_batch(const Op& op, const int (&cj)[NB], double (&xv)[NB]) {
+    if constexpr (gathers_of<Op>::v > 1) {
+        typename Op::G gv[NB];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) gv[t] = op.gather(cj[t]);
+#pragma unroll
+        for (int t = 0; t < NB; ++t) xv[t] = op.combine(gv[t]);
+    } else {
+#pragma unroll
+        for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
+    }
+}
+
 // ---- TMA 1-D bulk copy + mbarrier helpers (sm_90+/sm_100a PTX) ----------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -200,16 +228,14 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
                             int cj[NB];
 #pragma unroll
                             for (int t = 0; t < NB; ++t) cj[t] = colof(row, s_col[w][st][k + (t < cnt ? t : 0)]);
-#pragma unroll
-                            for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
+                            gather_batch<NB>(op, cj, xv);
                         } else if constexpr (CODED) {
                             // decode the batch first (unpredicated shared-memory reads),
-                            // then the predicated gathers
+                            // then the gathers (all issued before the first use)
                             int cj[NB];
 #pragma unroll
                             for (int t = 0; t < NB; ++t) cj[t] = colof(row, s_col[w][st][k + (t < cnt ? t : 0)]);
-#pragma unroll
-                            for (int t = 0; t < NB; ++t) xv[t] = op.x(cj[t]);
+                            gather_batch<NB>(op, cj, xv);
                         } else {
 #pragma unroll
                             for (int t = 0; t < NB; ++t) xv[t] = t < cnt ? op.x(s_col[w][st][k + t]) : 0.0;
@@ -312,7 +338,12 @@ struct OpDownP {
     const double* w;
     double om;
     double* r;
-    __device__ double x(int j) const { return dadd(0.0, dmul(dmul(om, __ldg(w + j)), __ldg(f + j))); }
+    struct G {
+        double w, f;
+    };
+    __device__ G gather(int j) const { return {__ldg(w + j), __ldg(f + j)}; }
+    __device__ double combine(const G& g) const { return dadd(0.0, dmul(dmul(om, g.w), g.f)); }
+    __device__ double x(int j) const { return combine(gather(j)); }
     __device__ Row load(int i) const { return {__ldg(f + i)}; }
     __device__ void finish(int i, double s, const Row& q, double*) const { r[i] = dsub(q.a, s); }
 };
@@ -460,7 +491,12 @@ struct OpChebStep {
     int k;
     double* xout;
     double* dout;
-    __device__ double x(int j) const { return dadd(__ldg(xv + j), __ldg(dv + j)); }
+    struct G {
+        double x, d;
+    };
+    __device__ G gather(int j) const { return {__ldg(xv + j), __ldg(dv + j)}; }
+    __device__ double combine(const G& g) const { return dadd(g.x, g.d); }
+    __device__ double x(int j) const { return combine(gather(j)); }
     __device__ Row load(int i) const { return {__ldg(f + i), __ldg(w + i), __ldg(xv + i), __ldg(dv + i)}; }
     __device__ void finish(int i, double s, const Row& q, double*) const {
         const double xn = dadd(q.x, q.d);
@@ -489,15 +525,6 @@ int rp_blocks_w12() {
     return blocks;
 }
 
-// operand gathers per stored entry of a row-pass Op (default 1)
-template <class Op, class = void>
-struct gathers_of {
-    static constexpr int v = 1;
-};
-template <class Op>
-struct gathers_of<Op, std::void_t<decltype(Op::GATHERS)>> {
-    static constexpr int v = Op::GATHERS;
-};
 
 template <class Op, int CH, int GATHER, class CT>
 void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
@@ -522,14 +549,12 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
     if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
-    // coded columns: uint8 only on <= 8 nnz/row, uint16 only above (encode_columns).
-    // Ops that gather two operands per entry (OpDownP) read the raw columns:
-    // with the extra dictionary lookup per entry they ran 9% slower coded.
-    if (A.cmode == 1 && !(gathers_of<Op>::v > 1))
+    // coded columns: uint8 only on <= 8 nnz/row, uint16 only above (encode_columns)
+    if (A.cmode == 1)
         launch_tma<Op, RP_CH, 0, uint8_t>(c, fam, bytes, A, op, g, s, grid);
-    else if (A.cmode == 2 && !(gathers_of<Op>::v > 1) && A.nnz > 12 * A.n)
+    else if (A.cmode == 2 && A.nnz > 12 * A.n)
         launch_tma<Op, RP_CH, 8, uint16_t>(c, fam, bytes, A, op, g, s, grid);
-    else if (A.cmode == 2 && !(gathers_of<Op>::v > 1))
+    else if (A.cmode == 2)
         launch_tma<Op, RP_CH, 12, uint16_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.nnz > 8 * A.n && A.nnz <= 12 * A.n && !fixed_grid) {
         // 8..12 entries per row (C3 level 1): a 32-row group (~350 entries)
@@ -1472,8 +1497,7 @@ void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double*
     launch_rowpass(c, "prolong", bytes, P, OpProlongG{e, u, out}, g, {}, false);
 }
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
-    // OpDownP always reads int32 columns (gathers_of<OpDownP> = 2, launch_rowpass)
-    const double bytes = 12.0 * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDownP{f, w, om, r}, g, {}, false);
 }
 void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, const int* agg,
@@ -1663,9 +1687,7 @@ void cheb_zero(Ctx& c, int64_t n, const double* f, const double* w, const double
 }
 void cheb_step(Ctx& c, const CsrView& A, const double* f, const double* w, const double* x, const double* d,
                const double* coef, int k, double* xout, double* dout, Gate g) {
-    // OpChebStep reads int32 columns (two gathers per entry, launch_rowpass)
-    const double raw = 12.0 * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
-    launch_rowpass(c, "cheb", raw + 40.0 * A.n, A, OpChebStep{f, w, x, d, coef, k, xout, dout}, g, {},
+    launch_rowpass(c, "cheb", spmv_bytes(A) + 40.0 * A.n, A, OpChebStep{f, w, x, d, coef, k, xout, dout}, g, {},
                    false);
 }
 void axpy1(Ctx& c, int64_t n, double* x, const double* d, Gate g) {
