@@ -510,14 +510,15 @@ int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 
 
 // resident blocks per SM of the 384-entry-chunk variant (persistent grid)
-template <class Op>
+template <class Op, class CT = int>
 int rp_blocks_w12() {
     static int blocks = -1;
     if (blocks < 0) {
-        constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * RP_CH_W12 * 12 + RP_WARPS * 2 * sizeof(uint64_t);
-        CK(cudaFuncSetAttribute(k_rowpass<Op, RP_CH_W12, 12, int>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        constexpr size_t smem =
+            static_cast<size_t>(RP_WARPS) * 2 * RP_CH_W12 * (8 + sizeof(CT)) + RP_WARPS * 2 * sizeof(uint64_t);
+        CK(cudaFuncSetAttribute(k_rowpass<Op, RP_CH_W12, 12, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_rowpass<Op, RP_CH_W12, 12, int>, RP_BLOCK,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_rowpass<Op, RP_CH_W12, 12, CT>, RP_BLOCK,
                                                          smem));
         if (blocks < 1) blocks = 1;
         if (blocks > RP_BLOCKS_PER_SM) blocks = RP_BLOCKS_PER_SM;
@@ -554,6 +555,11 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
         launch_tma<Op, RP_CH, 0, uint8_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.cmode == 2 && A.nnz > 12 * A.n)
         launch_tma<Op, RP_CH, 8, uint16_t>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.cmode == 2 && !fixed_grid)
+        launch_tma<Op, RP_CH_W12, 12, uint16_t>(
+            c, fam, bytes, A, op, g, s,
+            static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) *
+                                                              rp_blocks_w12<Op, uint16_t>())));
     else if (A.cmode == 2)
         launch_tma<Op, RP_CH, 12, uint16_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.nnz > 8 * A.n && A.nnz <= 12 * A.n && !fixed_grid) {

@@ -815,17 +815,17 @@ __global__ void k_encode(int64_t n, const int* __restrict__ rp, const int* __res
 
 void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out) {
     out = ColCode{};
-    // AMGR_COLCODE: 0 = off, 16 = also uint16 codes on the wider levels
-    // (measured slower: level-1 smoothing 255 -> 268 us at 256^3, the
-    // dictionary lookup goes through L1), default = uint8 codes only
+    // Default: uint8 codes on <= 8 entries/row (C3 level 0), uint16 codes on
+    // 8..12 entries/row (level 1, read with 384-entry chunks: 211/227 ->
+    // 202/214 us at 256^3).  AMGR_COLCODE=16 also codes the > 12 entries/row
+    // levels (measured slower: their dictionary reads through L1 are not
+    // hidden), AMGR_COLCODE=0 disables coding.
     const char* e = std::getenv("AMGR_COLCODE");
     if (e && std::strcmp(e, "0") == 0) return;
     const bool wide_ok = e && std::strcmp(e, "16") == 0;
     if (nnz <= 0 || n <= 0) return;
-    // 1-byte codes only where the row pass gathers in batches of 8 (<= 8 nnz/row),
-    // 2-byte codes for the wider rows: two code widths per gather variant
     const bool narrow = nnz <= 8 * n;
-    if (!narrow && !wide_ok) return;
+    if (nnz > 12 * n && !wide_ok) return;
     const int limit = narrow ? 256 : 65536;
     DevArray<uint32_t> k0(nnz, c.stream), k1(nnz, c.stream);
     const unsigned grid = grid_for(n, SB, c.num_sms * 16);

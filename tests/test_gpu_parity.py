@@ -474,10 +474,13 @@ def test_coded_columns_match_raw_columns(ctx, kind, g, monkeypatch):
 
     A = P.grid3d_values(kind, g, 9)
     n = g ** 3
-    h = amg.setup(A, ctx=ctx)  # default: uint8 codes on the 7-point level only
+    h = amg.setup(A, ctx=ctx)  # default: uint8 on the 7-point level, uint16 on 8..12 entries/row
     lay = [h.level_layout(l) for l in range(h.num_levels())]
     assert lay[0] == {"col_bytes": 1, "ndict": 7}
-    assert all(x["col_bytes"] == 4 for x in lay[1:])
+    for l in range(1, h.num_levels() - 1):
+        d = h.level_dims(l)
+        mid = 8 * d["nrows"] < d["nnz"] <= 12 * d["nrows"]
+        assert lay[l]["col_bytes"] == (2 if mid else 4), (l, d, lay[l])
     monkeypatch.setenv("AMGR_COLCODE", "16")
     hw = amg.setup(A, ctx=ctx)
     assert all(hw.level_layout(l)["col_bytes"] == 2 for l in range(1, hw.num_levels() - 1))
