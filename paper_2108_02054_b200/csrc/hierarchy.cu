@@ -465,8 +465,12 @@ Work& work(Hier& h) {
 // setup's temporaries are carved from.
 static void reserve_pool(Ctx& c, int64_t nnz) {
     const char* e = std::getenv("AMGR_POOL_RESERVE_BYTES_PER_NNZ");
-    const double per = e ? std::atof(e) : 96.0;  // setup peak measured 82 B/nnz at 256^3 (AMGR_TRACE_SETUP)
-    const size_t want = static_cast<size_t>(per * static_cast<double>(nnz));
+    // setup peak measured 82 B/nnz at 256^3 (AMGR_TRACE_SETUP), the hierarchy
+    // itself 57 B/nnz; 256 B/nnz leaves room for a no-reuse step's new setup
+    // while the previous hierarchy is alive (with 96 B/nnz the bench's
+    // no-reuse steps still hit 0.2-2 s pool-growth stalls)
+    const double per = e ? std::atof(e) : 256.0;
+    size_t want = static_cast<size_t>(per * static_cast<double>(nnz));
     if (want == 0) return;
     cudaMemPool_t pool;
     CK(cudaDeviceGetMemPool(&pool, c.device));
@@ -478,7 +482,8 @@ static void reserve_pool(Ctx& c, int64_t nnz) {
     if (reserved - used >= want) return;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    if (want > free_b / 2) return;  // never take more than half of what is free
+    if (want > free_b / 2) want = free_b / 2;  // never take more than half of what is free
+    if (reserved - used >= want) return;
     void* p = nullptr;
     if (cudaMallocAsync(&p, want, c.stream) != cudaSuccess) {
         cudaGetLastError();
