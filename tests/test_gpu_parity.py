@@ -474,6 +474,7 @@ def test_coded_columns_match_raw_columns(ctx, kind, g, monkeypatch):
 
     A = P.grid3d_values(kind, g, 9)
     n = g ** 3
+    monkeypatch.delenv("AMGR_COLCODE", raising=False)
     h = amg.setup(A, ctx=ctx)  # default: uint8 on the 7-point level, uint16 on 8..12 entries/row
     lay = [h.level_layout(l) for l in range(h.num_levels())]
     assert lay[0] == {"col_bytes": 1, "ndict": 7}
