@@ -21,7 +21,7 @@ for _ in range(3):
     amg.vcycle_device(h, fptr, u.data_ptr())
 ctx.synchronize()
 out = []
-for l in range(min(h.num_levels() - 1, 6)):
+for l in range(min(h.num_levels() - 1, int(os.environ.get("LEVELS", "6")))):
     row = [l, h.level_layout(l)["col_bytes"]]
     for fam in (f"vcycle_down@{l}", f"vcycle_smooth@{l}"):
         ctx.probe(fam)
