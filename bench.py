@@ -204,8 +204,10 @@ def run_reference_arm(a):
     out = {"metric": METRIC, "value": r["value"], "unit": "ms/step", "impl": "reference", "n_gpus": a.gpus,
            "steps": r["steps"], "warmup": 0, "ms_per_step": r["value"], "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"C3 dam-break {g}^3 partial reuse", "problem": a.problem, "grid": g,
-                      "reuse": "partial"},
+           "config": {"workload": f"C3 dam-break {g}^3, partial reuse (BASELINE.json configs[2])",
+                      "problem": a.problem, "grid": g, "n": g ** 3, "nnz": 7 * g ** 3 - 6 * g ** 2,
+                      "sequence_steps": a.nsteps, "reuse": "partial", "smoother": "jacobi",
+                      "parallelism": "reference CPU path, 1 host thread"},
            "rebuild_ms_per_step": r["rebuild_ms"], "solve_ms_per_step": r["per_iteration_ms"] * iters,
            "cpu_baseline": {"value": r["value"], "unit": "ms/step", "cores": cores, "kind": "reference",
                             "sample": sample},
