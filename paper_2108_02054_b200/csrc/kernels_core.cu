@@ -512,17 +512,16 @@ int persistent_grid(const Ctx& c) { return c.num_sms * RP_BLOCKS_PER_SM; }
 // resident blocks per SM of the 384-entry-chunk variant (persistent grid)
 template <class Op, class CT = int>
 int rp_blocks_w12() {
-    static int blocks = -1;
-    if (blocks < 0) {
+    // function-local static: initialised once, thread-safe (one context per host thread is allowed)
+    static const int blocks = [] {
         constexpr size_t smem =
             static_cast<size_t>(RP_WARPS) * 2 * RP_CH_W12 * (8 + sizeof(CT)) + RP_WARPS * 2 * sizeof(uint64_t);
         CK(cudaFuncSetAttribute(k_rowpass<Op, RP_CH_W12, 12, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_rowpass<Op, RP_CH_W12, 12, CT>, RP_BLOCK,
-                                                         smem));
-        if (blocks < 1) blocks = 1;
-        if (blocks > RP_BLOCKS_PER_SM) blocks = RP_BLOCKS_PER_SM;
-    }
+        int b = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_rowpass<Op, RP_CH_W12, 12, CT>, RP_BLOCK, smem));
+        return b < 1 ? 1 : (b > RP_BLOCKS_PER_SM ? RP_BLOCKS_PER_SM : b);
+    }();
     return blocks;
 }
 
@@ -532,12 +531,12 @@ void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const O
                 unsigned grid) {
     constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * CH * (8 + sizeof(CT)) +
                             RP_WARPS * 2 * sizeof(uint64_t) + (sizeof(CT) == 1 ? 256 * sizeof(int) : 0);
-    static bool configured = false;
-    if (!configured) {
+    static const bool configured = [] {
         CK(cudaFuncSetAttribute(k_rowpass<Op, CH, GATHER, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, GATHER, CT>), grid, RP_BLOCK, smem, A, op, g, s);
 }
 
@@ -831,11 +830,11 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
 template <int PER, int B>
 void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
                     double* ac, int cstage, size_t sm) {
-    static bool attr = false;  // opt in once (dynamic + static may exceed 48 KB)
-    if (!attr) {
+    static const bool attr = [] {  // opt in once (dynamic + static may exceed 48 KB)
         CK(cudaFuncSetAttribute(k_rap_tma<PER, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     int res = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_rap_tma<PER, B>, RT_BLOCK, sm));
     const int64_t chunks = (nnz_c + RT_CH - 1) / RT_CH;
@@ -1582,8 +1581,11 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr,
         }
     }
     // persistent grid: exactly the resident blocks, so the sweep stays in order
-    static int resident = 0;
-    if (!resident) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_rap, RAP_BLOCK, 0));
+    static const int resident = [] {
+        int r = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_rap, RAP_BLOCK, 0));
+        return r;
+    }();
     const int64_t chunks = (nnz_c + RAP_BLOCK * RAP_ILP - 1) / (RAP_BLOCK * RAP_ILP);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * resident));
     LAUNCH(c, "rap", bytes, k_rap, grid, RAP_BLOCK, 0, nnz_c, cptr, contrib, af, ac);
@@ -1611,12 +1613,12 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
         const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
         // always opt in: dynamic + static shared memory above 48 KB needs the
         // attribute even when the dynamic part alone is below it (n = 72..78)
-        static bool attr = false;
-        if (!attr) {
+        static const bool attr = [] {
             CK(cudaFuncSetAttribute(k_dense_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sizeof(double) * DR_MAXN * DR_MAXN)));
-            attr = true;
-        }
+            return true;
+        }();
+        (void)attr;
         LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status);
         return;
     }
@@ -1633,11 +1635,11 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     const size_t full = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + 3 * n);
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);
-    static bool attr = false;  // opt in once (dynamic + static may exceed 48 KB)
-    if (!attr) {
+    static const bool attr = [] {  // opt in once (dynamic + static may exceed 48 KB)
         CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
 }
 
@@ -1657,11 +1659,11 @@ void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* 
 void inv_apply(Ctx& c, int64_t n, const double* inv, const double* b, double* x, Gate g) {
     if (n == 0) return;
     const size_t sm = sizeof(double) * static_cast<size_t>(n);
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {
         CK(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     LAUNCH_PDL(c, "coarse_solve", 0.0, k_inv_apply, 1, 1024, sm, static_cast<int>(n), inv, b, x, g);
 }
 

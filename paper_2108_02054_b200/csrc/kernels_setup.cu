@@ -430,8 +430,11 @@ int64_t aggregate(Ctx& c, const GraphDev& g, DevArray<int>& agg, int64_t* rounds
     const char* pe = std::getenv("AMGR_AGG_PERSISTENT");
     const bool persistent = !(pe && pe[0] == '0');
     if (persistent) {
-        static int per_sm = -1;
-        if (per_sm < 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_persistent, SB, 0));
+        static const int per_sm = [] {
+            int b = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_agg_persistent, SB, 0));
+            return b;
+        }();
         int64_t blocks = (n + SB - 1) / SB;
         const int64_t cap = static_cast<int64_t>(c.num_sms) * per_sm;
         if (blocks > cap) blocks = cap;

@@ -121,8 +121,7 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_up(TailDesc d, double om, Gat
 }
 
 template <class K>
-void launch_coop(Ctx& c, const char* fam, K kernel, int& per_sm, const TailDesc& d, double om, Gate g) {
-    if (per_sm < 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TL_BLOCK, 0));
+void launch_coop(Ctx& c, const char* fam, K kernel, const TailDesc& d, double om, Gate g) {
     // enough threads for the largest tail level, at most one full wave
     int64_t nmax = 0;
     for (int l = 0; l < d.count; ++l) nmax = d.lv[l].n > nmax ? d.lv[l].n : nmax;
@@ -144,13 +143,11 @@ void launch_coop(Ctx& c, const char* fam, K kernel, int& per_sm, const TailDesc&
 }  // namespace
 
 void tail_down(Ctx& c, const TailDesc& d, double om, Gate g) {
-    static int per_sm = -1;
-    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_down, per_sm, d, om, g);
+    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_down, d, om, g);
 }
 
 void tail_up(Ctx& c, const TailDesc& d, double om, Gate g) {
-    static int per_sm = -1;
-    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_up, per_sm, d, om, g);
+    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_up, d, om, g);
 }
 
 }  // namespace amgr
