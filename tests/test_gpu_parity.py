@@ -537,3 +537,36 @@ def test_chebyshev_solve_without_prior_vcycle(ctx):
     _, st = amg.bicgstab(h, fr)
     so = O.bicgstab(O.setup(A, O.params(**kw)), fr)
     assert st.converged and so.converged and abs(st.iterations - so.iterations) <= 1
+
+
+def test_pipelining_entry_points_validate_arguments(ctx):
+    """amgr_stage_rhs / amgr_download_async / STAGED solve argument checks
+    (the reference-style error texts come back through amgr_last_error)."""
+    import ctypes
+
+    import torch
+
+    L = amg.lib()
+    A = P.grid3d_values("poisson", 8, 0)
+    h = amg.setup(A, ctx=ctx)
+    n = 8 ** 3
+    u = torch.zeros(n, dtype=torch.float64, device=torch.device("cuda", ctx.device))
+    host = torch.empty(n, dtype=torch.float64).pin_memory()
+    assert L.amgr_download_async(ctx.ptr, u.data_ptr(), host.data_ptr(), -1) != 0
+    assert L.amgr_download_async(ctx.ptr, None, host.data_ptr(), n) != 0
+    assert L.amgr_download_async(ctx.ptr, u.data_ptr(), host.data_ptr(), 0) == 0
+    assert L.amgr_stage_rhs(h._p, None, amg.HOST) != 0
+    with pytest.raises(amg.InvalidArgument, match="location must be HOST or DEVICE"):
+        amg._check(L.amgr_stage_rhs(h._p, u.data_ptr(), amg.STAGED), ctx.ptr)
+    # f = NULL is only accepted with AMGR_STAGED
+    sp, st = amg._SolveParams(1e-8, 10), amg._SolveStats()
+    assert L.amgr_bicgstab(h._p, None, u.data_ptr(), u.data_ptr(), ctypes.byref(sp), ctypes.byref(st),
+                           amg.DEVICE) != 0
+    # a staged RHS is consumed by the next STAGED rebuild, then solved with
+    h.stage_values(A[2])
+    h.stage_rhs(np.ones(n))
+    h.rebuild_staged()
+    _, s1 = amg.bicgstab(h, amg.STAGED_RHS, (u.data_ptr(), u.data_ptr()))
+    u2, s2 = amg.bicgstab(h, np.ones(n))
+    assert s1.iterations == s2.iterations and s1.converged
+    np.testing.assert_array_equal(_bits(u.cpu().numpy()), _bits(u2))
