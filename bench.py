@@ -212,7 +212,7 @@ def run_reference_arm(a):
            "cpu_baseline": {"value": r["value"], "unit": "ms/step", "cores": cores, "kind": "reference",
                             "sample": sample},
            "e2e": {"value": r["value"], "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # --------------------------------------------------------------------------------------
@@ -364,30 +364,35 @@ def run_partitioned(a, rank, world, local):
                "note": ("one global system row-partitioned over the ranks (amgr_dist_*: NCCL halo send/recv, "
                         "transition allgather, rank-ordered dots); levels below replicate_below rows replicated; "
                         f"replicate_below={a.replicate_below}")}
-        print(json.dumps(out), flush=True)
+        emit(out)
     ds.close()
 
 
+_JSON_FD = None  # the process's real stdout while fd 1 is pointed at stderr
+
+
+def emit(out):
+    """The one JSON line of this run, on the real stdout."""
+    line = (json.dumps(out) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+
+
 def main():
+    # stdout carries exactly one JSON line: anything native code prints on
+    # fd 1 (e.g. NCCL's version banner at communicator init) goes to stderr
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     a = args_parse()
     if a.impl == "reference":
         run_reference_arm(a)
         return
     rank, world, local = dist_env()
-    if a.partitioned or (world > 1 and not a.replicas):
-        import torch
-
-        torch.cuda.set_device(local)
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        run_partitioned(a, rank, world, local)
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.destroy_process_group()
-        return
     import torch
 
     torch.cuda.set_device(local)
@@ -395,6 +400,32 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fallback = None
+    if a.partitioned or (world > 1 and not a.replicas):
+        try:
+            run_partitioned(a, rank, world, local)
+        except Exception as e:  # noqa: BLE001 -- reported, then the replica run below measures instead
+            if world == 1 or a.partitioned:
+                raise
+            fallback = f"row-partitioned run failed ({type(e).__name__}: {str(e)[:200]}); independent replicas"
+            print(f"[bench] {fallback}", file=sys.stderr, flush=True)
+        if fallback is None:
+            if world > 1:
+                import torch.distributed as dist
+
+                dist.destroy_process_group()
+            return
+    run_replicas(a, rank, world, local, fallback)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_replicas(a, rank, world, local, fallback=None):
+    """N independent single-GPU systems (one per rank) or the N = 1 run."""
+    import torch
+
     import paper_2108_02054_b200 as amg
 
     L = amg.lib()
@@ -668,11 +699,9 @@ def main():
                "clocks": clk.summary(), "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
                "strategies": strategies, "phase_rooflines": phases,
                "cpu_baseline": cpu}
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
+        if fallback:
+            out["note"] = fallback
+        emit(out)
 
 
 if __name__ == "__main__":
