@@ -7,10 +7,16 @@ One step = one time step of the sequence: partial rebuild of the hierarchy
 from A_k (numeric Galerkin RAP on the frozen transfers + smoothers + coarse
 LU, `amgr_rebuild_values`) followed by the AMG-preconditioned BiCGStab solve
 (`amgr_bicgstab`, tol 1e-8, <= 100 iterations) from the previous step's
-solution — exactly the reference's `run_sequence` partial-reuse step
-(proj/src/reuse.cpp:85-114).  The matrices A_k are generated on the device
-before the timed region (ingestion is excluded, reuse.cpp:65) and are larger
-than L2 (0.94 GB of values), so no explicit flush is needed.
+solution: the reference's `run_sequence` partial-reuse step
+(proj/src/reuse.cpp:85-114) with its V-cycle algorithm (hierarchy.cpp:152-186,
+smoothing applied) and, by default, its coarse LU solve replayed
+exactly (dense_lu.cpp:52-73; `--coarse inverse` selects the explicit-inverse
+extension).  The hierarchy, the rebuild and the V-cycle are bit-identical to
+the reference's at this size (tests/test_gpu_parity_large.py); the Krylov dots
+use the fast blocked order (the sequential-dot parity mode is not benchmarked).
+The matrices A_k are generated on the device before the timed region
+(ingestion is excluded, reuse.cpp:65) and are larger than L2 (0.94 GB of
+values), so no explicit flush is needed.
 
 value        = device time of K steps / K (CUDA events on the library stream,
                barrier + synchronize both sides, max over ranks)      [ms/step]
@@ -20,18 +26,22 @@ e2e          = the same through the C-ABI with HOST buffers: per step the
 roofline     = the dominant kernel (level-0 post-smoothing sweep, the largest
                single kernel of the step) probed with CUDA events on its stream
 cpu_baseline = the unmodified reference (oracle/_ref, single-threaded as
-               shipped) on a bounded sample of the same workload
---impl reference runs that reference arm alone (rank 0).
+               shipped) on a bounded, extrapolated sample of the same workload
+--impl reference runs the reference arm alone (rank 0): one full reference
+               step measured end to end (partial_update + BiCGStab to
+               convergence, the reference's own iteration count).
 
 strategies   = none / full / partial reuse through the library's run_sequence
-               (rebuild, solve and total ms per step; not part of `value`)
+               over steps 0..W-1 of the same sequence (rebuild, solve and
+               total ms per step; not part of `value`)
 
-Multi-GPU (torchrun, N>1): ONE global 256^3 system row-partitioned over
-the ranks (amgr_dist_*: NCCL halo send/recv, transition allgather,
-rank-ordered dots; levels below --replicate-below (150K) rows replicated), strong
-scaling.  `--replicas` runs N independent systems instead.  The multi-rank
-device path is verified on one GPU through the loopback transport
-(tests/test_gpu_dist.py) — see DESIGN.md §5.
+Multi-GPU (torchrun, N>1): N independent single-GPU systems (replicas, weak
+scaling) by default.  `--partitioned` (opt-in) runs ONE global 256^3 system
+row-partitioned over the ranks (amgr_dist_*: NCCL halo send/recv, transition
+allgather, rank-ordered dots; levels below --replicate-below rows
+replicated), strong scaling; verified on one GPU through the loopback
+transport and at world size 1 over NCCL (tests/test_gpu_dist.py), never yet
+at world > 1 over NCCL — see DESIGN.md §5.
 """
 from __future__ import annotations
 
@@ -50,7 +60,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "partial-reuse AMG rebuild ms/step + solve ms/step, 256^3 Poisson; HBM GB/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-ITER_RECORD = os.path.join(ROOT, "profiles", "c3_iterations.json")
 TRAFFIC_RECORD = os.path.join(ROOT, "profiles", "r01_traffic.json")
 
 
@@ -63,19 +72,22 @@ def args_parse():
     p.add_argument("--size", type=int, default=256)
     p.add_argument("--problem", default="dambreak")
     p.add_argument("--nsteps", type=int, default=50, help="length of the time sequence (configs[2]: 50)")
-    p.add_argument("--coarse", default="inverse", choices=["exact", "inverse"],
-                   help="coarsest solve: exact replay of dense_lu.cpp (bit-exact V-cycle) or the explicit inverse")
+    p.add_argument("--coarse", default="exact", choices=["exact", "inverse"],
+                   help="coarsest solve: exact replay of dense_lu.cpp (bit-exact V-cycle; default) or the "
+                        "explicit-inverse extension")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--partitioned", action="store_true",
-                   help="row-partitioned NCCL solve of ONE global system over all ranks (strong scaling); the "
-                        "default when launched with more than one rank")
+                   help="row-partitioned NCCL solve of ONE global system over all ranks (strong scaling); opt-in "
+                        "(the default with N ranks is N independent replicas)")
     p.add_argument("--replicas", action="store_true",
-                   help="with N ranks, run N independent systems instead of partitioning one")
+                   help="with N ranks, run N independent systems (the default unless --partitioned)")
     p.add_argument("--replicate-below", type=int, default=150000,
                    help="partitioned mode: levels with fewer rows are replicated on every rank")
     p.add_argument("--no-strategies", action="store_true",
-                   help="skip the none/full/partial reuse comparison (run_sequence over 4 steps each)")
+                   help="skip the none/full/partial reuse comparison (run_sequence over a window of the sequence)")
+    p.add_argument("--strategy-window", type=int, default=6,
+                   help="steps 0..W-1 of the --nsteps sequence for the none/full/partial comparison")
     return p.parse_args()
 
 
@@ -177,41 +189,75 @@ def host_problem(g, kind, k, nsteps):
     return P.grid3d_values(kind, g, k, nsteps)
 
 
+def host_cpu():
+    """Model name and core counts of this host (state the host)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except Exception:
+        avail = os.cpu_count()
+    return {"model": model, "nproc": os.cpu_count(), "available": avail}
+
+
 def run_reference_arm(a):
+    """The unmodified reference (oracle/_ref) on the host, one FULL partial-reuse
+    step of the sequence measured end to end, as run_sequence runs it
+    (reuse.cpp:85-114): setup(A_0) and the step-0 solve from zero are the
+    untimed prelude (the step-0 solution is the step-1 initial guess,
+    reuse.cpp:108-109); the timed step is partial_update(A_1) + bicgstab over
+    the (fixed) V-cycle to convergence, with the reference's own
+    iteration count.  Times are the reference's own clocks around those two
+    calls (oracle/ref_shim.cpp).  The reference is single-threaded as shipped."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    g = a.size
-    try:
-        rec = json.load(open(ITER_RECORD))
-        iters = float(rec["avg_iterations"])
-        src = f"avg BiCGStab iterations of the same sequence recorded in {os.path.relpath(ITER_RECORD, ROOT)}"
-    except Exception:
-        iters, src = 80.0, "assumed 80 iterations/step (no recorded count)"
-    import numpy as np  # noqa: F811
-
     from oracle import problems as P
+    from oracle import ref
 
-    ks = list(range(1 + a.warmup, 1 + a.warmup + min(a.steps, 3)))
+    g = a.size
+    t_all = time.perf_counter()
     A0 = host_problem(g, a.problem, 0, a.nsteps)
-    Aks = [host_problem(g, a.problem, k, a.nsteps) for k in ks]
     f = P.rhs(g ** 3)
-    r = reference_sample(A0, Aks, f, iters, len(ks))
-    cores = 1
-    sample = (f"{r['steps']} partial_update steps of the {g}^3 {a.problem} sequence timed in full + fixed-V "
-              f"BiCGStab timed for 2 iterations per step; solve = per-iteration time x {iters:.1f} ({src}); "
-              f"reference setup {r['setup_s']:.1f} s untimed; single-threaded as shipped")
-    out = {"metric": METRIC, "value": r["value"], "unit": "ms/step", "impl": "reference", "n_gpus": a.gpus,
-           "steps": r["steps"], "warmup": 0, "ms_per_step": r["value"], "higher_is_better": False,
+    p = ref.params()
+    t0 = time.perf_counter()
+    h0 = ref.setup(A0, p)
+    setup_s = time.perf_counter() - t0
+    del A0
+    s0 = ref.bicgstab(h0, f, fixed=True, prm=p)
+    A1 = host_problem(g, a.problem, 1, a.nsteps)
+    h1 = ref.partial_update(h0, A1, p)
+    h0.free()
+    s1 = ref.bicgstab(h1, f, u0=s0.u, fixed=True, prm=p)
+    h1.free()
+    rebuild_ms, solve_ms = h1.seconds * 1e3, s1.seconds * 1e3
+    value = rebuild_ms + solve_ms
+    cpu = host_cpu()
+    sample = (f"1 full partial-reuse step (step 1 of the {a.nsteps}-step {g}^3 {a.problem} sequence) timed end to "
+              f"end: partial_update {rebuild_ms:.0f} ms + fixed-V BiCGStab to convergence from the step-0 solution, "
+              f"{s1.iterations} iterations ({'converged' if s1.converged else 'NOT converged'}), {solve_ms:.0f} ms; "
+              f"untimed prelude: setup {setup_s:.1f} s, step-0 solve from zero {s0.iterations} iterations "
+              f"{s0.seconds:.1f} s; unmodified reference, single-threaded as shipped; host {cpu['model']}, "
+              f"nproc {cpu['nproc']}")
+    out = {"metric": METRIC, "value": value, "unit": "ms/step", "impl": "reference", "n_gpus": a.gpus,
+           "steps": 1, "warmup": 0, "ms_per_step": value, "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"C3 dam-break {g}^3, partial reuse (BASELINE.json configs[2])",
                       "problem": a.problem, "grid": g, "n": g ** 3, "nnz": 7 * g ** 3 - 6 * g ** 2,
-                      "sequence_steps": a.nsteps, "reuse": "partial", "smoother": "jacobi",
-                      "parallelism": "reference CPU path, 1 host thread"},
-           "rebuild_ms_per_step": r["rebuild_ms"], "solve_ms_per_step": r["per_iteration_ms"] * iters,
-           "cpu_baseline": {"value": r["value"], "unit": "ms/step", "cores": cores, "kind": "reference",
-                            "sample": sample},
-           "e2e": {"value": r["value"], "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                      "sequence_steps": a.nsteps, "timed_steps": "1", "reuse": "partial", "smoother": "jacobi",
+                      "coarse_solve": "exact (dense_lu.cpp)", "parallelism": "reference CPU path, 1 host thread"},
+           "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": [s1.iterations],
+           "converged": bool(s1.converged), "relative_residual": s1.relative_residual,
+           "step0_iterations": s0.iterations, "setup_s": setup_s, "host": cpu,
+           "arm_wall_s": time.perf_counter() - t_all,
+           "cpu_baseline": {"value": value, "unit": "ms/step", "cores": 1, "kind": "reference", "sample": sample},
+           "e2e": {"value": value, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
 
 
@@ -400,29 +446,19 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    fallback = None
-    if a.partitioned or (world > 1 and not a.replicas):
-        try:
-            run_partitioned(a, rank, world, local)
-        except Exception as e:  # noqa: BLE001 -- reported, then the replica run below measures instead
-            if world == 1 or a.partitioned:
-                raise
-            fallback = f"row-partitioned run failed ({type(e).__name__}: {str(e)[:200]}); independent replicas"
-            print(f"[bench] {fallback}", file=sys.stderr, flush=True)
-        if fallback is None:
-            if world > 1:
-                import torch.distributed as dist
-
-                dist.destroy_process_group()
-            return
-    run_replicas(a, rank, world, local, fallback)
+    if a.partitioned:
+        # opt-in: one global system over all ranks; no silent fallback (a
+        # rank-local failure inside NCCL cannot be recovered consistently)
+        run_partitioned(a, rank, world, local)
+    else:
+        run_replicas(a, rank, world, local)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
 
 
-def run_replicas(a, rank, world, local, fallback=None):
+def run_replicas(a, rank, world, local):
     """N independent single-GPU systems (one per rank) or the N = 1 run."""
     import torch
 
@@ -640,10 +676,11 @@ def run_replicas(a, rank, world, local, fallback=None):
         from paper_2108_02054_b200 import reuse as R
 
         strategies = {}
-        seq = R.DeviceGridSequence(a.problem, g, 4, ctx=ctx)
+        wn = max(a.strategy_window, 2)
+        seq = R.DeviceGridSequence(a.problem, g, wn, ctx=ctx, total=a.nsteps, first=0)
         # warm-up (untimed): a 2-step no-reuse run grows the stream-ordered
         # pool to the setup's peak once, as the main loop's warm-up steps do
-        R.run_sequence(R.DeviceGridSequence(a.problem, g, 2, ctx=ctx), R.StrategyConfig(R.StrategyKind.none), prm,
+        R.run_sequence(R.DeviceGridSequence(a.problem, g, 2, ctx=ctx, total=a.nsteps), R.StrategyConfig(R.StrategyKind.none), prm,
                        sp, ctx=ctx, keep_solutions=False)
         for kind in ("none", "full", "partial"):
             res = R.run_sequence(seq, R.StrategyConfig(R.StrategyKind[kind]), prm, sp, ctx=ctx, keep_solutions=False)
@@ -652,9 +689,13 @@ def run_replicas(a, rank, world, local, fallback=None):
             so = 1e3 * sum(s.solve_time for s in st) / len(st)
             strategies[kind] = {"rebuild_ms_per_step": rb, "solve_ms_per_step": so, "total_ms_per_step": rb + so,
                                 "iterations": [s.iterations for s in st], "converged": all(s.converged for s in st)}
-        strategies["note"] = (f"{a.problem} {g}^3 sequence steps 1..3 of a 4-step run_sequence per strategy; "
-                              "times from the driver's own per-step device clocks; 'full' solves with the "
-                              "step-0 hierarchy operator, as the reference does (reuse.cpp:104)")
+        if strategies["none"]["iterations"]:
+            strategies["partial_over_none_iterations"] = (
+                float(np.mean(strategies["partial"]["iterations"])) / float(np.mean(strategies["none"]["iterations"])))
+        strategies["note"] = (f"steps 1..{wn - 1} of the {a.nsteps}-step {a.problem} {g}^3 sequence (the bench's own "
+                              f"sequence), run_sequence per strategy from step 0; times from the driver's own "
+                              "per-step device clocks; 'full' solves with the step-0 hierarchy operator, as the "
+                              "reference does (reuse.cpp:104)")
         del seq
 
     # ---- CPU baseline (rank 0, N=1) ----
@@ -667,23 +708,18 @@ def run_replicas(a, rank, world, local, fallback=None):
             Akh = host_problem(g, a.problem, k1 % a.nsteps, a.nsteps)
             fh_np = f.cpu().numpy()
             r = reference_sample(A0h, [Akh], fh_np, avg_it, 1)
+            hc = host_cpu()
             cpu = {"value": r["value"], "unit": "ms/step", "cores": 1, "kind": "reference",
-                   "sample": (f"1 partial_update of step {k1} timed in full ({r['rebuild_ms']:.0f} ms) + fixed-V "
-                              f"BiCGStab timed for 2 iterations ({r['per_iteration_ms']:.0f} ms/iteration) x "
-                              f"{avg_it:.1f} iterations (this run's average); reference setup "
-                              f"{r['setup_s']:.1f} s untimed; unmodified reference, single-threaded as shipped")}
+                   "sample": (f"bounded sample, EXTRAPOLATED: 1 partial_update of step {k1} timed in full "
+                              f"({r['rebuild_ms']:.0f} ms) + fixed-V BiCGStab timed for 2 iterations "
+                              f"({r['per_iteration_ms']:.0f} ms/iteration) x {avg_it:.1f} iterations (this run's "
+                              f"device average); reference setup {r['setup_s']:.1f} s untimed; unmodified reference, "
+                              f"single-threaded as shipped; the measured full reference step is the --impl "
+                              f"reference arm; host {hc['model']}, nproc {hc['nproc']}")}
         except Exception as e:  # never let the baseline kill the bench line
             cpu = {"value": None, "unit": "ms/step", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
-        # record the per-step iteration count of this sequence for the reference arm
-        try:
-            os.makedirs(os.path.dirname(ITER_RECORD), exist_ok=True)
-            if not os.path.exists(ITER_RECORD):
-                json.dump({"workload": f"{a.problem} {g}^3 steps {1 + W}..{W + K}", "iterations": iters,
-                           "avg_iterations": avg_it}, open(ITER_RECORD, "w"))
-        except Exception:
-            pass
         out = {"metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": world, "steps": K,
                "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated dam-break sequence)",
@@ -699,8 +735,6 @@ def run_replicas(a, rank, world, local, fallback=None):
                "clocks": clk.summary(), "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
                "strategies": strategies, "phase_rooflines": phases,
                "cpu_baseline": cpu}
-        if fallback:
-            out["note"] = fallback
         emit(out)
 
 

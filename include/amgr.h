@@ -145,6 +145,19 @@ amgr_status amgr_ctx_create(int device, void* stream, amgr_ctx** out);
 void amgr_ctx_destroy(amgr_ctx* ctx);
 const char* amgr_last_error(const amgr_ctx* ctx);
 void* amgr_ctx_stream(const amgr_ctx* ctx);
+/* Dot-product order of amgr_bicgstab / amgr_cg (parity mode, extension).
+ * AMGR_DOTS_BLOCKED (default): deterministic per-block partials fused into the
+ * producing kernels, fixed-order grid reduction.  AMGR_DOTS_SEQUENTIAL: every
+ * dot and norm summed strictly left to right from 0.0 with rounded products,
+ * exactly the reference's dot/norm2 (proj/src/bicgstab.cpp:11-17), so with
+ * the exact coarse solve the iterates are bit-identical to the reference's
+ * bicgstab (bicgstab.cpp:21-135) over the fixed V-cycle.  One CTA runs each
+ * sum: ~8 ms per dot at 2.1M rows.  The environment variable AMGR_SEQ_DOTS=1
+ * sets it at context creation. */
+#define AMGR_DOTS_BLOCKED 0
+#define AMGR_DOTS_SEQUENTIAL 1
+amgr_status amgr_ctx_set_dot_order(amgr_ctx* ctx, int order);
+int amgr_ctx_dot_order(const amgr_ctx* ctx);
 /* Waits for the context stream and the copy / download streams. */
 amgr_status amgr_ctx_synchronize(amgr_ctx* ctx);
 /* Pipelining (extension): snapshot n doubles of device memory on the context

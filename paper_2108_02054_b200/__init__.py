@@ -106,6 +106,8 @@ PROTOTYPES = {
     "amgr_last_error": (C.c_char_p, [_V]),
     "amgr_ctx_stream": (_V, [_V]),
     "amgr_ctx_synchronize": (_I, [_V]),
+    "amgr_ctx_set_dot_order": (_I, [_V, _I]),
+    "amgr_ctx_dot_order": (_I, [_V]),
     "amgr_version": (C.c_char_p, []),
     "amgr_amg_params_default": (None, [_P(_AmgParams)]),
     "amgr_solve_params_default": (None, [_P(_SolveParams)]),
@@ -159,6 +161,8 @@ PROTOTYPES = {
     "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),
     "amgr_dist_destroy": (None, [_V]),
 }
+
+DOTS_BLOCKED, DOTS_SEQUENTIAL = 0, 1
 
 _lib = None
 
@@ -314,6 +318,16 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().amgr_launch_count(self._p))
+
+    @property
+    def sequential_dots(self) -> bool:
+        """amgr_ctx_dot_order: True when every Krylov dot/norm is summed strictly
+        left to right as the reference's dot (bicgstab.cpp:11-17)."""
+        return int(lib().amgr_ctx_dot_order(self._p)) == DOTS_SEQUENTIAL
+
+    @sequential_dots.setter
+    def sequential_dots(self, on: bool):
+        _check(lib().amgr_ctx_set_dot_order(self._p, DOTS_SEQUENTIAL if on else DOTS_BLOCKED), self._p)
 
     def probe(self, family: str | None):
         _check(lib().amgr_probe_enable(self._p, (family or "").encode()), self._p)

@@ -108,6 +108,8 @@ amgr_status amgr_ctx_create(int device, void* stream, amgr_ctx** out) {
         {
             const char* e = std::getenv("AMGR_PDL");
             ctx->c.pdl = !(e && std::string(e) == "0");
+            const char* sd = std::getenv("AMGR_SEQ_DOTS");
+            ctx->c.seq_dots = sd && std::string(sd) == "1";
         }
         if (stream) {
             ctx->c.stream = static_cast<cudaStream_t>(stream);
@@ -167,6 +169,20 @@ amgr_status amgr_ctx_synchronize(amgr_ctx* ctx) {
         if (ctx->c.copy) CK(cudaStreamSynchronize(ctx->c.copy));
         if (ctx->c.d2h) CK(cudaStreamSynchronize(ctx->c.d2h));
     });
+}
+
+amgr_status amgr_ctx_set_dot_order(amgr_ctx* ctx, int order) {
+    if (!ctx) return AMGR_E_INVALID_ARGUMENT;
+    if (order != AMGR_DOTS_BLOCKED && order != AMGR_DOTS_SEQUENTIAL) {
+        ctx->c.last_error = "amgr_ctx_set_dot_order: order must be AMGR_DOTS_BLOCKED or AMGR_DOTS_SEQUENTIAL";
+        return AMGR_E_INVALID_ARGUMENT;
+    }
+    ctx->c.seq_dots = order == AMGR_DOTS_SEQUENTIAL;
+    return AMGR_OK;
+}
+
+int amgr_ctx_dot_order(const amgr_ctx* ctx) {
+    return ctx && ctx->c.seq_dots ? AMGR_DOTS_SEQUENTIAL : AMGR_DOTS_BLOCKED;
 }
 
 amgr_status amgr_download_async(amgr_ctx* ctx, const double* device_src, double* host_dst, int64_t n) {

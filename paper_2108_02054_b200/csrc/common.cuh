@@ -65,6 +65,11 @@ struct Ctx {
     // auxiliary stream for independent work inside one call (created lazily,
     // joined back into `stream` before the call returns)
     bool pdl = true;  // AMGR_PDL=0 disables programmatic dependent launch
+    // dot-product order of the Krylov solvers: false = deterministic block
+    // reduction (fused into the producing kernels), true = strictly sequential
+    // left-to-right sums exactly as bicgstab.cpp:11-17 (AMGR_SEQ_DOTS=1 or
+    // amgr_ctx_set_dot_order); a parity mode, ~8 cycles per element
+    bool seq_dots = false;
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaStream_t copy = nullptr;  // staged H2D of the next step's values (lazily created)

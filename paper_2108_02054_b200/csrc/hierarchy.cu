@@ -185,14 +185,15 @@ void coarse_factorize(Hier& h, int* status) {
         lu_inverse(c, h.nL, h.lu.get(), h.piv.get(), h.inv.get());
         return;
     }
-    lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status);
+    if (h.perm.size() != h.nL) h.perm.alloc(h.nL, c.stream);
+    lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status, h.perm.get());
 }
 
 static void coarse_solve(Hier& h, const double* b, double* x, Gate g) {
     if (h.prm.coarse_solve == AMGR_COARSE_INVERSE)
         inv_apply(*h.ctx, h.nL, h.inv.get(), b, x, g);
     else
-        lu_solve(*h.ctx, h.nL, h.lu.get(), h.piv.get(), b, x, g);
+        lu_solve(*h.ctx, h.nL, h.lu.get(), h.piv.get(), b, x, g, h.perm.get());
 }
 
 void throw_lu(int st) {
@@ -680,6 +681,11 @@ static void rebuild_into(Hier& h, const amgr_csr& A) {
     if (!same) {
         h.lv.front().pat = np;
         symbolic_pass(h);
+        // the new patterns need their coded column streams too (as setup)
+        for (size_t l = 0; l + 1 < h.lv.size(); ++l) {
+            Pattern& P = *h.lv[l].pat;
+            encode_columns(c, P.n, P.nnz, P.rp.get(), P.col.get(), P.cc);
+        }
         h.ws.reset();
     }
     work(h);
@@ -1077,6 +1083,7 @@ namespace {
 
 struct KrylovBufs {
     double *r, *rt, *p, *v, *s, *t, *ph, *sh;
+    double* q;  // sequential-dot mode only (else null)
 };
 
 KrylovBufs krylov_bufs(Hier& h) {
@@ -1093,7 +1100,9 @@ KrylovBufs krylov_bufs(Hier& h) {
         W.kph.alloc(n, c.stream);
         W.ksh.alloc(n, c.stream);
     }
-    return {W.kr.get(), W.krt.get(), W.kp.get(), W.kv.get(), W.ks.get(), W.kt.get(), W.kph.get(), W.ksh.get()};
+    if (c.seq_dots && W.kq.size() != n) W.kq.alloc(n, c.stream);
+    return {W.kr.get(), W.krt.get(), W.kp.get(), W.kv.get(), W.ks.get(), W.kt.get(), W.kph.get(), W.ksh.get(),
+            c.seq_dots ? W.kq.get() : nullptr};
 }
 
 DotSink sink(Hier& h, double* out) {
@@ -1113,6 +1122,32 @@ void write_state(Hier& h, const KState& s) {
 }
 
 #define ST_FIELD(st, f) (&(st)->f)
+
+// Sequential-dot mode (Ctx::seq_dots, amgr_ctx_set_dot_order): after each
+// kernel that produced a fused blocked dot, the same dot is recomputed strictly
+// left to right (seq_dot) into the same state field, gated like the producer.
+struct SeqDots {
+    Ctx& c;
+    int64_t n;
+    bool on;
+    void operator()(const double* a, const double* b, double* out, Gate g = {}) const {
+        if (on) seq_dot(c, n, a, b, out, g);
+    }
+};
+
+// ||f - A u||^2 into *out (the reference's true_residual sum, bicgstab.cpp:45-53;
+// also norm2(r)^2 of the initial residual when r is given)
+void resid_sq(Hier& h, const CsrView& A, const double* f, const double* u, double* r, double* r2,
+              const KrylovBufs& B, double* out, Gate g = {}) {
+    Ctx& c = *h.ctx;
+    if (!c.seq_dots) {
+        resid_norm(c, A, f, u, r, r2, DotSink{work(h).partials.get(), work(h).ticket.get(), out}, g);
+        return;
+    }
+    double* d = r ? r : B.q;
+    resid_norm(c, A, f, u, d, r2, DotSink{work(h).partials.get(), work(h).ticket.get(), out}, g);
+    seq_dot(c, A.n, d, d, out, g);
+}
 
 }  // namespace
 
@@ -1188,9 +1223,11 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
     KState* st = work(h).st.get();
     out = amgr_solve_stats{0, 0.0, 0, 0};
 
+    const SeqDots SD{c, n, c.seq_dots};
     KState s0;
     write_state(h, s0);
     dot(c, n, f, f, sink(h, ST_FIELD(st, d_true)));
+    SD(f, f, ST_FIELD(st, d_true));
     KState s = read_state(h);
     const double normf = std::sqrt(s.d_true);
     if (normf == 0.0) {
@@ -1200,12 +1237,13 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
     }
     if (u != u0) copy(c, u, u0, n);
     // r = f - A u ; rtilde = r   (bicgstab.cpp:41-43)
-    resid_norm(c, A, f, u, B.r, B.rt, sink(h, ST_FIELD(st, d_rr)));
+    resid_sq(h, A, f, u, B.r, B.rt, B, ST_FIELD(st, d_rr));
     dot(c, n, B.rt, B.r, sink(h, ST_FIELD(st, d_rtr)));
+    SD(B.rt, B.r, ST_FIELD(st, d_rtr));
     s = read_state(h);
     out.relative_residual = std::sqrt(s.d_rr) / normf;
     if (out.relative_residual <= sp.tol) {
-        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+        resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true));
         s = read_state(h);
         out.relative_residual = std::sqrt(s.d_true) / normf;
         if (out.relative_residual <= sp.tol) {
@@ -1233,19 +1271,26 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
         bicg_p(c, st, n, B.r, B.p, B.v);
         vcycle(h, B.p, B.ph, G);
         spmv_dot(c, A, B.ph, B.v, B.rt, sink(h, ST_FIELD(st, d_rtv)), G);
+        SD(B.rt, B.v, ST_FIELD(st, d_rtv), G);
         bicg_alpha(c, st);
         bicg_s(c, st, n, B.r, B.v, B.s, sink(h, ST_FIELD(st, d_ss)));
+        SD(B.s, B.s, ST_FIELD(st, d_ss), G);
         bicg_half_test(c, st);
         bicg_half_u(c, st, n, u, B.ph);
-        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GH);
+        resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true), GH);
         bicg_half_check(c, st);
         bicg_half_r(c, st, n, B.r, B.s, B.rt, sink(h, ST_FIELD(st, d_rtr)));
+        SD(B.rt, B.r, ST_FIELD(st, d_rtr), GH);
         vcycle(h, B.s, B.sh, GF);
         spmv_dot2(c, A, B.sh, B.t, B.s, sink(h, ST_FIELD(st, d_ts)), GF);
+        SD(B.t, B.s, ST_FIELD(st, d_ts), GF);
+        SD(B.t, B.t, ST_FIELD(st, d_tt), GF);
         bicg_omega(c, st);
         bicg_update(c, st, n, u, B.ph, B.sh, B.r, B.s, B.t, B.rt, sink(h, ST_FIELD(st, d_rr)));
+        SD(B.r, B.r, ST_FIELD(st, d_rr), GF);
+        SD(B.rt, B.r, ST_FIELD(st, d_rtr), GF);
         bicg_end_test(c, st);
-        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GC);
+        resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true), GC);
         bicg_end_check(c, st);
     };
     run_iterations(h, iter, s);
@@ -1256,7 +1301,7 @@ void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_
         return;
     }
     out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
-    resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+    resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true));
     s = read_state(h);
     out.relative_residual = std::sqrt(s.d_true) / normf;
     out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;
@@ -1273,9 +1318,11 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
     KrylovBufs B = krylov_bufs(h);
     KState* st = work(h).st.get();
     out = amgr_solve_stats{0, 0.0, 0, 0};
+    const SeqDots SD{c, n, c.seq_dots};
     KState s0;
     write_state(h, s0);
     dot(c, n, f, f, sink(h, ST_FIELD(st, d_true)));
+    SD(f, f, ST_FIELD(st, d_true));
     KState s = read_state(h);
     const double normf = std::sqrt(s.d_true);
     if (normf == 0.0) {
@@ -1284,7 +1331,7 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
         return;
     }
     if (u != u0) copy(c, u, u0, n);
-    resid_norm(c, A, f, u, B.r, nullptr, sink(h, ST_FIELD(st, d_rr)));
+    resid_sq(h, A, f, u, B.r, nullptr, B, ST_FIELD(st, d_rr));
     s = read_state(h);
     out.relative_residual = std::sqrt(s.d_rr) / normf;
     if (out.relative_residual <= sp.tol) {
@@ -1295,6 +1342,7 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
     vcycle(h, B.r, B.s, {});
     copy(c, B.p, B.s, n);
     dot(c, n, B.r, B.s, sink(h, ST_FIELD(st, d_rz)));
+    SD(B.r, B.s, ST_FIELD(st, d_rz));
     s = read_state(h);
     s.normf = normf;
     s.floor = 1e-30 * normf * normf;
@@ -1309,13 +1357,16 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
     auto iter = [&]() {
         cg_begin(c, st);
         spmv_dot(c, A, B.p, B.v, B.p, sink(h, ST_FIELD(st, d_pq)), G);
+        SD(B.p, B.v, ST_FIELD(st, d_pq), G);
         cg_alpha(c, st);
         cg_update(c, st, n, u, B.r, B.p, B.v, sink(h, ST_FIELD(st, d_rr)));
+        SD(B.r, B.r, ST_FIELD(st, d_rr), G);
         cg_test(c, st);
-        resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)), GC);
+        resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true), GC);
         cg_check(c, st);
         vcycle(h, B.r, B.s, G);
         dot(c, n, B.r, B.s, sink(h, ST_FIELD(st, d_rz)), G);
+        SD(B.r, B.s, ST_FIELD(st, d_rz), G);
         cg_beta(c, st);
         cg_p(c, st, n, B.s, B.p);
     };
@@ -1327,7 +1378,7 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
         return;
     }
     out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
-    resid_norm(c, A, f, u, nullptr, nullptr, sink(h, ST_FIELD(st, d_true)));
+    resid_sq(h, A, f, u, nullptr, nullptr, B, ST_FIELD(st, d_true));
     s = read_state(h);
     out.relative_residual = std::sqrt(s.d_true) / normf;
     out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;

@@ -102,6 +102,7 @@ struct Work {
     std::vector<DevArray<double>> u, t, f, r;
     std::vector<DevArray<double>> d0, d1;  // Chebyshev direction vectors (lazily allocated)
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh;
+    DevArray<double> kq;  // sequential-dot mode: f - A u scratch
     DevArray<KState> st;
     DevArray<double> partials;
     DevArray<unsigned> ticket;
@@ -120,6 +121,7 @@ struct Hier {
     DevArray<double> lu;
     bool lu_formed = false;   // false in the inverse mode when the direct Gauss-Jordan kernel ran
     DevArray<int64_t> piv;
+    DevArray<int> perm;    // composed pivot swaps (lu_solve fast path)
     DevArray<double> inv;  // AMGR_COARSE_INVERSE
     DevArray<double> staged;  // next step's A_0 values (amgr_stage_values)
     cudaEvent_t staged_ev = nullptr, main_ev = nullptr;

@@ -122,10 +122,12 @@ void spai0_rebuild(Ctx& c, const CsrView& A, const int* diag_pos, double* w, int
 // ---- coarse direct solver (dense_lu.cpp) ------------------------------------
 void lu_densify(Ctx& c, const CsrView& A, double* dense);
 // in-place LU with partial pivoting; piv[k]; *status = -1 ok, else the zero-pivot step
-void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status);
-// x = LU \ b in the reference's order; x may alias b
+// perm (optional, n ints): the composed row swaps for lu_solve's fast path
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm = nullptr);
+// x = LU \ b in the reference's order; x may alias b.  With perm (from
+// lu_factor) and n <= 160: the single-warp kernel (k_lu_solve_warp)
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x,
-              Gate g = {});
+              Gate g = {}, const int* perm = nullptr);
 
 // FAST mode (extension): explicit inverse from the LU factors, applied as a matvec
 void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv);

@@ -1273,6 +1273,148 @@ __global__ void __launch_bounds__(LS_THREADS) k_lu_solve(int n, const double* __
     for (int i = tid; i < n; i += LS_THREADS) x[i] = xs[i];
 }
 
+// Single-warp exact solve for n <= 32*LW_Q (the register/shared-memory path
+// used whenever the factor fits in shared memory).  Same arithmetic as
+// dense_lu.cpp:52-73, in the same order per row:
+//  * pivots: x = b[perm] with perm the composition of the reference's
+//    sequential swaps (precomputed once per factorization, k_lu_perm);
+//  * forward: column-oriented, lane l owns rows l, l+32, ... in registers;
+//    step j broadcasts y_j with one shuffle, every row i > j subtracts
+//    L_ij*y_j — per row still ascending j;
+//  * backward: lane 0 runs the reference's row chain
+//    s = y_i - U_i,i+1 x_i+1 - ... - U_i,n-1 x_n-1 with the products of the
+//    next 8-entry chunk formed while the current chunk's dependent DSUBs issue
+//    (software pipelined), so the sweep runs at the DSUB latency; no block
+//    barriers at all.
+constexpr int LW_Q = 5;  // rows per lane (n <= 160)
+
+__device__ __forceinline__ double bwd_chain(const double* __restrict__ mi, const double* __restrict__ xs, int j0,
+                                            int n, double s) {
+    // s -= mi[j]*xs[j] for j = j0 .. n-1, ascending, in 8-entry chunks whose
+    // products are formed one chunk ahead.  The leading (n - j0) % 8 entries go
+    // first so the chunks end exactly at n.
+    int j = j0;
+    const int rem = (n - j0) & 7;
+    double p[8], q[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) p[t] = (t < rem) ? dmul(mi[j + t], xs[j + t]) : 0.0;
+    j += rem;
+    const bool more = j < n;
+    if (more) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) q[t] = dmul(mi[j + t], xs[j + t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+        if (t < rem) s = dsub(s, p[t]);
+    if (!more) return s;
+    for (;;) {
+        j += 8;
+        if (j < n) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                s = dsub(s, q[t]);
+                p[t] = dmul(mi[j + t], xs[j + t]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) s = dsub(s, q[t]);
+            return s;
+        }
+        j += 8;
+        if (j < n) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                s = dsub(s, p[t]);
+                q[t] = dmul(mi[j + t], xs[j + t]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) s = dsub(s, p[t]);
+            return s;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __restrict__ m,
+                                                      const int* __restrict__ perm, const double* b, double* x,
+                                                      Gate g) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const int lane = threadIdx.x;
+    const int nn2 = (n * n + 1) & ~1;
+    double* ms = sm;        // n*n factor (TMA target)
+    double* xs = sm + nn2;  // n (+8 slack read by the chunked chain)
+    if (lane == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        const uint32_t bytes = static_cast<uint32_t>(nn2 * 8);
+        mbar_expect_tx(&bar, bytes);
+        tma_load_1d(ms, m, bytes, &bar);
+    }
+    double y[LW_Q];
+#pragma unroll
+    for (int q = 0; q < LW_Q; ++q) {
+        const int i = 32 * q + lane;
+        y[q] = i < n ? b[perm[i]] : 0.0;
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    // forward (unit L)
+#pragma unroll
+    for (int gq = 0; gq < LW_Q; ++gq) {
+        if (32 * gq >= n - 1) break;
+        for (int t = 0; t < 32; ++t) {
+            const int j = 32 * gq + t;
+            if (j >= n - 1) break;
+            const double yj = __shfl_sync(0xffffffffu, y[gq], t);
+#pragma unroll
+            for (int q = gq; q < LW_Q; ++q) {
+                const int i = 32 * q + lane;
+                if (i > j && i < n) y[q] = dsub(y[q], dmul(ms[i * n + j], yj));
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < LW_Q; ++q) {
+        const int i = 32 * q + lane;
+        if (i < n) xs[i] = y[q];
+    }
+    if (lane < 8) xs[n + lane] = 0.0;
+    __syncwarp();
+    // backward (row chain, lane 0)
+    if (lane == 0) {
+        double xn = __ddiv_rn(xs[n - 1], ms[(n - 1) * n + (n - 1)]);
+        xs[n - 1] = xn;
+        for (int i = n - 2; i >= 0; --i) {
+            const double* mi = ms + i * n;
+            double s = dsub(xs[i], dmul(mi[i + 1], xn));
+            if (i + 2 < n) s = bwd_chain(mi, xs, i + 2, n, s);
+            xn = __ddiv_rn(s, mi[i]);
+            xs[i] = xn;
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) x[i] = xs[i];
+}
+
+// perm[i] = the rhs index that lands at position i after the reference's
+// sequential swaps for k = 0..n-1: swap(x[k], x[piv[k]]) (dense_lu.cpp:60-61)
+__global__ void k_lu_perm(int n, const int64_t* __restrict__ piv, int* __restrict__ perm) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int k = 0; k < n; ++k) {
+        const int p = static_cast<int>(piv[k]);
+        if (p != k) {
+            const int t = perm[k];
+            perm[k] = perm[p];
+            perm[p] = t;
+        }
+    }
+}
+
 // ---- FAST coarse solve (AMGR_COARSE_INVERSE, extension) -------------------
 // Inverse of the coarsest matrix from its LU factors: warp per column,
 // column-oriented forward and backward sweeps on the unit vectors (rounding
@@ -1607,7 +1749,11 @@ void lu_densify(Ctx& c, const CsrView& A, double* dense) {
     LAUNCH(c, "coarse", 0.0, k_densify_fill, grid_for(A.n, 128, c.num_sms * 8), 128, 0, A, dense);
 }
 
-void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
+static void lu_perm(Ctx& c, int64_t n, const int64_t* piv, int* perm) {
+    if (perm) LAUNCH(c, "coarse", 0.0, k_lu_perm, 1, 32, 0, static_cast<int>(n), piv, perm);
+}
+
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm) {
     if (n == 0) return;
     if (n <= DR_MAXN) {
         const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
@@ -1620,6 +1766,7 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
         }();
         (void)attr;
         LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status);
+        lu_perm(c, n, piv, perm);
         return;
     }
     if (n > 2048) invalid("coarse_factorize: coarse system larger than 2048 unknowns is not supported on device");
@@ -1628,10 +1775,24 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status) {
     if (use_smem) CK(cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
     LAUNCH(c, "coarse", 0.0, k_lu_factor, 1, LU_THREADS, use_smem ? sm : 0, static_cast<int>(n), m, piv, status,
            use_smem);
+    lu_perm(c, n, piv, perm);
 }
 
-void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g) {
+void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g,
+              const int* perm) {
     if (n == 0) return;
+    const char* old = std::getenv("AMGR_LU_SOLVE_OLD");
+    if (perm && n <= 32 * LW_Q && !(old && old[0] == '1')) {
+        static const bool attr = [] {
+            CK(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(double) * (32 * LW_Q * 32 * LW_Q + 32 * LW_Q + 8))));
+            return true;
+        }();
+        (void)attr;
+        const size_t sm = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + n + 8);
+        LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve_warp, 1, 32, sm, static_cast<int>(n), m, perm, b, x, g);
+        return;
+    }
     const size_t full = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + 3 * n);
     const int use_smem = full <= 200 * 1024 ? 1 : 0;
     const size_t sm = use_smem ? full : sizeof(double) * static_cast<size_t>(3 * n);

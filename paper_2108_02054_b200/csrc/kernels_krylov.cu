@@ -264,7 +264,60 @@ __global__ void __launch_bounds__(VB) k_dot(int n, const double* __restrict__ a,
     block_dots<1>(d, ds);
 }
 
+constexpr int SD_THREADS = 256, SD_CH = 2048;
+
+__global__ void __launch_bounds__(SD_THREADS) k_seq_dot(int64_t n, const double* __restrict__ a,
+                                                        const double* __restrict__ b, double* out, Gate g) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    __shared__ __align__(16) double buf[2][SD_CH + 8];
+    const int tid = threadIdx.x;
+    const int64_t nch = (n + SD_CH - 1) / SD_CH;
+    auto fill = [&](int64_t ch, double* dst, int t0, int nt) {
+        const int64_t base = ch * SD_CH;
+        const int len = static_cast<int>(n - base < SD_CH ? n - base : SD_CH);
+        for (int i = t0; i < len; i += nt) dst[i] = dmul(__ldg(a + base + i), __ldg(b + base + i));
+        for (int i = len + t0; i < SD_CH + 8; i += nt) dst[i] = 0.0;
+    };
+    if (nch > 0) fill(0, buf[0], tid, SD_THREADS);
+    __syncthreads();
+    double s = 0.0;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        if (tid >= 32) {
+            if (ch + 1 < nch) fill(ch + 1, buf[(ch + 1) & 1], tid - 32, SD_THREADS - 32);
+        } else if (tid == 0) {
+            const int64_t base = ch * SD_CH;
+            const int len = static_cast<int>(n - base < SD_CH ? n - base : SD_CH);
+            const double* p = buf[ch & 1];
+            // s += p[i] for i < len, in order; 8-entry chunks read one chunk ahead
+            int i = 0;
+            double q[8], r[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) q[t] = p[t];
+            for (; i + 16 <= len; i += 16) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    r[t] = p[i + 8 + t];
+                    s = dadd(s, q[t]);
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    q[t] = p[i + 16 + t];
+                    s = dadd(s, r[t]);
+                }
+            }
+            for (; i < len; ++i) s = dadd(s, p[i]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *out = s;
+}
+
 }  // namespace
+
+void seq_dot(Ctx& c, int64_t n, const double* a, const double* b, double* out, Gate g) {
+    LAUNCH_PDL(c, "seq_dot", 16.0 * n, k_seq_dot, 1, SD_THREADS, 0, n, a, b, out, g);
+}
 
 Gate gate_of(const KState* st, int skip, int need) { return Gate{&st->flags, skip, need}; }
 

@@ -57,4 +57,10 @@ void dot(Ctx& c, int64_t n, const double* a, const double* b, DotSink ds, Gate g
 
 Gate gate_of(const KState* st, int skip, int need = 0);
 
+// *out = sum_i a[i]*b[i] accumulated strictly left to right from 0.0, each
+// product rounded before the add: the reference's dot (bicgstab.cpp:11-15)
+// bit for bit.  One CTA; the products of the next chunk are formed by the
+// other warps while one thread runs the dependent add chain.
+void seq_dot(Ctx& c, int64_t n, const double* a, const double* b, double* out, Gate g = {});
+
 }  // namespace amgr

@@ -195,15 +195,23 @@ def full_build_phase_totals(report: RunReport) -> PhaseTimings:
 class DeviceGridSequence:
     """ProblemSequence (sequence.hpp:17-23) generated on the device: the 3D
     synthetic sequences of SURVEY.md 8(d) (poisson / blob / dambreak /
-    convdiff), fixed RHS U(0.1, 1) from std::mt19937_64(seed)."""
+    convdiff), fixed RHS U(0.1, 1) from std::mt19937_64(seed).
 
-    def __init__(self, kind: str, g: int, steps: int, seed: int = 42, ctx: Context | None = None):
+    `steps` systems are served; with `total` and `first` they are the window
+    first .. first+steps-1 of a `total`-step sequence (e.g. steps 0..5 of the
+    50-step C3 dam-break sequence)."""
+
+    def __init__(self, kind: str, g: int, steps: int, seed: int = 42, ctx: Context | None = None,
+                 total: int | None = None, first: int = 0):
         import torch
 
         from . import DEVICE, PROBLEM
 
         self.ctx = ctx or default_context()
         self.kind, self.g, self.steps = PROBLEM[kind], g, steps
+        self.total, self.first = (total or steps), first
+        if first < 0 or first + steps > self.total:
+            raise ValueError("DeviceGridSequence: window outside the sequence")
         L = lib()
         n, nnz = g ** 3, int(L.amgr_problem_nnz(g))
         self.n, self.nnz = n, nnz
@@ -222,7 +230,8 @@ class DeviceGridSequence:
 
     def step(self, k: int):
         L = lib()
-        _check(L.amgr_problem_values(self.ctx.ptr, self.kind, self.g, k, self.steps, self.v.data_ptr()), self.ctx.ptr)
+        _check(L.amgr_problem_values(self.ctx.ptr, self.kind, self.g, self.first + k, self.total, self.v.data_ptr()),
+               self.ctx.ptr)
         self.ctx.synchronize()
         return DeviceCsr(self.n, self.n, self.nnz, self.rp.data_ptr(), self.ci.data_ptr(), self.v.data_ptr()), \
             self.f.data_ptr()

@@ -570,3 +570,34 @@ def test_pipelining_entry_points_validate_arguments(ctx):
     u2, s2 = amg.bicgstab(h, np.ones(n))
     assert s1.iterations == s2.iterations and s1.converged
     np.testing.assert_array_equal(_bits(u.cpu().numpy()), _bits(u2))
+
+
+def test_pattern_change_keeps_coded_columns(ctx):
+    """A pattern-changing partial update re-encodes the column streams
+    (hierarchy.cu rebuild_into), so the row passes keep their 1-byte coded
+    level 0 instead of silently falling back to int32 columns."""
+    A = P.grid3d_values("dambreak", 16, 3)
+    h = amg.setup(A, ctx=ctx)
+    before = [h.level_layout(l)["col_bytes"] for l in range(h.num_levels() - 1)]
+    assert before[0] == 1
+    # drop the couplings of every 5th row to its +x neighbour (and the
+    # symmetric entry): same dimensions, new sparsity pattern
+    rp, ci, v = (np.asarray(x) for x in A)
+    n = len(rp) - 1
+    keep = np.ones(len(ci), bool)
+    for i in range(0, n - 1, 5):
+        for a, b in ((i, i + 1), (i + 1, i)):
+            s, e = rp[a], rp[a + 1]
+            hit = np.nonzero(ci[s:e] == b)[0]
+            keep[s + hit] = False
+    rows = np.repeat(np.arange(n), np.diff(rp))[keep]
+    rp2 = np.zeros(n + 1, np.int64)
+    np.add.at(rp2, rows + 1, 1)
+    B = (np.cumsum(rp2), ci[keep], v[keep])
+    hu = amg.partial_update(h, B)
+    ru = ref.partial_update(ref.setup(A), B)
+    assert_same_hierarchy(hu, ru)
+    after = [hu.level_layout(l)["col_bytes"] for l in range(hu.num_levels() - 1)]
+    assert after[0] == 1, after
+    f = P.rhs(n)
+    assert np.array_equal(_bits(amg.vcycle(hu, f)), _bits(ref.vcycle(ru, f, fixed=True)))
