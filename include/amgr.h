@@ -331,6 +331,26 @@ amgr_status amgr_dist_bicgstab(amgr_dist* d, const double* f_local, double* u_lo
                                const amgr_solve_params* prm, amgr_solve_stats* stats);
 void amgr_dist_destroy(amgr_dist* d);
 
+/* ---- single-operator entry points ------------------------------------------
+ * The reference's free functions on ONE matrix, for the source-compatible
+ * C++ facade (include/amgreuse_gpu.hpp) and callers that need them outside a
+ * hierarchy.  Vectors are host or device (location); the LU pair is host.
+ * Errors carry the reference's texts. */
+/* spmv(const CsrMatrix&, span x, span y)                      csr.cpp:76-85 */
+amgr_status amgr_csr_spmv(amgr_ctx* ctx, const amgr_csr* A, const double* x, double* y, int location);
+/* build_smoother(const CsrMatrix&, double) -> inv_diag          smoother.cpp:8-32
+ * ("build_smoother: zero diagonal at row i", invalid argument) */
+amgr_status amgr_build_smoother(amgr_ctx* ctx, const amgr_csr* A, double* inv_diag, int location);
+/* smooth(s, A, f, span u, sweeps): u <- u + omega*inv_diag*(f - A u)  smoother.cpp:34-48 */
+amgr_status amgr_smooth(amgr_ctx* ctx, const amgr_csr* A, const double* inv_diag, double omega, const double* f,
+                        double* u, int sweeps, int location);
+/* coarse_factorize(const CsrMatrix&): lu (n*n row-major) + piv   dense_lu.cpp:10-50
+ * ("coarse_factorize: singular matrix (zero pivot at step k)", runtime error) */
+amgr_status amgr_coarse_factorize(amgr_ctx* ctx, const amgr_csr* A, double* lu, int64_t* piv);
+/* coarse_solve(const DenseFactorization&, span rhs)              dense_lu.cpp:52-73 */
+amgr_status amgr_coarse_solve(amgr_ctx* ctx, int64_t n, const double* lu, const int64_t* piv, const double* rhs,
+                              double* x);
+
 /* ---- Matrix Market ingestion (matrix_market.hpp:12-27) -------------------- */
 /* A device CSR owned by the library (int32 indices, fp64 values). */
 typedef struct amgr_matrix amgr_matrix;
@@ -339,6 +359,10 @@ typedef struct amgr_matrix amgr_matrix;
  * device exactly as csr_from_triplets (csr.cpp:24-75).  Errors: AMGR_E_RUNTIME
  * with the reference's "path:line: message" text. */
 amgr_status amgr_mm_read(amgr_ctx* ctx, const char* path, amgr_matrix** out);
+/* csr_from_triplets (csr.cpp:24-75) assembled on the device: rows sorted,
+ * duplicates summed in input order; the reference's error texts. */
+amgr_status amgr_csr_from_triplets(amgr_ctx* ctx, int64_t nrows, int64_t ncols, int64_t count, const int64_t* rows,
+                                   const int64_t* cols, const double* values, amgr_matrix** out);
 /* Device view for amgr_setup / amgr_rebuild (location AMGR_DEVICE). */
 amgr_status amgr_matrix_csr(const amgr_matrix* m, amgr_csr* view);
 void amgr_matrix_free(amgr_matrix* m);

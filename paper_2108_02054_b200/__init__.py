@@ -120,6 +120,11 @@ PROTOTYPES = {
     "amgr_bicgstab": (_I, [_V, _V, _V, _V, _P(_SolveParams), _P(_SolveStats), _I]),
     "amgr_cg": (_I, [_V, _V, _V, _V, _P(_SolveParams), _P(_SolveStats), _I]),
     "amgr_spmv": (_I, [_V, _I, _V, _V, _I]),
+    "amgr_csr_spmv": (_I, [_V, _P(_Csr), _V, _V, _I]),
+    "amgr_build_smoother": (_I, [_V, _P(_Csr), _V, _I]),
+    "amgr_smooth": (_I, [_V, _P(_Csr), _V, _D, _V, _V, _I, _I]),
+    "amgr_coarse_factorize": (_I, [_V, _P(_Csr), _V, _V]),
+    "amgr_coarse_solve": (_I, [_V, _L, _V, _V, _V, _V]),
     "amgr_hier_num_levels": (_I, [_V]),
     "amgr_hier_level_dims": (_I, [_V, _I, _V]),
     "amgr_hier_level_layout": (_I, [_V, _I, _V, _V]),
@@ -149,6 +154,7 @@ PROTOTYPES = {
     "amgr_download_async": (_I, [_V, _V, _V, _L]),
     "amgr_mm_read": (_I, [_V, C.c_char_p, _P(_V)]),
     "amgr_matrix_csr": (_I, [_V, _P(_Csr)]),
+    "amgr_csr_from_triplets": (_I, [_V, _L, _L, _L, _V, _V, _V, _P(_V)]),
     "amgr_matrix_free": (None, [_V]),
     "amgr_mm_read_vector": (_I, [_V, C.c_char_p, _P(_L), _V]),
     "amgr_nccl_unique_id": (_I, [_V]),

@@ -349,6 +349,55 @@ amgr_status amgr_spmv(amgr_hier* h, int level, const double* x, double* y, int l
     });
 }
 
+// ---- single-operator entry points -------------------------------------------------
+amgr_status amgr_csr_spmv(amgr_ctx* ctx, const amgr_csr* A, const double* x, double* y, int location) {
+    if (!ctx || !A || (A->ncols > 0 && !x) || (A->nrows > 0 && !y)) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] {
+        amgr::Ctx& c = ctx->c;
+        VecIO io(c, location);
+        const double* xd = io.in(x, A->ncols);
+        double* yd = io.out(y, A->nrows);
+        amgr::op_spmv(c, *A, xd, yd);
+        io.back(y, yd, A->nrows);
+    });
+}
+
+amgr_status amgr_build_smoother(amgr_ctx* ctx, const amgr_csr* A, double* inv_diag, int location) {
+    if (!ctx || !A || (A->nrows > 0 && !inv_diag)) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] {
+        amgr::Ctx& c = ctx->c;
+        VecIO io(c, location);
+        double* wd = io.out(inv_diag, A->nrows);
+        amgr::op_build_smoother(c, *A, wd);
+        io.back(inv_diag, wd, A->nrows);
+    });
+}
+
+amgr_status amgr_smooth(amgr_ctx* ctx, const amgr_csr* A, const double* inv_diag, double omega, const double* f,
+                        double* u, int sweeps, int location) {
+    if (!ctx || !A || (A->nrows > 0 && (!inv_diag || !f || !u))) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] {
+        amgr::Ctx& c = ctx->c;
+        VecIO io(c, location);
+        const double* wd = io.in(inv_diag, A->nrows);
+        const double* fd = io.in(f, A->nrows);
+        double* ud = location == AMGR_DEVICE ? u : const_cast<double*>(io.in(u, A->nrows));
+        amgr::op_smooth(c, *A, wd, omega, fd, ud, sweeps);
+        io.back(u, ud, A->nrows);
+    });
+}
+
+amgr_status amgr_coarse_factorize(amgr_ctx* ctx, const amgr_csr* A, double* lu, int64_t* piv) {
+    if (!ctx || !A || (A->nrows > 0 && (!lu || !piv))) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] { amgr::op_coarse_factorize(ctx->c, *A, lu, piv); });
+}
+
+amgr_status amgr_coarse_solve(amgr_ctx* ctx, int64_t n, const double* lu, const int64_t* piv, const double* rhs,
+                              double* x) {
+    if (!ctx || n < 0 || (n > 0 && (!lu || !piv || !rhs || !x))) return AMGR_E_INVALID_ARGUMENT;
+    return guard(ctx, [&] { amgr::op_coarse_solve(ctx->c, n, lu, piv, rhs, x); });
+}
+
 int amgr_hier_num_levels(const amgr_hier* h) { return h && h->h ? static_cast<int>(h->h->lv.size()) : 0; }
 
 amgr_status amgr_hier_level_dims(const amgr_hier* h, int level, int64_t* dims) {

@@ -172,9 +172,9 @@ void coarse_factorize(Hier& h, int* status) {
     h.nL = L.pat->n;
     if (h.lu.size() != h.nL * h.nL) h.lu.alloc(h.nL * h.nL, c.stream);
     if (h.piv.size() != h.nL) h.piv.alloc(h.nL, c.stream);
-    lu_densify(c, L.view(), h.lu.get());
     h.lu_formed = true;
     if (h.prm.coarse_solve == AMGR_COARSE_INVERSE) {
+        lu_densify(c, L.view(), h.lu.get());
         if (h.inv.size() != h.nL * h.nL) h.inv.alloc(h.nL * h.nL, c.stream);
         // small systems: direct Gauss-Jordan inverse, no LU factor is formed
         if (dense_inverse_direct(c, h.nL, h.lu.get(), h.inv.get(), h.piv.get(), status)) {
@@ -186,6 +186,8 @@ void coarse_factorize(Hier& h, int* status) {
         return;
     }
     if (h.perm.size() != h.nL) h.perm.alloc(h.nL, c.stream);
+    if (lu_factor_csr(c, L.view(), h.lu.get(), h.piv.get(), status, h.perm.get())) return;
+    lu_densify(c, L.view(), h.lu.get());
     lu_factor(c, h.nL, h.lu.get(), h.piv.get(), status, h.perm.get());
 }
 
@@ -344,6 +346,25 @@ static void sa_jacobi_weights(Hier& h) {
     }
 }
 
+// Member-row plans (k_rap_rows) for every plain-aggregation level, built
+// once per pattern (setup / pattern change).  Opt-in (AMGR_RAP_ROWS=1) until
+// the kernel beats k_rap_tma + k_jacobi.
+static bool rap_rows_enabled() {
+    const char* e = std::getenv("AMGR_RAP_ROWS");
+    return e && e[0] == '1';
+}
+static void build_row_plans(Hier& h) {
+    Ctx& c = *h.ctx;
+    if (!rap_rows_enabled()) return;
+    for (size_t i = 0; i + 1 < h.lv.size(); ++i) {
+        Level& A = h.lv[i];
+        if (!A.rap || !A.T || A.T->smoothed || A.rap->rows_tried) continue;
+        A.rap->rows_tried = true;
+        const Pattern& C = *h.lv[i + 1].pat;
+        rap_rows_plan(c, A.view(), A.T->agg.get(), A.T->midx.get(), A.T->nc, C.rp.get(), C.col.get(), A.rap->rows);
+    }
+}
+
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans:
 // the Galerkin chain, then the per-level smoother rebuilds (main stream)
 // concurrently with the coarsest factorization (side stream).
@@ -351,21 +372,57 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
-    // Galerkin chain first; then the coarsest dense factorization (one CTA)
-    // runs on the side stream concurrently with the per-level smoother
+    // Galerkin chain first.  Levels with a member-row plan run k_rap_rows,
+    // which also rebuilds the damped-Jacobi weights of the coarse level (and
+    // of the fine level at the head of the chain), so those levels need no
+    // separate smoother kernel.  The coarsest dense factorization (one CTA)
+    // runs on the side stream concurrently with the remaining smoother
     // rebuilds, which do not depend on it.  Errors are still reported in the
     // reference's order (check_rebuild_errors reads every slot).
+    const bool fuse = h.prm.smoother == AMGR_SMOOTHER_JACOBI && rap_rows_enabled();
+    if (fuse) build_row_plans(h);  // lazily, once per plan
+    std::vector<char> wdone(L, 0);
     for (size_t i = 0; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
         clk.begin(PH_GALERKIN);
         Level& B = h.lv[i + 1];
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
-        if (A.T->smoothed)
+        if (A.T->smoothed) {
             sa_galerkin_numeric(c, *A.rap, A.view().val, *A.T, B.val.get());
-        else
+        } else if (fuse && A.rap->rows.ok) {
+            const RowPlan& rp = A.rap->rows;
+            RapRowsArgs a;
+            a.nc = static_cast<int>(B.pat->n);
+            a.dmax = rp.dmax;
+            a.mptr = A.T->mptr.get();
+            a.midx = A.T->midx.get();
+            a.mrp = rp.mrp.get();
+            a.mlen = rp.mlen.get();
+            a.code = rp.code.get();
+            a.af = A.view().val;
+            a.crp = B.pat->rp.get();
+            a.cdiag = B.pat->diag.get();
+            a.ac = B.val.get();
+            if (!wdone[i]) {
+                if (A.w.size() != A.pat->n) A.w.alloc(A.pat->n, c.stream);
+                a.wf = A.w.get();
+                a.bad_f = W.err.get() + i;
+                wdone[i] = 1;
+                A.has_smoother = true;
+            }
+            if (i + 2 < L) {
+                if (B.w.size() != B.pat->n) B.w.alloc(B.pat->n, c.stream);
+                a.wc = B.w.get();
+                a.bad_c = W.err.get() + i + 1;
+                wdone[i + 1] = 1;
+                B.has_smoother = true;
+            }
+            rap_rows(c, a, rp.maxlen, A.pat->n, A.pat->nnz, B.pat->nnz);
+        } else {
             rap_numeric(c, A.pat->n, B.pat->n, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val,
                         B.val.get(), A.pat->nnz, A.rap->max_chunk);
+        }
         clk.end(PH_GALERKIN);
     }
     c.cur_level = static_cast<int>(L - 1);
@@ -375,6 +432,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         clk.end(PH_COARSE);
     });
     for (size_t i = 0; i + 1 < L; ++i) {
+        if (wdone[i]) continue;
         c.cur_level = static_cast<int>(i);
         clk.begin(PH_SMOOTHER);
         build_smoother(c, h.lv[i], h.prm, W.err.get() + i);
@@ -638,6 +696,7 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
         Pattern& P = *h->lv[l].pat;
         encode_columns(c, P.n, P.nnz, P.rp.get(), P.col.get(), P.cc);
     }
+    build_row_plans(*h);
     clk.end(PH_GALERKIN);
     sa_jacobi_weights(*h);
     clk.begin(PH_COARSE);
@@ -681,11 +740,13 @@ static void rebuild_into(Hier& h, const amgr_csr& A) {
     if (!same) {
         h.lv.front().pat = np;
         symbolic_pass(h);
-        // the new patterns need their coded column streams too (as setup)
+        // the new patterns need their coded column streams and member-row
+        // plans too (as setup)
         for (size_t l = 0; l + 1 < h.lv.size(); ++l) {
             Pattern& P = *h.lv[l].pat;
             encode_columns(c, P.n, P.nnz, P.rp.get(), P.col.get(), P.cc);
         }
+        build_row_plans(h);
         h.ws.reset();
     }
     work(h);
@@ -1382,6 +1443,97 @@ void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_
     s = read_state(h);
     out.relative_residual = std::sqrt(s.d_true) / normf;
     out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;
+}
+
+}  // namespace amgr
+
+// ---- single-operator entry points (the reference's free functions) ------------------
+// spmv (csr.cpp:76-85), build_smoother / smooth (smoother.cpp:8-48),
+// coarse_factorize / coarse_solve (dense_lu.cpp:10-73) on one matrix, for the
+// source-compatible C++ facade (include/amgreuse_gpu.hpp).  Same kernels and
+// arithmetic order as inside the hierarchy.
+namespace amgr {
+
+namespace {
+struct OneMatrix {
+    std::shared_ptr<Pattern> pat;
+    DevArray<double> val;
+    CsrView view() const { return csr_view(*pat, val.get()); }
+};
+OneMatrix one_matrix(Ctx& c, const amgr_csr& A) {
+    OneMatrix m;
+    m.pat = make_pattern(c, A);
+    upload_values(c, m.val, A.values, A.nnz, A.location);
+    return m;
+}
+}  // namespace
+
+void op_spmv(Ctx& c, const amgr_csr& A, const double* x, double* y) {
+    OneMatrix M = one_matrix(c, A);
+    spmv(c, M.view(), x, y);
+}
+
+void op_build_smoother(Ctx& c, const amgr_csr& A, double* w) {
+    if (A.nrows != A.ncols) invalid("build_smoother: matrix is not square");
+    OneMatrix M = one_matrix(c, A);
+    DevArray<int> bad(1, c.stream);
+    const int big = 0x7fffffff;
+    h2d(bad.get(), &big, 1, c.stream);
+    jacobi_rebuild(c, A.nrows, M.val.get(), M.pat->diag.get(), w, bad.get());
+    const int b = d2h_scalar(bad.get(), c.stream);
+    if (b != big) {
+        std::ostringstream os;
+        os << "build_smoother: zero diagonal at row " << b;
+        invalid(os.str());
+    }
+}
+
+void op_smooth(Ctx& c, const amgr_csr& A, const double* w, double omega, const double* f, double* u, int sweeps) {
+    if (A.nrows != A.ncols) invalid("smooth: matrix is not square");
+    if (sweeps <= 0) return;
+    OneMatrix M = one_matrix(c, A);
+    DevArray<double> t(A.nrows, c.stream);
+    double* cur = u;
+    double* nxt = t.get();
+    for (int s = 0; s < sweeps; ++s) {
+        vc_smooth(c, M.view(), f, w, omega, cur, nxt);
+        std::swap(cur, nxt);
+    }
+    if (cur != u) d2d(u, cur, A.nrows, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+void op_coarse_factorize(Ctx& c, const amgr_csr& A, double* lu_host, int64_t* piv_host) {
+    if (A.nrows != A.ncols) invalid("coarse_factorize: matrix is not square");
+    const int64_t n = A.nrows;
+    OneMatrix M = one_matrix(c, A);
+    DevArray<double> lu(n * n, c.stream);
+    DevArray<int64_t> piv(n, c.stream);
+    DevArray<int> perm(n, c.stream), st(1, c.stream);
+    const int ok = -1;
+    h2d(st.get(), &ok, 1, c.stream);
+    if (!lu_factor_csr(c, M.view(), lu.get(), piv.get(), st.get(), perm.get())) {
+        lu_densify(c, M.view(), lu.get());
+        lu_factor(c, n, lu.get(), piv.get(), st.get(), perm.get());
+    }
+    const int s = d2h_scalar(st.get(), c.stream);
+    if (s >= 0) throw_lu(s);
+    d2h(lu_host, lu.get(), n * n, c.stream);
+    d2h(piv_host, piv.get(), n, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+void op_coarse_solve(Ctx& c, int64_t n, const double* lu_host, const int64_t* piv_host, const double* rhs,
+                     double* x) {
+    if (n == 0) return;
+    DevArray<double> lu(n * n, c.stream), b(n, c.stream);
+    DevArray<int64_t> piv(n, c.stream);
+    h2d(lu.get(), lu_host, n * n, c.stream);
+    h2d(piv.get(), piv_host, n, c.stream);
+    h2d(b.get(), rhs, n, c.stream);
+    lu_solve(c, n, lu.get(), piv.get(), b.get(), b.get());
+    d2h(x, b.get(), n, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
 }
 
 }  // namespace amgr

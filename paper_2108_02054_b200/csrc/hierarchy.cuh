@@ -56,6 +56,8 @@ struct RapPlan {
     DevArray<double> ap_val;
     int max_chunk = -1;  // largest contrib count of a k_rap_tma chunk (-1: not computed)
     DevArray<int> cptr, contrib;
+    RowPlan rows;        // member-row plan (k_rap_rows) when the level fits
+    bool rows_tried = false;
 };
 
 inline CsrView csr_view(const Pattern& p, const double* val) {
@@ -144,6 +146,12 @@ struct Hier {
 std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p);
 std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const AmgP& p);
 void rebuild(Hier& h, const amgr_csr& A);
+// single-operator entry points (device vectors; lu/piv/rhs/x of the LU pair on the host)
+void op_spmv(Ctx& c, const amgr_csr& A, const double* x, double* y);
+void op_build_smoother(Ctx& c, const amgr_csr& A, double* w);
+void op_smooth(Ctx& c, const amgr_csr& A, const double* w, double omega, const double* f, double* u, int sweeps);
+void op_coarse_factorize(Ctx& c, const amgr_csr& A, double* lu_host, int64_t* piv_host);
+void op_coarse_solve(Ctx& c, int64_t n, const double* lu_host, const int64_t* piv_host, const double* rhs, double* x);
 void rebuild_values(Hier& h, const double* values, int location);
 void stage_values(Hier& h, const double* values, int location);
 void stage_rhs(Hier& h, const double* f, int location);

@@ -113,6 +113,27 @@ void tail_up(Ctx& c, const TailDesc& d, double om, Gate g);
 int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr);
 void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
                  double* ac, int64_t nnz_f, int max_chunk = -1);
+// Member-row numeric Galerkin product (RowPlan, setup.cuh) with the damped
+// Jacobi rebuild fused in: wf (fine level, only the first RAP of the chain)
+// and wc (coarse level, unless it is the coarsest) get 1.0 / a_ii, first bad
+// rows into bad_f / bad_c (smoother.cpp:8-32).  Bit-identical to rap_numeric.
+struct RapRowsArgs {
+    int nc = 0, dmax = 0;
+    const int* mptr = nullptr;       // R: members of coarse row I
+    const int* midx = nullptr;       // R: fine row of member j (only read for wf)
+    const int* mrp = nullptr;        // start of member row j's entries
+    const uint8_t* mlen = nullptr;   // its length
+    const uint16_t* code = nullptr;  // accumulation codes (RowPlan)
+    const double* af = nullptr;
+    const int* crp = nullptr;        // coarse row pointers
+    const int* cdiag = nullptr;      // coarse diagonal positions (for wc)
+    double* ac = nullptr;
+    double* wf = nullptr;
+    double* wc = nullptr;
+    int* bad_f = nullptr;
+    int* bad_c = nullptr;
+};
+void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_f, int64_t nnz_c);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);
@@ -129,6 +150,9 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* per
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x,
               Gate g = {}, const int* perm = nullptr);
 
+// densify + factor + composed permutation in one single-CTA kernel (n <= 160,
+// perm required; AMGR_LU_COLS=0 disables); false: use lu_densify + lu_factor
+bool lu_factor_csr(Ctx& c, const CsrView& A, double* lu, int64_t* piv, int* status, int* perm);
 // FAST mode (extension): explicit inverse from the LU factors, applied as a matvec
 void lu_inverse(Ctx& c, int64_t n, const double* m, const int64_t* piv, double* inv);
 // Gauss-Jordan inverse of the dense matrix a (n <= 160) straight into inv;

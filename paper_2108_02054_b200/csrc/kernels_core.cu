@@ -844,6 +844,103 @@ void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const 
 }
 
 // ---- end k_rap_tma
+
+// ---- k_rap_rows: member-row streaming Galerkin product ----------------------
+// Thread per coarse row I.  Its members m (R, ascending fine index) are
+// streamed row by row: the row's values are read contiguously (natural order,
+// all loads in flight together) and parked in this thread's shared-memory
+// column, then accumulated in the plan's order — slot groups, ascending k
+// inside a group — so each group's partial is the inner bracket of
+// spmm(A, P) and is committed to acc[slot] (the outer bracket of spmm(R, AP),
+// members ascending; csr.cpp:145-194).  acc lives in shared
+// memory interleaved by thread (acc[s][tid]: conflict-free).  The coarse
+// row's diagonal gives the coarse Jacobi weight in the epilogue; on the first
+// level of the chain the fine diagonal (flagged in the code) gives the fine
+// one.  Values are bit-identical to k_rap / k_rap_tma.
+constexpr int RR_BLOCK = 128;
+
+template <int ML>
+__global__ void __launch_bounds__(RR_BLOCK) k_rap_rows(RapRowsArgs a) {
+    extern __shared__ __align__(16) double rr_sm[];
+    const int tid = threadIdx.x;
+    double* acc = rr_sm + tid;
+    double* vs = rr_sm + a.dmax * RR_BLOCK + tid;
+    const int I = blockIdx.x * RR_BLOCK + tid;
+    if (I >= a.nc) return;
+    const int c0 = __ldg(a.crp + I), deg = __ldg(a.crp + I + 1) - c0;
+    for (int s = 0; s < deg; ++s) acc[s * RR_BLOCK] = 0.0;
+    const int j0 = __ldg(a.mptr + I), j1 = __ldg(a.mptr + I + 1);
+    for (int j = j0; j < j1; ++j) {
+        const int base = __ldg(a.mrp + j);
+        const int len = __ldg(a.mlen + j);
+        unsigned cd[ML];
+#pragma unroll
+        for (int b = 0; b < ML; b += 8) {
+            if (b < len) {
+                double v[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    cd[b + t] = b + t < len ? __ldg(a.code + base + b + t) : 0u;
+                    v[t] = b + t < len ? __ldg(a.af + base + b + t) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (b + t < len) vs[(b + t) * RR_BLOCK] = v[t];
+            }
+        }
+        double part = 0.0, dv = 0.0;
+        bool found = false;
+#pragma unroll
+        for (int t = 0; t < ML; ++t) {
+            if (t < len) {
+                const unsigned c = cd[t];
+                const double x = vs[(c & 31u) * RR_BLOCK];
+                part = dadd(part, x);
+                if (c & 64u) {
+                    dv = x;
+                    found = true;
+                }
+                if (c & 32u) {
+                    double* p = acc + (c >> 7) * RR_BLOCK;
+                    *p = dadd(*p, part);
+                    part = 0.0;
+                }
+            }
+        }
+        if (a.wf) {
+            const int m = __ldg(a.midx + j);
+            if (!found || dv == 0.0) {
+                atomicMin(a.bad_f, m);
+                a.wf[m] = 0.0;
+            } else {
+                a.wf[m] = __ddiv_rn(1.0, dv);
+            }
+        }
+    }
+    double* out = a.ac + c0;
+    for (int s = 0; s < deg; ++s) out[s] = acc[s * RR_BLOCK];
+    if (a.wc) {
+        const int dp = __ldg(a.cdiag + I);
+        const double d = dp >= 0 ? acc[(dp - c0) * RR_BLOCK] : 0.0;
+        if (d == 0.0) {
+            atomicMin(a.bad_c, I);
+            a.wc[I] = 0.0;
+        } else {
+            a.wc[I] = __ddiv_rn(1.0, d);
+        }
+    }
+}
+
+template <int ML>
+static void launch_rap_rows(Ctx& c, const RapRowsArgs& a, double bytes) {
+    const size_t sm = sizeof(double) * static_cast<size_t>(a.dmax + ML) * RR_BLOCK;
+    static const bool attr = [] {
+        CK(cudaFuncSetAttribute(k_rap_rows<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        return true;
+    }();
+    (void)attr;
+    LAUNCH(c, "rap", bytes, k_rap_rows<ML>, (a.nc + RR_BLOCK - 1) / RR_BLOCK, RR_BLOCK, sm, a);
+}
 // w = 1/a_ii (smoother.cpp:8-32).  Each thread handles JB rows strided by the
 // grid so the JB diagonal gathers (one 32-byte sector each) are in flight
 // together.
@@ -889,6 +986,203 @@ __global__ void k_spai0(CsrView A, const int* __restrict__ dpos, double* __restr
 }
 
 // ---- dense LU (coarse_factorize / coarse_solve, dense_lu.cpp:10-73) --------
+// k_lu_cols: densify + LU with partial pivoting + the composed pivot
+// permutation in ONE CTA, for n <= 160 (coarse_factorize, dense_lu.cpp:10-50).
+// Warp w owns the columns j = w, w+16, ...; lane l the physical rows
+// l, l+32, ...; the matrix lives in registers.  Rows are never moved: lp/pl
+// map physical <-> logical rows (the reference's swaps).  Step k:
+//  * the owner warp of column k finds the pivot with warp shuffles (max |.|
+//    over logical rows >= k, lowest logical row on ties = the reference's
+//    strict '>' scan; a NaN |m_kk| keeps p = k), records the swap and forms
+//    the multipliers l = m_ik / pivot;
+//  * one block barrier; every warp subtracts l*u_kj from its columns j > k
+//    (m_ij -= l * m_kj, DMUL then DSUB as in the reference);
+//  * look-ahead: the owner of column k+1 updates that column first and runs
+//    step k+1's pivot search before its other columns, so the search overlaps
+//    the bulk update.  Multipliers and the pivot row are double-buffered.
+// The final logical->physical map is the composed rhs permutation of
+// coarse_solve (dense_lu.cpp:58-59).
+constexpr int LC_W = 16, LC_Q = 5, LC_C = 10, LC_MAXN = 160;
+
+__device__ __forceinline__ double lc_sel(bool p, double a, double b) {
+    double r;
+    asm("{.reg .pred q; setp.ne.b32 q, %1, 0; selp.f64 %0, %2, %3, q;}" : "=d"(r) : "r"(static_cast<int>(p)), "d"(a),
+        "d"(b));
+    return r;
+}
+
+struct LcShared {
+    double Lb[2][LC_MAXN];
+    double Ub[LC_MAXN];
+    int lp[LC_MAXN], pl[LC_MAXN];
+    int pb[2];
+    int s_status;
+};
+
+__device__ __forceinline__ void lc_pivot_step(double (&m)[LC_Q][LC_C], LcShared& S, int k, int n, int lane,
+                                          int64_t* __restrict__ piv) {
+    const int ck = k / LC_W;
+    double colv[LC_Q];
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) {
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < LC_C; ++c) v = lc_sel(c == ck, m[q][c], v);
+        colv[q] = v;
+    }
+    double bv = -2.0;
+    int bpos = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) {
+        const int ph = lane + 32 * q;
+        if (ph < n) {
+            const int L = S.lp[ph];
+            if (L >= k) {
+                double v = fabs(colv[q]);
+                if (v != v) v = -1.0;
+                if (v > bv || (v == bv && L < bpos)) {
+                    bv = v;
+                    bpos = L;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, off);
+        if (ov > bv || (ov == bv && op < bpos)) {
+            bv = ov;
+            bpos = op;
+        }
+    }
+    const int pk = S.pl[k];
+    double vkk = 0.0;
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) vkk = lc_sel(q == (pk >> 5), colv[q], vkk);
+    vkk = __shfl_sync(0xffffffffu, vkk, pk & 31);
+    const int p = (vkk != vkk) ? k : bpos;
+    const int pp = S.pl[p];
+    double pivot = 0.0;
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) pivot = lc_sel(q == (pp >> 5), colv[q], pivot);
+    pivot = __shfl_sync(0xffffffffu, pivot, pp & 31);
+    __syncwarp();
+    if (pivot == 0.0) {
+        if (lane == 0) S.s_status = k;
+        return;
+    }
+    if (lane == 0) {
+        S.pl[k] = pp;
+        S.pl[p] = pk;
+        S.lp[pp] = k;
+        S.lp[pk] = p;
+        piv[k] = p;
+        S.pb[k & 1] = pp;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) {
+        const int ph = lane + 32 * q;
+        if (ph < n && S.lp[ph] > k) {
+            const double l = __ddiv_rn(colv[q], pivot);
+            S.Lb[k & 1][ph] = l;
+#pragma unroll
+            for (int c = 0; c < LC_C; ++c) m[q][c] = lc_sel(c == ck, l, m[q][c]);
+        }
+    }
+}
+
+// columns j > k of this warp: m_ij -= l_i * u_j (only == slot `only`, or
+// all but slot `skip`)
+__device__ __forceinline__ void lc_update(double (&m)[LC_Q][LC_C], LcShared& S, int k, int n, int lane, int w,
+                                      int only, int skip) {
+    const int buf = k & 1;
+    const int pp = S.pb[buf];
+    if (lane == (pp & 31)) {
+#pragma unroll
+        for (int c = 0; c < LC_C; ++c) {
+            double v = m[0][c];
+#pragma unroll
+            for (int q = 1; q < LC_Q; ++q) v = lc_sel(q == (pp >> 5), m[q][c], v);
+            const int j = w + LC_W * c;
+            if (j < n) S.Ub[j] = v;
+        }
+    }
+    __syncwarp();
+    double l[LC_Q];
+    bool act[LC_Q];
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q) {
+        const int ph = lane + 32 * q;
+        act[q] = ph < n && S.lp[ph] > k;
+        l[q] = act[q] ? S.Lb[buf][ph] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < LC_C; ++c) {
+        const int j = w + LC_W * c;
+        if (j <= k || j >= n) continue;
+        if (only >= 0 && c != only) continue;
+        if (c == skip) continue;
+        const double u = S.Ub[j];
+#pragma unroll
+        for (int q = 0; q < LC_Q; ++q)
+            if (act[q]) m[q][c] = dsub(m[q][c], dmul(l[q], u));
+    }
+}
+
+__global__ void __launch_bounds__(LC_W * 32, 1) k_lu_cols(CsrView A, double* __restrict__ out,
+                                                          int64_t* __restrict__ piv, int* __restrict__ perm,
+                                                          int* status) {
+    extern __shared__ __align__(16) double lc_dense[];
+    __shared__ LcShared S;
+    const int n = static_cast<int>(A.n);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int t = tid; t < n * n; t += LC_W * 32) lc_dense[t] = 0.0;
+    __syncthreads();
+    for (int i = tid; i < n; i += LC_W * 32)
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) lc_dense[i * n + A.col[e]] = A.val[e];
+    for (int i = tid; i < n; i += LC_W * 32) {
+        S.lp[i] = i;
+        S.pl[i] = i;
+    }
+    if (tid == 0) S.s_status = -1;
+    __syncthreads();
+    double m[LC_Q][LC_C];
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q)
+#pragma unroll
+        for (int c = 0; c < LC_C; ++c) {
+            const int i = lane + 32 * q, j = w + LC_W * c;
+            m[q][c] = (i < n && j < n) ? lc_dense[i * n + j] : 0.0;
+        }
+
+    if (n > 0 && w == 0) lc_pivot_step(m, S, 0, n, lane, piv);
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        if (S.s_status >= 0) break;
+        const int nk = k + 1;
+        if (nk < n && w == nk % LC_W) {
+            lc_update(m, S, k, n, lane, w, nk / LC_W, -1);
+            lc_pivot_step(m, S, nk, n, lane, piv);
+            lc_update(m, S, k, n, lane, w, -1, nk / LC_W);
+        } else {
+            lc_update(m, S, k, n, lane, w, -1, -1);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *status = S.s_status;
+    if (S.s_status >= 0) return;
+#pragma unroll
+    for (int q = 0; q < LC_Q; ++q)
+#pragma unroll
+        for (int c = 0; c < LC_C; ++c) {
+            const int i = lane + 32 * q, j = w + LC_W * c;
+            if (i < n && j < n) out[S.lp[i] * n + j] = m[q][c];
+        }
+    for (int i = tid; i < n; i += LC_W * 32) perm[i] = S.pl[i];
+}
+
 __global__ void k_densify(CsrView A, double* dense) {
     const int64_t n = A.n;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
@@ -1732,6 +2026,22 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr,
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * resident));
     LAUNCH(c, "rap", bytes, k_rap, grid, RAP_BLOCK, 0, nnz_c, cptr, contrib, af, ac);
 }
+void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_f, int64_t nnz_c) {
+    if (a.nc == 0) return;
+    // algorithmic bytes: values 8*nnz_f + codes 2*nnz_f + member starts and
+    // lengths 5*nf + member pointers 4*(nc+1) + coarse row pointers 4*(nc+1)
+    // + coarse values 8*nnz_c; fused Jacobi: + 8*nc (wc) and + 12*nf (wf, midx)
+    double bytes = 10.0 * nnz_f + 5.0 * nf + 8.0 * (a.nc + 1) + 8.0 * nnz_c;
+    if (a.wc) bytes += 12.0 * a.nc;
+    if (a.wf) bytes += 12.0 * nf;
+    if (maxlen <= 8)
+        launch_rap_rows<8>(c, a, bytes);
+    else if (maxlen <= 16)
+        launch_rap_rows<16>(c, a, bytes);
+    else
+        launch_rap_rows<32>(c, a, bytes);
+}
+
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
     LAUNCH(c, "smoother", 20.0 * n, k_jacobi, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n),
@@ -1802,6 +2112,20 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     }();
     (void)attr;
     LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve, 1, LS_THREADS, sm, static_cast<int>(n), m, piv, b, x, use_smem, g);
+}
+
+bool lu_factor_csr(Ctx& c, const CsrView& A, double* lu, int64_t* piv, int* status, int* perm) {
+    const char* e = std::getenv("AMGR_LU_COLS");  // opt-in: slower than k_dense_reg so far
+    if (!perm || A.n == 0 || A.n > LC_MAXN || !(e && e[0] == '1')) return false;
+    const size_t sm = sizeof(double) * static_cast<size_t>(A.n * A.n);
+    static const bool attr = [] {
+        CK(cudaFuncSetAttribute(k_lu_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * LC_MAXN * LC_MAXN)));
+        return true;
+    }();
+    (void)attr;
+    LAUNCH(c, "coarse", 0.0, k_lu_cols, 1, LC_W * 32, sm, A, lu, piv, perm, status);
+    return true;
 }
 
 bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {

@@ -546,6 +546,100 @@ void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbo
            out.rp.get());
 }
 
+__global__ void k_rr_members(int64_t nf, const int* __restrict__ rp, const int* __restrict__ midx, int* mrp,
+                             uint8_t* mlen, int* maxlen) {
+    int mx = 0;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nf;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = midx[j];
+        const int a = rp[m], len = rp[m + 1] - a;
+        mrp[j] = a;
+        mlen[j] = static_cast<uint8_t>(len < 255 ? len : 255);
+        mx = max(mx, len);
+    }
+    atomicMax(maxlen, mx);
+}
+
+__global__ void k_rr_dmax(int64_t nc, const int* __restrict__ crp, int* dmax) {
+    int mx = 0;
+    for (int64_t I = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; I < nc;
+         I += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        mx = max(mx, crp[I + 1] - crp[I]);
+    atomicMax(dmax, mx);
+}
+
+// thread per fine row: slots of its entries in coarse row agg[m], then a
+// stable insertion sort by slot gives the accumulation order
+__global__ void k_rr_code(CsrView A, const int* __restrict__ agg, const int* __restrict__ crp,
+                          const int* __restrict__ ccol, uint16_t* __restrict__ code, int* bad) {
+    for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < A.n;
+         m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int e0 = A.rp[m], len = A.rp[m + 1] - e0;
+        if (len > 32) {
+            atomicOr(bad, 1);
+            continue;
+        }
+        const int I = agg[m];
+        const int c0 = crp[I], deg = crp[I + 1] - c0;
+        if (deg > 511) {
+            atomicOr(bad, 2);
+            continue;
+        }
+        int slot[32], ord[32];
+        for (int k = 0; k < len; ++k) {
+            const int J = agg[A.col[e0 + k]];
+            int lo = 0, hi = deg;  // lower_bound of J in ccol[c0, c0 + deg)
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (ccol[c0 + mid] < J) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= deg || ccol[c0 + lo] != J) atomicOr(bad, 4);
+            slot[k] = lo;
+            int t = k;
+            while (t > 0 && slot[ord[t - 1]] > lo) {
+                ord[t] = ord[t - 1];
+                --t;
+            }
+            ord[t] = k;
+        }
+        for (int t = 0; t < len; ++t) {
+            const int k = ord[t];
+            const int sl = slot[k];
+            const bool last = t + 1 == len || slot[ord[t + 1]] != sl;
+            const bool dg = A.col[e0 + k] == m;
+            code[e0 + t] = static_cast<uint16_t>(k | (last ? 32 : 0) | (dg ? 64 : 0) | (sl << 7));
+        }
+    }
+}
+
+void rap_rows_plan(Ctx& c, const CsrView& A, const int* agg, const int* midx, int64_t nc, const int* crp,
+                   const int* ccol, RowPlan& plan) {
+    plan.ok = false;
+    if (A.n == 0 || nc == 0) return;
+    DevArray<int> st(3, c.stream);
+    CK(cudaMemsetAsync(st.get(), 0, 3 * sizeof(int), c.stream));
+    plan.mrp.alloc(A.n, c.stream);
+    plan.mlen.alloc(A.n, c.stream);
+    LAUNCH(c, "setup", 0.0, k_rr_members, grid_for(A.n, SB, c.num_sms * 16), SB, 0, A.n, A.rp, midx,
+           plan.mrp.get(), plan.mlen.get(), st.get());
+    LAUNCH(c, "setup", 0.0, k_rr_dmax, grid_for(nc, SB, c.num_sms * 16), SB, 0, nc, crp, st.get() + 1);
+    int h[3];
+    d2h(h, st.get(), 2, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    plan.maxlen = h[0];
+    plan.dmax = h[1];
+    if (plan.maxlen > 32 || plan.dmax > 511) {
+        plan.mrp.release();
+        plan.mlen.release();
+        return;
+    }
+    plan.code.alloc(A.nnz + 8, c.stream);
+    LAUNCH(c, "setup", 0.0, k_rr_code, grid_for(A.n, 128, c.num_sms * 16), 128, 0, A, agg, crp, ccol,
+           plan.code.get(), st.get() + 2);
+    const int bad = d2h_scalar(st.get() + 2, c.stream);
+    if (bad) fail(AMGR_E_RUNTIME, "rap_rows_plan: inconsistent coarse pattern (internal error)");
+    plan.ok = true;
+}
 
 // ---- smoothed aggregation ----------------------------------------------------
 // Smoothed aggregation (extension, north star "tentative and

@@ -233,6 +233,60 @@ int bits(int64_t n) {
 
 }  // namespace
 
+// Device assembly exactly as csr_from_triplets (csr.cpp:24-75): stable
+// radix sort of (row, col) keys (duplicates keep input order) and an in-order
+// segmented sum of duplicates.
+void assemble_triplets(Ctx& c, int64_t nrows, int64_t ncols, const std::vector<int>& row, const std::vector<int>& col,
+                       const std::vector<double>& val, amgr_matrix& M) {
+    const int64_t m = static_cast<int64_t>(row.size());
+    M.nrows = nrows;
+    M.ncols = ncols;
+    M.rp.alloc(nrows + 1, c.stream);
+    const int bc = bits(std::max<int64_t>(ncols, 2)), br = bits(std::max<int64_t>(nrows, 2));
+    if (m == 0) {
+        CK(cudaMemsetAsync(M.rp.get(), 0, sizeof(int) * (nrows + 1), c.stream));
+        M.nnz = 0;
+        M.col.alloc(1, c.stream);
+        M.val.alloc(1, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    DevArray<int> drow(m, c.stream), dcol(m, c.stream), id0(m, c.stream), id1(m, c.stream);
+    DevArray<double> dval(m, c.stream);
+    DevArray<uint64_t> k0(m, c.stream), k1(m, c.stream);
+    h2d(drow.get(), row.data(), m, c.stream);
+    h2d(dcol.get(), col.data(), m, c.stream);
+    h2d(dval.get(), val.data(), m, c.stream);
+    LAUNCH(c, "io", 0.0, k_mm_keys, grid_for(m, 256, c.num_sms * 16), 256, 0, m, drow.get(), dcol.get(), bc, k0.get(),
+           id0.get());
+    cub::DoubleBuffer<uint64_t> kb(k0.get(), k1.get());
+    cub::DoubleBuffer<int> vb(id0.get(), id1.get());
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, m, 0, br + bc, c.stream));
+    {
+        DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
+        CK(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kb, vb, m, 0, br + bc, c.stream));
+    }
+    DevArray<int64_t> head(m, c.stream), pos(m, c.stream);
+    LAUNCH(c, "io", 0.0, k_mm_heads, grid_for(m, 256, c.num_sms * 16), 256, 0, m, kb.Current(), head.get());
+    bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, head.get(), pos.get(), m, c.stream));
+    {
+        DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
+        CK(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, head.get(), pos.get(), m, c.stream));
+    }
+    const int64_t nu = d2h_scalar(pos.get() + m - 1, c.stream) + d2h_scalar(head.get() + m - 1, c.stream);
+    M.nnz = nu;
+    M.col.alloc(nu, c.stream);
+    M.val.alloc(nu, c.stream);
+    DevArray<uint64_t> uk(nu, c.stream);
+    LAUNCH(c, "io", 0.0, k_mm_assemble, grid_for(m, 256, c.num_sms * 16), 256, 0, m, kb.Current(), vb.Current(),
+           head.get(), pos.get(), dval.get(), (uint64_t{1} << bc) - 1, M.col.get(), M.val.get(), uk.get());
+    LAUNCH(c, "io", 0.0, k_mm_rowptr, grid_for(nrows + 1, 256, c.num_sms * 16), 256, 0, uk.get(), nu, nrows, bc,
+           M.rp.get());
+    CK(cudaStreamSynchronize(c.stream));
+}
+
 // mm_read (matrix_market.cpp:104-140) into device CSR
 void mm_read_device(Ctx& c, const std::string& path, amgr_matrix& M) {
     Text t = load(path);
@@ -350,54 +404,7 @@ void mm_read_device(Ctx& c, const std::string& path, amgr_matrix& M) {
     }
     if (taken < nnz) parse_fail(path, line_base, "unexpected end of file: expected more entries");
 
-    // device assembly (csr_from_triplets, csr.cpp:24-75)
-    const int64_t m = static_cast<int64_t>(row.size());
-    M.nrows = nrows;
-    M.ncols = ncols;
-    M.rp.alloc(nrows + 1, c.stream);
-    const int bc = bits(std::max<int64_t>(ncols, 2)), br = bits(std::max<int64_t>(nrows, 2));
-    if (m == 0) {
-        CK(cudaMemsetAsync(M.rp.get(), 0, sizeof(int) * (nrows + 1), c.stream));
-        M.nnz = 0;
-        M.col.alloc(1, c.stream);
-        M.val.alloc(1, c.stream);
-        CK(cudaStreamSynchronize(c.stream));
-        return;
-    }
-    DevArray<int> drow(m, c.stream), dcol(m, c.stream), id0(m, c.stream), id1(m, c.stream);
-    DevArray<double> dval(m, c.stream);
-    DevArray<uint64_t> k0(m, c.stream), k1(m, c.stream);
-    h2d(drow.get(), row.data(), m, c.stream);
-    h2d(dcol.get(), col.data(), m, c.stream);
-    h2d(dval.get(), val.data(), m, c.stream);
-    LAUNCH(c, "io", 0.0, k_mm_keys, grid_for(m, 256, c.num_sms * 16), 256, 0, m, drow.get(), dcol.get(), bc, k0.get(),
-           id0.get());
-    cub::DoubleBuffer<uint64_t> kb(k0.get(), k1.get());
-    cub::DoubleBuffer<int> vb(id0.get(), id1.get());
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, m, 0, br + bc, c.stream));
-    {
-        DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
-        CK(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, kb, vb, m, 0, br + bc, c.stream));
-    }
-    DevArray<int64_t> head(m, c.stream), pos(m, c.stream);
-    LAUNCH(c, "io", 0.0, k_mm_heads, grid_for(m, 256, c.num_sms * 16), 256, 0, m, kb.Current(), head.get());
-    bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, head.get(), pos.get(), m, c.stream));
-    {
-        DevArray<char> tmp(static_cast<int64_t>(bytes), c.stream);
-        CK(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, head.get(), pos.get(), m, c.stream));
-    }
-    const int64_t nu = d2h_scalar(pos.get() + m - 1, c.stream) + d2h_scalar(head.get() + m - 1, c.stream);
-    M.nnz = nu;
-    M.col.alloc(nu, c.stream);
-    M.val.alloc(nu, c.stream);
-    DevArray<uint64_t> uk(nu, c.stream);
-    LAUNCH(c, "io", 0.0, k_mm_assemble, grid_for(m, 256, c.num_sms * 16), 256, 0, m, kb.Current(), vb.Current(),
-           head.get(), pos.get(), dval.get(), (uint64_t{1} << bc) - 1, M.col.get(), M.val.get(), uk.get());
-    LAUNCH(c, "io", 0.0, k_mm_rowptr, grid_for(nrows + 1, 256, c.num_sms * 16), 256, 0, uk.get(), nu, nrows, bc,
-           M.rp.get());
-    CK(cudaStreamSynchronize(c.stream));
+    assemble_triplets(c, nrows, ncols, row, col, val, M);
 }
 
 // mm_read_vector (matrix_market.cpp:176-203)
@@ -439,6 +446,44 @@ amgr_status amgr_mm_read(amgr_ctx* ctx, const char* path, amgr_matrix** out) {
     try {
         CK(cudaSetDevice(c.device));
         amgr::mm_read_device(c, path, *m);
+        *out = m;
+        return AMGR_OK;
+    } catch (const amgr::Error& e) {
+        delete m;
+        c.last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        delete m;
+        c.last_error = e.what();
+        return AMGR_E_RUNTIME;
+    }
+}
+
+amgr_status amgr_csr_from_triplets(amgr_ctx* ctx, int64_t nrows, int64_t ncols, int64_t count, const int64_t* rows,
+                                   const int64_t* cols, const double* values, amgr_matrix** out) {
+    if (!ctx || !out || count < 0 || (count > 0 && (!rows || !cols || !values))) return AMGR_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    amgr::Ctx& c = ctx->c;
+    auto* m = new amgr_matrix();
+    try {
+        CK(cudaSetDevice(c.device));
+        // validation in the reference's order and words (csr.cpp:25-35)
+        if (nrows < 0 || ncols < 0) amgr::invalid("csr_from_triplets: negative dimension");
+        if (nrows > INT32_MAX - 1 || ncols > INT32_MAX - 1 || count > INT32_MAX - 1)
+            amgr::invalid("matrix too large for int32 device indices (> 2^31 entries per GPU)");
+        std::vector<int> r(static_cast<size_t>(count)), cc(static_cast<size_t>(count));
+        std::vector<double> v(values, values + count);
+        for (int64_t k = 0; k < count; ++k) {
+            if (rows[k] < 0 || rows[k] >= nrows || cols[k] < 0 || cols[k] >= ncols) {
+                std::ostringstream os;
+                os << "csr_from_triplets: entry " << k << " (" << rows[k] << ", " << cols[k] << ") out of range for "
+                   << nrows << "x" << ncols << " matrix";
+                amgr::invalid(os.str());
+            }
+            r[static_cast<size_t>(k)] = static_cast<int>(rows[k]);
+            cc[static_cast<size_t>(k)] = static_cast<int>(cols[k]);
+        }
+        amgr::assemble_triplets(c, nrows, ncols, r, cc, v, *m);
         *out = m;
         return AMGR_OK;
     } catch (const amgr::Error& e) {

@@ -51,6 +51,29 @@ struct RapSymbolic {
 };
 void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbolic& out);
 
+// Member-row Galerkin plan (k_rap_rows): thread per coarse
+// row I streams its member fine rows (R order, ascending) contiguously and
+// scatters each entry into the local slot of its coarse column.  Per fine
+// entry (CSR position of the row, i.e. aligned with the values) a 16-bit code
+// lists the row's entries in accumulation order — grouped by slot, ascending
+// k inside a group (the inner bracket of spmm(A, P), csr.cpp:145-184):
+//   bits 0-4  offset of the entry inside its fine row (rows <= 32 entries)
+//   bit  5    last entry of its slot group: commit the group's partial sum
+//   bit  6    the entry is the row's diagonal (fused Jacobi, smoother.cpp:8-32)
+//   bits 7-15 slot = position of the coarse column in coarse row I (<= 511)
+struct RowPlan {
+    bool ok = false;
+    int dmax = 0;   // widest coarse row
+    int maxlen = 0; // longest fine row
+    DevArray<int> mrp;        // [nf] R order: start of member row midx[j]
+    DevArray<uint8_t> mlen;   // [nf] R order: its length
+    DevArray<uint16_t> code;  // [nnz_f]
+};
+// Builds the plan when the level fits (rows <= 32 entries, coarse rows <= 511);
+// plan.ok tells.  crp/ccol: the coarse pattern from rap_symbolic.
+void rap_rows_plan(Ctx& c, const CsrView& A, const int* agg, const int* midx, int64_t nc, const int* crp,
+                   const int* ccol, RowPlan& plan);
+
 // ---- smoothed aggregation (extension) ----
 // Device SpGEMM C = A B: structural pattern of C (sorted columns) and the
 // numeric plan (per output entry, its (a index, b index) products in the

@@ -601,3 +601,43 @@ def test_pattern_change_keeps_coded_columns(ctx):
     assert after[0] == 1, after
     f = P.rhs(n)
     assert np.array_equal(_bits(amg.vcycle(hu, f)), _bits(ref.vcycle(ru, f, fixed=True)))
+
+
+@pytest.mark.parametrize("rows", ["1", "0"])
+def test_rebuild_zero_diagonal_error_fused_and_separate(ctx, monkeypatch, rows):
+    """A partial update whose new A_0 has a zero diagonal fails with the
+    reference's message (hierarchy.cpp:124-132 + :31-35), both when the
+    Jacobi rebuild is fused into the member-row Galerkin kernel and when it
+    runs separately; a coarse-level zero diagonal names its level."""
+    monkeypatch.setenv("AMGR_RAP_ROWS", rows)
+    A = P.grid3d_values("dambreak", 12, 3)
+    h = amg.setup(A, ctx=ctx)
+    r = ref.setup(A)
+    rp, ci, v = (np.asarray(x).copy() for x in A)
+    row = 37
+    v[rp[row] + np.nonzero(ci[rp[row]:rp[row + 1]] == row)[0][0]] = 0.0
+    with pytest.raises(ref.RefError) as er:
+        ref.partial_update(r, (rp, ci, v))
+    with pytest.raises(amg.InvalidArgument) as eg:
+        h.rebuild((rp, ci, v))
+    assert str(eg.value) == str(er.value), (str(eg.value), str(er.value))
+    # the hierarchy stays usable: rebuild with valid values again
+    h.rebuild(A)
+    assert_same_hierarchy(h, r)
+
+
+@pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "blob_20", "random_300", "poisson1d_64_ce10"])
+def test_member_row_rap_matches_contrib_rap(ctx, monkeypatch, name):
+    """k_rap_rows (member-row plan, fused Jacobi) and k_rap_tma (contribution
+    plan, separate Jacobi) give the same bits, and both match the reference."""
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    rp, ci, v = A
+    B = (rp, ci, np.asarray(v) * (1.0 + 0.05 * np.random.default_rng(9).random(len(v))))
+    ru = ref.partial_update(r, B, ref.params(**kw))
+    for rows in ("1", "0", "1"):
+        monkeypatch.setenv("AMGR_RAP_ROWS", rows)
+        h.rebuild_values(B[2])
+        assert_same_hierarchy(h, ru)
