@@ -381,6 +381,16 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     // reference's order (check_rebuild_errors reads every slot).
     const bool fuse = h.prm.smoother == AMGR_SMOOTHER_JACOBI && rap_rows_enabled();
     if (fuse) build_row_plans(h);  // lazily, once per plan
+    // Jacobi fused into k_rap_tma (default; AMGR_FUSE_JACOBI=0 runs k_jacobi per level)
+    // AMGR_FUSE_JACOBI=1 (opt-in): the coarse level's weights come from the
+    // RAP thread that sums each coarse diagonal (levels >= 1); level 0's
+    // k_jacobi runs after the chain.  Measured slower at 256^3 (2.54 vs
+    // 2.38 ms per rebuild: the fused k_rap_tma variant loses more than the
+    // removed k_jacobi launches save, and the coarsest factorization is no
+    // longer hidden behind the smoother kernels), so by default every level
+    // runs k_jacobi after the chain, concurrently with the factorization.
+    const char* fe = std::getenv("AMGR_FUSE_JACOBI");
+    const bool jac = h.prm.smoother == AMGR_SMOOTHER_JACOBI && fe && fe[0] == '1';
     std::vector<char> wdone(L, 0);
     for (size_t i = 0; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
@@ -419,6 +429,22 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
                 B.has_smoother = true;
             }
             rap_rows(c, a, rp.maxlen, A.pat->n, A.pat->nnz, B.pat->nnz);
+        } else if (jac) {
+            // k_rap_tma with the Jacobi rebuild of the coarse level (and of the
+            // fine level at the head of the chain) in its epilogue
+            RapPlan& rp = *A.rap;
+            RapJacobi fj;
+            if (i + 2 < L) {
+                if (B.w.size() != B.pat->n) B.w.alloc(B.pat->n, c.stream);
+                fj.ccol = B.pat->col.get();
+                fj.wc = B.w.get();
+                fj.bad_c = W.err.get() + i + 1;
+            }
+            if (rap_numeric(c, A.pat->n, B.pat->n, rp.nnz_c, rp.cptr.get(), rp.contrib.get(), A.view().val,
+                            B.val.get(), A.pat->nnz, rp.max_chunk, fj.wc ? &fj : nullptr)) {
+                wdone[i + 1] = 1;
+                B.has_smoother = true;
+            }
         } else {
             rap_numeric(c, A.pat->n, B.pat->n, A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.view().val,
                         B.val.get(), A.pat->nnz, A.rap->max_chunk);

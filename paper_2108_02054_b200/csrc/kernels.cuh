@@ -111,8 +111,17 @@ void tail_up(Ctx& c, const TailDesc& d, double om, Gate g);
 
 // largest contrib count of any RT_CH-entry chunk of a plan (TMA stage size; host sync)
 int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr);
-void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
-                 double* ac, int64_t nnz_f, int max_chunk = -1);
+// Fused damped-Jacobi rebuild of the COARSE level inside the numeric RAP:
+// the thread that sums a coarse diagonal entry (flagged in cptr bit 30 by
+// rap_symbolic) writes wc[I] = 1/(A_{i+1})_II; first zero -> bad_c.
+struct RapJacobi {
+    const int* ccol = nullptr;  // coarse columns (I of a flagged diagonal entry)
+    double* wc = nullptr;
+    int* bad_c = nullptr;
+};
+// returns true when the coarse Jacobi rebuild was fused (TMA path taken)
+bool rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f, int max_chunk = -1, const RapJacobi* fj = nullptr);
 // Member-row numeric Galerkin product (RowPlan, setup.cuh) with the damped
 // Jacobi rebuild fused in: wf (fine level, only the first RAP of the chain)
 // and wc (coarse level, unless it is the coarsest) get 1.0 / a_ii, first bad

@@ -661,6 +661,9 @@ __global__ void k_prolong(int n, const double* __restrict__ u, const int* __rest
 // the first two contributions loaded speculatively (avg 1.3 per entry at
 // L0), so the cptr -> contrib -> value chains overlap.
 constexpr int RAP_ILP = 4, RAP_BLOCK = 256;
+// cptr entries: bit 30 flags a coarse diagonal entry (rap_symbolic), the
+// low 30 bits are the contribution offset
+constexpr int CP_DIAG = 1 << 30, CP_MASK = CP_DIAG - 1;
 
 __device__ __forceinline__ void rap_acc(double v, int e, double& acc, double& part) {
     part = dadd(part, v);
@@ -680,8 +683,8 @@ __global__ void __launch_bounds__(RAP_BLOCK) k_rap(int64_t nnz_c, const int* __r
 #pragma unroll
         for (int k = 0; k < RAP_ILP; ++k) {
             const int64_t c = base + k * RAP_BLOCK + threadIdx.x;
-            p0[k] = c < nnz_c ? __ldcs(cptr + c) : 0;
-            p1[k] = c < nnz_c ? __ldcs(cptr + c + 1) : 0;
+            p0[k] = c < nnz_c ? (__ldcs(cptr + c) & CP_MASK) : 0;
+            p1[k] = c < nnz_c ? (__ldcs(cptr + c + 1) & CP_MASK) : 0;
         }
 #pragma unroll
         for (int k = 0; k < RAP_ILP; ++k) {
@@ -718,11 +721,11 @@ constexpr int RT_CH = 1024, RT_BLOCK = 256;
 // PER entries per thread (strided by RT_BLOCK inside the chunk), the first B
 // contributions of each loaded speculatively, the rest in batches of B; the
 // accumulation is always the strict per-entry sequence of rap_acc.
-template <int PER, int B>
+template <int PER, int B, int FUSE>
 __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const int* __restrict__ cptr,
                                                          const int* __restrict__ contrib,
                                                          const double* __restrict__ af, double* __restrict__ ac,
-                                                         int cstage) {
+                                                         int cstage, RapJacobi fj) {
     static_assert(PER * RT_BLOCK <= RT_CH && RT_CH % (PER * RT_BLOCK) == 0, "chunk split");
     extern __shared__ __align__(128) unsigned char rt_smem[];
     int* s_cp = reinterpret_cast<int*>(rt_smem);  // [2][RT_CH + 4]
@@ -753,8 +756,8 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
     };
     auto range = [&](int64_t j, int& a, int& b) {
         const int64_t c0 = j * RT_CH;
-        a = __ldg(cptr + c0);
-        b = __ldg(cptr + (c0 + RT_CH < nnz_c ? c0 + RT_CH : nnz_c));
+        a = __ldg(cptr + c0) & CP_MASK;
+        b = __ldg(cptr + (c0 + RT_CH < nnz_c ? c0 + RT_CH : nnz_c)) & CP_MASK;
     };
     int64_t j = blockIdx.x;
     if (tid == 0) {
@@ -783,13 +786,17 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
         const int ab = s_ab[st];
         for (int sub = 0; sub < RT_CH; sub += PER * RT_BLOCK) {
             int p0[PER], p1[PER], e[PER][B];
+            int dI[PER];  // coarse row of a diagonal entry (-1: not diagonal)
             double v[PER][B];
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int x = sub + k * RT_BLOCK + tid;
                 const bool ok = c0 + x < nnz_c;
-                p0[k] = ok ? cp[x] - ab : 0;
-                p1[k] = ok ? cp[x + 1] - ab : 0;
+                const int cx = ok ? cp[x] : 0;
+                // prefetched with the plan so its latency overlaps the gathers
+                dI[k] = (FUSE > 0 && (cx & CP_DIAG)) ? __ldg(fj.ccol + c0 + x) : -1;
+                p0[k] = ok ? (cx & CP_MASK) - ab : 0;
+                p1[k] = ok ? (cp[x + 1] & CP_MASK) - ab : 0;
 #pragma unroll
                 for (int t = 0; t < B; ++t) e[k][t] = p0[k] + t < p1[k] ? cn[p0[k] + t] : 0;
             }
@@ -819,6 +826,19 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
                         if (q + t < p1[k]) rap_acc(vv[t], ee[t], acc, part);
                 }
                 __stcs(ac + c, acc);
+                if constexpr (FUSE > 0) {
+                    // this thread holds a coarse diagonal a_II: the damped-Jacobi
+                    // weight of row I = its column (smoother.cpp:8-32)
+                    if (dI[k] >= 0) {
+                        const int I = dI[k];
+                        if (acc == 0.0) {
+                            atomicMin(fj.bad_c, I);
+                            fj.wc[I] = 0.0;
+                        } else {
+                            fj.wc[I] = __drcp_rn(acc);  // == 1.0 / acc, both correctly rounded
+                        }
+                    }
+                }
             }
         }
         __syncthreads();  // stage st consumed
@@ -827,20 +847,29 @@ __global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const in
     }
 }
 
-template <int PER, int B>
+template <int PER, int B, int FUSE>
 void launch_rap_tma(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
-                    double* ac, int cstage, size_t sm) {
+                    double* ac, int cstage, size_t sm, const RapJacobi& fj) {
     static const bool attr = [] {  // opt in once (dynamic + static may exceed 48 KB)
-        CK(cudaFuncSetAttribute(k_rap_tma<PER, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        CK(cudaFuncSetAttribute(k_rap_tma<PER, B, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         return true;
     }();
     (void)attr;
     int res = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_rap_tma<PER, B>, RT_BLOCK, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_rap_tma<PER, B, FUSE>, RT_BLOCK, sm));
     const int64_t chunks = (nnz_c + RT_CH - 1) / RT_CH;
     const unsigned grid =
         static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * std::max(res, 1)));
-    LAUNCH(c, "rap", bytes, (k_rap_tma<PER, B>), grid, RT_BLOCK, sm, nnz_c, cptr, contrib, af, ac, cstage);
+    LAUNCH(c, "rap", bytes, (k_rap_tma<PER, B, FUSE>), grid, RT_BLOCK, sm, nnz_c, cptr, contrib, af, ac, cstage, fj);
+}
+
+template <int PER, int B>
+void launch_rap_tma_fused(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, const int* contrib,
+                          const double* af, double* ac, int cstage, size_t sm, const RapJacobi* fj) {
+    if (!fj || !fj->wc)
+        launch_rap_tma<PER, B, 0>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, RapJacobi{});
+    else
+        launch_rap_tma<PER, B, 1>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, *fj);
 }
 
 // ---- end k_rap_tma
@@ -1306,7 +1335,7 @@ __device__ __forceinline__ double dr_sel(bool p, double a, double b) {
 
 template <bool GJ>
 __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double* gin, double* gout,
-                                                             int64_t* piv, int* status) {
+                                                             int64_t* piv, int* status, int* perm) {
     extern __shared__ double Ls[];  // LU: n x n multiplier history, row = physical row
     __shared__ double colbuf[2][DR_MAXN], coll[DR_MAXN], rowbuf[DR_MAXN], lbuf[DR_MAXN];
     __shared__ int lp[DR_MAXN], posof[DR_MAXN];
@@ -1476,6 +1505,10 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
             }
         }
     }
+    // the composed row swaps = the logical -> physical map (coarse_solve's
+    // rhs permutation, dense_lu.cpp:58-59)
+    if (!GJ && perm)
+        for (int i = tid; i < n; i += DR_THREADS) perm[i] = lp[i];
 }
 
 constexpr int LS_THREADS = 64;
@@ -1584,50 +1617,59 @@ constexpr int LW_Q = 5;  // rows per lane (n <= 160)
 
 __device__ __forceinline__ double bwd_chain(const double* __restrict__ mi, const double* __restrict__ xs, int j0,
                                             int n, double s) {
-    // s -= mi[j]*xs[j] for j = j0 .. n-1, ascending, in 8-entry chunks whose
-    // products are formed one chunk ahead.  The leading (n - j0) % 8 entries go
-    // first so the chunks end exactly at n.
-    int j = j0;
+    // s -= mi[j]*xs[j] for j = j0 .. n-1, ascending.  The leading (n - j0) % 8
+    // entries go first so the 8-entry chunks end exactly at n.  Three-stage
+    // software pipeline over the chunks: the shared-memory loads of chunk c+2
+    // and the products of chunk c+1 issue while chunk c's dependent DSUB
+    // chain runs, so (in-order issue) no instruction of the chain waits on a
+    // load: the sweep runs at the DSUB latency.
     const int rem = (n - j0) & 7;
-    double p[8], q[8];
+    const int jf = j0 + rem;          // first full chunk
+    const int nch = (n - jf) >> 3;    // full chunks
+    double ra[8], rx[8], p[8];
+    // issue everything the first chunks need up front
 #pragma unroll
-    for (int t = 0; t < 8; ++t) p[t] = (t < rem) ? dmul(mi[j + t], xs[j + t]) : 0.0;
-    j += rem;
-    const bool more = j < n;
-    if (more) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) q[t] = dmul(mi[j + t], xs[j + t]);
+    for (int t = 0; t < 8; ++t) {
+        ra[t] = mi[j0 + t];  // remainder (first rem used); reads stay inside the factor + slack
+        rx[t] = xs[j0 + t];
     }
+    double fa[8], fx[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        fa[t] = mi[jf + t];  // chunk 0 (harmless reads when nch == 0)
+        fx[t] = xs[jf + t];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) p[t] = dmul(ra[t], rx[t]);
 #pragma unroll
     for (int t = 0; t < 8; ++t)
         if (t < rem) s = dsub(s, p[t]);
-    if (!more) return s;
-    for (;;) {
-        j += 8;
-        if (j < n) {
+    if (nch == 0) return s;
+    // chunk 0 products; raw loads of chunk 1
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                s = dsub(s, q[t]);
-                p[t] = dmul(mi[j + t], xs[j + t]);
-            }
-        } else {
+    for (int t = 0; t < 8; ++t) p[t] = dmul(fa[t], fx[t]);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) s = dsub(s, q[t]);
-            return s;
-        }
-        j += 8;
-        if (j < n) {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                s = dsub(s, p[t]);
-                q[t] = dmul(mi[j + t], xs[j + t]);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) s = dsub(s, p[t]);
-            return s;
-        }
+    for (int t = 0; t < 8; ++t) {
+        ra[t] = mi[jf + 8 + t];
+        rx[t] = xs[jf + 8 + t];
     }
+    int jn = jf + 16;  // raw chunk to load next
+    for (int c = 0; c < nch; ++c) {
+        double q[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            s = dsub(s, p[t]);
+            q[t] = dmul(ra[t], rx[t]);  // chunk c+1 (garbage past the end, unused)
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            ra[t] = mi[jn + t];  // chunk c+2
+            rx[t] = xs[jn + t];
+            p[t] = q[t];
+        }
+        jn += 8;
+    }
+    return s;
 }
 
 __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __restrict__ m,
@@ -1640,7 +1682,7 @@ __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __res
     const int lane = threadIdx.x;
     const int nn2 = (n * n + 1) & ~1;
     double* ms = sm;        // n*n factor (TMA target)
-    double* xs = sm + nn2;  // n (+8 slack read by the chunked chain)
+    double* xs = sm + nn2;  // n (+16 slack read by the chunked chain)
     if (lane == 0) {
         mbar_init(&bar, 1);
         mbar_fence_init();
@@ -1676,7 +1718,7 @@ __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __res
         const int i = 32 * q + lane;
         if (i < n) xs[i] = y[q];
     }
-    if (lane < 8) xs[n + lane] = 0.0;
+    if (lane < 16) xs[n + lane] = 0.0;
     __syncwarp();
     // backward (row chain, lane 0)
     if (lane == 0) {
@@ -1982,7 +2024,7 @@ __global__ void k_rap_chunk_max(int64_t nnz_c, const int* __restrict__ cptr, int
     for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nchunks;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t c1 = (j + 1) * RT_CH < nnz_c ? (j + 1) * RT_CH : nnz_c;
-        m = max(m, cptr[c1] - cptr[j * RT_CH]);
+        m = max(m, (cptr[c1] & CP_MASK) - (cptr[j * RT_CH] & CP_MASK));
     }
     atomicMax(out, m);
 }
@@ -1999,21 +2041,24 @@ int rap_chunk_max(Ctx& c, int64_t nnz_c, const int* cptr) {
     return h;
 }
 
-void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
-                 double* ac, int64_t nnz_f, int max_chunk) {
-    if (nnz_c == 0) return;
-    // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1)
-    const double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
+bool rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr, const int* contrib, const double* af,
+                 double* ac, int64_t nnz_f, int max_chunk, const RapJacobi* fj) {
+    if (nnz_c == 0) return false;
+    // SURVEY.md 8(d) algorithmic bytes: 12*nnz(A_i) + 8*nnz(A_{i+1}) + 4*n_i + 4*(n_{i+1}+1);
+    // fused Jacobi (SURVEY.md 8(d) Jacobi 20*n per level; the fine diagonal
+    // value is gathered by the RAP itself): + 12*n_c (coarse) + 16*n_f (fine)
+    double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
+    if (fj && fj->wc) bytes += 12.0 * nc;
     if (max_chunk >= 0) {
         const int cstage = (max_chunk + 8 + 3) & ~3;
         const size_t sm = sizeof(int) * (2 * (RT_CH + 4) + 2 * static_cast<size_t>(cstage));
         if (sm <= 96 * 1024) {
             // contributions per coarse entry: 1.3 (C3 L0), 2.4 (L1), 3-6 below
             if (2 * nnz_f <= 5 * nnz_c)
-                launch_rap_tma<4, 2>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm);
+                launch_rap_tma_fused<4, 2>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, fj);
             else
-                launch_rap_tma<2, 4>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm);
-            return;
+                launch_rap_tma_fused<2, 4>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, fj);
+            return fj != nullptr && fj->wc != nullptr;
         }
     }
     // persistent grid: exactly the resident blocks, so the sweep stays in order
@@ -2025,6 +2070,7 @@ void rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr,
     const int64_t chunks = (nnz_c + RAP_BLOCK * RAP_ILP - 1) / (RAP_BLOCK * RAP_ILP);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * resident));
     LAUNCH(c, "rap", bytes, k_rap, grid, RAP_BLOCK, 0, nnz_c, cptr, contrib, af, ac);
+    return false;
 }
 void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_f, int64_t nnz_c) {
     if (a.nc == 0) return;
@@ -2075,8 +2121,8 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* per
             return true;
         }();
         (void)attr;
-        LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status);
-        lu_perm(c, n, piv, perm);
+        LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status,
+               perm);
         return;
     }
     if (n > 2048) invalid("coarse_factorize: coarse system larger than 2048 unknowns is not supported on device");
@@ -2095,11 +2141,11 @@ void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const doub
     if (perm && n <= 32 * LW_Q && !(old && old[0] == '1')) {
         static const bool attr = [] {
             CK(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(double) * (32 * LW_Q * 32 * LW_Q + 32 * LW_Q + 8))));
+                                    static_cast<int>(sizeof(double) * (32 * LW_Q * 32 * LW_Q + 32 * LW_Q + 16))));
             return true;
         }();
         (void)attr;
-        const size_t sm = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + n + 8);
+        const size_t sm = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + n + 16);
         LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve_warp, 1, 32, sm, static_cast<int>(n), m, perm, b, x, g);
         return;
     }
@@ -2130,7 +2176,8 @@ bool lu_factor_csr(Ctx& c, const CsrView& A, double* lu, int64_t* piv, int* stat
 
 bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {
     if (n == 0 || n > DR_MAXN) return false;
-    LAUNCH(c, "coarse", 0.0, k_dense_reg<true>, 1, DR_THREADS, 0, static_cast<int>(n), a, inv, piv, status);
+    LAUNCH(c, "coarse", 0.0, k_dense_reg<true>, 1, DR_THREADS, 0, static_cast<int>(n), a, inv, piv, status,
+           static_cast<int*>(nullptr));
     return true;
 }
 

@@ -366,8 +366,14 @@ __global__ void k_rap_plan(const uint64_t* keys, const int* vals, const int* row
         }
     }
 }
-__global__ void k_coarse_col(const uint64_t* ukeys, int64_t nnz_c, uint64_t mask, int* col) {
-    GRID_STRIDE(c, nnz_c) col[c] = static_cast<int>(ukeys[c] & mask);
+// coarse columns; bit 30 of cptr flags the diagonal entries (the numeric RAP
+// fuses the coarse Jacobi rebuild there, kernels.cuh RapJacobi)
+__global__ void k_coarse_col(const uint64_t* ukeys, int64_t nnz_c, uint64_t mask, int b, int* col, int* cptr) {
+    GRID_STRIDE(c, nnz_c) {
+        const int J = static_cast<int>(ukeys[c] & mask);
+        col[c] = J;
+        if (static_cast<int>(ukeys[c] >> b) == J) cptr[c] |= (1 << 30);
+    }
 }
 __global__ void k_set_int(int* p, int v) { *p = v; }
 
@@ -539,8 +545,9 @@ void rap_symbolic(Ctx& c, const CsrView& A, const int* agg, int64_t nc, RapSymbo
            pos.get(), m, out.contrib.get(), out.cptr.get(), ukeys);
     LAUNCH(c, "setup", 0.0, k_set_int, 1, 1, 0, out.cptr.get() + nnz_c, static_cast<int>(m));
     out.col.alloc(nnz_c, c.stream);
-    LAUNCH(c, "setup", 0.0, k_coarse_col, grid_for(nnz_c, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, mask,
-           out.col.get());
+    if (m >= (int64_t{1} << 30)) invalid("galerkin plan: more than 2^30 fine entries per GPU");
+    LAUNCH(c, "setup", 0.0, k_coarse_col, grid_for(nnz_c, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, mask, b,
+           out.col.get(), out.cptr.get());
     out.rp.alloc(nc + 1, c.stream);
     LAUNCH(c, "setup", 0.0, k_graph_ptr, grid_for(nc + 1, SB, c.num_sms * 16), SB, 0, ukeys, nnz_c, nc, b,
            out.rp.get());
