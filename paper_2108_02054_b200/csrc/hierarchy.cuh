@@ -31,6 +31,7 @@ struct Pattern {
     int max_span = 0;
     DevArray<int> rp, col, diag;
     ColCode cc;  // coded column stream for the row passes (mode 0: none)
+    int lag_groups = -1;  // max |j - i| / 32 + 2 of a coded pattern (k_rowpass_lag), lazily
 };
 inline void set_code(CsrView& v, const ColCode& cc) {
     v.cmode = cc.mode;
@@ -105,6 +106,7 @@ struct Work {
     std::vector<DevArray<double>> d0, d1;  // Chebyshev direction vectors (lazily allocated)
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh;
     DevArray<double> kq;  // sequential-dot mode: f - A u scratch
+    DevArray<int> lagdone;  // k_rowpass_lag round counters
     DevArray<KState> st;
     DevArray<double> partials;
     DevArray<unsigned> ticket;
@@ -158,8 +160,18 @@ void stage_rhs(Hier& h, const double* f, int location);
 // the RHS committed by the last STAGED rebuild (amgr_stage_rhs staged it)
 const double* committed_rhs(Hier& h);
 void commit_rhs(Hier& h);
-void vcycle(Hier& h, const double* f, double* u, Gate g = {});
-void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g = {});
+// The SpMV a Krylov solver applies to the V-cycle's output next (v = A u with
+// its dots): vcycle() fuses it into the last level-0 smoothing sweep
+// (smooth_then_spmv) when it can and sets done; else the caller runs it.
+struct NextSpmv {
+    int kind = 1;            // 1: spmv_dot (out[0] = ab . y), 2: spmv_dot2 (y . ab, y . y)
+    double* y = nullptr;
+    const double* ab = nullptr;
+    DotSink sink;
+    bool done = false;
+};
+void vcycle(Hier& h, const double* f, double* u, Gate g = {}, NextSpmv* nx = nullptr);
+void vcycle_from(Hier& h, size_t s, const double* f, double* u, Gate g = {}, NextSpmv* nx = nullptr);
 void bicgstab(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,
               amgr_solve_stats& st);
 void cg(Hier& h, const double* f, const double* u0, double* u, const amgr_solve_params& sp,

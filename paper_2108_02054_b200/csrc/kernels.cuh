@@ -74,6 +74,16 @@ void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double
 // y = A x ; out[0] = y . b ; out[1] = y . y
 void spmv_dot2(Ctx& c, const CsrView& A, const double* x, double* y, const double* b, DotSink s,
                Gate g = {});
+// Fused (k_rowpass_lag): one smoothing sweep out = u + (om*w)(f - A u) and
+// then y = A out with the Krylov dots of spmv_dot (kind 1: out[0] = ab . y)
+// or spmv_dot2 (kind 2: out[0] = y . ab, out[1] = y . y), in one persistent
+// kernel that re-reads A from L2 for the second pass.  Bit-identical to
+// vc_smooth + spmv_dot/spmv_dot2.  false: not applicable (only the coded
+// 1-byte level-0 layout), nothing launched.  done: >= 64 * rounds ints of
+// scratch; dgroups: max |j - i| / 32 + 2 over the matrix.
+bool smooth_then_spmv(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
+                      double* out, int kind, double* y, const double* ab, DotSink s, int* done, int dgroups,
+                      Gate g = {});
 // out[0] = || f - A x ||^2 ; optionally r = f - A x and r2 = r
 void resid_norm(Ctx& c, const CsrView& A, const double* f, const double* x, double* r, double* r2,
                 DotSink s, Gate g = {});

@@ -281,6 +281,223 @@ __global__ void __launch_bounds__(RP_BLOCK) k_rowpass(CsrView A, Op op, Gate g, 
     if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
 }
 
+// ---- k_rowpass_lag: two dependent row passes over the same matrix in ONE sweep
+// Op1 (a smoothing sweep producing x) and Op2 (an SpMV over that x) run in the
+// same persistent kernel: warp w processes, round by round, Op1 on its group
+// of round k and Op2 on its group of round k - LAG.  Op2 of a group gathers
+// x_j of rows up to `dgroups` groups away, so before it starts, lane 0 waits
+// (acquire) until every warp has published (release) Op1 of all rounds that
+// cover them.  The matrix rows of a group are thus streamed from DRAM once for
+// Op1 and re-read from L2 by Op2 LAG rounds later (one round = W groups =
+// ~9.5 MB of level-0 entries), saving one DRAM sweep of A per fused pair.
+// Rows, the group -> warp map, the grid and the per-thread dot order are those
+// of the separate passes, so results (and the blocked dots) are bit-identical.
+// All blocks must be co-resident (persistent grid at the kernel's occupancy).
+constexpr int LAG_SLOTS = 64;
+
+// Round counters: relaxed polling (an acquire would invalidate the SM's L1 on
+// every poll and cost the gathers of all warps their L1 hits) against
+// release increments.  When a reader sees round r complete, the rows of
+// every round <= r were performed in L2 before the counters moved; the
+// completed region is a prefix of whole 32-row groups (256-byte aligned), so
+// no L1 line holding a row of it can have been filled before the row was
+// final (rows are only gathered inside completed prefixes) — the Op2 gathers
+// may go through L1.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class Op1, class Op2, class CT>
+__global__ void __launch_bounds__(RP_BLOCK, RP_BLOCKS_PER_SM) k_rowpass_lag(CsrView A, Op1 op1, Op2 op2, Gate g, DotSink sink,
+                                                          int* __restrict__ done, int dgroups, int LAG_ROUNDS) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    constexpr int CH = RP_CH;
+    constexpr int ND = Op2::NDOT > 0 ? Op2::NDOT : 1;
+    constexpr bool CODED = sizeof(CT) < 4;
+    constexpr int ALN = 16 / static_cast<int>(sizeof(CT));
+    extern __shared__ __align__(128) unsigned char rp_smem[];
+    auto s_val = reinterpret_cast<double(*)[2][CH]>(rp_smem);
+    auto s_col = reinterpret_cast<CT(*)[2][CH]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH);
+    auto s_bar = reinterpret_cast<uint64_t(*)[2]>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH +
+                                                  sizeof(CT) * RP_WARPS * 2 * CH);
+    int* s_dict = reinterpret_cast<int*>(rp_smem + sizeof(double) * RP_WARPS * 2 * CH +
+                                         sizeof(CT) * RP_WARPS * 2 * CH + sizeof(uint64_t) * RP_WARPS * 2);
+    const CT* colstream = CODED ? static_cast<const CT*>(A.code) : reinterpret_cast<const CT*>(A.col);
+    if constexpr (sizeof(CT) == 1) {
+        for (int t = threadIdx.x; t < A.ndict; t += blockDim.x) s_dict[t] = __ldg(A.dict + t);
+        __syncthreads();
+    }
+    const int nnz4 = static_cast<int>((A.nnz + 3) & ~int64_t{3});
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = static_cast<int>(A.n);
+    const int ngroups = (n + 31) >> 5;
+    const int W = gridDim.x * RP_WARPS;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    const int G0 = blockIdx.x * RP_WARPS + w;
+    if (G0 < ngroups) {
+        uint64_t* bar = s_bar[w];
+        if (lane == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            mbar_fence_init();
+        }
+        __syncwarp();
+        auto issue = [&](int base, int end, int st) {
+            const int cnt = min(CH, end - base);
+            if (lane == 0) {
+                fence_proxy_async();
+                const int vcnt = CODED ? min(cnt, nnz4 - base) : cnt;
+                const uint32_t bv = static_cast<uint32_t>(vcnt) * 8u,
+                               bc = static_cast<uint32_t>(cnt) * static_cast<uint32_t>(sizeof(CT));
+                mbar_expect_tx(&bar[st], bv + bc);
+                tma_load_1d(&s_val[w][st][0], A.val + base, bv, &bar[st]);
+                tma_load_1d(&s_col[w][st][0], colstream + base, bc, &bar[st]);
+            }
+        };
+        auto colof = [&](int row, CT code) -> int {
+            if constexpr (sizeof(CT) == 1) return row + s_dict[code];
+            else if constexpr (sizeof(CT) == 2) return row + __ldg(A.dict + code);
+            else return code;
+        };
+        // aligned nnz range of a group (warp-uniform)
+        auto range_of = [&](int grp, int& ab, int& ae) {
+            const int row = grp * 32 + lane;
+            const int last = min(grp * 32 + 32, n);
+            const int rs = row < n ? __ldg(A.rp + row) : __ldg(A.rp + last);
+            const int re = row < n ? __ldg(A.rp + row + 1) : rs;
+            const int gs = __shfl_sync(0xffffffffu, rs, 0), ge = __shfl_sync(0xffffffffu, re, 31);
+            ab = gs & ~(ALN - 1);
+            ae = (ge + ALN - 1) & ~(ALN - 1);
+        };
+        const int nround = (ngroups - G0 + W - 1) / W;
+        const int nitem = 2 * (nround + LAG_ROUNDS);
+        // item t: round k = t / 2; t even: Op1 on round k, t odd: Op2 on round k - LAG
+        auto valid = [&](int t) {
+            const int k = t >> 1;
+            return (t & 1) == 0 ? k < nround : (k >= LAG_ROUNDS && k - LAG_ROUNDS < nround);
+        };
+        auto group_of = [&](int t) { return G0 + ((t & 1) == 0 ? (t >> 1) : (t >> 1) - LAG_ROUNDS) * W; };
+        auto next_valid = [&](int t) {
+            for (++t; t < nitem; ++t)
+                if (valid(t)) return t;
+            return -1;
+        };
+        int t = 0;  // item 0 (Op1, round 0) is always valid
+        int ab, ae;
+        range_of(G0, ab, ae);
+        int st = 0;
+        uint32_t phase = 0;
+        bool ready = false;
+        if (ae > ab) {
+            issue(ab, ae, st);
+            ready = true;
+        }
+        int ok_round = -1;  // rounds whose Op1 is known complete on every warp
+        while (t >= 0) {
+            const int G = group_of(t);
+            const bool second = (t & 1) != 0;
+            const int row = G * 32 + lane;
+            const int rs = row < n ? __ldg(A.rp + row) : 0, re = row < n ? __ldg(A.rp + row + 1) : 0;
+            typename Op1::Row rw1;
+            typename Op2::Row rw2;
+            if (row < n) {
+                if (second) rw2 = op2.load(row);
+                else rw1 = op1.load(row);
+            }
+            const int tn = next_valid(t);
+            int nab = 0, nae = 0;
+            if (tn >= 0) range_of(group_of(tn), nab, nae);
+            if (second) {
+                // every group Op2 of G gathers from must have finished Op1
+                // (round counters are split over LAG_SLOTS addresses so the
+                // release atomics of a round do not serialise on one line)
+                const int need = min(G + dgroups, ngroups - 1) / W;
+                while (ok_round < need) {
+                    const int r = ok_round + 1;
+                    const int act = min(W, ngroups - r * W);  // warps with a group in round r
+                    const int s0 = lane, s1 = lane + 32;
+                    const int e0 = act > s0 ? (act - 1 - s0) / LAG_SLOTS + 1 : 0;
+                    const int e1 = act > s1 ? (act - 1 - s1) / LAG_SLOTS + 1 : 0;
+                    const int* d = done + static_cast<int64_t>(r) * LAG_SLOTS;
+                    while (!__all_sync(0xffffffffu, ld_relaxed(d + s0) >= e0 && ld_relaxed(d + s1) >= e1))
+                        __nanosleep(32);
+                    ok_round = r;
+                }
+            }
+            int cb = ab;
+            // the chunk stream of this item, specialised per operator (one
+            // clean loop per Op instead of a per-batch branch)
+            auto run = [&](const auto& op, const auto& rw) {
+                double sum = 0.0;
+                while (ae > ab) {
+                    if (!ready) issue(cb, ae, st);
+                    int pb = -1, pe = 0;
+                    if (cb + CH < ae) {
+                        pb = cb + CH;
+                        pe = ae;
+                    } else if (tn >= 0 && nae > nab) {
+                        pb = nab;
+                        pe = nae;
+                    }
+                    if (pb >= 0) issue(pb, pe, st ^ 1);
+                    mbar_wait(&bar[st], (phase >> st) & 1u);
+                    phase ^= (1u << st);
+                    {
+                        int a = max(rs, cb);
+                        const int b = min(re, cb + CH);
+                        while (a < b) {
+                            const int cnt = min(RP_BATCH, b - a);
+                            const int k = a - cb;
+                            double xv[RP_BATCH];
+                            int cj[RP_BATCH];
+#pragma unroll
+                            for (int q = 0; q < RP_BATCH; ++q) cj[q] = colof(row, s_col[w][st][k + (q < cnt ? q : 0)]);
+                            gather_batch<RP_BATCH>(op, cj, xv);
+#pragma unroll
+                            for (int q = 0; q < RP_BATCH; ++q)
+                                if (q < cnt) sum = dadd(sum, dmul(s_val[w][st][k + q], xv[q]));
+                            a += cnt;
+                        }
+                    }
+                    __syncwarp();
+                    st ^= 1;
+                    const bool last = cb + CH >= ae;
+                    ready = pb >= 0;
+                    cb = pb;
+                    if (last) break;
+                }
+                if (row < n) op.finish(row, sum, rw, dots);
+            };
+            if (second)
+                run(op2, rw2);
+            else
+                run(op1, rw1);
+            if (!second) {
+                __syncwarp();  // the warp's rows of x, then one release increment
+                if (lane == 0) red_release_add(done + static_cast<int64_t>(t >> 1) * LAG_SLOTS + (G0 & (LAG_SLOTS - 1)), 1);
+            }
+            // rotate to the next item; its first chunk was prefetched if the
+            // current item had entries (else it is issued at the loop top)
+            if (tn < 0) break;
+            if (!ready || cb != nab) {
+                ready = false;
+            }
+            ab = nab;
+            ae = nae;
+            t = tn;
+        }
+    }
+    if constexpr (Op2::NDOT > 0) block_dots<Op2::NDOT>(dots, sink);
+}
+
 // ---- row-pass operators ----------------------------------------------------
 struct NoRow {};
 struct Row1 {
@@ -409,6 +626,36 @@ struct OpSpmvDot {
 };
 
 struct OpSpmvDot2 {
+    static constexpr int NDOT = 2;
+    using Row = Row1;
+    const double* xv;
+    double* y;
+    const double* b;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ Row load(int i) const { return {__ldg(b + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
+        y[i] = s;
+        d[0] = dadd(d[0], dmul(s, q.a));
+        d[1] = dadd(d[1], dmul(s, s));
+    }
+};
+
+// Op2 of k_rowpass_lag: x was written by other SMs inside the same kernel;
+// gathered only from completed 256-byte-aligned prefixes (see ld_relaxed)
+struct OpSpmvDotL2 {
+    static constexpr int NDOT = 1;
+    using Row = Row1;
+    const double* xv;
+    double* y;
+    const double* a;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ Row load(int i) const { return {__ldg(a + i)}; }
+    __device__ void finish(int i, double s, const Row& q, double* d) const {
+        y[i] = s;
+        d[0] = dadd(d[0], dmul(q.a, s));
+    }
+};
+struct OpSpmvDot2L2 {
     static constexpr int NDOT = 2;
     using Row = Row1;
     const double* xv;
@@ -2006,6 +2253,44 @@ void restrict_sum(Ctx& c, int64_t nc, const int* mptr, const int* midx, const do
     LAUNCH_PDL(c, "restrict", 0.0, k_restrict, grid_for(nc, 256, c.num_sms * 16), 256, 0, static_cast<int>(nc), mptr,
            midx, r, fc, wc, om, u0c, g);
 }
+template <class Op2>
+static bool launch_lag(Ctx& c, const CsrView& A, const OpSmooth& op1, const Op2& op2, Gate g, DotSink s,
+                       int* done, int dgroups, double bytes) {
+    using K = decltype(&k_rowpass_lag<OpSmooth, Op2, uint8_t>);
+    const K kern = &k_rowpass_lag<OpSmooth, Op2, uint8_t>;
+    constexpr size_t smem = static_cast<size_t>(RP_WARPS) * 2 * RP_CH * (8 + 1) + RP_WARPS * 2 * sizeof(uint64_t) +
+                            256 * sizeof(int);
+    static const int resident = [&] {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int b = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, RP_BLOCK, smem));
+        return b;
+    }();
+    if (resident < RP_BLOCKS_PER_SM) return false;  // the whole persistent grid must be co-resident
+    const int grid = c.num_sms * RP_BLOCKS_PER_SM;
+    const int W = grid * RP_WARPS;
+    const int64_t groups = (A.n + 31) / 32;
+    const int64_t rounds = (groups + W - 1) / W;
+    CK(cudaMemsetAsync(done, 0, sizeof(int) * static_cast<size_t>(rounds * LAG_SLOTS), c.stream));
+    static const int lag = [] {
+        const char* e = std::getenv("AMGR_LAG_ROUNDS");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    LAUNCH_PDL(c, "smooth_spmv", bytes, kern, grid, RP_BLOCK, smem, A, op1, op2, g, s, done, dgroups, lag);
+    return true;
+}
+
+bool smooth_then_spmv(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
+                      double* out, int kind, double* y, const double* ab, DotSink s, int* done, int dgroups,
+                      Gate g) {
+    if (A.cmode != 1 || A.n == 0 || dgroups <= 0) return false;
+    // one DRAM sweep of A (+ the vectors of both passes); the second sweep is L2
+    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n + (kind == 1 ? 24.0 : 24.0) * A.n;
+    const OpSmooth op1{f, w, om, u, out};
+    if (kind == 1) return launch_lag(c, A, op1, OpSpmvDotL2{out, y, ab}, g, s, done, dgroups, bytes);
+    return launch_lag(c, A, op1, OpSpmvDot2L2{out, y, ab}, g, s, done, dgroups, bytes);
+}
+
 void spmv_dot(Ctx& c, const CsrView& A, const double* x, double* y, const double* a, DotSink s, Gate g) {
     launch_rowpass(c, "spmv_dot", spmv_bytes(A) + 8.0 * A.n, A, OpSpmvDot{x, y, a}, g, s, true);
 }

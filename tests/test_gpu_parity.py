@@ -666,3 +666,22 @@ def test_rebuild_coarse_level_zero_diagonal_names_its_level(ctx, monkeypatch):
         with pytest.raises(amg.InvalidArgument) as eg:
             h.rebuild((rp, ci, v))
         assert str(eg.value) == str(er.value)
+
+
+@pytest.mark.parametrize("g,k", [(48, 7), (96, 20)])
+def test_lag_fused_smoothing_spmv_is_bit_identical(ctx, monkeypatch, g, k):
+    """k_rowpass_lag (last level-0 smoothing sweep + the Krylov SpMV/dots in
+    one pass over A_0) gives exactly the separate kernels' BiCGStab: same
+    iterations, same iterate bits, same residual."""
+    A = P.grid3d_values("dambreak", g, k)
+    f = P.rhs(g ** 3)
+    out = {}
+    for lag in ("0", "1"):
+        monkeypatch.setenv("AMGR_LAG_FUSE", lag)  # opt-in fused kernel vs the default separate passes
+        h = amg.setup(A, ctx=ctx)
+        u, st = amg.bicgstab(h, f)
+        out[lag] = (u, st)
+    (u0, s0), (u1, s1) = out["0"], out["1"]
+    assert s0.iterations == s1.iterations and s0.converged == s1.converged
+    assert np.array_equal(_bits(u0), _bits(u1))
+    assert _bits([s0.relative_residual])[0] == _bits([s1.relative_residual])[0]

@@ -32,7 +32,7 @@ def main():
     amg._check(L.amgr_problem_rhs(ctx.ptr, n, 42, f.data_ptr(), amg.DEVICE), ctx.ptr)
     u = torch.zeros(n, dtype=torch.float64, device="cuda")
     ctx.synchronize()
-    prm = amg.AmgParams(coarse_solve=os.environ.get("AMGR_COARSE", "inverse"))  # bench default
+    prm = amg.AmgParams(coarse_solve=os.environ.get("AMGR_COARSE", "exact"))  # bench default
     h = amg.setup(amg.DeviceCsr(n, n, nnz, rp.data_ptr(), ci.data_ptr(), v0.data_ptr()), prm, ctx=ctx)
     # warm-up
     h.rebuild_values(v1.data_ptr())
