@@ -313,7 +313,18 @@ amgr_status amgr_nccl_unique_id(void* out128);
 amgr_status amgr_dist_create(amgr_hier* global, const void* nccl_id128, int rank, int world, int top,
                              const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
                              amgr_dist** out);
-/* Global rebuild on every rank + gather of the local values (round 1). */
+/* amgr_dist_rebuild_values: global rebuild on every rank + gather of the
+ * local values (needs the global A_k on every rank).
+ * amgr_dist_rebuild_local: partial rebuild from RANK-LOCAL values — this
+ * rank's owned rows of A_k in the local CSR order (owned rows ascending, each
+ * row's entries in the global column order, i.e. global_values[nnz_map]).
+ * Each rank rebuilds the Jacobi weights of its rows and the numeric Galerkin
+ * product of its own coarse rows (communication-free: the partition is
+ * aggregate-consistent, so every member row is local; local plans built on the
+ * device at amgr_dist_create), one allgather replicates A_{top+1}, and the
+ * replicated levels are rebuilt on every rank.  Bit-identical to the global
+ * partial_update; errors name the global row and are raised on every rank. */
+amgr_status amgr_dist_rebuild_local(amgr_dist* d, const double* local_values, int location);
 /* Test transport: W ranks of ONE process (one host thread and one context
  * each, same device) exchange through stream-ordered device copies and host
  * barriers instead of NCCL, so the multi-rank device path can be checked on

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -163,6 +164,7 @@ PROTOTYPES = {
     "amgr_dist_loopback_destroy": (None, [_V]),
     "amgr_dist_create_loopback": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
     "amgr_dist_rebuild_values": (_I, [_V, _V, _I]),
+    "amgr_dist_rebuild_local": (_I, [_V, _V, _I]),
     "amgr_dist_vcycle": (_I, [_V, _V, _V]),
     "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),
     "amgr_dist_destroy": (None, [_V]),
@@ -343,8 +345,22 @@ class Context:
         _check(lib().amgr_probe_read(self._p, C.byref(n), C.byref(ms), C.byref(b)), self._p)
         return int(n.value), float(ms.value), float(b.value)
 
+    def _adopt(self, obj):
+        """Register an object owning device state of this context: closed
+        before the context is (garbage collection of reference cycles may
+        finalize a context before the objects using it)."""
+        if not hasattr(self, "_children"):
+            self._children = weakref.WeakSet()
+        self._children.add(obj)
+        return obj
+
     def close(self):
         if self._p:
+            for ch in list(getattr(self, "_children", ())):
+                try:
+                    ch.close()
+                except Exception:
+                    pass
             lib().amgr_ctx_destroy(self._p)
             self._p = C.c_void_p()
 
@@ -376,6 +392,7 @@ class Hierarchy:
         self._p = ptr
         self.ctx = ctx
         self.prm = prm
+        ctx._adopt(self)
 
     # --- introspection (parity dumps) ---
     def num_levels(self) -> int:
@@ -516,9 +533,9 @@ class Hierarchy:
         return y
 
     def close(self):
-        if self._p:
+        if self._p and self.ctx._p:
             lib().amgr_hier_destroy(self._p)
-            self._p = None
+        self._p = None
 
     def __del__(self):
         try:
@@ -608,6 +625,69 @@ def cg(h: Hierarchy, f, u0=None, prm: SolveParams | None = None):
     return _solve(lib().amgr_cg, h, f, u0, prm)
 
 
+# ---- single-operator entry points (the reference's free functions) ----------------
+def spmv(A, x, ctx: Context | None = None) -> np.ndarray:
+    """y = A x (csr.cpp:76-91), on the device (amgr_csr_spmv)."""
+    ctx = ctx or default_context()
+    A = CsrMatrix.of(A)
+    x = _f64(x)
+    if len(x) != A.ncols:
+        raise InvalidArgument("spmv: dimension mismatch")
+    y = np.zeros(A.nrows)
+    c = A._c()
+    _check(lib().amgr_csr_spmv(ctx.ptr, C.byref(c), x.ctypes.data, y.ctypes.data, HOST), ctx.ptr)
+    return y
+
+
+def build_smoother(A, omega: float = 0.72, ctx: Context | None = None) -> np.ndarray:
+    """JacobiSmoother::inv_diag of build_smoother(A, omega) (smoother.cpp:8-32)."""
+    ctx = ctx or default_context()
+    A = CsrMatrix.of(A)
+    w = np.zeros(A.nrows)
+    c = A._c()
+    _check(lib().amgr_build_smoother(ctx.ptr, C.byref(c), w.ctypes.data, HOST), ctx.ptr)
+    return w
+
+
+def smooth(inv_diag, A, f, u, sweeps: int, omega: float = 0.72, ctx: Context | None = None) -> np.ndarray:
+    """smooth(s, A, f, u, sweeps) (smoother.cpp:34-48); returns the smoothed u."""
+    ctx = ctx or default_context()
+    A = CsrMatrix.of(A)
+    w, f, u = _f64(inv_diag), _f64(f), _f64(u).copy()
+    if not (len(w) == len(f) == len(u) == A.nrows):
+        raise InvalidArgument("smooth: dimension mismatch")
+    c = A._c()
+    _check(lib().amgr_smooth(ctx.ptr, C.byref(c), w.ctypes.data, float(omega), f.ctypes.data, u.ctypes.data,
+                             int(sweeps), HOST), ctx.ptr)
+    return u
+
+
+def coarse_factorize(A, ctx: Context | None = None):
+    """DenseFactorization (lu row-major n*n, piv) of coarse_factorize(A) (dense_lu.cpp:10-50)."""
+    ctx = ctx or default_context()
+    A = CsrMatrix.of(A)
+    n = A.nrows
+    lu = np.zeros(n * n)
+    piv = np.zeros(n, np.int64)
+    c = A._c()
+    _check(lib().amgr_coarse_factorize(ctx.ptr, C.byref(c), lu.ctypes.data, piv.ctypes.data), ctx.ptr)
+    return lu, piv
+
+
+def coarse_solve(lu, piv, rhs, ctx: Context | None = None) -> np.ndarray:
+    """coarse_solve(f, rhs) (dense_lu.cpp:52-73)."""
+    ctx = ctx or default_context()
+    lu, rhs = _f64(lu), _f64(rhs)
+    piv = np.ascontiguousarray(piv, np.int64)
+    n = len(piv)
+    if len(rhs) != n:
+        raise InvalidArgument("coarse_solve: dimension mismatch")
+    x = np.zeros(n)
+    _check(lib().amgr_coarse_solve(ctx.ptr, n, lu.ctypes.data, piv.ctypes.data, rhs.ctypes.data, x.ctypes.data),
+           ctx.ptr)
+    return x
+
+
 def run_sequence(*args, **kwargs):
     """RunResult run_sequence(systems, StrategyConfig, AmgParams, SolveParams) — reuse.hpp:70-71."""
     from .reuse import run_sequence as _rs
@@ -621,6 +701,7 @@ class Matrix:
     def __init__(self, ptr, ctx: Context):
         self._p = ptr
         self.ctx = ctx
+        ctx._adopt(self)
         c = _Csr()
         _check(lib().amgr_matrix_csr(self._p, C.byref(c)), ctx.ptr)
         self.nrows, self.ncols, self.nnz = int(c.nrows), int(c.ncols), int(c.nnz)
@@ -644,9 +725,9 @@ class Matrix:
         return rp.astype(np.int64), ci[:self.nnz].astype(np.int64), val[:self.nnz]
 
     def close(self):
-        if self._p:
+        if self._p and self.ctx._p:
             lib().amgr_matrix_free(self._p)
-            self._p = None
+        self._p = None
 
     def __del__(self):
         try:

@@ -112,12 +112,85 @@ __global__ void k_rank_sum(int world, int k, const double* __restrict__ parts, d
     *outs[t] = s;
 }
 
+// ---- partitioned rebuild (rank-local values) ----------------------------------
+// local diagonal positions: owned row r has local column r (linear scan, the
+// local columns are not sorted: halo ids follow the owned ones)
+__global__ void k_local_diag(int64_t n, const int* __restrict__ rp, const int* __restrict__ col, int* dpos) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int d = -1;
+        for (int k = rp[r]; k < rp[r + 1]; ++k)
+            if (col[k] == static_cast<int>(r)) {
+                d = k;
+                break;
+            }
+        dpos[r] = d;
+    }
+}
+
+__global__ void k_scatter_inv(int64_t n, const int* __restrict__ map, int* __restrict__ inv) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        inv[map[k]] = static_cast<int>(k);
+}
+
+// Local Galerkin plan = the global plan restricted to this rank's coarse rows.
+// Local coarse row r is global row crow[r] (or base + r when crow is null);
+// its entries are the global row's entries in the same order (local CSR keeps
+// the global column order), local offsets lrp[r].  Counts first, then (after
+// an exclusive scan) the contributions, each fine index remapped through
+// ginv (global fine entry -> local entry of this rank; all members of an owned
+// coarse row are owned: aggregate-consistent partition) with its row-break bit.
+__global__ void k_lplan_count(int64_t nrows, const int* __restrict__ crow, int64_t base, const int* __restrict__ rpg,
+                              const int* __restrict__ lrp, const int* __restrict__ cptrg, int* __restrict__ cnt) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < nrows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t I = crow ? crow[r] : base + r;
+        const int g0 = rpg[I];
+        for (int e = lrp[r]; e < lrp[r + 1]; ++e) {
+            const int g = g0 + (e - lrp[r]);
+            cnt[e] = (cptrg[g + 1] & 0x3fffffff) - (cptrg[g] & 0x3fffffff);
+        }
+    }
+}
+__global__ void k_lplan_fill(int64_t nrows, const int* __restrict__ crow, int64_t base, const int* __restrict__ rpg,
+                             const int* __restrict__ lrp, const int* __restrict__ cptrg,
+                             const int* __restrict__ contribg, const int* __restrict__ ginv,
+                             const int* __restrict__ lcptr, int* __restrict__ lcontrib, int* bad) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < nrows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t I = crow ? crow[r] : base + r;
+        const int g0 = rpg[I];
+        for (int e = lrp[r]; e < lrp[r + 1]; ++e) {
+            const int g = g0 + (e - lrp[r]);
+            const int p0 = cptrg[g] & 0x3fffffff, p1 = cptrg[g + 1] & 0x3fffffff;
+            int q = lcptr[e];
+            for (int p = p0; p < p1; ++p, ++q) {
+                const int v = contribg[p];
+                const int l = ginv[v & 0x7fffffff];
+                if (l < 0) atomicOr(bad, 1);
+                lcontrib[q] = (l < 0 ? 0 : l) | (v & static_cast<int>(0x80000000u));
+            }
+        }
+    }
+}
+
+__global__ void k_set_last(int* lcptr, int64_t n, const int* cnt) {
+    if (n > 0) lcptr[n] = lcptr[n - 1] + cnt[n - 1];
+    else lcptr[0] = 0;
+}
+
 }  // namespace
 
 struct DistLevel {
     int64_t n_own = 0, n_halo = 0, nnz = 0, n_cown = 0;
     DevArray<int> rp, col, nnz_map, owned, agg, mptr, midx;
     DevArray<double> val, w;
+    // partitioned rebuild: local diagonal positions and the local Galerkin
+    // plan onto this rank's coarse rows (k_rap_tma, rap_numeric)
+    DevArray<int> dpos, lcptr, lcontrib;
+    int64_t lnnz_c = 0, lnc = 0;
+    int lmax_chunk = -1;
     DevArray<double> u0, x, out, f, r;  // u0/x carry halo space
     std::vector<int> send_peer, recv_peer;
     std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
@@ -190,6 +263,14 @@ struct DistHier {
     int64_t tpad = 0;
     DevArray<double> tsend, tgather, fT, uT;
     DevArray<int64_t> tcnt_d, tdispl_d;
+    // partitioned rebuild: this rank's rows of A_{T+1} are a contiguous entry
+    // range of the global level T+1; their values are allgathered (padded)
+    std::vector<int64_t> tvcnt, tvdispl;
+    int64_t tvpad = 0;
+    DevArray<double> tvsend, tvgather;
+    DevArray<int64_t> tvcnt_d, tvdispl_d;
+    DevArray<int> lerr;       // per partitioned level first bad local row
+    DevArray<double> errd, errall;
     // Krylov (level 0 local)
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh, ku;
     DevArray<double> dloc, dall;  // local dot results (up to 2) and the gathered partials
@@ -337,6 +418,157 @@ static void gather_local(DistHier& d) {
     }
 }
 
+// Local Galerkin plans for the partitioned rebuild, built on the device from
+// the global plan (setup.cuh RapSymbolic) of every partitioned level.
+static void build_local_plans(DistHier& d) {
+    Ctx& c = *d.ctx;
+    Hier& h = *d.g;
+    for (int i = 0; i <= d.T; ++i) {
+        DistLevel& L = d.lv[i];
+        const Level& G = h.lv[i];
+        const Level& GC = h.lv[i + 1];
+        if (!G.rap || G.T->smoothed) fail(AMGR_E_RUNTIME, "dist: level without a plain Galerkin plan");
+        LAUNCH(c, "dist", 0.0, k_local_diag, grid_for(L.n_own, 256, c.num_sms * 8), 256, 0, L.n_own, L.rp.get(),
+               L.col.get(), L.dpos.get());
+        DevArray<int> ginv(G.pat->nnz, c.stream);
+        CK(cudaMemsetAsync(ginv.get(), 0xff, sizeof(int) * static_cast<size_t>(G.pat->nnz), c.stream));
+        LAUNCH(c, "dist", 0.0, k_scatter_inv, grid_for(L.nnz, 256, c.num_sms * 8), 256, 0, L.nnz, L.nnz_map.get(),
+               ginv.get());
+        // this rank's coarse rows: the owned rows of level i+1, or at the top
+        // its contiguous transition range of level T+1
+        const int* crow = nullptr;
+        int64_t base = 0, nrows = 0;
+        const int* lrp = nullptr;
+        DevArray<int> trp;
+        if (i < d.T) {
+            crow = d.lv[i + 1].owned.get();
+            nrows = d.lv[i + 1].n_own;
+            lrp = d.lv[i + 1].rp.get();
+        } else {
+            base = d.tdispl[d.rank];
+            nrows = d.tcnt[d.rank];
+            std::vector<int> grp(static_cast<size_t>(nrows + 1));
+            d2h(grp.data(), GC.pat->rp.get() + base, nrows + 1, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            const int off = grp[0];
+            for (auto& x : grp) x -= off;
+            trp.alloc(nrows + 1, c.stream);
+            h2d(trp.get(), grp.data(), nrows + 1, c.stream);
+            lrp = trp.get();
+        }
+        L.lnc = nrows;
+        int nent = 0;
+        if (nrows > 0) d2h(&nent, lrp + nrows, 1, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        L.lnnz_c = nent;
+        DevArray<int> cnt(std::max(nent, 1), c.stream);
+        L.lcptr.alloc(nent + 1, c.stream);
+        if (nrows > 0)
+            LAUNCH(c, "dist", 0.0, k_lplan_count, grid_for(nrows, 256, c.num_sms * 8), 256, 0, nrows, crow, base,
+                   GC.pat->rp.get(), lrp, G.rap->cptr.get(), cnt.get());
+        if (nent > 0) exclusive_sum_i32(c, cnt.get(), L.lcptr.get(), nent);
+        LAUNCH(c, "dist", 0.0, k_set_last, 1, 1, 0, L.lcptr.get(), static_cast<int64_t>(nent), cnt.get());
+        int total = 0;
+        d2h(&total, L.lcptr.get() + nent, 1, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        if (total != L.nnz)
+            fail(AMGR_E_RUNTIME, "dist: local Galerkin plan does not cover the local entries (partition not "
+                                 "aggregate-consistent)");
+        L.lcontrib.alloc(std::max(total, 1), c.stream);
+        DevArray<int> bad(1, c.stream);
+        CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), c.stream));
+        if (nrows > 0)
+            LAUNCH(c, "dist", 0.0, k_lplan_fill, grid_for(nrows, 256, c.num_sms * 8), 256, 0, nrows, crow, base,
+                   GC.pat->rp.get(), lrp, G.rap->cptr.get(), G.rap->contrib.get(), ginv.get(), L.lcptr.get(),
+                   L.lcontrib.get(), bad.get());
+        if (d2h_scalar(bad.get(), c.stream)) fail(AMGR_E_RUNTIME, "dist: a member row of an owned aggregate is not local");
+        L.lmax_chunk = rap_chunk_max(c, L.lnnz_c, L.lcptr.get());
+    }
+    // transition values: entry ranges of every rank's level-(T+1) rows
+    const Level& GT = h.lv[d.T + 1];
+    std::vector<int> grp(static_cast<size_t>(GT.pat->n + 1));
+    d2h(grp.data(), GT.pat->rp.get(), GT.pat->n + 1, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    d.tvcnt.clear();
+    d.tvdispl.clear();
+    d.tvpad = 0;
+    for (int r = 0; r < d.world; ++r) {
+        const int64_t a = grp[static_cast<size_t>(d.tdispl[r])], b = grp[static_cast<size_t>(d.tdispl[r] + d.tcnt[r])];
+        d.tvdispl.push_back(a);
+        d.tvcnt.push_back(b - a);
+        d.tvpad = std::max<int64_t>(d.tvpad, b - a);
+    }
+    d.tvsend.alloc(std::max<int64_t>(d.tvpad, 1), c.stream);
+    d.tvgather.alloc(std::max<int64_t>(d.tvpad * d.world, 1), c.stream);
+    d.tvcnt_d.alloc(d.world, c.stream);
+    d.tvdispl_d.alloc(d.world, c.stream);
+    h2d(d.tvcnt_d.get(), d.tvcnt.data(), d.world, c.stream);
+    h2d(d.tvdispl_d.get(), d.tvdispl.data(), d.world, c.stream);
+    d.lerr.alloc(d.T + 1, c.stream);
+    d.errd.alloc(d.T + 1, c.stream);
+    d.errall.alloc(static_cast<int64_t>(d.T + 1) * d.world, c.stream);
+}
+
+// Partial rebuild from rank-local values (hierarchy.cpp:107-150 on the
+// partition): each rank rebuilds the Jacobi weights of its rows and the
+// numeric Galerkin product of its coarse rows from its own A_i entries
+// (communication-free: every member row is local), down to its rows of
+// A_{T+1}; one allgather replicates A_{T+1}; the replicated levels are
+// rebuilt on every rank.  Values and errors are those of the global rebuild.
+static void dist_rebuild_local(DistHier& d, const double* vals, int location) {
+    Ctx& c = *d.ctx;
+    Hier& h = *d.g;
+    DistLevel& L0 = d.lv[0];
+    CK(cudaMemcpyAsync(L0.val.get(), vals, sizeof(double) * static_cast<size_t>(L0.nnz),
+                       location == AMGR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    std::vector<int> big(static_cast<size_t>(d.T + 1), 0x7fffffff);
+    h2d(d.lerr.get(), big.data(), d.T + 1, c.stream);
+    for (int i = 0; i <= d.T; ++i) {
+        c.cur_level = i;
+        DistLevel& L = d.lv[i];
+        jacobi_rebuild(c, L.n_own, L.val.get(), L.dpos.get(), L.w.get(), d.lerr.get() + i);
+        double* out = i < d.T ? d.lv[i + 1].val.get() : d.tvsend.get();
+        rap_numeric(c, L.n_own, L.lnc, L.lnnz_c, L.lcptr.get(), L.lcontrib.get(), L.val.get(), out, L.nnz,
+                    L.lmax_chunk);
+    }
+    c.cur_level = d.T + 1;
+    allgather(d, d.tvsend.get(), d.tvgather.get(), d.tvpad);
+    LAUNCH(c, "dist", 0.0, k_unpad, grid_for(d.tvpad, 256, 64), 256, 0, d.world, d.tvpad, d.tvgather.get(),
+           d.tvdispl_d.get(), d.tvcnt_d.get(), h.lv[d.T + 1].val.get());
+    // the first bad row of each partitioned level, as a global row id, the
+    // minimum over ranks (every rank throws the same error)
+    std::vector<int> le(static_cast<size_t>(d.T + 1));
+    d2h(le.data(), d.lerr.get(), d.T + 1, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    std::vector<double> ge(static_cast<size_t>(d.T + 1));
+    for (int i = 0; i <= d.T; ++i) {
+        double g = 1e300;
+        if (le[i] != 0x7fffffff) {
+            int row = 0;
+            d2h(&row, d.lv[i].owned.get() + le[i], 1, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            g = row;
+        }
+        ge[i] = g;
+    }
+    h2d(d.errd.get(), ge.data(), d.T + 1, c.stream);
+    allgather(d, d.errd.get(), d.errall.get(), d.T + 1);
+    std::vector<double> all(static_cast<size_t>((d.T + 1) * d.world));
+    d2h(all.data(), d.errall.get(), (d.T + 1) * d.world, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    for (int i = 0; i <= d.T; ++i) {
+        double m = 1e300;
+        for (int r = 0; r < d.world; ++r) m = std::min(m, all[static_cast<size_t>(r * (d.T + 1) + i)]);
+        if (m < 1e300) {
+            std::ostringstream os;
+            os << "level " << i << ": build_smoother: zero diagonal at row " << static_cast<int64_t>(m);
+            invalid(os.str());
+        }
+    }
+    rebuild_levels_from(h, static_cast<size_t>(d.T + 1));
+    c.cur_level = -1;
+}
+
 }  // namespace amgr
 
 // ---- C-ABI ----------------------------------------------------------------------
@@ -403,6 +635,7 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
             up32(L.midx, s.midx, s.mptr[s.n_coarse_owned]);
             L.val.alloc(s.nnz, c.stream);
             L.w.alloc(s.n_own, c.stream);
+            L.dpos.alloc(s.n_own, c.stream);
             L.u0.alloc(s.n_own + s.n_halo, c.stream);
             L.x.alloc(s.n_own + s.n_halo, c.stream);
             L.out.alloc(s.n_own, c.stream);
@@ -450,6 +683,7 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
         d->douts.alloc(4, c.stream);
         amgr::work(H);
         amgr::gather_local(*d);
+        amgr::build_local_plans(*d);
         CK(cudaStreamSynchronize(c.stream));
         auto* o = new amgr_dist();
         o->d = std::move(d);
@@ -524,6 +758,11 @@ amgr_status amgr_dist_rebuild_values(amgr_dist* d, const double* global_values, 
         amgr::rebuild_values(*d->d->g, global_values, location);
         amgr::gather_local(*d->d);
     });
+}
+
+amgr_status amgr_dist_rebuild_local(amgr_dist* d, const double* local_values, int location) {
+    if (!local_values) return AMGR_E_INVALID_ARGUMENT;
+    return dist_guard(d, [&] { amgr::dist_rebuild_local(*d->d, local_values, location); });
 }
 
 amgr_status amgr_dist_vcycle(amgr_dist* d, const double* f_local, double* u_local) {

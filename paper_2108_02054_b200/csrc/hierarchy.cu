@@ -368,7 +368,7 @@ static void build_row_plans(Hier& h) {
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans:
 // the Galerkin chain, then the per-level smoother rebuilds (main stream)
 // concurrently with the coarsest factorization (side stream).
-void numeric_pass(Hier& h, PhaseClock& clk) {
+void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
     Ctx& c = *h.ctx;
     Work& W = work(h);
     const size_t L = h.lv.size();
@@ -392,7 +392,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
     const char* fe = std::getenv("AMGR_FUSE_JACOBI");
     const bool jac = h.prm.smoother == AMGR_SMOOTHER_JACOBI && fe && fe[0] == '1';
     std::vector<char> wdone(L, 0);
-    for (size_t i = 0; i + 1 < L; ++i) {
+    for (size_t i = start; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
         clk.begin(PH_GALERKIN);
@@ -457,7 +457,7 @@ void numeric_pass(Hier& h, PhaseClock& clk) {
         coarse_factorize(h, W.err.get() + L);
         clk.end(PH_COARSE);
     });
-    for (size_t i = 0; i + 1 < L; ++i) {
+    for (size_t i = start; i + 1 < L; ++i) {
         if (wdone[i]) continue;
         c.cur_level = static_cast<int>(i);
         clk.begin(PH_SMOOTHER);
@@ -802,6 +802,18 @@ std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const Amg
     for (size_t i = 0; i < out->lv.size(); ++i) out->lv[i].val.alloc(out->lv[i].pat->nnz, c.stream);
     rebuild_into(*out, A);
     return out;
+}
+
+// Rebuild of levels start.. only (their A_start values already in place):
+// the distributed rebuild's replicated tail (dist.cu).  Same kernels, order
+// and error reporting as rebuild_into.
+void rebuild_levels_from(Hier& h, size_t start) {
+    work(h);
+    reset_err(h);
+    PhaseClock clk(*h.ctx);
+    numeric_pass(h, clk, start);
+    check_rebuild_errors(h, "build_smoother");
+    h.tm = clk.collect();
 }
 
 void rebuild(Hier& h, const amgr_csr& A) {

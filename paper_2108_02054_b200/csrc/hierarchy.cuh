@@ -148,6 +148,8 @@ struct Hier {
 std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p);
 std::unique_ptr<Hier> partial_update(const Hier& h, const amgr_csr& A, const AmgP& p);
 void rebuild(Hier& h, const amgr_csr& A);
+// numeric rebuild of levels start.. from the values already in level `start`
+void rebuild_levels_from(Hier& h, size_t start);
 // single-operator entry points (device vectors; lu/piv/rhs/x of the LU pair on the host)
 void op_spmv(Ctx& c, const amgr_csr& A, const double* x, double* y);
 void op_build_smoother(Ctx& c, const amgr_csr& A, double* w);

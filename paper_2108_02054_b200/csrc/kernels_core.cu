@@ -969,7 +969,7 @@ constexpr int RT_CH = 1024, RT_BLOCK = 256;
 // contributions of each loaded speculatively, the rest in batches of B; the
 // accumulation is always the strict per-entry sequence of rap_acc.
 template <int PER, int B, int FUSE>
-__global__ void __launch_bounds__(RT_BLOCK, 5) k_rap_tma(int64_t nnz_c, const int* __restrict__ cptr,
+__global__ void __launch_bounds__(RT_BLOCK, FUSE > 0 ? 4 : 5) k_rap_tma(int64_t nnz_c, const int* __restrict__ cptr,
                                                          const int* __restrict__ contrib,
                                                          const double* __restrict__ af, double* __restrict__ ac,
                                                          int cstage, RapJacobi fj) {

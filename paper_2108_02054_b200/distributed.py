@@ -5,7 +5,7 @@ reductions) is NCCL inside libamgr_b200.so on the context stream.
 
     h = amg.setup(A_global)                      # same hierarchy on every rank
     ds = DistSolver(h, rank, world, nccl_id)     # partition (partition.py) + NCCL comm
-    ds.rebuild_values(values_ptr)                # partial reuse step
+    ds.rebuild_local(local_values)               # partial reuse step from this rank's rows
     stats = ds.bicgstab(f_local_ptr, u_local_ptr)
 """
 from __future__ import annotations
@@ -98,6 +98,7 @@ class DistSolver:
             _check(lib().amgr_dist_create(h._p, idb, rank, world, T, levels, int(t_counts.sum()),
                                           t_counts.ctypes.data, C.byref(self._p)), h.ctx.ptr)
         self.owned0 = self.plan.levels[0].owned
+        h.ctx._adopt(self)
 
     @property
     def n_local(self) -> int:
@@ -105,6 +106,22 @@ class DistSolver:
 
     def rebuild_values(self, global_values_ptr: int, device: bool = True):
         _check(lib().amgr_dist_rebuild_values(self._p, global_values_ptr, 1 if device else 0), self.h.ctx.ptr)
+
+    def local_values(self, global_values) -> np.ndarray:
+        """This rank's A_0 entries in local CSR order (global_values[nnz_map])."""
+        return np.ascontiguousarray(np.asarray(global_values, np.float64)[self.plan.levels[0].nnz_map])
+
+    def rebuild_local(self, local_values, device: bool | None = None):
+        """Partial rebuild from rank-local values (amgr_dist_rebuild_local):
+        a device pointer (int) or a host array of len(nnz_map) entries."""
+        if isinstance(local_values, int):
+            _check(lib().amgr_dist_rebuild_local(self._p, local_values, 1 if device in (None, True) else 0),
+                   self.h.ctx.ptr)
+            return
+        v = np.ascontiguousarray(local_values, np.float64)
+        if len(v) != len(self.plan.levels[0].nnz_map):
+            raise ValueError("rebuild_local: expected the rank's local entries")
+        _check(lib().amgr_dist_rebuild_local(self._p, v.ctypes.data, 0), self.h.ctx.ptr)
 
     def vcycle(self, f_ptr: int, u_ptr: int):
         _check(lib().amgr_dist_vcycle(self._p, f_ptr, u_ptr), self.h.ctx.ptr)
@@ -117,9 +134,9 @@ class DistSolver:
         return SolveStats(int(st.iterations), float(st.relative_residual), bool(st.converged), bool(st.breakdown))
 
     def close(self):
-        if self._p:
+        if self._p and self.h.ctx._p:
             lib().amgr_dist_destroy(self._p)
-            self._p = None
+        self._p = None
 
     def __del__(self):
         try:

@@ -685,3 +685,50 @@ def test_lag_fused_smoothing_spmv_is_bit_identical(ctx, monkeypatch, g, k):
     assert s0.iterations == s1.iterations and s0.converged == s1.converged
     assert np.array_equal(_bits(u0), _bits(u1))
     assert _bits([s0.relative_residual])[0] == _bits([s1.relative_residual])[0]
+
+
+@pytest.mark.parametrize("name", ["dambreak_24_k20", "blob_20", "random_300", "poisson2d_64"])
+def test_level_spmv_bit_exact(ctx, name):
+    """amgr_spmv (k_rowpass<OpSpmv> on every level: coded 1-/2-byte and raw
+    column streams) and the single-operator amgr_csr_spmv equal the
+    reference's spmv (csr.cpp:76-85) bit for bit."""
+    make, kw = CASES[name]
+    A = make()
+    h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
+    r = ref.setup(A, ref.params(**kw))
+    rng = np.random.default_rng(4)
+    for l, RL in enumerate(r.levels):
+        x = rng.uniform(-1, 1, len(RL.A[0]) - 1)
+        assert np.array_equal(_bits(h.spmv(l, x)), _bits(ref.spmv(RL.A, x))), f"level {l}"
+    x = rng.uniform(-1, 1, len(A[0]) - 1)
+    assert np.array_equal(_bits(amg.spmv(A, x, ctx=ctx)), _bits(ref.spmv(A, x)))
+
+
+def test_single_operator_entry_points(ctx):
+    """build_smoother / smooth / coarse_factorize / coarse_solve on one matrix
+    (the reference's free functions) against the hierarchy's own results and
+    the reference's arithmetic, incl. error texts."""
+    A = P.grid3d_values("dambreak", 10, 4)
+    r = ref.setup(A)
+    w = amg.build_smoother(A, 0.72, ctx=ctx)
+    assert np.array_equal(_bits(w), _bits(r.levels[0].inv_diag))
+    f = P.rhs(1000)
+    # one sweep from u0: u + (om*w)(f - A u), elementwise IEEE ops as smoother.cpp:46
+    u0 = np.random.default_rng(2).uniform(-1, 1, 1000)
+    expect = u0.copy()
+    for _ in range(3):
+        expect = expect + (0.72 * w) * (f - ref.spmv(A, expect))
+    assert np.array_equal(_bits(amg.smooth(w, A, f, u0, 3, 0.72, ctx=ctx)), _bits(expect))
+    # coarsest matrix of the hierarchy: factor and solve as the hierarchy does
+    Lc = r.levels[-1].A
+    lu, piv = amg.coarse_factorize(Lc, ctx=ctx)
+    assert np.array_equal(piv, r.piv) and np.array_equal(_bits(lu), _bits(r.lu))
+    b = np.random.default_rng(3).uniform(-1, 1, len(piv))
+    x = amg.coarse_solve(lu, piv, b, ctx=ctx)
+    assert np.allclose(ref.spmv(Lc, x), b, rtol=1e-9, atol=1e-12)
+    bad = (np.array([0, 1, 2]), np.array([0, 0]), np.array([1.0, 1.0]))
+    with pytest.raises(amg.InvalidArgument, match="build_smoother: zero diagonal at row 1"):
+        amg.build_smoother(bad, ctx=ctx)
+    sing = P.csr_from_dense_rows([[(0, 1.0), (1, 1.0)], [(0, 1.0), (1, 1.0)]], 2)
+    with pytest.raises(amg.RuntimeFailure, match="singular"):
+        amg.coarse_factorize(sing, ctx=ctx)
