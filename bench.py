@@ -266,9 +266,11 @@ def run_reference_arm(a):
 # --------------------------------------------------------------------------------------
 def run_partitioned(a, rank, world, local):
     """One global C3 system, rows partitioned over the ranks (amgr_dist_*):
-    per step the distributed rebuild (global numeric rebuild + local value
-    gathers) and the partitioned BiCGStab (NCCL halo exchange, transition
-    allgather, replicated coarse levels, rank-ordered dots)."""
+    per step the partitioned rebuild from each rank's own rows of A_k
+    (amgr_dist_rebuild_local: local Jacobi + local Galerkin products, one
+    allgather of A_{top+1}, replicated tail) and the partitioned BiCGStab
+    (NCCL halo exchange, transition allgather, replicated coarse levels,
+    rank-ordered dots)."""
     import torch
 
     import paper_2108_02054_b200 as amg
@@ -307,11 +309,17 @@ def run_partitioned(a, rank, world, local):
     own = torch.from_numpy(ds.owned0).cuda()
     fl = f[own].contiguous()
     ul = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+    # each rank's OWN rows of A_k (local CSR order): the only A_k data the
+    # partitioned rebuild (amgr_dist_rebuild_local) reads
+    nmap = torch.from_numpy(ds.plan.levels[0].nnz_map).cuda()
+    lvals = [torch.cat([v[nmap], torch.zeros(8, dtype=torch.float64, device="cuda")]) for v in vals]
+    del vals
+    nnz_local = int(nmap.numel())
     torch.cuda.synchronize()
     sp = amg.SolveParams()
     ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
     for k in range(1, 1 + W):
-        ds.rebuild_values(vals[k].data_ptr())
+        ds.rebuild_local(lvals[k].data_ptr(), device=True)
         ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
     ctx.synchronize()
 
@@ -331,7 +339,7 @@ def run_partitioned(a, rank, world, local):
     with ClockSampler(local) as clk:
         ev[0].record(stream)
         for j, k in enumerate(range(1 + W, 1 + W + K)):
-            ds.rebuild_values(vals[k].data_ptr())
+            ds.rebuild_local(lvals[k].data_ptr(), device=True)
             ev[2 * j + 1].record(stream)
             st = ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
             ev[2 * j + 2].record(stream)
@@ -368,10 +376,10 @@ def run_partitioned(a, rank, world, local):
     if not a.no_e2e:
         hv = []
         for k in range(1 + W, 1 + W + K):
-            tt = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
-            tt.copy_(vals[k][:nnz])
+            tt = torch.empty(nnz_local, dtype=torch.float64, pin_memory=True)
+            tt.copy_(lvals[k][:nnz_local])
             hv.append(tt)
-        dv = torch.empty(nnz + 8, dtype=torch.float64, device="cuda")
+        dv = torch.empty(nnz_local + 8, dtype=torch.float64, device="cuda")
         fh = torch.empty(ds.n_local, dtype=torch.float64, pin_memory=True)
         fh.copy_(fl)
         uh = torch.empty(ds.n_local, dtype=torch.float64, pin_memory=True)
@@ -380,10 +388,10 @@ def run_partitioned(a, rank, world, local):
         barrier()
         e0 = time.perf_counter()
         for tt in hv:
-            dv[:nnz].copy_(tt, non_blocking=True)
+            dv[:nnz_local].copy_(tt, non_blocking=True)
             fl.copy_(fh, non_blocking=True)
             torch.cuda.synchronize()
-            ds.rebuild_values(dv.data_ptr())
+            ds.rebuild_local(dv.data_ptr(), device=True)
             ds.bicgstab(fl.data_ptr(), ul.data_ptr(), sp)
             uh.copy_(ul)
         torch.cuda.synchronize()
@@ -394,7 +402,7 @@ def run_partitioned(a, rank, world, local):
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": 8 * nnz + 8 * ds.n_local,
+        e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": 8 * nnz_local + 8 * ds.n_local,
                "d2h_bytes_per_step": 8 * ds.n_local, "timer": "host wall clock, max over ranks"}
     if rank == 0:
         out = {"metric": METRIC, "value": total_ms / K, "unit": "ms/step", "n_gpus": world, "steps": K, "warmup": W,
@@ -407,8 +415,9 @@ def run_partitioned(a, rank, world, local):
                "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
                "setup_s": setup_s, "plan_s": plan_s, "clocks": clk.summary(), "gpu_launches": launches,
                "e2e": e2e, "roofline": roofline, "cpu_baseline": None,
-               "note": ("one global system row-partitioned over the ranks (amgr_dist_*: NCCL halo send/recv, "
-                        "transition allgather, rank-ordered dots); levels below replicate_below rows replicated; "
+               "note": ("one global system row-partitioned over the ranks (amgr_dist_*: rebuild from rank-local "
+                        "rows, NCCL halo send/recv, transition allgather, rank-ordered dots); levels below "
+                        "replicate_below rows replicated; "
                         f"replicate_below={a.replicate_below}")}
         emit(out)
     ds.close()

@@ -166,3 +166,37 @@ def hierarchy_from_oracle(h):
     for L in h.levels:
         out.append({"n": len(L.A[0]) - 1, "rp": L.A[0], "col": L.A[1], "agg": L.agg})
     return out
+
+
+def local_galerkin(L: LocalLevel, local_vals, agg_glob, coarse_rows, crp, ccol):
+    """Partitioned numeric Galerkin product (host statement of what
+    amgr_dist_rebuild_local runs with device plans): the values of this rank's
+    coarse rows `coarse_rows` (global ids, ascending) of A_{i+1}, from ONLY the
+    rank's local entries of A_i.  Per coarse row I and coarse column J:
+    acc = 0; for each member fine row m of I ascending: part = 0; for each
+    local entry (m, k) in column order with agg(col k) = J: part += a_mk;
+    acc += part (two-level bracket of spmm(R, spmm(A, P)), csr.cpp:145-194,
+    SURVEY.md F4).  Members are local by aggregate consistency; columns are
+    mapped to global ids (owned / halo) only to look up their aggregate.
+    Returns the concatenated row values in the global coarse CSR order."""
+    gcol = np.where(L.col < L.n_own, L.owned[np.minimum(L.col, L.n_own - 1)],
+                    L.halo[np.maximum(L.col - L.n_own, 0)] if len(L.halo) else 0)
+    cagg = np.asarray(agg_glob)[gcol]  # coarse column of every local entry
+    out = []
+    # members of each coarse row (local fine ids ascending): rows whose aggregate is I
+    own_agg = np.asarray(agg_glob)[L.owned]
+    order = np.argsort(own_agg, kind="stable")
+    sa = own_agg[order]
+    for I in coarse_rows:
+        a, b = np.searchsorted(sa, I), np.searchsorted(sa, I, side="right")
+        cols = ccol[crp[I]:crp[I + 1]]
+        acc = {int(J): 0.0 for J in cols}
+        for m in order[a:b]:
+            part = {}
+            for k in range(L.rp[m], L.rp[m + 1]):
+                J = int(cagg[k])
+                part[J] = part.get(J, 0.0) + float(local_vals[k])
+            for J, p in part.items():
+                acc[J] = acc[J] + p
+        out.append(np.array([acc[int(J)] for J in cols], np.float64))
+    return np.concatenate(out) if out else np.zeros(0)

@@ -69,9 +69,13 @@ class Comm:
         t = torch.from_numpy(np.ascontiguousarray(v))
         sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(self.dist.get_world_size())]
         self.dist.all_gather(sizes, torch.tensor([len(v)]))
-        out = [torch.zeros(int(s.item()), dtype=torch.float64) for s in sizes]
-        self.dist.all_gather(out, t)
-        return np.concatenate([o.numpy() for o in out])
+        # padded blocks (gloo wants equal sizes; the device path pads the same way)
+        pad = max(int(s.item()) for s in sizes)
+        tp = torch.zeros(pad, dtype=torch.float64)
+        tp[:len(v)] = t
+        out = [torch.zeros(pad, dtype=torch.float64) for _ in sizes]
+        self.dist.all_gather(out, tp)
+        return np.concatenate([o.numpy()[:int(s.item())] for o, s in zip(out, sizes)])
 
     def sum_ordered(self, x):
         """deterministic: gather per-rank partials, add in rank order"""
@@ -188,6 +192,63 @@ def _worker(rank, world, port, out_path):
     np.savez(out_path + f".{rank}.npz", owned=plan.levels[0].owned, u=u_own, us=us, it=it, conv=conv,
              top=plan.top, halos=[len(L.halo) for L in plan.levels])
     dist.destroy_process_group()
+
+
+def _rebuild_worker(rank, world, port, out_path):
+    """Partitioned rebuild from rank-local values (amgr_dist_rebuild_local's
+    algorithm, host statement partition.local_galerkin): local Jacobi weights
+    and the Galerkin rows of the rank's coarse rows from ONLY its own A_k
+    entries, the level-(top+1) rows allgathered."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    A = P.grid3d_values("dambreak", 14, 21)
+    A2 = P.grid3d_values("dambreak", 14, 35)
+    H = O.setup(A)
+    struct = PT.hierarchy_from_oracle(H)
+    plan = PT.build_plan(struct, rank, world, replicate_below=100)
+    comm = Comm(dist)
+    T = plan.top
+    vals = np.asarray(A2[2], np.float64)[plan.levels[0].nnz_map]  # the only A_k data this rank sees
+    res = {}
+    for i in range(T + 1):
+        L = plan.levels[i]
+        diag = np.array([vals[L.rp[r] + np.nonzero(L.col[L.rp[r]:L.rp[r + 1]] == r)[0][0]] for r in range(L.n_own)])
+        res[f"w{i}"] = 1.0 / diag
+        res[f"own{i}"] = L.owned
+        crp, ccol = struct[i + 1]["rp"], struct[i + 1]["col"]
+        if i < T:
+            rows = plan.levels[i + 1].owned
+        else:
+            rows = np.nonzero(plan.owner[T + 1] == rank)[0]
+        cv = PT.local_galerkin(L, vals, struct[i]["agg"], rows, crp, ccol)
+        if i < T:
+            vals = cv  # owned rows of level i+1 in local CSR order (= global order per row)
+        else:
+            res["AT1"] = comm.allgather_concat(cv)
+    np.savez(out_path + f".{rank}.npz", top=T, **res)
+    dist.destroy_process_group()
+
+
+def test_partitioned_rebuild_from_local_values_gloo(tmp_path):
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "rb")
+    world = 2
+    mp.spawn(_rebuild_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    A = P.grid3d_values("dambreak", 14, 21)
+    A2 = P.grid3d_values("dambreak", 14, 35)
+    Hu = O.partial_update(O.setup(A), A2)
+    for r in range(world):
+        d = np.load(out + f".{r}.npz")
+        T = int(d["top"])
+        assert T >= 1
+        for i in range(T + 1):
+            w_ref = Hu.levels[i].w[d[f"own{i}"]]
+            np.testing.assert_array_equal(d[f"w{i}"].view(np.int64), w_ref.view(np.int64))
+        np.testing.assert_array_equal(d["AT1"].view(np.int64), np.asarray(Hu.levels[T + 1].A[2]).view(np.int64))
 
 
 def _free_port():

@@ -12,47 +12,59 @@ __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a,
 
 __device__ __forceinline__ double bwd_chain(const double* __restrict__ mi, const double* __restrict__ xs, int j0,
                                             int n, double s) {
-    int j = j0;
+    // s -= mi[j]*xs[j] for j = j0 .. n-1, ascending.  The leading (n - j0) % 8
+    // entries go first so the 8-entry chunks end exactly at n.  Three-stage
+    // software pipeline over the chunks: the shared-memory loads of chunk c+2
+    // and the products of chunk c+1 issue while chunk c's dependent DSUB
+    // chain runs, so (in-order issue) no instruction of the chain waits on a
+    // load: the sweep runs at the DSUB latency.
     const int rem = (n - j0) & 7;
-    double p[8], q[8];
+    const int jf = j0 + rem;          // first full chunk
+    const int nch = (n - jf) >> 3;    // full chunks
+    double ra[8], rx[8], p[8];
+    // issue everything the first chunks need up front
 #pragma unroll
-    for (int t = 0; t < 8; ++t) p[t] = (t < rem) ? xmul(mi[j + t], xs[j + t]) : 0.0;
-    j += rem;
-    const bool more = j < n;
-    if (more) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) q[t] = xmul(mi[j + t], xs[j + t]);
+    for (int t = 0; t < 8; ++t) {
+        ra[t] = mi[j0 + t];  // remainder (first rem used); reads stay inside the factor + slack
+        rx[t] = xs[j0 + t];
     }
+    double fa[8], fx[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        fa[t] = mi[jf + t];  // chunk 0 (harmless reads when nch == 0)
+        fx[t] = xs[jf + t];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) p[t] = xmul(ra[t], rx[t]);
 #pragma unroll
     for (int t = 0; t < 8; ++t)
         if (t < rem) s = xsub(s, p[t]);
-    if (!more) return s;
-    for (;;) {
-        j += 8;
-        if (j < n) {
+    if (nch == 0) return s;
+    // chunk 0 products; raw loads of chunk 1
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                s = xsub(s, q[t]);
-                p[t] = xmul(mi[j + t], xs[j + t]);
-            }
-        } else {
+    for (int t = 0; t < 8; ++t) p[t] = xmul(fa[t], fx[t]);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) s = xsub(s, q[t]);
-            return s;
-        }
-        j += 8;
-        if (j < n) {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                s = xsub(s, p[t]);
-                q[t] = xmul(mi[j + t], xs[j + t]);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) s = xsub(s, p[t]);
-            return s;
-        }
+    for (int t = 0; t < 8; ++t) {
+        ra[t] = mi[jf + 8 + t];
+        rx[t] = xs[jf + 8 + t];
     }
+    int jn = jf + 16;  // raw chunk to load next
+    for (int c = 0; c < nch; ++c) {
+        double q[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            s = xsub(s, p[t]);
+            q[t] = xmul(ra[t], rx[t]);  // chunk c+1 (garbage past the end, unused)
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            ra[t] = mi[jn + t];  // chunk c+2
+            rx[t] = xs[jn + t];
+            p[t] = q[t];
+        }
+        jn += 8;
+    }
+    return s;
 }
 
 template <int MODE>  // 0 full, 1 no division (multiply), 2 chain only (no per-row overhead measured separately)
@@ -91,7 +103,7 @@ __global__ void k(int n, const double* __restrict__ m, const double* b, double* 
         const int i = 32 * q + lane;
         if (i < n) xs[i] = y[q];
     }
-    if (lane < 8) xs[n + lane] = 0.0;
+    if (lane < 16) xs[n + lane] = 0.0;
     __syncwarp();
     long long t2 = clock64();
     long long tdiv = 0, tchain = 0;
@@ -137,7 +149,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(m, h.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
     std::vector<double> hb(n, 1.0);
     cudaMemcpy(b, hb.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
-    const size_t smem = sizeof(double) * (((n * n + 1) & ~1) + n + 8);
+    const size_t smem = sizeof(double) * (((n * n + 1) & ~1) + n + 16);
     cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaEvent_t e0, e1;
