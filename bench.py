@@ -60,7 +60,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "partial-reuse AMG rebuild ms/step + solve ms/step, 256^3 Poisson; HBM GB/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_RECORD = os.path.join(ROOT, "profiles", "r01_traffic.json")
+TRAFFIC_RECORD = os.path.join(ROOT, "profiles", "r02_traffic.json")
 
 
 def args_parse():
