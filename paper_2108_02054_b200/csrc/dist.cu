@@ -191,6 +191,7 @@ struct DistLevel {
     DevArray<int> dpos, lcptr, lcontrib;
     int64_t lnnz_c = 0, lnc = 0;
     int lmax_chunk = -1;
+    ColCode cc;  // coded column stream of the local pattern (when its offsets are few: no / few halos)
     DevArray<double> u0, x, out, f, r;  // u0/x carry halo space
     std::vector<int> send_peer, recv_peer;
     std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
@@ -206,6 +207,7 @@ struct DistLevel {
         v.col = col.get();
         v.val = val.get();
         v.max_span = max_span;
+        set_code(v, cc);
         return v;
     }
 };
@@ -274,7 +276,9 @@ struct DistHier {
     // Krylov (level 0 local)
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh, ku;
     DevArray<double> dloc, dall;  // local dot results (up to 2) and the gathered partials
-    DevArray<double*> douts;
+    DevArray<double*> douts;      // table of dot output pointer sets (out_slot)
+    std::vector<std::vector<double*>> dtab;
+    std::vector<int64_t> dtab_off;
 };
 
 static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
@@ -352,12 +356,26 @@ static void allgather(DistHier& d, const double* send, double* recv, int64_t cou
 }
 
 // deterministic cross-rank sum of k local dots (d.dloc[0..k)) into outs
+// The output pointer sets live in a device table (registered once, outside
+// any graph capture), so an iteration enqueues no host-to-device copies and
+// the NCCL path can be captured into a CUDA graph.
+static double* const* out_slot(DistHier& d, std::initializer_list<double*> outs) {
+    std::vector<double*> o(outs);
+    for (size_t i = 0; i < d.dtab.size(); ++i)
+        if (d.dtab[i] == o) return d.douts.get() + d.dtab_off[i];
+    const int64_t off = d.dtab_off.empty() ? 0 : d.dtab_off.back() + static_cast<int64_t>(d.dtab.back().size());
+    if (off + static_cast<int64_t>(o.size()) > d.douts.size()) fail(AMGR_E_RUNTIME, "dist: dot output table full");
+    h2d(d.douts.get() + off, o.data(), static_cast<int64_t>(o.size()), d.ctx->stream);
+    d.dtab.push_back(o);
+    d.dtab_off.push_back(off);
+    return d.douts.get() + off;
+}
+
 static void allsum(DistHier& d, int k, std::initializer_list<double*> outs) {
     Ctx& c = *d.ctx;
-    std::vector<double*> o(outs);
-    h2d(d.douts.get(), o.data(), static_cast<int64_t>(o.size()), c.stream);
+    double* const* slot = out_slot(d, outs);
     allgather(d, d.dloc.get(), d.dall.get(), k);
-    LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), d.douts.get());
+    LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), const_cast<double**>(slot));
 }
 
 static DotSink local_sink(DistHier& d, int slot) {
@@ -656,6 +674,10 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
                 L.recv_cnt.push_back(s.recv_cnt[k]);
             }
             L.max_span = amgr::max_group_span(c, L.rp.get(), L.n_own);
+            // local columns keep the stencil offsets of owned neighbours; halo
+            // columns (numbered after the owned rows) add distinct offsets, so
+            // the encoder only codes levels whose halos are small or absent
+            amgr::encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc);
         }
         // transition allgather layout
         int64_t disp = 0;
@@ -680,7 +702,7 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
         for (auto* v : {&d->kph, &d->ksh, &d->ku}) v->alloc(n0 + h0, c.stream);
         d->dloc.alloc(4, c.stream);
         d->dall.alloc(4 * world, c.stream);
-        d->douts.alloc(4, c.stream);
+        d->douts.alloc(64, c.stream);
         amgr::work(H);
         amgr::gather_local(*d);
         amgr::build_local_plans(*d);
@@ -825,8 +847,13 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
     const Gate GH = gate_of(st, KF_DONE, KF_HALF);
     const Gate GF = gate_of(st, KF_DONE | KF_HALF);
     const Gate GC = gate_of(st, KF_DONE | KF_HALF, KF_CHECK);
-    // one iteration of look-ahead, no per-iteration host sync; no CUDA graph
-    // (the loopback test transport synchronises host threads while enqueuing)
+    // one iteration of look-ahead, no per-iteration host sync; over NCCL the
+    // iteration is captured once into a CUDA graph (halo send/recv and the
+    // allgathers are capturable); the loopback test transport synchronises
+    // host threads while enqueuing and runs kernel by kernel
+    for (auto outs : {std::initializer_list<double*>{&st->d_rtv}, {&st->d_ss}, {&st->d_true}, {&st->d_rtr},
+                      {&st->d_ts, &st->d_tt}, {&st->d_rr, &st->d_rtr}})
+        out_slot(d, outs);  // register before any capture
     auto iter = [&]() {
         bicg_begin(c, st);
         bicg_p(c, st, n, d.kr.get(), d.kp.get(), d.kv.get());
@@ -859,7 +886,7 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
         allsum(d, 1, {&st->d_true});
         bicg_end_check(c, st);
     };
-    run_iterations(h, iter, s, false);
+    run_iterations(h, iter, s, d.lb == nullptr && !std::getenv("AMGR_DIST_NO_GRAPH"));
     out.iterations = s.it;
     if (s.flags & KF_CONVERGED) {
         out.converged = 1;
