@@ -253,6 +253,10 @@ struct Loopback {
 };
 
 struct DistHier {
+    DistHier() = default;
+    DistHier(const DistHier&) = delete;
+    DistHier& operator=(const DistHier&) = delete;
+    ~DistHier();
     Hier* g = nullptr;
     Ctx* ctx = nullptr;
     ncclComm_t comm = nullptr;
@@ -421,6 +425,64 @@ static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
         uc = out;
     }
     c.cur_level = -1;
+}
+
+// the communicator and events of a handle (also of a failed amgr_dist_create)
+DistHier::~DistHier() {
+    if (comm) {
+        if (const NcclApi* a = nccl_api()) a->CommDestroy(comm);
+    }
+    if (ev_ready) cudaEventDestroy(ev_ready);
+    if (ev_consumed) cudaEventDestroy(ev_consumed);
+}
+
+// Plan validation, before any communicator is created: every index the
+// kernels and exchanges will use is in range and the transition counts agree.
+static void validate_plan(const Hier& H, int rank, int world, int top, const amgr_dist_level* levels,
+                          const int64_t* t_counts) {
+    auto bad = [&](int i, const char* what) {
+        std::ostringstream os;
+        os << "amgr_dist_create: level " << i << ": " << what;
+        invalid(os.str());
+    };
+    auto in = [](const int64_t* a, int64_t n, int64_t lo, int64_t hi) {
+        for (int64_t k = 0; k < n; ++k)
+            if (a[k] < lo || a[k] >= hi) return false;
+        return true;
+    };
+    for (int r = 0; r < world; ++r)
+        if (t_counts[r] < 0) invalid("amgr_dist_create: negative transition count");
+    for (int i = 0; i <= top; ++i) {
+        const amgr_dist_level& s = levels[i];
+        const int64_t ng = H.lv[i].pat->n, nnzg = H.lv[i].pat->nnz;
+        if (s.n_own < 0 || s.n_halo < 0 || s.nnz < 0 || s.n_coarse_owned < 0 || s.n_own > ng) bad(i, "bad sizes");
+        if (!s.row_ptr || s.row_ptr[0] != 0 || s.row_ptr[s.n_own] != s.nnz) bad(i, "row_ptr does not span nnz");
+        for (int64_t r = 0; r < s.n_own; ++r)
+            if (s.row_ptr[r + 1] < s.row_ptr[r]) bad(i, "row_ptr decreasing");
+        if (!in(s.col, s.nnz, 0, s.n_own + s.n_halo)) bad(i, "column id out of [0, n_own + n_halo)");
+        if (!in(s.nnz_map, s.nnz, 0, nnzg)) bad(i, "nnz_map out of the global level");
+        if (!in(s.owned, s.n_own, 0, ng)) bad(i, "owned row out of the global level");
+        const int64_t nc_local = i < top ? levels[i + 1].n_own : H.lv[top + 1].pat->n;
+        if (!in(s.agg, s.n_own, 0, nc_local)) bad(i, "aggregate id out of range");
+        if (i < top && s.n_coarse_owned != levels[i + 1].n_own) bad(i, "owned coarse rows != next level's rows");
+        if (i == top && s.n_coarse_owned != t_counts[rank]) bad(i, "owned coarse rows != this rank's transition count");
+        if (!s.mptr || s.mptr[0] != 0) bad(i, "member pointers");
+        for (int64_t r = 0; r < s.n_coarse_owned; ++r)
+            if (s.mptr[r + 1] < s.mptr[r]) bad(i, "member pointers decreasing");
+        if (!in(s.midx, s.mptr[s.n_coarse_owned], 0, s.n_own)) bad(i, "member id out of the owned rows");
+        int64_t sent = 0;
+        for (int k = 0; k < s.n_send_peers; ++k) {
+            if (s.send_peer[k] < 0 || s.send_peer[k] >= world || s.send_peer[k] == rank) bad(i, "bad send peer");
+            if (s.send_cnt[k] < 0) bad(i, "negative send count");
+            sent += s.send_cnt[k];
+        }
+        if (!in(s.send_idx, sent, 0, s.n_own)) bad(i, "send index out of the owned rows");
+        for (int k = 0; k < s.n_recv_peers; ++k) {
+            if (s.recv_peer[k] < 0 || s.recv_peer[k] >= world || s.recv_peer[k] == rank) bad(i, "bad recv peer");
+            if (s.recv_off[k] < 0 || s.recv_cnt[k] < 0 || s.recv_off[k] + s.recv_cnt[k] > s.n_halo)
+                bad(i, "recv block outside the halo");
+        }
+    }
 }
 
 static void gather_local(DistHier& d) {
@@ -623,13 +685,14 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
         for (const auto& l : H.lv)
             if (l.T && l.T->smoothed)
                 amgr::invalid("amgr_dist_create: the partitioned solve supports plain (tentative) aggregation only");
+        amgr::validate_plan(H, rank, world, top, levels, t_counts);
         auto d = std::make_unique<amgr::DistHier>();
         d->g = &H;
         d->ctx = &c;
         d->rank = rank;
         d->world = world;
         d->T = top;
-        connect(*d);
+        connect(*d);  // after validation; a later failure destroys d (and its communicator)
         auto up32 = [&](amgr::DevArray<int>& dst, const int64_t* src, int64_t n) {
             std::vector<int> tmp(static_cast<size_t>(n));
             for (int64_t k = 0; k < n; ++k) tmp[k] = static_cast<int>(src[k]);
@@ -751,13 +814,7 @@ amgr_status amgr_dist_create_loopback(amgr_hier* hg, amgr_loopback* lbh, int ran
     });
 }
 
-void amgr_dist_destroy(amgr_dist* d) {
-    if (!d) return;
-    if (d->d && d->d->comm) amgr::nccl_api()->CommDestroy(d->d->comm);
-    if (d->d && d->d->ev_ready) cudaEventDestroy(d->d->ev_ready);
-    if (d->d && d->d->ev_consumed) cudaEventDestroy(d->d->ev_consumed);
-    delete d;
-}
+void amgr_dist_destroy(amgr_dist* d) { delete d; }  // ~DistHier releases the communicator and events
 
 static amgr_status dist_guard(amgr_dist* d, const std::function<void()>& fn) {
     if (!d || !d->d) return AMGR_E_INVALID_ARGUMENT;

@@ -224,3 +224,21 @@ def test_dist_rebuild_from_rank_local_values_bit_exact(world):
         R["ds"].close()
     if lb:
         lb.close()
+
+
+def test_dist_create_validates_the_plan_before_connecting(ctx):
+    """A corrupt plan is rejected with a message before any NCCL
+    communicator exists (indices and transition counts checked)."""
+    from paper_2108_02054_b200 import distributed as D
+    from paper_2108_02054_b200 import partition as PT
+
+    A = P.grid3d_values("dambreak", 12, 3)
+    h = amg.setup(A, ctx=ctx)
+    for corrupt, msg in ((lambda p: p.levels[0].col.__setitem__(0, 10 ** 8), "column id"),
+                         (lambda p: p.levels[0].send.__setitem__(0, np.array([1])), "send peer"),
+                         (lambda p: setattr(p.levels[p.top], "mptr", p.levels[p.top].mptr[:-1]),
+                          "owned coarse rows")):
+        plan = PT.build_plan(D.hierarchy_structure(h), 0, 1, replicate_below=100)
+        corrupt(plan)
+        with pytest.raises(amg.InvalidArgument, match=msg):
+            D.DistSolver(h, 0, 1, D.nccl_unique_id(), plan=plan)
