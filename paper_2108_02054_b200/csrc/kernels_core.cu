@@ -2339,7 +2339,11 @@ bool rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr,
         const size_t sm = sizeof(int) * (2 * (RT_CH + 4) + 2 * static_cast<size_t>(cstage));
         if (sm <= 96 * 1024) {
             // contributions per coarse entry: 1.3 (C3 L0), 2.4 (L1), 3-6 below
-            if (2 * nnz_f <= 5 * nnz_c)
+            static const double split = [] {  // contributions per coarse entry above which B = 4
+                const char* e = std::getenv("AMGR_RAP_SPLIT");
+                return e ? std::atof(e) : 2.5;
+            }();
+            if (static_cast<double>(nnz_f) <= split * static_cast<double>(nnz_c))
                 launch_rap_tma_fused<4, 2>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, fj);
             else
                 launch_rap_tma_fused<2, 4>(c, bytes, nnz_c, cptr, contrib, af, ac, cstage, sm, fj);
