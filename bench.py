@@ -304,7 +304,7 @@ def run_partitioned(a, rank, world, local):
 
         dist.broadcast_object_list(ids, src=0)
     t0 = time.perf_counter()
-    ds = D.DistSolver(h, rank, world, ids[0], replicate_below=a.replicate_below)
+    ds = D.DistSolver(h, rank, world, ids[0], replicate_below=a.replicate_below, device_plan=True)
     plan_s = time.perf_counter() - t0
     own = torch.from_numpy(ds.owned0).cuda()
     fl = f[own].contiguous()
@@ -411,6 +411,7 @@ def run_partitioned(a, rank, world, local):
                "config": {"workload": f"C3 dam-break {g}^3, partial reuse, row-partitioned over {world} GPU(s)",
                           "problem": a.problem, "grid": g, "n": n, "nnz": nnz, "coarse_solve": a.coarse,
                           "parallelism": f"rows{world}", "partitioned_levels": ds.plan.top + 1,
+                          "plan": "device-built (amgr_dist_create_auto)",
                           "local_rows_rank0": ds.n_local},
                "rebuild_ms_per_step": rebuild_ms, "solve_ms_per_step": solve_ms, "iterations": iters,
                "setup_s": setup_s, "plan_s": plan_s, "clocks": clk.summary(), "gpu_launches": launches,

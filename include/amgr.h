@@ -325,6 +325,16 @@ amgr_status amgr_dist_create(amgr_hier* global, const void* nccl_id128, int rank
  * replicated levels are rebuilt on every rank.  Bit-identical to the global
  * partial_update; errors name the global row and are raised on every rank. */
 amgr_status amgr_dist_rebuild_local(amgr_dist* d, const double* local_values, int location);
+/* Partition built ON THE DEVICE from the hierarchy's own patterns and
+ * aggregates (dist_plan.cu; the rules of partition.py, identical arrays):
+ * levels with >= replicate_below rows (never the coarsest) are partitioned.
+ * No host plan, no pattern download. */
+amgr_status amgr_dist_create_auto(amgr_hier* global, const void* nccl_id128, int rank, int world,
+                                  int64_t replicate_below, amgr_dist** out);
+/* dims: {n_own, n_halo, nnz, n_coarse_owned, top} of partitioned level `level`. */
+amgr_status amgr_dist_level_dims(const amgr_dist* d, int level, int64_t* dims);
+/* owned: n_own global row ids; nnz_map: nnz global entry ids (either may be NULL). */
+amgr_status amgr_dist_level_maps(amgr_dist* d, int level, int64_t* owned, int64_t* nnz_map);
 /* Test transport: W ranks of ONE process (one host thread and one context
  * each, same device) exchange through stream-ordered device copies and host
  * barriers instead of NCCL, so the multi-rank device path can be checked on
@@ -332,6 +342,8 @@ amgr_status amgr_dist_rebuild_local(amgr_dist* d, const double* local_values, in
 typedef struct amgr_loopback amgr_loopback;
 amgr_status amgr_dist_loopback_create(int world, amgr_loopback** out);
 void amgr_dist_loopback_destroy(amgr_loopback* lb);
+amgr_status amgr_dist_create_auto_loopback(amgr_hier* global, amgr_loopback* lb, int rank, int world,
+                                           int64_t replicate_below, amgr_dist** out);
 amgr_status amgr_dist_create_loopback(amgr_hier* global, amgr_loopback* lb, int rank, int world, int top,
                                       const amgr_dist_level* levels, int64_t t_count_total, const int64_t* t_counts,
                                       amgr_dist** out);

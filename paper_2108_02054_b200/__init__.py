@@ -164,6 +164,10 @@ PROTOTYPES = {
     "amgr_dist_loopback_destroy": (None, [_V]),
     "amgr_dist_create_loopback": (_I, [_V, _V, _I, _I, _I, _V, _L, _V, _P(_V)]),
     "amgr_dist_rebuild_values": (_I, [_V, _V, _I]),
+    "amgr_dist_create_auto": (_I, [_V, _V, _I, _I, _L, _P(_V)]),
+    "amgr_dist_create_auto_loopback": (_I, [_V, _V, _I, _I, _L, _P(_V)]),
+    "amgr_dist_level_dims": (_I, [_V, _I, _V]),
+    "amgr_dist_level_maps": (_I, [_V, _I, _V, _V]),
     "amgr_dist_rebuild_local": (_I, [_V, _V, _I]),
     "amgr_dist_vcycle": (_I, [_V, _V, _V]),
     "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),

@@ -26,6 +26,7 @@
 #include <mutex>
 #include <sstream>
 
+#include "dist_plan.cuh"
 #include "hierarchy.cuh"
 #include "reduce.cuh"
 
@@ -649,6 +650,84 @@ static void dist_rebuild_local(DistHier& d, const double* vals, int location) {
     c.cur_level = -1;
 }
 
+// common tail of amgr_dist_create*: transition layout, local work vectors,
+// local values/weights, local Galerkin plans
+static void dist_finish(DistHier& d, const int64_t* t_counts, int64_t t_count_total) {
+    Hier& H = *d.g;
+    Ctx& c = *d.ctx;
+    const int world = d.world, top = d.T;
+    // transition allgather layout
+    int64_t disp = 0;
+    for (int r = 0; r < world; ++r) {
+        d.tcnt.push_back(t_counts[r]);
+        d.tdispl.push_back(disp);
+        disp += t_counts[r];
+        d.tpad = std::max<int64_t>(d.tpad, t_counts[r]);
+    }
+    if (disp != t_count_total || disp != H.lv[top + 1].pat->n)
+        invalid("amgr_dist_create: transition counts do not cover level top+1");
+    d.tsend.alloc(std::max<int64_t>(d.tpad, 1), c.stream);
+    d.tgather.alloc(std::max<int64_t>(d.tpad * world, 1), c.stream);
+    d.tcnt_d.alloc(world, c.stream);
+    d.tdispl_d.alloc(world, c.stream);
+    h2d(d.tcnt_d.get(), d.tcnt.data(), world, c.stream);
+    h2d(d.tdispl_d.get(), d.tdispl.data(), world, c.stream);
+    d.fT.alloc(disp, c.stream);
+    d.uT.alloc(disp, c.stream);
+    const int64_t n0 = d.lv[0].n_own, h0 = d.lv[0].n_halo;
+    for (auto* v : {&d.kr, &d.krt, &d.kp, &d.kv, &d.ks, &d.kt}) v->alloc(n0, c.stream);
+    for (auto* v : {&d.kph, &d.ksh, &d.ku}) v->alloc(n0 + h0, c.stream);
+    d.dloc.alloc(4, c.stream);
+    d.dall.alloc(4 * world, c.stream);
+    d.douts.alloc(64, c.stream);
+    work(H);
+    gather_local(d);
+    build_local_plans(d);
+}
+
+// levels of a device-built plan (dist_plan.cu): the arrays move in as they are
+static void levels_from_device_plan(DistHier& d, DevicePlan& P) {
+    Ctx& c = *d.ctx;
+    d.lv.resize(static_cast<size_t>(P.top + 1));
+    for (int i = 0; i <= P.top; ++i) {
+        PlanLevel& s = P.lv[i];
+        DistLevel& L = d.lv[i];
+        L.n_own = s.n_own;
+        L.n_halo = s.n_halo;
+        L.nnz = s.nnz;
+        L.n_cown = s.n_cown;
+        L.rp = std::move(s.rp);
+        L.col = std::move(s.col);
+        L.nnz_map = std::move(s.nnz_map);
+        L.owned = std::move(s.owned);
+        L.agg = std::move(s.agg);
+        L.mptr = std::move(s.mptr);
+        L.midx = std::move(s.midx);
+        L.send_idx = std::move(s.send_idx);
+        L.val.alloc(s.nnz, c.stream);
+        L.w.alloc(s.n_own, c.stream);
+        L.dpos.alloc(s.n_own, c.stream);
+        L.u0.alloc(s.n_own + s.n_halo, c.stream);
+        L.x.alloc(s.n_own + s.n_halo, c.stream);
+        L.out.alloc(s.n_own, c.stream);
+        L.f.alloc(s.n_own, c.stream);
+        L.r.alloc(s.n_own, c.stream);
+        int64_t off = 0;
+        for (size_t k = 0; k < s.send_peer.size(); ++k) {
+            L.send_peer.push_back(s.send_peer[k]);
+            L.send_off.push_back(off);
+            L.send_cnt.push_back(s.send_cnt[k]);
+            off += s.send_cnt[k];
+        }
+        L.send_buf.alloc(off, c.stream);
+        L.recv_peer = s.recv_peer;
+        L.recv_off = s.recv_off;
+        L.recv_cnt = s.recv_cnt;
+        L.max_span = max_group_span(c, L.rp.get(), L.n_own);
+        encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc);
+    }
+}
+
 }  // namespace amgr
 
 // ---- C-ABI ----------------------------------------------------------------------
@@ -742,33 +821,7 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
             // the encoder only codes levels whose halos are small or absent
             amgr::encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc);
         }
-        // transition allgather layout
-        int64_t disp = 0;
-        for (int r = 0; r < world; ++r) {
-            d->tcnt.push_back(t_counts[r]);
-            d->tdispl.push_back(disp);
-            disp += t_counts[r];
-            d->tpad = std::max<int64_t>(d->tpad, t_counts[r]);
-        }
-        if (disp != t_count_total || disp != H.lv[top + 1].pat->n)
-            amgr::invalid("amgr_dist_create: transition counts do not cover level top+1");
-        d->tsend.alloc(std::max<int64_t>(d->tpad, 1), c.stream);
-        d->tgather.alloc(std::max<int64_t>(d->tpad * world, 1), c.stream);
-        d->tcnt_d.alloc(world, c.stream);
-        d->tdispl_d.alloc(world, c.stream);
-        amgr::h2d(d->tcnt_d.get(), d->tcnt.data(), world, c.stream);
-        amgr::h2d(d->tdispl_d.get(), d->tdispl.data(), world, c.stream);
-        d->fT.alloc(disp, c.stream);
-        d->uT.alloc(disp, c.stream);
-        const int64_t n0 = d->lv[0].n_own, h0 = d->lv[0].n_halo;
-        for (auto* v : {&d->kr, &d->krt, &d->kp, &d->kv, &d->ks, &d->kt}) v->alloc(n0, c.stream);
-        for (auto* v : {&d->kph, &d->ksh, &d->ku}) v->alloc(n0 + h0, c.stream);
-        d->dloc.alloc(4, c.stream);
-        d->dall.alloc(4 * world, c.stream);
-        d->douts.alloc(64, c.stream);
-        amgr::work(H);
-        amgr::gather_local(*d);
-        amgr::build_local_plans(*d);
+        amgr::dist_finish(*d, t_counts, t_count_total);
         CK(cudaStreamSynchronize(c.stream));
         auto* o = new amgr_dist();
         o->d = std::move(d);
@@ -814,6 +867,75 @@ amgr_status amgr_dist_create_loopback(amgr_hier* hg, amgr_loopback* lbh, int ran
     });
 }
 
+static amgr_status dist_create_auto_impl(amgr_hier* hg, int rank, int world, int64_t replicate_below,
+                                         amgr_dist** out, const std::function<void(amgr::DistHier&)>& connect) {
+    if (!hg || !out || world < 1 || rank < 0 || rank >= world) return AMGR_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    amgr::Hier& H = *hg->h;
+    amgr::Ctx& c = *H.ctx;
+    try {
+        CK(cudaSetDevice(c.device));
+        if (H.prm.pre != 1 || H.prm.post != 1 || H.prm.smoother == AMGR_SMOOTHER_CHEBYSHEV)
+            amgr::invalid("amgr_dist_create: the partitioned solve supports 1+1 Jacobi/SPAI0 sweeps");
+        amgr::DevicePlan P = amgr::build_device_plan(H, rank, world, replicate_below);  // before any communicator
+        auto d = std::make_unique<amgr::DistHier>();
+        d->g = &H;
+        d->ctx = &c;
+        d->rank = rank;
+        d->world = world;
+        d->T = P.top;
+        connect(*d);
+        amgr::levels_from_device_plan(*d, P);
+        int64_t tot = 0;
+        for (int64_t t : P.t_counts) tot += t;
+        amgr::dist_finish(*d, P.t_counts.data(), tot);
+        CK(cudaStreamSynchronize(c.stream));
+        auto* o = new amgr_dist();
+        o->d = std::move(d);
+        *out = o;
+        return AMGR_OK;
+    } catch (const amgr::Error& e) {
+        c.last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        c.last_error = e.what();
+        return AMGR_E_RUNTIME;
+    }
+}
+
+amgr_status amgr_dist_create_auto(amgr_hier* hg, const void* nccl_id128, int rank, int world,
+                                  int64_t replicate_below, amgr_dist** out) {
+    if (!nccl_id128) return AMGR_E_INVALID_ARGUMENT;
+    return dist_create_auto_impl(hg, rank, world, replicate_below, out, [&](amgr::DistHier& d) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof(id));
+        NK(::amgr::N().CommInitRank(&d.comm, world, id, rank));
+    });
+}
+
+amgr_status amgr_dist_create_auto_loopback(amgr_hier* hg, amgr_loopback* lbh, int rank, int world,
+                                           int64_t replicate_below, amgr_dist** out) {
+    auto* lb = reinterpret_cast<amgr::Loopback*>(lbh);
+    if (!lb || lb->world != world) return AMGR_E_INVALID_ARGUMENT;
+    return dist_create_auto_impl(hg, rank, world, replicate_below, out, [&](amgr::DistHier& d) {
+        d.lb = lb;
+        CK(cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&d.ev_consumed, cudaEventDisableTiming));
+    });
+}
+
+// dims: {n_own, n_halo, nnz, n_coarse_owned, top}
+amgr_status amgr_dist_level_dims(const amgr_dist* d, int level, int64_t* dims) {
+    if (!d || !d->d || !dims || level < 0 || level > d->d->T) return AMGR_E_INVALID_ARGUMENT;
+    const amgr::DistLevel& L = d->d->lv[level];
+    dims[0] = L.n_own;
+    dims[1] = L.n_halo;
+    dims[2] = L.nnz;
+    dims[3] = L.n_cown;
+    dims[4] = d->d->T;
+    return AMGR_OK;
+}
+
 void amgr_dist_destroy(amgr_dist* d) { delete d; }  // ~DistHier releases the communicator and events
 
 static amgr_status dist_guard(amgr_dist* d, const std::function<void()>& fn) {
@@ -830,6 +952,28 @@ static amgr_status dist_guard(amgr_dist* d, const std::function<void()>& fn) {
         c.last_error = e.what();
         return AMGR_E_RUNTIME;
     }
+}
+
+// owned: n_own global rows; nnz_map: nnz global entry ids (either may be null)
+amgr_status amgr_dist_level_maps(amgr_dist* d, int level, int64_t* owned, int64_t* nnz_map) {
+    if (!d || !d->d || level < 0 || level > d->d->T) return AMGR_E_INVALID_ARGUMENT;
+    return dist_guard(d, [&] {
+        amgr::DistLevel& L = d->d->lv[level];
+        amgr::Ctx& c = *d->d->ctx;
+        std::vector<int> tmp;
+        if (owned) {
+            tmp.resize(static_cast<size_t>(L.n_own));
+            amgr::d2h(tmp.data(), L.owned.get(), L.n_own, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            for (int64_t k = 0; k < L.n_own; ++k) owned[k] = tmp[static_cast<size_t>(k)];
+        }
+        if (nnz_map) {
+            tmp.resize(static_cast<size_t>(L.nnz));
+            amgr::d2h(tmp.data(), L.nnz_map.get(), L.nnz, c.stream);
+            CK(cudaStreamSynchronize(c.stream));
+            for (int64_t k = 0; k < L.nnz; ++k) nnz_map[k] = tmp[static_cast<size_t>(k)];
+        }
+    });
 }
 
 amgr_status amgr_dist_rebuild_values(amgr_dist* d, const double* global_values, int location) {

@@ -60,16 +60,60 @@ def hierarchy_structure(h: Hierarchy):
     return out
 
 
+class _DeviceLevel:
+    """What the caller needs of a device-built plan level (sizes; level 0 maps)."""
+
+    def __init__(self, dims, owned=None, nnz_map=None):
+        self.n_own, n_halo, nnz, self.n_coarse_owned, _ = (int(x) for x in dims)
+        self.halo = np.zeros(n_halo, np.int64)  # only its length is meaningful
+        self.nnz = nnz
+        self.owned, self.nnz_map = owned, nnz_map
+
+
+class _DevicePlan:
+    def __init__(self, top, levels):
+        self.top, self.levels = top, levels
+
+
 class DistSolver:
     def __init__(self, h: Hierarchy, rank: int, world: int, nccl_id: bytes | None = None,
-                 replicate_below: int = 20000, plan: PT.Plan | None = None, loopback: Loopback | None = None):
+                 replicate_below: int = 20000, plan: PT.Plan | None = None, loopback: Loopback | None = None,
+                 device_plan: bool = False):
         self.h, self.rank, self.world = h, rank, world
+        self._keep = []
+        if device_plan:
+            # partition built on the device (amgr_dist_create_auto): no host plan, no pattern download
+            self._p = C.c_void_p()
+            if loopback is not None:
+                _check(lib().amgr_dist_create_auto_loopback(h._p, loopback._p, rank, world, int(replicate_below),
+                                                            C.byref(self._p)), h.ctx.ptr)
+            else:
+                idb = C.create_string_buffer(nccl_id, 128)
+                _check(lib().amgr_dist_create_auto(h._p, idb, rank, world, int(replicate_below), C.byref(self._p)),
+                       h.ctx.ptr)
+            d = np.zeros(5, np.int64)
+            _check(lib().amgr_dist_level_dims(self._p, 0, d.ctypes.data), h.ctx.ptr)
+            top = int(d[4])
+            levels = []
+            for lvl in range(top + 1):
+                d = np.zeros(5, np.int64)
+                _check(lib().amgr_dist_level_dims(self._p, lvl, d.ctypes.data), h.ctx.ptr)
+                if lvl == 0:
+                    own = np.zeros(int(d[0]), np.int64)
+                    nm = np.zeros(int(d[2]), np.int64)
+                    _check(lib().amgr_dist_level_maps(self._p, 0, own.ctypes.data, nm.ctypes.data), h.ctx.ptr)
+                    levels.append(_DeviceLevel(d, own, nm))
+                else:
+                    levels.append(_DeviceLevel(d))
+            self.plan = _DevicePlan(top, levels)
+            self.owned0 = levels[0].owned
+            h.ctx._adopt(self)
+            return
         struct = hierarchy_structure(h)
         self.plan = plan or PT.build_plan(struct, rank, world, replicate_below)
         T = self.plan.top
         if T < 0:
             raise ValueError("hierarchy too small to partition (raise replicate_below or the problem size)")
-        self._keep = []
 
         def arr(a, dt=np.int64):
             a = np.ascontiguousarray(a, dt)

@@ -242,3 +242,70 @@ def test_dist_create_validates_the_plan_before_connecting(ctx):
         corrupt(plan)
         with pytest.raises(amg.InvalidArgument, match=msg):
             D.DistSolver(h, 0, 1, D.nccl_unique_id(), plan=plan)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_built_plan_matches_host_plan_and_solves(world):
+    """amgr_dist_create_auto builds the partition on the device (dist_plan.cu):
+    owned rows, local CSR maps and halo sizes equal partition.py's on every
+    rank, and a loopback run on the device plans (rank-local rebuild, V-cycle,
+    BiCGStab) is bit-identical to the single-GPU path."""
+    import torch
+
+    from paper_2108_02054_b200 import distributed as D
+    from paper_2108_02054_b200 import partition as PT
+
+    A = P.grid3d_values("dambreak", 20, 9)
+    A2 = P.grid3d_values("dambreak", 20, 30)
+    n = 20 ** 3
+    f = np.random.default_rng(11).uniform(-1, 1, n)
+    fr = P.rhs(n)
+    ref_ctx = amg.Context(0)
+    h_ref = amg.setup(A, ctx=ref_ctx)
+    h_ref.rebuild_values(A2[2])
+    u_ref = amg.vcycle(h_ref, f)
+    _, st_ref = amg.bicgstab(h_ref, fr)
+    struct = D.hierarchy_structure(h_ref)
+
+    lb = D.Loopback(world)
+    ranks = []
+    for r in range(world):
+        ctx = amg.Context(0)
+        h = amg.setup(A, ctx=ctx)
+        ds = D.DistSolver(h, r, world, replicate_below=300, loopback=lb, device_plan=True)
+        hp = PT.build_plan(struct, r, world, replicate_below=300)
+        assert ds.plan.top == hp.top
+        for lvl in range(hp.top + 1):
+            assert ds.plan.levels[lvl].n_own == hp.levels[lvl].n_own
+            assert len(ds.plan.levels[lvl].halo) == len(hp.levels[lvl].halo)
+            assert ds.plan.levels[lvl].n_coarse_owned == len(hp.levels[lvl].mptr) - 1
+        np.testing.assert_array_equal(ds.owned0, hp.levels[0].owned)
+        np.testing.assert_array_equal(ds.plan.levels[0].nnz_map, hp.levels[0].nnz_map)
+        ranks.append({"ctx": ctx, "ds": ds, "own": ds.owned0})
+
+    def fn(r):
+        R = ranks[r]
+        ds = R["ds"]
+        ds.rebuild_local(ds.local_values(A2[2]))
+        fd = torch.from_numpy(f[R["own"]]).cuda()
+        ud = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        ds.vcycle(fd.data_ptr(), ud.data_ptr())
+        R["ctx"].synchronize()
+        frd = torch.from_numpy(fr[R["own"]]).cuda()
+        ur = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        st = ds.bicgstab(frd.data_ptr(), ur.data_ptr())
+        return ud.cpu().numpy(), st
+
+    out, errs = _run_ranks(world, fn)
+    assert not errs, errs
+    u = np.zeros(n)
+    for r in range(world):
+        u[ranks[r]["own"]] = out[r][0]
+    np.testing.assert_array_equal(u.view(np.int64), u_ref.view(np.int64))
+    for r in range(world):
+        assert out[r][1].converged and out[r][1].iterations == st_ref.iterations
+    for R in ranks:
+        R["ds"].close()
+    lb.close()
