@@ -265,9 +265,10 @@ DevicePlan build_device_plan(Hier& h, int rank, int world, int64_t replicate_bel
         const int64_t ns = sort_unique(c, sk, G.nnz, su);
         DevArray<int> scol(std::max<int64_t>(ns, 1), c.stream), speer(std::max<int64_t>(ns, 1), c.stream);
         LAUNCH(c, "dist_plan", 0.0, k_key_low, grid_of(c, ns), PB, 0, ns, su.get(), scol.get(), speer.get());
-        L.send_idx.alloc(std::max<int64_t>(ns, 1), c.stream);
-        LAUNCH(c, "dist_plan", 0.0, k_gather_i, grid_of(c, ns), PB, 0, ns, scol.get(), g2l[i].get(),
-               L.send_idx.get());
+        L.send_idx.alloc(ns, c.stream);  // exact size: the halo pack keys on it (0: nothing to send)
+        if (ns > 0)
+            LAUNCH(c, "dist_plan", 0.0, k_gather_i, grid_of(c, ns), PB, 0, ns, scol.get(), g2l[i].get(),
+                   L.send_idx.get());
         std::vector<int> sp(static_cast<size_t>(ns));
         d2h(sp.data(), speer.get(), ns, c.stream);
         CK(cudaStreamSynchronize(c.stream));

@@ -309,3 +309,32 @@ def test_device_built_plan_matches_host_plan_and_solves(world):
     for R in ranks:
         R["ds"].close()
     lb.close()
+
+
+def test_device_built_plan_world1_nccl(ctx):
+    """World 1 over NCCL on a device-built plan (no halos, no send lists):
+    rank-local rebuild + BiCGStab equal the single-GPU path."""
+    import torch
+
+    from paper_2108_02054_b200 import distributed as D
+
+    A = P.grid3d_values("dambreak", 20, 9)
+    A2 = P.grid3d_values("dambreak", 20, 30)
+    n = 20 ** 3
+    fr = P.rhs(n)
+    h = amg.setup(A, ctx=ctx)
+    ds = D.DistSolver(h, 0, 1, D.nccl_unique_id(), replicate_below=300, device_plan=True)
+    assert ds.plan.top >= 1 and len(ds.plan.levels[0].halo) == 0
+    ds.rebuild_local(ds.local_values(A2[2]))
+    frd = torch.from_numpy(fr[ds.owned0]).cuda()
+    ur = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    st = ds.bicgstab(frd.data_ptr(), ur.data_ptr())
+    h2 = amg.setup(A, ctx=ctx)
+    h2.rebuild_values(A2[2])
+    u2, st2 = amg.bicgstab(h2, fr)
+    assert st.converged and st.iterations == st2.iterations
+    u = np.zeros(n)
+    u[ds.owned0] = ur.cpu().numpy()
+    np.testing.assert_array_equal(u.view(np.int64), u2.view(np.int64))
+    ds.close()
