@@ -365,6 +365,26 @@ static void build_row_plans(Hier& h) {
     }
 }
 
+// Warp-group plans (k_rap_grp) for every plain-aggregation level, built
+// lazily once per Galerkin plan.  Default; AMGR_RAP_GROUPS=0 keeps k_rap_tma
+// + k_jacobi.
+static bool rap_grp_enabled() {
+    const char* e = std::getenv("AMGR_RAP_GROUPS");
+    return !(e && e[0] == '0');
+}
+static void build_grp_plans(Hier& h, size_t start) {
+    Ctx& c = *h.ctx;
+    if (!rap_grp_enabled()) return;
+    for (size_t i = start; i + 1 < h.lv.size(); ++i) {
+        Level& A = h.lv[i];
+        if (!A.rap || !A.T || A.T->smoothed || A.rap->grp_tried) continue;
+        A.rap->grp_tried = true;
+        const Pattern& C = *h.lv[i + 1].pat;
+        rap_grp_plan(c, A.view(), A.T->agg.get(), A.T->mptr.get(), A.T->midx.get(), A.pat->diag.get(), A.T->nc,
+                     C.rp.get(), A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.rap->grp);
+    }
+}
+
 // Numeric pass of partial_update (hierarchy.cpp:121-147) on existing plans:
 // the Galerkin chain, then the per-level smoother rebuilds (main stream)
 // concurrently with the coarsest factorization (side stream).
@@ -392,6 +412,7 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
     const char* fe = std::getenv("AMGR_FUSE_JACOBI");
     const bool jac = h.prm.smoother == AMGR_SMOOTHER_JACOBI && fe && fe[0] == '1';
     std::vector<char> wdone(L, 0);
+    build_grp_plans(h, start);
     for (size_t i = start; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
         Level& A = h.lv[i];
@@ -400,6 +421,28 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
         if (B.val.size() != B.pat->nnz) B.val.alloc(B.pat->nnz, c.stream);
         if (A.T->smoothed) {
             sa_galerkin_numeric(c, *A.rap, A.view().val, *A.T, B.val.get());
+        } else if (A.rap->grp.ok && rap_grp_enabled() && !(fuse && A.rap->rows.ok)) {
+            // warp-group RAP; the fine level's damped-Jacobi weights come
+            // from the member rows it stages (its values are final here)
+            const GrpPlan& gp = A.rap->grp;
+            GrpArgs ga;
+            ga.ngroups = gp.ngroups;
+            ga.desc = gp.desc.get();
+            ga.mstart = gp.mstart.get();
+            ga.mdoff = gp.mdoff.get();
+            ga.midx = A.T->midx.get();
+            ga.code = gp.code.get();
+            ga.lanes = gp.lanes.get();
+            ga.af = A.view().val;
+            ga.ac = B.val.get();
+            if (h.prm.smoother == AMGR_SMOOTHER_JACOBI && !wdone[i]) {
+                if (A.w.size() != A.pat->n) A.w.alloc(A.pat->n, c.stream);
+                ga.wf = A.w.get();
+                ga.bad_f = W.err.get() + i;
+                wdone[i] = 1;
+                A.has_smoother = true;
+            }
+            rap_grp(c, ga, A.pat->n, B.pat->n, A.pat->nnz, B.pat->nnz);
         } else if (fuse && A.rap->rows.ok) {
             const RowPlan& rp = A.rap->rows;
             RapRowsArgs a;

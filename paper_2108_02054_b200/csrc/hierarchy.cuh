@@ -59,6 +59,8 @@ struct RapPlan {
     DevArray<int> cptr, contrib;
     RowPlan rows;        // member-row plan (k_rap_rows) when the level fits
     bool rows_tried = false;
+    GrpPlan grp;         // warp-group plan (k_rap_grp, default) when the level fits
+    bool grp_tried = false;
 };
 
 inline CsrView csr_view(const Pattern& p, const double* val) {

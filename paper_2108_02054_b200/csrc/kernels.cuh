@@ -153,6 +153,24 @@ struct RapRowsArgs {
     int* bad_c = nullptr;
 };
 void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_f, int64_t nnz_c);
+// Warp-group numeric Galerkin product (GrpPlan, setup.cuh), default for
+// plain-aggregation levels whose plan fits; with wf set it also rebuilds the
+// fine level's damped-Jacobi weights (first bad row into bad_f).
+// Bit-identical to rap_numeric + jacobi_rebuild.
+struct GrpArgs {
+    int64_t ngroups = 0;
+    const int4* desc = nullptr;
+    const int* mstart = nullptr;
+    const uint8_t* mdoff = nullptr;
+    const int* midx = nullptr;
+    const uint16_t* code = nullptr;
+    const uint16_t* lanes = nullptr;
+    const double* af = nullptr;
+    double* ac = nullptr;
+    double* wf = nullptr;
+    int* bad_f = nullptr;
+};
+void rap_grp(Ctx& c, const GrpArgs& a, int64_t nf, int64_t nc, int64_t nnz_f, int64_t nnz_c);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);

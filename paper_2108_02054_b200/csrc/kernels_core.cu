@@ -1121,6 +1121,158 @@ void launch_rap_tma_fused(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, 
 
 // ---- end k_rap_tma
 
+// ---- k_rap_grp: warp-group Galerkin product (default) -----------------------
+// One warp per group of consecutive coarse rows (GrpPlan, setup.cuh):
+//  1. the group's member-row starts (<= 64) go to shared memory, its 2-byte
+//     contribution codes arrive as aligned words;
+//  2. gather, slot-parallel: lane l fetches contribution pairs 2l, 2l+1,
+//     2l+64, ... from af[start of its member row + its offset] into shared
+//     memory, in the plan's order — 64 entries of the group's neighbouring
+//     member rows per instruction pair;
+//  3. lane l sums the coarse entries of its run (the plan splits a group's
+//     entries into 32 contiguous runs balanced by contribution count), each
+//     over its contiguous contributions with the reference's bracket: the
+//     partial of one member row is committed at the bracket bit
+//     (csr.cpp:145-194) — the same arithmetic as k_rap /
+//     k_rap_tma, bit for bit;
+//  4. (JAC) w_i = 1.0 / a_ii of the member rows, first bad row into bad_f
+//     (smoother.cpp:8-32, as k_jacobi).
+// Plan bytes per fine entry drop from 4 (contrib) + 4 per coarse entry
+// (cptr) to 2 + 0.25.  Measured and dropped (256^3): prefetching the next
+// group's plan slice one group ahead, by per-lane cp.async (LDGSTS: 1.5x
+// slower, MIO-throttled, +1 GB DRAM) or by per-warp TMA bulk copies
+// (4 small copies per group: 10% slower).
+#ifndef RG_MINB
+#define RG_MINB 5
+#endif
+constexpr int RG_WARPS = 8, RG_BUF = 256, RG_MEM = 64;
+struct RgSmem {
+    double x[RG_BUF];
+    uint32_t codew[RG_BUF / 2 + 2];
+    int mst[RG_MEM];
+};
+
+template <bool JAC>
+__global__ void __launch_bounds__(RG_WARPS * 32, RG_MINB) k_rap_grp(GrpArgs a) {
+    extern __shared__ __align__(16) unsigned char rg_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    RgSmem& S = reinterpret_cast<RgSmem*>(rg_smem)[wid];
+    uint16_t* s_code = reinterpret_cast<uint16_t*>(S.codew);
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * RG_WARPS;
+    int64_t g = static_cast<int64_t>(blockIdx.x) * RG_WARPS + wid;
+    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
+    if (g < a.ngroups) {
+        d0 = __ldg(a.desc + g);
+        d1 = __ldg(a.desc + g + 1);
+    }
+    for (; g < a.ngroups; g += nw) {
+        // next group's descriptor, in flight during this one
+        int4 n0 = d1, n1 = d1;
+        if (g + nw < a.ngroups) {
+            n0 = __ldg(a.desc + g + nw);
+            n1 = __ldg(a.desc + g + nw + 1);
+        }
+        const int nmem = d1.y - d0.y, nbuf = d1.w - d0.w;
+        const unsigned lt = __ldg(a.lanes + g * 32 + lane);
+        int ms[2], md[2], mi[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int m = lane + 32 * k;
+            const bool ok = m < nmem;
+            ms[k] = ok ? __ldg(a.mstart + d0.y + m) : 0;
+            md[k] = JAC && ok ? __ldg(a.mdoff + d0.y + m) : 255;
+            mi[k] = JAC && ok ? __ldg(a.midx + d0.y + m) : 0;
+        }
+        const int dp = d0.w & 1;
+        const int pw = (nbuf + dp + 1) >> 1;  // <= 128 words
+        const uint32_t* cp = reinterpret_cast<const uint32_t*>(a.code) + ((d0.w - dp) >> 1);
+        uint32_t wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int t = lane + 32 * k;
+            wv[k] = t < pw ? __ldg(cp + t) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            if (lane + 32 * k < nmem) S.mst[lane + 32 * k] = ms[k];
+        __syncwarp();
+        // word w holds contributions 2w - dp and 2w - dp + 1
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int w = lane + 32 * k;
+            const int t = 2 * w - dp;
+            const uint32_t c2 = wv[k];
+            const unsigned lo = c2 & 0xffffu, hi = c2 >> 16;
+            v[2 * k] = t >= 0 && t < nbuf ? __ldg(a.af + S.mst[(lo >> 8) & 63u] + (lo & 255u)) : 0.0;
+            v[2 * k + 1] = t + 1 < nbuf ? __ldg(a.af + S.mst[(hi >> 8) & 63u] + (hi & 255u)) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int w = lane + 32 * k;
+            const int t = 2 * w - dp;
+            if (w < pw) S.codew[w] = wv[k];
+            if (t >= 0 && t < nbuf) S.x[t] = v[2 * k];
+            if (t + 1 < nbuf) S.x[t + 1] = v[2 * k + 1];
+        }
+        __syncwarp();
+        if (lane == 0) s_code[dp + nbuf] = 0x4000u;  // the end of the group closes the last entry
+        __syncwarp();
+        // this lane's run of coarse entries: contributions [p, e)
+        int p = lt & 255u;
+        const unsigned ln = __shfl_down_sync(0xffffffffu, lt, 1);
+        const int e = lane < 31 ? static_cast<int>(ln & 255u) : nbuf;
+        double* out = a.ac + d0.z + (lt >> 8);
+        double acc = 0.0, part = 0.0;
+        unsigned cd = p < e ? s_code[dp + p] : 0u;
+        while (p < e) {
+            part = dadd(part, S.x[p]);
+            ++p;
+            const unsigned nx = s_code[dp + p];
+            if (cd & 0x8000u) {
+                acc = dadd(acc, part);
+                part = 0.0;
+            }
+            if (nx & 0x4000u) {
+                __stcs(out++, acc);
+                acc = 0.0;
+            }
+            cd = nx;
+        }
+        if constexpr (JAC) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (lane + 32 * k < nmem) {
+                    const double d = md[k] != 255 ? __ldg(a.af + ms[k] + md[k]) : 0.0;
+                    if (d == 0.0) {
+                        atomicMin(a.bad_f, mi[k]);
+                        a.wf[mi[k]] = 0.0;
+                    } else {
+                        a.wf[mi[k]] = __ddiv_rn(1.0, d);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        d0 = n0;
+        d1 = n1;
+    }
+}
+
+template <bool JAC>
+static void launch_rap_grp(Ctx& c, const GrpArgs& a, double bytes) {
+    const size_t sm = sizeof(RgSmem) * RG_WARPS;
+    static const int res = [sm] {
+        CK(cudaFuncSetAttribute(k_rap_grp<JAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        int r = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_rap_grp<JAC>, RG_WARPS * 32, sm));
+        return r < 1 ? 1 : r;
+    }();
+    const int64_t need = (a.ngroups + RG_WARPS - 1) / RG_WARPS;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t{c.num_sms} * res)));
+    LAUNCH(c, "rap", bytes, k_rap_grp<JAC>, grid, RG_WARPS * 32, sm, a);
+}
+
 // ---- k_rap_rows: member-row streaming Galerkin product ----------------------
 // Thread per coarse row I.  Its members m (R, ascending fine index) are
 // streamed row by row: the row's values are read contiguously (natural order,
@@ -2360,6 +2512,16 @@ bool rap_numeric(Ctx& c, int64_t nf, int64_t nc, int64_t nnz_c, const int* cptr,
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, static_cast<int64_t>(c.num_sms) * resident));
     LAUNCH(c, "rap", bytes, k_rap, grid, RAP_BLOCK, 0, nnz_c, cptr, contrib, af, ac);
     return false;
+}
+void rap_grp(Ctx& c, const GrpArgs& a, int64_t nf, int64_t nc, int64_t nnz_f, int64_t nnz_c) {
+    if (a.ngroups == 0) return;
+    // RAP 12*nnz_f + 8*nnz_c + 4*nf + 4*(nc+1); fused Jacobi + 20*nf
+    double bytes = 12.0 * nnz_f + 8.0 * nnz_c + 4.0 * nf + 4.0 * (nc + 1);
+    if (a.wf) {
+        launch_rap_grp<true>(c, a, bytes + 20.0 * nf);
+    } else {
+        launch_rap_grp<false>(c, a, bytes);
+    }
 }
 void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_f, int64_t nnz_c) {
     if (a.nc == 0) return;

@@ -6,6 +6,7 @@
 #include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -645,6 +646,209 @@ void rap_rows_plan(Ctx& c, const CsrView& A, const int* agg, const int* midx, in
            plan.code.get(), st.get() + 2);
     const int bad = d2h_scalar(st.get() + 2, c.stream);
     if (bad) fail(AMGR_E_RUNTIME, "rap_rows_plan: inconsistent coarse pattern (internal error)");
+    plan.ok = true;
+}
+
+// ---- warp-group Galerkin plan (k_rap_grp) ------------------------------------
+namespace {
+constexpr int GP_BUF = 255, GP_MEM = 64;
+constexpr int GP_MASK = (1 << 30) - 1;  // cptr bit 30 flags the coarse diagonal
+
+// group of coarse row I: the last group whose first row is <= I
+__device__ __forceinline__ int64_t gp_group_of(const int4* desc, int64_t ngroups, int64_t I) {
+    int64_t lo = 0, hi = ngroups;  // answer in [0, ngroups)
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (desc[mid].x <= I) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+__global__ void k_gp_pb(int64_t nc, const int* __restrict__ crp, const int* __restrict__ cptr, int* pb) {
+    for (int64_t I = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; I <= nc;
+         I += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        pb[I] = cptr[crp[I]] & GP_MASK;
+}
+
+// st[0]: longest member row
+__global__ void k_gp_members(int64_t nf, const int* __restrict__ rp, const int* __restrict__ midx,
+                             const int* __restrict__ dpos, int* mstart, uint8_t* mdoff, int* st) {
+    int mx = 0;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nf;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = midx[j];
+        const int a = rp[m], len = rp[m + 1] - a, d = dpos[m];
+        mstart[j] = a;
+        mdoff[j] = static_cast<uint8_t>(d >= a && d - a < 255 ? d - a : 255);
+        mx = max(mx, len);
+    }
+    atomicMax(st, mx);
+}
+// st[1]: largest coarse row (contributions), st[2]: most members of a coarse row
+__global__ void k_gp_rows(int64_t nc, const int* __restrict__ crp, const int* __restrict__ cptr,
+                          const int* __restrict__ mptr, int* st) {
+    int mr = 0, mm = 0;
+    for (int64_t I = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; I < nc;
+         I += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        mr = max(mr, (cptr[crp[I + 1]] & GP_MASK) - (cptr[crp[I]] & GP_MASK));
+        mm = max(mm, mptr[I + 1] - mptr[I]);
+    }
+    atomicMax(st + 1, mr);
+    atomicMax(st + 2, mm);
+}
+__global__ void k_gp_desc(int64_t ngroups, const int* __restrict__ first, const int* __restrict__ crp,
+                          const int* __restrict__ cptr, const int* __restrict__ mptr, int4* desc) {
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g <= ngroups;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int I = first[g];
+        const int c0 = crp[I];
+        desc[g] = make_int4(I, mptr[I], c0, cptr[c0] & GP_MASK);
+    }
+}
+// st[3]: most contributions of a group, st[4]: most members of a group (checks)
+__global__ void k_gp_check(int64_t ngroups, const int4* __restrict__ desc, int* st) {
+    int mb = 0, mm = 0;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < ngroups;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        mb = max(mb, desc[g + 1].w - desc[g].w);
+        mm = max(mm, desc[g + 1].y - desc[g].y);
+    }
+    atomicMax(st + 3, mb);
+    atomicMax(st + 4, mm);
+}
+// per fine entry: its offset in the member row | the member's number in its group << 8
+__global__ void k_gp_emap(int64_t nf, const int* __restrict__ midx, const int* __restrict__ agg,
+                          const int* __restrict__ rp, int64_t ngroups, const int4* __restrict__ desc,
+                          uint16_t* emap) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nf;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = midx[j];
+        const int64_t g = gp_group_of(desc, ngroups, agg[i]);
+        const int loc = static_cast<int>(j - desc[g].y);
+        for (int e = rp[i]; e < rp[i + 1]; ++e) emap[e] = static_cast<uint16_t>((e - rp[i]) | (loc << 8));
+    }
+}
+__global__ void k_gp_code(int64_t m, const int* __restrict__ contrib, const uint16_t* __restrict__ emap,
+                          uint16_t* code) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int e = contrib[p];
+        code[p] = static_cast<uint16_t>(emap[e & 0x7fffffff] | (e < 0 ? 0x8000 : 0));
+    }
+}
+__global__ void k_gp_entry_start(int64_t nnz_c, const int* __restrict__ cptr, uint16_t* code) {
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz_c;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        code[cptr[q] & GP_MASK] |= 0x4000;
+}
+// per group: split its coarse entries into <= 32 contiguous runs of at most
+// L contributions (L = the smallest bound >= max(ceil(nbuf / 32), longest
+// entry) for which greedy cutting needs <= 32 runs); lane k's run starts at
+// contribution (low byte) and entry (high byte) of lanes[32 g + k]
+__global__ void k_gp_lanes(int64_t ngroups, const int4* __restrict__ desc, const int* __restrict__ cptr,
+                           uint16_t* lanes) {
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < ngroups;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int4 d0 = desc[g], d1 = desc[g + 1];
+        const int nent = d1.z - d0.z, nbuf = d1.w - d0.w;
+        int longest = 0;
+        for (int q = 0; q < nent; ++q)
+            longest = max(longest, (cptr[d0.z + q + 1] & GP_MASK) - (cptr[d0.z + q] & GP_MASK));
+        int L = max((nbuf + 31) / 32, longest);
+        for (;; ++L) {
+            int runs = 0, cur = L + 1;
+            for (int q = 0; q < nent; ++q) {
+                const int k = (cptr[d0.z + q + 1] & GP_MASK) - (cptr[d0.z + q] & GP_MASK);
+                if (cur + k > L) {
+                    ++runs;
+                    cur = 0;
+                }
+                cur += k;
+            }
+            if (runs <= 32) break;
+        }
+        uint16_t* out = lanes + g * 32;
+        int lane = 0, cur = L + 1;
+        for (int q = 0; q < nent; ++q) {
+            const int p = (cptr[d0.z + q] & GP_MASK) - d0.w;
+            const int k = (cptr[d0.z + q + 1] & GP_MASK) - (cptr[d0.z + q] & GP_MASK);
+            if (cur + k > L) {
+                out[lane++] = static_cast<uint16_t>(p | (q << 8));
+                cur = 0;
+            }
+            cur += k;
+        }
+        for (; lane < 32; ++lane) out[lane] = static_cast<uint16_t>(nbuf | (nent << 8));
+    }
+}
+}  // namespace
+
+void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, const int* midx, const int* dpos,
+                  int64_t nc, const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan) {
+    plan = GrpPlan{};
+    const int64_t nf = A.n, m = A.nnz;
+    if (nf == 0 || nc == 0 || nnz_c == 0 || m >= (int64_t{1} << 30)) return;
+    DevArray<int> st(5, c.stream);
+    CK(cudaMemsetAsync(st.get(), 0, 5 * sizeof(int), c.stream));
+    plan.mstart.alloc(nf + 8, c.stream);  // + slack: k_rap_grp's 16-byte bulk-copy windows
+    plan.mdoff.alloc(nf + 16, c.stream);
+    LAUNCH(c, "setup", 0.0, k_gp_members, grid_for(nf, SB, c.num_sms * 16), SB, 0, nf, A.rp, midx, dpos,
+           plan.mstart.get(), plan.mdoff.get(), st.get());
+    LAUNCH(c, "setup", 0.0, k_gp_rows, grid_for(nc, SB, c.num_sms * 16), SB, 0, nc, crp, cptr, mptr, st.get());
+    int h[5];
+    d2h(h, st.get(), 3, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    // member rows <= 255 entries (8-bit offsets), every coarse row fits a
+    // group (<= 256 contributions, <= 64 members)
+    if (h[0] > 255 || h[1] > GP_BUF || h[2] > GP_MEM) {
+        plan = GrpPlan{};
+        return;
+    }
+    // greedy packing of consecutive coarse rows (host, once per pattern)
+    std::vector<int> pbh(nc + 1), mph(nc + 1), first;
+    {
+        DevArray<int> pb(nc + 1, c.stream);
+        LAUNCH(c, "setup", 0.0, k_gp_pb, grid_for(nc + 1, SB, c.num_sms * 16), SB, 0, nc, crp, cptr, pb.get());
+        d2h(pbh.data(), pb.get(), nc + 1, c.stream);
+        d2h(mph.data(), mptr, nc + 1, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+    }
+    first.reserve(static_cast<size_t>(pbh[nc] / 200 + 16));
+    int g0 = 0;
+    first.push_back(0);
+    for (int64_t I = 0; I < nc; ++I) {
+        if (pbh[I + 1] - pbh[g0] > GP_BUF || mph[I + 1] - mph[g0] > GP_MEM) {
+            g0 = static_cast<int>(I);
+            first.push_back(g0);
+        }
+    }
+    plan.ngroups = static_cast<int64_t>(first.size());
+    first.push_back(static_cast<int>(nc));
+    {
+        DevArray<int> fd(plan.ngroups + 1, c.stream);
+        h2d(fd.get(), first.data(), plan.ngroups + 1, c.stream);
+        plan.desc.alloc(plan.ngroups + 1, c.stream);
+        LAUNCH(c, "setup", 0.0, k_gp_desc, grid_for(plan.ngroups + 1, SB, c.num_sms * 16), SB, 0, plan.ngroups,
+               fd.get(), crp, cptr, mptr, plan.desc.get());
+        LAUNCH(c, "setup", 0.0, k_gp_check, grid_for(plan.ngroups, SB, c.num_sms * 16), SB, 0, plan.ngroups,
+               plan.desc.get(), st.get());
+        d2h(h + 3, st.get() + 3, 2, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+    }
+    if (h[3] > GP_BUF || h[4] > GP_MEM) fail(AMGR_E_RUNTIME, "rap_grp_plan: group bounds violated (internal error)");
+    {
+        DevArray<uint16_t> emap(m, c.stream);
+        LAUNCH(c, "setup", 0.0, k_gp_emap, grid_for(nf, SB, c.num_sms * 16), SB, 0, nf, midx, agg, A.rp,
+               plan.ngroups, plan.desc.get(), emap.get());
+        plan.code.alloc(m + 8, c.stream);
+        CK(cudaMemsetAsync(plan.code.get() + m, 0, 8 * sizeof(uint16_t), c.stream));
+        LAUNCH(c, "setup", 0.0, k_gp_code, grid_for(m, SB, c.num_sms * 16), SB, 0, m, contrib, emap.get(),
+               plan.code.get());
+    }
+    LAUNCH(c, "setup", 0.0, k_gp_entry_start, grid_for(nnz_c, SB, c.num_sms * 16), SB, 0, nnz_c, cptr,
+           plan.code.get());
+    plan.lanes.alloc(plan.ngroups * 32, c.stream);
+    LAUNCH(c, "setup", 0.0, k_gp_lanes, grid_for(plan.ngroups, 128, c.num_sms * 16), 128, 0, plan.ngroups,
+           plan.desc.get(), cptr, plan.lanes.get());
     plan.ok = true;
 }
 

@@ -74,6 +74,31 @@ struct RowPlan {
 void rap_rows_plan(Ctx& c, const CsrView& A, const int* agg, const int* midx, int64_t nc, const int* crp,
                    const int* ccol, RowPlan& plan);
 
+// Warp-group Galerkin plan (k_rap_grp).  Coarse rows are
+// cut into groups of consecutive rows with <= 255 contributions (= entries
+// of their member rows) and <= 64 member rows; a warp gathers a group's
+// contributions into shared memory in the plan's order (cptr/contrib, the
+// reference's bracket, csr.cpp:145-194) and each lane sums one of 32
+// contiguous runs of coarse entries, balanced by contribution count.  Per contribution the plan keeps 2 bytes
+// (offset inside its member row, the member's number in the group, a bit
+// for the first contribution of a coarse entry, the bracket bit), per member
+// row its CSR start and diagonal offset (fused damped-Jacobi rebuild,
+// smoother.cpp:8-32).
+struct GrpPlan {
+    bool ok = false;
+    int64_t ngroups = 0;
+    DevArray<int4> desc;      // [ngroups + 1] {first coarse row, first member (R order), first coarse entry, first contribution}
+    DevArray<int> mstart;     // [nf] R order: first CSR position of member row midx[j]
+    DevArray<uint8_t> mdoff;  // [nf] diagonal offset inside it (255: no diagonal)
+    DevArray<uint16_t> code;  // [nnz_f + 8] row offset | member << 8 | entry start << 14 | bracket end << 15
+    DevArray<uint16_t> lanes; // [ngroups * 32] per lane: first contribution | first entry << 8 (balanced split)
+};
+// Builds the plan when the level fits (plan.ok tells).  mptr/midx: R;
+// dpos: diagonal CSR position per fine row (-1: none); crp: coarse row
+// pointers; cptr/contrib: the level's RapPlan.
+void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, const int* midx, const int* dpos,
+                  int64_t nc, const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan);
+
 // ---- smoothed aggregation (extension) ----
 // Device SpGEMM C = A B: structural pattern of C (sorted columns) and the
 // numeric plan (per output entry, its (a index, b index) products in the

@@ -603,12 +603,14 @@ def test_pattern_change_keeps_coded_columns(ctx):
     assert np.array_equal(_bits(amg.vcycle(hu, f)), _bits(ref.vcycle(ru, f, fixed=True)))
 
 
-@pytest.mark.parametrize("rows,fuse", [("1", "1"), ("0", "0"), ("0", "1")])
-def test_rebuild_zero_diagonal_error_fused_and_separate(ctx, monkeypatch, rows, fuse):
+@pytest.mark.parametrize("groups,rows,fuse", [("1", "0", "0"), ("0", "1", "1"), ("0", "0", "0"), ("0", "0", "1")])
+def test_rebuild_zero_diagonal_error_fused_and_separate(ctx, monkeypatch, groups, rows, fuse):
     """A partial update whose new A_0 has a zero diagonal fails with the
     reference's message (hierarchy.cpp:124-132 + :31-35), both when the
-    Jacobi rebuild is fused into the member-row Galerkin kernel and when it
-    runs separately; a coarse-level zero diagonal names its level."""
+    Jacobi rebuild is fused into a Galerkin kernel (warp-group, the default;
+    member-row) and when it runs separately; a coarse-level zero diagonal
+    names its level."""
+    monkeypatch.setenv("AMGR_RAP_GROUPS", groups)
     monkeypatch.setenv("AMGR_RAP_ROWS", rows)
     monkeypatch.setenv("AMGR_FUSE_JACOBI", fuse)
     A = P.grid3d_values("dambreak", 12, 3)
@@ -629,9 +631,10 @@ def test_rebuild_zero_diagonal_error_fused_and_separate(ctx, monkeypatch, rows, 
 
 @pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "blob_20", "random_300", "poisson1d_64_ce10"])
 def test_member_row_rap_matches_contrib_rap(ctx, monkeypatch, name):
-    """k_rap_rows (member-row plan, fused Jacobi), k_rap_tma with the Jacobi
-    rebuild fused into its chunk epilogue, and k_rap_tma + separate k_jacobi
-    give the same bits, and all match the reference."""
+    """k_rap_grp (warp-group plan, fused fine Jacobi; the default),
+    k_rap_rows (member-row plan, fused Jacobi), k_rap_tma with the coarse
+    Jacobi fused, and k_rap_tma + separate k_jacobi give the same bits, and
+    all match the reference."""
     make, kw = CASES[name]
     A = make()
     h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
@@ -639,7 +642,9 @@ def test_member_row_rap_matches_contrib_rap(ctx, monkeypatch, name):
     rp, ci, v = A
     B = (rp, ci, np.asarray(v) * (1.0 + 0.05 * np.random.default_rng(9).random(len(v))))
     ru = ref.partial_update(r, B, ref.params(**kw))
-    for rows, fuse in (("1", "1"), ("0", "0"), ("0", "1"), ("1", "0")):
+    for groups, rows, fuse in (("1", "0", "0"), ("0", "1", "1"), ("0", "0", "0"), ("0", "0", "1"), ("0", "1", "0"),
+                               ("1", "0", "1")):
+        monkeypatch.setenv("AMGR_RAP_GROUPS", groups)
         monkeypatch.setenv("AMGR_RAP_ROWS", rows)
         monkeypatch.setenv("AMGR_FUSE_JACOBI", fuse)
         h.rebuild_values(B[2])
@@ -660,7 +665,8 @@ def test_rebuild_coarse_level_zero_diagonal_names_its_level(ctx, monkeypatch):
     with pytest.raises(ref.RefError) as er:
         ref.partial_update(r, (rp, ci, v), ref.params(**prm))
     assert "level 1" in str(er.value)
-    for fuse in ("1", "0"):
+    for groups, fuse in (("1", "0"), ("0", "1"), ("0", "0")):
+        monkeypatch.setenv("AMGR_RAP_GROUPS", groups)
         monkeypatch.setenv("AMGR_FUSE_JACOBI", fuse)
         h = amg.setup(A, amg.AmgParams(**prm), ctx=ctx)
         with pytest.raises(amg.InvalidArgument) as eg:
