@@ -16,6 +16,10 @@
 
 #include "../../include/amgr.h"
 
+#ifndef GRP_BUF
+#define GRP_BUF 256  // contributions per k_rap_grp group buffer (<= 256: 8-bit offsets)
+#endif
+
 namespace amgr {
 
 // ---- errors ----------------------------------------------------------------

@@ -1145,7 +1145,7 @@ void launch_rap_tma_fused(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, 
 #ifndef RG_MINB
 #define RG_MINB 5
 #endif
-constexpr int RG_WARPS = 8, RG_BUF = 256, RG_MEM = 64;
+constexpr int RG_WARPS = 8, RG_BUF = GRP_BUF, RG_MEM = 64;
 struct RgSmem {
     double x[RG_BUF];
     uint32_t codew[RG_BUF / 2 + 2];
@@ -1186,9 +1186,9 @@ __global__ void __launch_bounds__(RG_WARPS * 32, RG_MINB) k_rap_grp(GrpArgs a) {
         const int dp = d0.w & 1;
         const int pw = (nbuf + dp + 1) >> 1;  // <= 128 words
         const uint32_t* cp = reinterpret_cast<const uint32_t*>(a.code) + ((d0.w - dp) >> 1);
-        uint32_t wv[4];
+        uint32_t wv[RG_BUF / 64];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < RG_BUF / 64; ++k) {
             const int t = lane + 32 * k;
             wv[k] = t < pw ? __ldg(cp + t) : 0u;
         }
@@ -1197,9 +1197,9 @@ __global__ void __launch_bounds__(RG_WARPS * 32, RG_MINB) k_rap_grp(GrpArgs a) {
             if (lane + 32 * k < nmem) S.mst[lane + 32 * k] = ms[k];
         __syncwarp();
         // word w holds contributions 2w - dp and 2w - dp + 1
-        double v[8];
+        double v[RG_BUF / 32];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < RG_BUF / 64; ++k) {
             const int w = lane + 32 * k;
             const int t = 2 * w - dp;
             const uint32_t c2 = wv[k];
@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(RG_WARPS * 32, RG_MINB) k_rap_grp(GrpArgs a) {
             v[2 * k + 1] = t + 1 < nbuf ? __ldg(a.af + S.mst[(hi >> 8) & 63u] + (hi & 255u)) : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < RG_BUF / 64; ++k) {
             const int w = lane + 32 * k;
             const int t = 2 * w - dp;
             if (w < pw) S.codew[w] = wv[k];

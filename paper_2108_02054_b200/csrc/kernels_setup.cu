@@ -651,7 +651,7 @@ void rap_rows_plan(Ctx& c, const CsrView& A, const int* agg, const int* midx, in
 
 // ---- warp-group Galerkin plan (k_rap_grp) ------------------------------------
 namespace {
-constexpr int GP_BUF = 255, GP_MEM = 64;
+constexpr int GP_BUF = GRP_BUF - 1, GP_MEM = 64;
 constexpr int GP_MASK = (1 << 30) - 1;  // cptr bit 30 flags the coarse diagonal
 
 // group of coarse row I: the last group whose first row is <= I
