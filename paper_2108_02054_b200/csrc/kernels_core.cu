@@ -2135,6 +2135,166 @@ __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __res
     for (int i = lane; i < n; i += 32) x[i] = xs[i];
 }
 
+// Multi-warp variant (default for n <= 160): warp 0 runs the forward sweep
+// (as above) and the backward row chain on lane 0; three helper warps form
+// the chain's products ahead of it.  Row i of the chain is
+//   s = y_i - U_i,i+1 x_i+1 - U_i,i+2 x_i+2 - P_i,i+3 - ... - P_i,n-1,
+// x_i = s / U_ii (dense_lu.cpp:64-72, same association): the two newest
+// products are formed by the chain itself, the rest (P_ij = U_ij x_j, all
+// x_j known two rows earlier) by the helpers into a 3-slot ring of product
+// rows, so the chain is one shared-memory load + one DSUB per entry.  The
+// division uses the reciprocal formed ahead by the helpers (correctly
+// rounded, __drcp_rn) and Markstein's correction q = s*y, r = s - U q
+// (exact, FMA), x = q + r*y, which is the correctly rounded s / U_ii when no
+// operand or result is near the under/overflow range (Markstein 1990; the
+// same final step as CUDA's own division) — elsewhere it falls back to
+// __ddiv_rn.  Bit-identical to the reference's solve.  The factor's TMA copy
+// is issued before the PDL wait (it does not depend on the previous kernel).
+constexpr int LM_HELP = 3, LM_PAD = 24;
+
+__device__ __forceinline__ bool mk_range(double v) {
+    const int e = (__double2hiint(v) >> 20) & 0x7ff;
+    return e >= 600 && e <= 1446;  // |v| in [2^-423, 2^424): quotient, residual and products stay normal
+}
+__device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+__global__ void __launch_bounds__(32 * (1 + LM_HELP)) k_lu_solve_mw(int n, const double* __restrict__ m,
+                                                                   const int* __restrict__ perm, const double* b,
+                                                                   double* x, Gate g) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_prog, s_ready[3];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nn2 = (n * n + 1) & ~1, W = n + LM_PAD;
+    double* ms = sm;            // n*n factor (TMA target)
+    double* xs = sm + nn2;      // y, then x (W)
+    double* pb = xs + W;        // 3 product rows (3W)
+    double* rd = pb + 3 * W;    // 1 / U_ii (n)
+    int* okd = reinterpret_cast<int*>(rd + n);  // U_ii in range (n)
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        const uint32_t bytes = static_cast<uint32_t>(nn2 * 8);
+        mbar_expect_tx(&bar, bytes);
+        tma_load_1d(ms, m, bytes, &bar);
+    }
+    pdl_enter();
+    const bool off = gated_off(g);
+    for (int i = tid; i < 4 * W; i += blockDim.x) xs[i] = 0.0;  // xs + product rows (+0.0 padding)
+    if (tid == 0) {
+        s_prog = n;
+        s_ready[0] = s_ready[1] = s_ready[2] = -1;
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    if (off) return;
+    if (wid == 0) {
+        double y[LW_Q];
+#pragma unroll
+        for (int q = 0; q < LW_Q; ++q) {
+            const int i = 32 * q + lane;
+            y[q] = i < n ? b[perm[i]] : 0.0;
+        }
+        // forward (unit L), column-oriented, rows in registers
+#pragma unroll
+        for (int gq = 0; gq < LW_Q; ++gq) {
+            if (32 * gq >= n - 1) break;
+            for (int t = 0; t < 32; ++t) {
+                const int j = 32 * gq + t;
+                if (j >= n - 1) break;
+                const double yj = __shfl_sync(0xffffffffu, y[gq], t);
+#pragma unroll
+                for (int q = gq; q < LW_Q; ++q) {
+                    const int i = 32 * q + lane;
+                    if (i > j && i < n) y[q] = dsub(y[q], dmul(ms[i * n + j], yj));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < LW_Q; ++q) {
+            const int i = 32 * q + lane;
+            if (i < n) xs[i] = y[q];
+        }
+    } else {
+        for (int i = tid - 32; i < n; i += 32 * LM_HELP) {
+            const double u = ms[i * n + i];
+            rd[i] = __drcp_rn(u);
+            okd[i] = mk_range(u) ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    if (wid == 0) {
+        if (lane == 0) {
+            auto mdiv = [&](double s, int i) -> double {
+                const double u = ms[i * n + i];
+                if (okd[i] && mk_range(s)) {
+                    const double yv = rd[i];
+                    const double q = __dmul_rn(s, yv);
+                    const double r = __fma_rn(-u, q, s);
+                    return __fma_rn(r, yv, q);
+                }
+                return __ddiv_rn(s, u);
+            };
+            double x1 = mdiv(xs[n - 1], n - 1), x2 = 0.0;
+            xs[n - 1] = x1;
+            __threadfence_block();
+            st_vol(&s_prog, n - 1);
+            for (int i = n - 2; i >= 0; --i) {
+                const double* mi = ms + i * n;
+                double s = dsub(xs[i], dmul(mi[i + 1], x1));
+                if (i + 2 < n) s = dsub(s, dmul(mi[i + 2], x2));
+                if (i + 3 < n) {
+                    const double* P = pb + (i % 3) * W;
+                    while (ld_vol(&s_ready[i % 3]) != i) {
+                    }
+                    int j = i + 3;
+                    double a[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) a[t] = P[j + t];
+                    for (; j < n; j += 8) {
+                        double c[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) c[t] = P[j + 8 + t];  // +0.0 past n
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) s = dsub(s, a[t]);   // padding: s - (+0.0) == s
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) a[t] = c[t];
+                    }
+                }
+                const double xi = mdiv(s, i);
+                xs[i] = xi;
+                __threadfence_block();
+                st_vol(&s_prog, i);
+                x2 = x1;
+                x1 = xi;
+            }
+        }
+    } else {
+        const int hid = tid - 32;
+        for (int i = n - 4; i >= 0; --i) {
+            // products P_ij = U_ij x_j, j >= i + 3, once x_{i+3} is out (the
+            // chain then no longer reads slot i % 3, last used by row i + 3)
+            if (hid == 0) {
+                while (ld_vol(&s_prog) > i + 3) {
+                }
+                __threadfence_block();
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LM_HELP) : "memory");
+            double* P = pb + (i % 3) * W;
+            const double* mi = ms + i * n;
+            for (int j = i + 3 + hid; j < n; j += 32 * LM_HELP) P[j] = dmul(mi[j], xs[j]);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LM_HELP) : "memory");
+            if (hid == 0) {
+                __threadfence_block();
+                st_vol(&s_ready[i % 3], i);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) x[i] = xs[i];
+}
+
 // perm[i] = the rhs index that lands at position i after the reference's
 // sequential swaps for k = 0..n-1: swap(x[k], x[piv[k]]) (dense_lu.cpp:60-61)
 __global__ void k_lu_perm(int n, const int64_t* __restrict__ piv, int* __restrict__ perm) {
@@ -2588,7 +2748,23 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* per
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x, Gate g,
               const int* perm) {
     if (n == 0) return;
-    const char* old = std::getenv("AMGR_LU_SOLVE_OLD");
+    const char* old = std::getenv("AMGR_LU_SOLVE_OLD");  // 1: k_lu_solve, 2: single-warp k_lu_solve_warp
+    if (perm && n <= 32 * LW_Q && !(old && (old[0] == '1' || old[0] == '2'))) {
+        static const bool attr = [] {
+            const int W = 32 * LW_Q + LM_PAD;
+            CK(cudaFuncSetAttribute(k_lu_solve_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(double) * (32 * LW_Q * 32 * LW_Q + 4 * W + 32 * LW_Q) +
+                                                     sizeof(int) * 32 * LW_Q)));
+            return true;
+        }();
+        (void)attr;
+        const int64_t W = n + LM_PAD;
+        const size_t sm = sizeof(double) * static_cast<size_t>(((n * n + 1) & ~1) + 4 * W + n) +
+                          sizeof(int) * static_cast<size_t>(n);
+        LAUNCH_PDL(c, "coarse_solve", 0.0, k_lu_solve_mw, 1, 32 * (1 + LM_HELP), sm, static_cast<int>(n), m, perm, b,
+                   x, g);
+        return;
+    }
     if (perm && n <= 32 * LW_Q && !(old && old[0] == '1')) {
         static const bool attr = [] {
             CK(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
