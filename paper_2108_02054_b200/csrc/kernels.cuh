@@ -181,7 +181,10 @@ void spai0_rebuild(Ctx& c, const CsrView& A, const int* diag_pos, double* w, int
 void lu_densify(Ctx& c, const CsrView& A, double* dense);
 // in-place LU with partial pivoting; piv[k]; *status = -1 ok, else the zero-pivot step
 // perm (optional, n ints): the composed row swaps for lu_solve's fast path
-void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm = nullptr);
+// A: the operator as CSR (the dense copy is staged in shared memory for
+// n <= 160, else densified into m first); null: m holds it dense
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm = nullptr,
+               const CsrView* A = nullptr);
 // x = LU \ b in the reference's order; x may alias b.  With perm (from
 // lu_factor) and n <= 160: the single-warp kernel (k_lu_solve_warp)
 void lu_solve(Ctx& c, int64_t n, const double* m, const int64_t* piv, const double* b, double* x,

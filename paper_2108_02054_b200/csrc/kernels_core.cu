@@ -1721,7 +1721,11 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_factor(int n, double* gm, int
 //               factor is written from Ls in the reference's swapped order.
 //   GJ = true : in-place Gauss-Jordan inverse for AMGR_COARSE_INVERSE
 //               (tolerance-level extension; output inv = A^{-1}).
-constexpr int DR_ROWS = 10, DR_COLS = 5, DR_THREADS = 512, DR_MAXN = 160;
+#ifndef DR_THREADS_CFG
+#define DR_THREADS_CFG 512
+#endif
+constexpr int DR_THREADS = DR_THREADS_CFG, DR_WARPS = DR_THREADS / 32, DR_ROWS = 160 / DR_WARPS, DR_COLS = 5,
+              DR_MAXN = 160;
 
 // predicated select in PTX: keeps NVVM from turning "for q: if (q == x) use
 // a[q]" into a dynamically indexed (local-memory) access to the register tile
@@ -1732,9 +1736,17 @@ __device__ __forceinline__ double dr_sel(bool p, double a, double b) {
     return r;
 }
 
+// csr: the coarsest operator straight from its CSR arrays (LU mode; the
+// dense copy then never exists in global memory: staged in Ls, which the
+// factorization overwrites later); else gin (n x n, row-major)
+struct CsrIn {
+    const int* rp = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
 template <bool GJ>
 __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double* gin, double* gout,
-                                                             int64_t* piv, int* status, int* perm) {
+                                                             int64_t* piv, int* status, int* perm, CsrIn csr) {
     extern __shared__ double Ls[];  // LU: n x n multiplier history, row = physical row
     __shared__ double colbuf[2][DR_MAXN], coll[DR_MAXN], rowbuf[DR_MAXN], lbuf[DR_MAXN];
     __shared__ int lp[DR_MAXN], posof[DR_MAXN];
@@ -1747,13 +1759,29 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
         colbuf[1][i] = 0.0;
         lbuf[i] = 0.0;
     }
+    if (!GJ && csr.rp) {
+        for (int t = tid; t < n * n; t += DR_THREADS) Ls[t] = 0.0;
+        __syncthreads();
+        for (int i = tid; i < n; i += DR_THREADS)
+            for (int k = csr.rp[i]; k < csr.rp[i + 1]; ++k) Ls[i * n + csr.col[k]] = csr.val[k];
+        __syncthreads();
 #pragma unroll
-    for (int q = 0; q < DR_ROWS; ++q)
+        for (int q = 0; q < DR_ROWS; ++q)
 #pragma unroll
-        for (int m = 0; m < DR_COLS; ++m) {
-            const int i = ty + 16 * q, j = tx + 32 * m;
-            a[q][m] = (i < n && j < n) ? gin[static_cast<int64_t>(i) * n + j] : 0.0;
-        }
+            for (int m = 0; m < DR_COLS; ++m) {
+                const int i = ty + DR_WARPS * q, j = tx + 32 * m;
+                a[q][m] = (i < n && j < n) ? Ls[i * n + j] : 0.0;
+            }
+        __syncthreads();  // Ls is the multiplier history from here on
+    } else {
+#pragma unroll
+        for (int q = 0; q < DR_ROWS; ++q)
+#pragma unroll
+            for (int m = 0; m < DR_COLS; ++m) {
+                const int i = ty + DR_WARPS * q, j = tx + 32 * m;
+                a[q][m] = (i < n && j < n) ? gin[static_cast<int64_t>(i) * n + j] : 0.0;
+            }
+    }
     for (int i = tid; i < DR_MAXN; i += DR_THREADS) {
         lp[i] = i;
         posof[i] = i;
@@ -1775,7 +1803,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
             if (tx == kl) {
 #pragma unroll
                 for (int q = 0; q < DR_ROWS; ++q) {
-                    const int i = ty + 16 * q;
+                    const int i = ty + DR_WARPS * q;
                     if (i < n) {
                         cb[i] = a[q][mb];
                         coll[posof[i]] = a[q][mb];
@@ -1831,9 +1859,9 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
             }
             const int r = s_r;
             const double pivot = s_piv;
-            // 3. pivot row -> smem (owner warp: ty == r % 16, register row r / 16)
-            if (ty == (r & 15)) {
-                const int qr = r >> 4;
+            // 3. pivot row -> smem (owner warp: ty == r % DR_WARPS, register row r / DR_WARPS)
+            if (ty == r % DR_WARPS) {
+                const int qr = r / DR_WARPS;
                 const double ip = GJ ? 1.0 / pivot : 0.0;
 #pragma unroll
                 for (int m = 0; m < DR_COLS; ++m) {
@@ -1872,15 +1900,15 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
             if (GJ) {
 #pragma unroll
                 for (int q = 0; q < DR_ROWS; ++q) {
-                    const double f = cb[ty + 16 * q];
-                    if (tx == kl) a[q][mb] = dr_sel(ty + 16 * q != r, 0.0, a[q][mb]);
+                    const double f = cb[ty + DR_WARPS * q];
+                    if (tx == kl) a[q][mb] = dr_sel(ty + DR_WARPS * q != r, 0.0, a[q][mb]);
 #pragma unroll
                     for (int m = 0; m < DR_COLS; ++m) a[q][m] = __fma_rn(-f, rb[m], a[q][m]);
                 }
             } else {
 #pragma unroll
                 for (int q = 0; q < DR_ROWS; ++q) {
-                    const double l = lbuf[ty + 16 * q];
+                    const double l = lbuf[ty + DR_WARPS * q];
 #pragma unroll
                     for (int m = mb; m < DR_COLS; ++m) a[q][m] = dsub(a[q][m], dmul(l, rb[m]));
                 }
@@ -1893,7 +1921,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
     // inverse un-permuted: inv[posof[p]][lp[j]] = a[p][j]
 #pragma unroll
     for (int q = 0; q < DR_ROWS; ++q) {
-        const int i = ty + 16 * q;
+        const int i = ty + DR_WARPS * q;
         if (i < n) {
             const int rl = posof[i];
             const int64_t row = static_cast<int64_t>(rl) * n;
@@ -2720,9 +2748,15 @@ static void lu_perm(Ctx& c, int64_t n, const int64_t* piv, int* perm) {
     if (perm) LAUNCH(c, "coarse", 0.0, k_lu_perm, 1, 32, 0, static_cast<int>(n), piv, perm);
 }
 
-void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm) {
+void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm, const CsrView* A) {
     if (n == 0) return;
     if (n <= DR_MAXN) {
+        CsrIn ci;
+        if (A) {
+            ci.rp = A->rp;
+            ci.col = A->col;
+            ci.val = A->val;
+        }
         const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
         // always opt in: dynamic + static shared memory above 48 KB needs the
         // attribute even when the dynamic part alone is below it (n = 72..78)
@@ -2733,9 +2767,10 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* per
         }();
         (void)attr;
         LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status,
-               perm);
+               perm, ci);
         return;
     }
+    if (A) lu_densify(c, *A, m);
     if (n > 2048) invalid("coarse_factorize: coarse system larger than 2048 unknowns is not supported on device");
     const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
     const int use_smem = sm <= 180 * 1024 ? 1 : 0;
@@ -2804,7 +2839,7 @@ bool lu_factor_csr(Ctx& c, const CsrView& A, double* lu, int64_t* piv, int* stat
 bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {
     if (n == 0 || n > DR_MAXN) return false;
     LAUNCH(c, "coarse", 0.0, k_dense_reg<true>, 1, DR_THREADS, 0, static_cast<int>(n), a, inv, piv, status,
-           static_cast<int*>(nullptr));
+           static_cast<int*>(nullptr), CsrIn{});
     return true;
 }
 

@@ -57,9 +57,26 @@ __device__ __forceinline__ double row_sum(const TailLevel& L, int i, X x) {
     return s;
 }
 
-__global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, Gate g) {
+// CL = false: cooperative grid (grid-wide barriers); CL = true: the grid is
+// ONE thread-block cluster (hardware cluster barriers, all CTAs in one GPC)
+template <bool CL>
+struct TailSync {
+    __device__ __forceinline__ void sync() {
+        if constexpr (CL)
+            cg::this_cluster().sync();
+        else
+            cg::this_grid().sync();
+    }
+};
+
+// cluster variant: 16 CTAs of 512 threads (a 16-CTA cluster of 1024-thread
+// CTAs does not fit a B200 GPC)
+constexpr int TL_CBLOCK = 512;
+template <bool CL>
+__global__ void __launch_bounds__(CL ? TL_CBLOCK : TL_BLOCK) k_tail_down(TailDesc d, double om, Gate g) {
+    if (CL) pdl_enter();
     if (gated_off(g)) return;
-    cg::grid_group grid = cg::this_grid();
+    TailSync<CL> grid;
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
     // unrolled: every descriptor access has a compile-time offset (a dynamic
@@ -96,9 +113,11 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_down(TailDesc d, double om, G
     }
 }
 
-__global__ void __launch_bounds__(TL_BLOCK) k_tail_up(TailDesc d, double om, Gate g) {
+template <bool CL>
+__global__ void __launch_bounds__(CL ? TL_CBLOCK : TL_BLOCK) k_tail_up(TailDesc d, double om, Gate g) {
+    if (CL) pdl_enter();
     if (gated_off(g)) return;
-    cg::grid_group grid = cg::this_grid();
+    TailSync<CL> grid;
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
 #pragma unroll
@@ -118,6 +137,12 @@ __global__ void __launch_bounds__(TL_BLOCK) k_tail_up(TailDesc d, double om, Gat
         }
         if (l > 0) grid.sync();
     }
+}
+
+// cluster size of the cluster-scoped tail (AMGR_TAIL_CLUSTER, 0: cooperative grid)
+int tail_cluster() {
+    const char* e = std::getenv("AMGR_TAIL_CLUSTER");
+    return e ? std::atoi(e) : 0;
 }
 
 template <class K>
@@ -140,14 +165,45 @@ void launch_coop(Ctx& c, const char* fam, K kernel, const TailDesc& d, double om
     ++c.launches;
 }
 
+template <class K>
+void launch_cluster(Ctx& c, const char* fam, K kernel, const TailDesc& d, double om, Gate g, int cs) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(cs));
+    cfg.blockDim = dim3(TL_CBLOCK);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c.pdl ? 2 : 1;
+    probe_begin(c, fam, 0.0);
+    CK(cudaLaunchKernelEx(&cfg, kernel, d, om, g));
+    probe_end(c, fam);
+    ++c.launches;
+}
+
 }  // namespace
 
 void tail_down(Ctx& c, const TailDesc& d, double om, Gate g) {
-    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_down, d, om, g);
+    if (d.count == 0) return;
+    if (const int cs = tail_cluster())
+        launch_cluster(c, "vcycle_tail", k_tail_down<true>, d, om, g, cs);
+    else
+        launch_coop(c, "vcycle_tail", k_tail_down<false>, d, om, g);
 }
 
 void tail_up(Ctx& c, const TailDesc& d, double om, Gate g) {
-    if (d.count > 0) launch_coop(c, "vcycle_tail", k_tail_up, d, om, g);
+    if (d.count == 0) return;
+    if (const int cs = tail_cluster())
+        launch_cluster(c, "vcycle_tail", k_tail_up<true>, d, om, g, cs);
+    else
+        launch_coop(c, "vcycle_tail", k_tail_up<false>, d, om, g);
 }
 
 }  // namespace amgr

@@ -265,10 +265,14 @@ def test_many_levels_and_launch_count(ctx):
 
 
 @pytest.mark.parametrize("name", ["poisson2d_64", "dambreak_24_k20", "random_300"])
-def test_vcycle_tail_kernels_bit_exact(ctx, name, monkeypatch):
-    """The cooperative V-cycle tail (AMGR_TAIL_NNZ, off by default) runs every
-    level in two grid-barrier kernels with prolongation fused into smoothing:
-    same bits as the reference's (fixed) V-cycle and the same solve."""
+@pytest.mark.parametrize("cluster", ["0", "8", "16"])
+def test_vcycle_tail_kernels_bit_exact(ctx, name, monkeypatch, cluster):
+    """The persistent V-cycle tail (AMGR_TAIL_NNZ) runs every level in two
+    kernels with prolongation fused into smoothing, as a cooperative grid
+    (grid barriers) or as one thread-block cluster (AMGR_TAIL_CLUSTER = 8 /
+    16 CTAs, cluster barriers): same bits as the reference's (fixed) V-cycle
+    and the same solve."""
+    monkeypatch.setenv("AMGR_TAIL_CLUSTER", cluster)
     make, kw = CASES[name]
     A = make()
     r = ref.setup(A, ref.params(**kw))
