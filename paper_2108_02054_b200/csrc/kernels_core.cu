@@ -1736,17 +1736,9 @@ __device__ __forceinline__ double dr_sel(bool p, double a, double b) {
     return r;
 }
 
-// csr: the coarsest operator straight from its CSR arrays (LU mode; the
-// dense copy then never exists in global memory: staged in Ls, which the
-// factorization overwrites later); else gin (n x n, row-major)
-struct CsrIn {
-    const int* rp = nullptr;
-    const int* col = nullptr;
-    const double* val = nullptr;
-};
 template <bool GJ>
 __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double* gin, double* gout,
-                                                             int64_t* piv, int* status, int* perm, CsrIn csr) {
+                                                             int64_t* piv, int* status, int* perm) {
     extern __shared__ double Ls[];  // LU: n x n multiplier history, row = physical row
     __shared__ double colbuf[2][DR_MAXN], coll[DR_MAXN], rowbuf[DR_MAXN], lbuf[DR_MAXN];
     __shared__ int lp[DR_MAXN], posof[DR_MAXN];
@@ -1759,29 +1751,13 @@ __global__ void __launch_bounds__(DR_THREADS, 1) k_dense_reg(int n, const double
         colbuf[1][i] = 0.0;
         lbuf[i] = 0.0;
     }
-    if (!GJ && csr.rp) {
-        for (int t = tid; t < n * n; t += DR_THREADS) Ls[t] = 0.0;
-        __syncthreads();
-        for (int i = tid; i < n; i += DR_THREADS)
-            for (int k = csr.rp[i]; k < csr.rp[i + 1]; ++k) Ls[i * n + csr.col[k]] = csr.val[k];
-        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < DR_ROWS; ++q)
+    for (int q = 0; q < DR_ROWS; ++q)
 #pragma unroll
-            for (int m = 0; m < DR_COLS; ++m) {
-                const int i = ty + DR_WARPS * q, j = tx + 32 * m;
-                a[q][m] = (i < n && j < n) ? Ls[i * n + j] : 0.0;
-            }
-        __syncthreads();  // Ls is the multiplier history from here on
-    } else {
-#pragma unroll
-        for (int q = 0; q < DR_ROWS; ++q)
-#pragma unroll
-            for (int m = 0; m < DR_COLS; ++m) {
-                const int i = ty + DR_WARPS * q, j = tx + 32 * m;
-                a[q][m] = (i < n && j < n) ? gin[static_cast<int64_t>(i) * n + j] : 0.0;
-            }
-    }
+        for (int m = 0; m < DR_COLS; ++m) {
+            const int i = ty + DR_WARPS * q, j = tx + 32 * m;
+            a[q][m] = (i < n && j < n) ? gin[static_cast<int64_t>(i) * n + j] : 0.0;
+        }
     for (int i = tid; i < DR_MAXN; i += DR_THREADS) {
         lp[i] = i;
         posof[i] = i;
@@ -2751,12 +2727,7 @@ static void lu_perm(Ctx& c, int64_t n, const int64_t* piv, int* perm) {
 void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* perm, const CsrView* A) {
     if (n == 0) return;
     if (n <= DR_MAXN) {
-        CsrIn ci;
-        if (A) {
-            ci.rp = A->rp;
-            ci.col = A->col;
-            ci.val = A->val;
-        }
+        if (A) lu_densify(c, *A, m);
         const size_t sm = sizeof(double) * static_cast<size_t>(n * n);
         // always opt in: dynamic + static shared memory above 48 KB needs the
         // attribute even when the dynamic part alone is below it (n = 72..78)
@@ -2767,7 +2738,7 @@ void lu_factor(Ctx& c, int64_t n, double* m, int64_t* piv, int* status, int* per
         }();
         (void)attr;
         LAUNCH(c, "coarse", 0.0, k_dense_reg<false>, 1, DR_THREADS, sm, static_cast<int>(n), m, m, piv, status,
-               perm, ci);
+               perm);
         return;
     }
     if (A) lu_densify(c, *A, m);
@@ -2839,7 +2810,7 @@ bool lu_factor_csr(Ctx& c, const CsrView& A, double* lu, int64_t* piv, int* stat
 bool dense_inverse_direct(Ctx& c, int64_t n, const double* a, double* inv, int64_t* piv, int* status) {
     if (n == 0 || n > DR_MAXN) return false;
     LAUNCH(c, "coarse", 0.0, k_dense_reg<true>, 1, DR_THREADS, 0, static_cast<int>(n), a, inv, piv, status,
-           static_cast<int*>(nullptr), CsrIn{});
+           static_cast<int*>(nullptr));
     return true;
 }
 

@@ -19,8 +19,11 @@ ALG = {  # name: (key, algorithmic bytes per launch, formula)
     "smooth_L0": ("vcycle_smooth@0", 9 * Z0 + 4 * (N0 + 1) + 32 * N0, "9*nnz + 4*(n+1) + 32*n (1-byte column codes)"),
     "down_L0": ("vcycle_down@0", 9 * Z0 + 4 * (N0 + 1) + 24 * N0, "9*nnz + 4*(n+1) + 24*n (1-byte codes; u0 folded: w replaces u0)"),
     "down_L1": ("vcycle_down@1", 10 * Z1 + 4 * (N1 + 1) + 24 * N1, "10*nnz + 4*(n+1) + 24*n (2-byte column codes)"),
-    "rap_L0": ("rap@0", 12 * Z0 + 8 * Z1 + 4 * N0 + 4 * (N1 + 1), "12*nnz_f + 8*nnz_c + 4*n_f + 4*(n_c+1)"),
-    "rap_L1": ("rap@1", 12 * Z1 + 8 * Z2 + 4 * N1 + 4 * (N2 + 1), "12*nnz_f + 8*nnz_c + 4*n_f + 4*(n_c+1)"),
+    # k_rap_grp (round 2): the Galerkin product + the fine level's fused damped-Jacobi rebuild
+    "rap_L0": ("rap@0", 12 * Z0 + 8 * Z1 + 4 * N0 + 4 * (N1 + 1) + 20 * N0,
+               "12*nnz_f + 8*nnz_c + 4*n_f + 4*(n_c+1) + 20*n_f (fused Jacobi)"),
+    "rap_L1": ("rap@1", 12 * Z1 + 8 * Z2 + 4 * N1 + 4 * (N2 + 1) + 20 * N1,
+               "12*nnz_f + 8*nnz_c + 4*n_f + 4*(n_c+1) + 20*n_f (fused Jacobi)"),
 }
 WANT = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",

@@ -20,8 +20,8 @@ python tools/region_driver.py 256 vcycle > gpurun_out/plain_v.log 2>&1 && {
   full down_L1 vcycle '^k_rowpass$' 1
 }
 python tools/region_driver.py 256 rebuild > gpurun_out/plain_r.log 2>&1 && {
-  full rap_L0 rebuild '^k_rap_tma$' 0
-  full rap_L1 rebuild '^k_rap_tma$' 1
+  full rap_L0 rebuild '^k_rap_grp$' 0
+  full rap_L1 rebuild '^k_rap_grp$' 1
 }
 python tools/ncu_summarize.py $R
 # (copy gpurun_out/${R}_launches.csv to profiles/${R}_launches_256_rebuild_vcycle_solve.csv)
