@@ -181,6 +181,16 @@ __global__ void k_set_last(int* lcptr, int64_t n, const int* cnt) {
     else lcptr[0] = 0;
 }
 
+// flag[i] = row i has a column in the halo (>= n_own)
+__global__ void k_halo_rows(int64_t n_own, const int* __restrict__ rp, const int* __restrict__ col, char* flag) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_own;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        char h = 0;
+        for (int k = rp[i]; k < rp[i + 1]; ++k) h |= col[k] >= n_own ? 1 : 0;
+        flag[i] = h;
+    }
+}
+
 }  // namespace
 
 struct DistLevel {
@@ -198,6 +208,8 @@ struct DistLevel {
     std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
     DevArray<int> send_idx;
     DevArray<double> send_buf;
+    DevArray<int> brows;  // owned rows with a halo column (recomputed after the exchange when overlapping)
+    int64_t nb = 0;
     int max_span = 0;
     CsrView view() const {
         CsrView v;
@@ -263,6 +275,11 @@ struct DistHier {
     ncclComm_t comm = nullptr;
     Loopback* lb = nullptr;  // test transport instead of NCCL
     cudaEvent_t ev_ready = nullptr, ev_consumed = nullptr;
+    // halo exchange overlapped with the V-cycle passes (world > 1): the
+    // exchange runs on cs while the full pass runs on the library stream
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool overlap = false;
     int rank = 0, world = 1, T = -1;
     std::vector<DistLevel> lv;
     // transition (level T -> T+1)
@@ -286,11 +303,20 @@ struct DistHier {
     std::vector<int64_t> dtab_off;
 };
 
-static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
+// Halo exchange of x's owned boundary values into the peers' halo slots.
+// async: the exchange itself (NCCL send/recv or the loopback copies) runs on
+// d.cs, forked after the pack kernel; the caller joins with halo_join before
+// reading the halo.
+static void halo(DistHier& d, DistLevel& L, double* x, Gate g, bool async = false) {
     Ctx& c = *d.ctx;
     if (L.send_idx.size() > 0)
         LAUNCH(c, "halo_pack", 16.0 * L.send_idx.size(), k_gather_d, grid_for(L.send_idx.size(), 256, c.num_sms * 8),
                256, 0, L.send_idx.size(), x, L.send_idx.get(), L.send_buf.get(), g);
+    const cudaStream_t xs = async ? d.cs : c.stream;
+    if (async) {
+        CK(cudaEventRecord(d.ev_fork, c.stream));
+        CK(cudaStreamWaitEvent(d.cs, d.ev_fork, 0));
+    }
     if (d.lb) {  // every rank enters both barriers, peers or not
         Loopback& lb = *d.lb;
         Loopback::Post& me = lb.post[d.rank];
@@ -309,26 +335,36 @@ static void halo(DistHier& d, DistLevel& L, double* x, Gate g) {
         for (size_t k = 0; k < L.recv_peer.size(); ++k) {
             const Loopback::Post& src = lb.post[L.recv_peer[k]];
             if (src.cnt[d.rank] != L.recv_cnt[k]) fail(AMGR_E_RUNTIME, "loopback halo: send/recv counts differ");
-            CK(cudaStreamWaitEvent(c.stream, src.ready, 0));
+            CK(cudaStreamWaitEvent(xs, src.ready, 0));
             CK(cudaMemcpyAsync(x + L.n_own + L.recv_off[k], src.ptr[d.rank], sizeof(double) * L.recv_cnt[k],
-                               cudaMemcpyDeviceToDevice, c.stream));
+                               cudaMemcpyDeviceToDevice, xs));
         }
-        CK(cudaEventRecord(d.ev_consumed, c.stream));
+        CK(cudaEventRecord(d.ev_consumed, xs));
+        if (async) CK(cudaEventRecord(d.ev_join, xs));
         lb.barrier();
         for (size_t k = 0; k < L.send_peer.size(); ++k)
             CK(cudaStreamWaitEvent(c.stream, lb.post[L.send_peer[k]].consumed, 0));
         lb.barrier();  // posts may be rewritten only after every rank has read them
         return;
     }
-    if (d.world == 1 || (L.send_peer.empty() && L.recv_peer.empty())) return;
-    NK(N().GroupStart());
-    for (size_t k = 0; k < L.send_peer.size(); ++k)
-        NK(N().Send(L.send_buf.get() + L.send_off[k], static_cast<size_t>(L.send_cnt[k]), ncclDouble, L.send_peer[k],
-                    d.comm, c.stream));
-    for (size_t k = 0; k < L.recv_peer.size(); ++k)
-        NK(N().Recv(x + L.n_own + L.recv_off[k], static_cast<size_t>(L.recv_cnt[k]), ncclDouble, L.recv_peer[k],
-                    d.comm, c.stream));
-    NK(N().GroupEnd());
+    if (!(d.world == 1 || (L.send_peer.empty() && L.recv_peer.empty()))) {
+        NK(N().GroupStart());
+        for (size_t k = 0; k < L.send_peer.size(); ++k)
+            NK(N().Send(L.send_buf.get() + L.send_off[k], static_cast<size_t>(L.send_cnt[k]), ncclDouble,
+                        L.send_peer[k], d.comm, xs));
+        for (size_t k = 0; k < L.recv_peer.size(); ++k)
+            NK(N().Recv(x + L.n_own + L.recv_off[k], static_cast<size_t>(L.recv_cnt[k]), ncclDouble, L.recv_peer[k],
+                        d.comm, xs));
+        NK(N().GroupEnd());
+    }
+    if (async) CK(cudaEventRecord(d.ev_join, xs));
+}
+static void halo_join(DistHier& d) { CK(cudaStreamWaitEvent(d.ctx->stream, d.ev_join, 0)); }
+// overlap this level's exchange with its pass: the full pass runs on stale
+// halo values while the exchange is in flight, then the boundary rows are
+// recomputed (k_rowlist, same arithmetic) once the halo has arrived
+static bool overlapped(const DistHier& d, const DistLevel& L) {
+    return d.overlap && L.nb > 0 && L.nb < L.n_own && (!L.send_peer.empty() || !L.recv_peer.empty());
 }
 
 // allgather of count doubles per rank (rank r's block at recv + r*count)
@@ -401,8 +437,15 @@ static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
     for (int i = 0; i <= T; ++i) {
         c.cur_level = i;
         DistLevel& L = d.lv[i];
-        halo(d, L, L.u0.get(), g);
-        vc_down(c, L.view(), fin[i], L.u0.get(), L.r.get(), g);
+        if (overlapped(d, L)) {
+            halo(d, L, L.u0.get(), g, true);
+            vc_down(c, L.view(), fin[i], L.u0.get(), L.r.get(), g);
+            halo_join(d);
+            vc_down_rows(c, L.view(), L.brows.get(), L.nb, fin[i], L.u0.get(), L.r.get(), g);
+        } else {
+            halo(d, L, L.u0.get(), g);
+            vc_down(c, L.view(), fin[i], L.u0.get(), L.r.get(), g);
+        }
         if (i < T) {
             DistLevel& N = d.lv[i + 1];
             restrict_sum(c, L.n_cown, L.mptr.get(), L.midx.get(), L.r.get(), N.f.get(), N.w.get(), om, N.u0.get(), g);
@@ -420,9 +463,16 @@ static void dist_vcycle(DistHier& d, const double* f0, double* u_out, Gate g) {
         c.cur_level = i;
         DistLevel& L = d.lv[i];
         vc_prolong(c, L.n_own, L.u0.get(), L.agg.get(), uc, L.x.get(), g);
-        halo(d, L, L.x.get(), g);
         double* out = (i == 0) ? u_out : L.out.get();
-        vc_smooth(c, L.view(), fin[i], L.w.get(), om, L.x.get(), out, g);
+        if (overlapped(d, L)) {
+            halo(d, L, L.x.get(), g, true);
+            vc_smooth(c, L.view(), fin[i], L.w.get(), om, L.x.get(), out, g);
+            halo_join(d);
+            vc_smooth_rows(c, L.view(), L.brows.get(), L.nb, fin[i], L.w.get(), om, L.x.get(), out, g);
+        } else {
+            halo(d, L, L.x.get(), g);
+            vc_smooth(c, L.view(), fin[i], L.w.get(), om, L.x.get(), out, g);
+        }
         uc = out;
     }
     c.cur_level = -1;
@@ -435,6 +485,9 @@ DistHier::~DistHier() {
     }
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_consumed) cudaEventDestroy(ev_consumed);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (cs) cudaStreamDestroy(cs);
 }
 
 // Plan validation, before any communicator is created: every index the
@@ -683,6 +736,22 @@ static void dist_finish(DistHier& d, const int64_t* t_counts, int64_t t_count_to
     work(H);
     gather_local(d);
     build_local_plans(d);
+    // halo overlap (world > 1, AMGR_DIST_OVERLAP=0 disables): the owned rows
+    // with a halo column, per partitioned level, and a stream for exchanges
+    const char* ov = std::getenv("AMGR_DIST_OVERLAP");
+    d.overlap = world > 1 && !(ov && ov[0] == '0');
+    if (d.overlap) {
+        CK(cudaStreamCreateWithFlags(&d.cs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming));
+        for (auto& L : d.lv) {
+            if (L.n_halo == 0 || L.n_own == 0) continue;
+            DevArray<char> flag(L.n_own, c.stream);
+            LAUNCH(c, "dist", 0.0, k_halo_rows, grid_for(L.n_own, 256, c.num_sms * 8), 256, 0, L.n_own, L.rp.get(),
+                   L.col.get(), flag.get());
+            L.nb = select_flagged(c, flag.get(), L.n_own, L.brows);
+        }
+    }
 }
 
 // levels of a device-built plan (dist_plan.cu): the arrays move in as they are

@@ -124,6 +124,8 @@ unsigned grid_of(const Ctx& c, int64_t n) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min(want, cap)));
 }
 
+}  // namespace
+
 // compact indices i in [0, n) with flag[i] into out; returns the count
 int64_t select_flagged(Ctx& c, const char* flag, int64_t n, DevArray<int>& out) {
     DevArray<int> tmp_out(std::max<int64_t>(n, 1), c.stream);
@@ -138,6 +140,8 @@ int64_t select_flagged(Ctx& c, const char* flag, int64_t n, DevArray<int>& out) 
     d2d(out.get(), tmp_out.get(), cnt, c.stream);
     return cnt;
 }
+
+namespace {
 
 // sort + unique of the valid keys (invalid = all ones, sorted last); returns
 // the unique valid keys

@@ -26,5 +26,7 @@ struct DevicePlan {
 // coarsest level (partition.py choose_top); -1: nothing to partition
 int choose_top_level(const Hier& h, int64_t replicate_below);
 DevicePlan build_device_plan(Hier& h, int rank, int world, int64_t replicate_below);
+// compact the indices i in [0, n) with flag[i] into out; returns the count
+int64_t select_flagged(Ctx& c, const char* flag, int64_t n, DevArray<int>& out);
 
 }  // namespace amgr

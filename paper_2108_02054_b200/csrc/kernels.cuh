@@ -48,6 +48,11 @@ void residual(Ctx& c, const CsrView& A, const double* f, const double* x, double
 void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, double* u0, Gate g = {});
 void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g = {});
 // one smoothing sweep: out = u + (om*w)(f - A u)     (smoother.cpp:42-47)
+// the same passes over a list of rows (bit-identical per row)
+void vc_down_rows(Ctx& c, const CsrView& A, const int* rows, int64_t nrows, const double* f, const double* u0,
+                  double* r, Gate g = {});
+void vc_smooth_rows(Ctx& c, const CsrView& A, const int* rows, int64_t nrows, const double* f, const double* w,
+                    double om, const double* u, double* out, Gate g = {});
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om,
                const double* u, double* out, Gate g = {});
 // prolongation (hierarchy.cpp:179-182): out = u + (0 + uc[agg])

@@ -2604,6 +2604,34 @@ void vc_prolong_premul(Ctx& c, int64_t n, const double* f, const double* w, doub
     LAUNCH_PDL(c, "prolong", 28.0 * n, k_prolong_p, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n), f,
                w, om, agg, uc, out, g);
 }
+// Row-list pass (the partitioned V-cycle's boundary rows after their halo
+// arrived, dist.cu): thread per listed row, the same per-row arithmetic as
+// k_rowpass — s = sum_j a_ij x_j in column order from 0.0, then Op::finish —
+// so a row recomputed here gets the bits the full pass would have given it.
+template <class Op>
+__global__ void k_rowlist(CsrView A, const int* __restrict__ rows, int nrows, Op op, Gate g) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * blockDim.x) {
+        const int i = __ldg(rows + t);
+        const typename Op::Row q = op.load(i);
+        double s = 0.0;
+        for (int k = __ldg(A.rp + i); k < __ldg(A.rp + i + 1); ++k) s = dadd(s, dmul(__ldg(A.val + k), op.x(__ldg(A.col + k))));
+        op.finish(i, s, q, nullptr);
+    }
+}
+void vc_down_rows(Ctx& c, const CsrView& A, const int* rows, int64_t nrows, const double* f, const double* u0,
+                  double* r, Gate g) {
+    if (nrows == 0) return;
+    LAUNCH_PDL(c, "vcycle_rows", 0.0, k_rowlist<OpDown>, grid_for(nrows, 128, c.num_sms * 8), 128, 0, A, rows,
+               static_cast<int>(nrows), OpDown{f, u0, r}, g);
+}
+void vc_smooth_rows(Ctx& c, const CsrView& A, const int* rows, int64_t nrows, const double* f, const double* w,
+                    double om, const double* u, double* out, Gate g) {
+    if (nrows == 0) return;
+    LAUNCH_PDL(c, "vcycle_rows", 0.0, k_rowlist<OpSmooth>, grid_for(nrows, 128, c.num_sms * 8), 128, 0, A, rows,
+               static_cast<int>(nrows), OpSmooth{f, w, om, u, out}, g);
+}
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
                double* out, Gate g) {
     const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;

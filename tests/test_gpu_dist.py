@@ -53,15 +53,21 @@ def test_dist_world1_matches_single_gpu(ctx):
     ds.close()
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_dist_multirank_loopback_matches_single_gpu(world):
+def test_dist_multirank_loopback_matches_single_gpu(world, overlap, monkeypatch):
     """The multi-rank device path (local CSR views with real halos, per-peer
     halo exchange, transition allgather of padded blocks, replicated coarse
     levels, rank-ordered dot sums, distributed rebuild) with `world` ranks in
     one process on the one GPU, exchanging through the loopback test
     transport: the assembled V-cycle is bit-identical to the single-GPU one
-    and every rank takes the single-GPU BiCGStab iteration count."""
+    and every rank takes the single-GPU BiCGStab iteration count.  With
+    overlap (the default for world > 1) each V-cycle pass runs on stale halo
+    values while the exchange is in flight on a second stream, then the
+    boundary rows are recomputed (k_rowlist): still the same bits."""
     import threading
+
+    monkeypatch.setenv("AMGR_DIST_OVERLAP", overlap)
 
     import torch
 
@@ -102,8 +108,11 @@ def test_dist_multirank_loopback_matches_single_gpu(world):
             frd = torch.from_numpy(fr).cuda()[R["own"]].contiguous()
             ur = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
             torch.cuda.synchronize()
+            R["ctx"].probe("vcycle_rows")
             ds.vcycle(fd.data_ptr(), ud.data_ptr())
             R["ctx"].synchronize()
+            R["rows_launches"] = R["ctx"].probe_read()[0]
+            R["ctx"].probe(None)
             st = ds.bicgstab(frd.data_ptr(), ur.data_ptr())
             ds.rebuild_values(vals2.data_ptr())
             ur.zero_()
@@ -125,6 +134,10 @@ def test_dist_multirank_loopback_matches_single_gpu(world):
     for r in range(world):
         u[ranks[r]["ds"].owned0] = out[r][0]
     np.testing.assert_array_equal(u.view(np.int64), u_ref.view(np.int64))
+    if overlap == "1":  # the boundary-row passes ran (2 per partitioned level with a halo)
+        assert all(R["rows_launches"] > 0 for R in ranks), [R["rows_launches"] for R in ranks]
+    else:
+        assert all(R["rows_launches"] == 0 for R in ranks)
     for r in range(world):
         assert out[r][1].converged and out[r][1].iterations == st_ref.iterations
         assert out[r][2].converged and out[r][2].iterations == st2_ref.iterations
