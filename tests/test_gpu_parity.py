@@ -655,6 +655,49 @@ def test_member_row_rap_matches_contrib_rap(ctx, monkeypatch, name):
         assert_same_hierarchy(h, ru)
 
 
+def _wide_row_poisson(g=24, eps=1e-3):
+    """2-D Poisson plus one node coupled (weakly, symmetrically) to every
+    other node: row 0 has g*g entries (> 255), beyond the warp-group Galerkin
+    plan's 8-bit row offsets, so that level falls back to k_rap_tma + k_jacobi."""
+    rp, ci, v = (np.asarray(x) for x in P.poisson2d(g))
+    n = len(rp) - 1
+    rows = []
+    for i in range(n):
+        cols = dict(zip(ci[rp[i]:rp[i + 1]].tolist(), v[rp[i]:rp[i + 1]].tolist()))
+        if i == 0:
+            for j in range(1, n):
+                cols[j] = cols.get(j, 0.0) - eps
+            cols[0] += eps * (n - 1)
+        else:
+            cols[0] = cols.get(0, 0.0) - eps
+            cols[i] += eps
+        rows.append(sorted(cols.items()))
+    rp2 = np.zeros(n + 1, np.int64)
+    rp2[1:] = np.cumsum([len(r) for r in rows])
+    ci2 = np.array([c for r in rows for c, _ in r], np.int64)
+    v2 = np.array([x for r in rows for _, x in r])
+    return rp2, ci2, v2
+
+
+@pytest.mark.parametrize("groups", ["1", "0"])
+def test_galerkin_group_plan_falls_back_on_long_rows(ctx, monkeypatch, groups):
+    """A level whose rows exceed the warp-group plan's bounds (a 576-entry
+    row) runs k_rap_tma + k_jacobi while the other levels run k_rap_grp: the
+    partial update is still bit-exact against the reference."""
+    monkeypatch.setenv("AMGR_RAP_GROUPS", groups)
+    A = _wide_row_poisson()
+    assert np.max(np.diff(A[0])) > 255
+    h = amg.setup(A, ctx=ctx)
+    r = ref.setup(A)
+    assert_same_hierarchy(h, r)
+    B = (A[0], A[1], A[2] * (1.0 + 0.05 * np.random.default_rng(4).random(len(A[2]))))
+    hu = amg.partial_update(h, B)
+    ru = ref.partial_update(r, B)
+    assert_same_hierarchy(hu, ru)
+    h.rebuild_values(B[2])
+    assert_same_hierarchy(h, ru)
+
+
 def test_rebuild_coarse_level_zero_diagonal_names_its_level(ctx, monkeypatch):
     """A zero diagonal that first appears on a coarse level during a partial
     update (the fused coarse-Jacobi epilogue) is reported with that level,
