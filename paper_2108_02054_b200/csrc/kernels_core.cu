@@ -1182,8 +1182,9 @@ void launch_rap_tma_fused(Ctx& c, double bytes, int64_t nnz_c, const int* cptr, 
 // Plan bytes per fine entry drop from 4 (contrib) + 4 per coarse entry
 // (cptr) to 2 + 0.25.  Measured and dropped (256^3): prefetching the next
 // group's plan slice one group ahead, by per-lane cp.async (LDGSTS: 1.5x
-// slower, MIO-throttled, +1 GB DRAM) or by per-warp TMA bulk copies
-// (4 small copies per group: 10% slower).
+// slower, MIO-throttled, +1 GB DRAM), by per-warp TMA bulk copies (4 small
+// copies per group: 10% slower) or into registers one group ahead (more
+// registers, fewer resident warps: 5-35% slower).
 #ifndef RG_MINB
 #define RG_MINB 5
 #endif
