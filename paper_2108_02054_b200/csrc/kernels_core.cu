@@ -1660,11 +1660,27 @@ __global__ void k_densify(CsrView A, double* dense) {
          t += static_cast<int64_t>(gridDim.x) * blockDim.x)
         dense[t] = 0.0;
 }
-__global__ void k_densify_fill(CsrView A, double* dense) {
+// thread per row; the row bounds are read once and the (<= 8 at a time)
+// entries loaded together (the stores could alias the CSR arrays for the
+// compiler, which otherwise re-reads rp[i+1] and serialises the loads)
+__global__ void k_densify_fill(CsrView A, double* __restrict__ dense) {
     const int64_t n = A.n;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) dense[i * n + A.col[k]] = A.val[k];
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int k0 = __ldg(A.rp + i), k1 = __ldg(A.rp + i + 1);
+        for (int k = k0; k < k1; k += 8) {
+            int cj[8];
+            double vj[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                cj[t] = k + t < k1 ? __ldg(A.col + k + t) : 0;
+                vj[t] = k + t < k1 ? __ldg(A.val + k + t) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (k + t < k1) dense[i * n + cj[t]] = vj[t];
+        }
+    }
 }
 
 constexpr int LU_THREADS = 1024;
