@@ -54,7 +54,7 @@ def test_dist_world1_matches_single_gpu(ctx):
 
 
 @pytest.mark.parametrize("overlap", ["1", "0"])
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_dist_multirank_loopback_matches_single_gpu(world, overlap, monkeypatch):
     """The multi-rank device path (local CSR views with real halos, per-peer
     halo exchange, transition allgather of padded blocks, replicated coarse
