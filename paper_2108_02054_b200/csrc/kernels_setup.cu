@@ -4,6 +4,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -663,6 +664,27 @@ __device__ __forceinline__ int64_t gp_group_of(const int4* desc, int64_t ngroups
     }
     return lo;
 }
+// flag[I] = coarse row I starts a group: chunk starts always, then the
+// greedy rule (the group [g0, I+1) would exceed the buffer or member bound)
+__global__ void k_gp_greedy(int64_t nc, int64_t chunk, const int* __restrict__ pb, const int* __restrict__ mptr,
+                            char* flag) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t a = t * chunk;
+    if (a >= nc) return;
+    const int64_t b = a + chunk < nc ? a + chunk : nc;
+    int p0 = pb[a], m0 = mptr[a];
+    flag[a] = 1;
+    for (int64_t I = a + 1; I < b; ++I) {
+        const int pe = pb[I + 1], me = mptr[I + 1];
+        const bool cut = pe - p0 > GP_BUF || me - m0 > GP_MEM;
+        flag[I] = cut ? 1 : 0;
+        if (cut) {
+            p0 = pb[I];
+            m0 = mptr[I];
+        }
+    }
+}
+__global__ void k_set_i32(int* p, int v) { *p = v; }
 __global__ void k_gp_pb(int64_t nc, const int* __restrict__ crp, const int* __restrict__ cptr, int* pb) {
     for (int64_t I = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; I <= nc;
          I += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -803,32 +825,34 @@ void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, con
         plan = GrpPlan{};
         return;
     }
-    // greedy packing of consecutive coarse rows (host, once per pattern)
-    std::vector<int> pbh(nc + 1), mph(nc + 1), first;
+    // greedy packing of consecutive coarse rows, on the device: the rows are
+    // cut into chunks (one thread each) that always start a group, and each
+    // thread packs its chunk greedily (a few % more groups than one global
+    // greedy pass; no host round trip of the row arrays)
+    DevArray<int> first;
     {
         DevArray<int> pb(nc + 1, c.stream);
         LAUNCH(c, "setup", 0.0, k_gp_pb, grid_for(nc + 1, SB, c.num_sms * 16), SB, 0, nc, crp, cptr, pb.get());
-        d2h(pbh.data(), pb.get(), nc + 1, c.stream);
-        d2h(mph.data(), mptr, nc + 1, c.stream);
-        CK(cudaStreamSynchronize(c.stream));
+        const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(nc, int64_t{c.num_sms} * 64));
+        const int64_t chunk = (nc + nchunk - 1) / nchunk;
+        DevArray<char> flag(nc, c.stream);
+        LAUNCH(c, "setup", 0.0, k_gp_greedy, grid_for(nchunk, 64), 64, 0, nc, chunk, pb.get(), mptr, flag.get());
+        DevArray<int> sel(nc, c.stream), nsel(1, c.stream);
+        cub::CountingInputIterator<int> it(0);
+        size_t bytes = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flag.get(), sel.get(), nsel.get(), nc, c.stream));
+        DevArray<char> tmp(static_cast<int64_t>(std::max<size_t>(bytes, 1)), c.stream);
+        CK(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flag.get(), sel.get(), nsel.get(), nc, c.stream));
+        ++c.launches;
+        plan.ngroups = d2h_scalar(nsel.get(), c.stream);
+        first.alloc(plan.ngroups + 1, c.stream);
+        d2d(first.get(), sel.get(), plan.ngroups, c.stream);
+        LAUNCH(c, "setup", 0.0, k_set_i32, 1, 1, 0, first.get() + plan.ngroups, static_cast<int>(nc));
     }
-    first.reserve(static_cast<size_t>(pbh[nc] / 200 + 16));
-    int g0 = 0;
-    first.push_back(0);
-    for (int64_t I = 0; I < nc; ++I) {
-        if (pbh[I + 1] - pbh[g0] > GP_BUF || mph[I + 1] - mph[g0] > GP_MEM) {
-            g0 = static_cast<int>(I);
-            first.push_back(g0);
-        }
-    }
-    plan.ngroups = static_cast<int64_t>(first.size());
-    first.push_back(static_cast<int>(nc));
     {
-        DevArray<int> fd(plan.ngroups + 1, c.stream);
-        h2d(fd.get(), first.data(), plan.ngroups + 1, c.stream);
         plan.desc.alloc(plan.ngroups + 1, c.stream);
         LAUNCH(c, "setup", 0.0, k_gp_desc, grid_for(plan.ngroups + 1, SB, c.num_sms * 16), SB, 0, plan.ngroups,
-               fd.get(), crp, cptr, mptr, plan.desc.get());
+               first.get(), crp, cptr, mptr, plan.desc.get());
         LAUNCH(c, "setup", 0.0, k_gp_check, grid_for(plan.ngroups, SB, c.num_sms * 16), SB, 0, plan.ngroups,
                plan.desc.get(), st.get());
         d2h(h + 3, st.get() + 3, 2, c.stream);
