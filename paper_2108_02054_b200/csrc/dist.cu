@@ -202,6 +202,7 @@ struct DistLevel {
     DevArray<int> dpos, lcptr, lcontrib;
     int64_t lnnz_c = 0, lnc = 0;
     int lmax_chunk = -1;
+    GrpPlan grp;  // warp-group form of the local plan (k_rap_grp with the Jacobi rebuild fused)
     ColCode cc;  // coded column stream of the local pattern (when its offsets are few: no / few halos)
     DevArray<double> u0, x, out, f, r;  // u0/x carry halo space
     std::vector<int> send_peer, recv_peer;
@@ -617,6 +618,10 @@ static void build_local_plans(DistHier& d) {
                    L.lcontrib.get(), bad.get());
         if (d2h_scalar(bad.get(), c.stream)) fail(AMGR_E_RUNTIME, "dist: a member row of an owned aggregate is not local");
         L.lmax_chunk = rap_chunk_max(c, L.lnnz_c, L.lcptr.get());
+        const char* ge = std::getenv("AMGR_RAP_GROUPS");
+        if (!(ge && ge[0] == '0') && L.n_own > 0 && nrows > 0)
+            rap_grp_plan(c, L.view(), L.mptr.get(), L.midx.get(), L.dpos.get(), nrows, lrp, L.lnnz_c,
+                         L.lcptr.get(), L.lcontrib.get(), L.grp);
     }
     // transition values: entry ranges of every rank's level-(T+1) rows
     const Level& GT = h.lv[d.T + 1];
@@ -660,10 +665,26 @@ static void dist_rebuild_local(DistHier& d, const double* vals, int location) {
     for (int i = 0; i <= d.T; ++i) {
         c.cur_level = i;
         DistLevel& L = d.lv[i];
-        jacobi_rebuild(c, L.n_own, L.val.get(), L.dpos.get(), L.w.get(), d.lerr.get() + i);
         double* out = i < d.T ? d.lv[i + 1].val.get() : d.tvsend.get();
-        rap_numeric(c, L.n_own, L.lnc, L.lnnz_c, L.lcptr.get(), L.lcontrib.get(), L.val.get(), out, L.nnz,
-                    L.lmax_chunk);
+        if (L.grp.ok) {  // Galerkin + damped-Jacobi rebuild in one pass
+            GrpArgs ga;
+            ga.ngroups = L.grp.ngroups;
+            ga.desc = L.grp.desc.get();
+            ga.mstart = L.grp.mstart.get();
+            ga.mdoff = L.grp.mdoff.get();
+            ga.midx = L.midx.get();
+            ga.code = L.grp.code.get();
+            ga.lanes = L.grp.lanes.get();
+            ga.af = L.val.get();
+            ga.ac = out;
+            ga.wf = L.w.get();
+            ga.bad_f = d.lerr.get() + i;
+            rap_grp(c, ga, L.n_own, L.lnc, L.nnz, L.lnnz_c);
+        } else {
+            jacobi_rebuild(c, L.n_own, L.val.get(), L.dpos.get(), L.w.get(), d.lerr.get() + i);
+            rap_numeric(c, L.n_own, L.lnc, L.lnnz_c, L.lcptr.get(), L.lcontrib.get(), L.val.get(), out, L.nnz,
+                        L.lmax_chunk);
+        }
     }
     c.cur_level = d.T + 1;
     allgather(d, d.tvsend.get(), d.tvgather.get(), d.tvpad);

@@ -382,8 +382,8 @@ static void build_grp_plans(Hier& h, size_t start) {
         if (!A.rap || !A.T || A.T->smoothed || A.rap->grp_tried) continue;
         A.rap->grp_tried = true;
         const Pattern& C = *h.lv[i + 1].pat;
-        rap_grp_plan(c, A.view(), A.T->agg.get(), A.T->mptr.get(), A.T->midx.get(), A.pat->diag.get(), A.T->nc,
-                     C.rp.get(), A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.rap->grp);
+        rap_grp_plan(c, A.view(), A.T->mptr.get(), A.T->midx.get(), A.pat->diag.get(), A.T->nc, C.rp.get(),
+                     A.rap->nnz_c, A.rap->cptr.get(), A.rap->contrib.get(), A.rap->grp);
     }
 }
 

@@ -737,16 +737,20 @@ __global__ void k_gp_check(int64_t ngroups, const int4* __restrict__ desc, int* 
     atomicMax(st + 3, mb);
     atomicMax(st + 4, mm);
 }
-// per fine entry: its offset in the member row | the member's number in its group << 8
-__global__ void k_gp_emap(int64_t nf, const int* __restrict__ midx, const int* __restrict__ agg,
+// per fine entry: its offset in the member row | the member's number in its
+// group << 8 (thread per coarse row I: its members j in R order)
+__global__ void k_gp_emap(int64_t nc, const int* __restrict__ mptr, const int* __restrict__ midx,
                           const int* __restrict__ rp, int64_t ngroups, const int4* __restrict__ desc,
                           uint16_t* emap) {
-    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nf;
-         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i = midx[j];
-        const int64_t g = gp_group_of(desc, ngroups, agg[i]);
-        const int loc = static_cast<int>(j - desc[g].y);
-        for (int e = rp[i]; e < rp[i + 1]; ++e) emap[e] = static_cast<uint16_t>((e - rp[i]) | (loc << 8));
+    for (int64_t I = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; I < nc;
+         I += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t g = gp_group_of(desc, ngroups, I);
+        const int m0 = desc[g].y;
+        for (int j = mptr[I]; j < mptr[I + 1]; ++j) {
+            const int i = midx[j];
+            const int loc = j - m0;
+            for (int e = rp[i]; e < rp[i + 1]; ++e) emap[e] = static_cast<uint16_t>((e - rp[i]) | (loc << 8));
+        }
     }
 }
 __global__ void k_gp_code(int64_t m, const int* __restrict__ contrib, const uint16_t* __restrict__ emap,
@@ -804,8 +808,8 @@ __global__ void k_gp_lanes(int64_t ngroups, const int4* __restrict__ desc, const
 }
 }  // namespace
 
-void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, const int* midx, const int* dpos,
-                  int64_t nc, const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan) {
+void rap_grp_plan(Ctx& c, const CsrView& A, const int* mptr, const int* midx, const int* dpos, int64_t nc,
+                  const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan) {
     plan = GrpPlan{};
     const int64_t nf = A.n, m = A.nnz;
     if (nf == 0 || nc == 0 || nnz_c == 0 || m >= (int64_t{1} << 30)) return;
@@ -861,7 +865,7 @@ void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, con
     if (h[3] > GP_BUF || h[4] > GP_MEM) fail(AMGR_E_RUNTIME, "rap_grp_plan: group bounds violated (internal error)");
     {
         DevArray<uint16_t> emap(m, c.stream);
-        LAUNCH(c, "setup", 0.0, k_gp_emap, grid_for(nf, SB, c.num_sms * 16), SB, 0, nf, midx, agg, A.rp,
+        LAUNCH(c, "setup", 0.0, k_gp_emap, grid_for(nc, SB, c.num_sms * 16), SB, 0, nc, mptr, midx, A.rp,
                plan.ngroups, plan.desc.get(), emap.get());
         plan.code.alloc(m + 8, c.stream);
         CK(cudaMemsetAsync(plan.code.get() + m, 0, 8 * sizeof(uint16_t), c.stream));

@@ -95,9 +95,10 @@ struct GrpPlan {
 };
 // Builds the plan when the level fits (plan.ok tells).  mptr/midx: R;
 // dpos: diagonal CSR position per fine row (-1: none); crp: coarse row
-// pointers; cptr/contrib: the level's RapPlan.
-void rap_grp_plan(Ctx& c, const CsrView& A, const int* agg, const int* mptr, const int* midx, const int* dpos,
-                  int64_t nc, const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan);
+// pointers; cptr/contrib: the level's RapPlan (global, or a rank's local
+// plan: dist.cu).
+void rap_grp_plan(Ctx& c, const CsrView& A, const int* mptr, const int* midx, const int* dpos, int64_t nc,
+                  const int* crp, int64_t nnz_c, const int* cptr, const int* contrib, GrpPlan& plan);
 
 // ---- smoothed aggregation (extension) ----
 // Device SpGEMM C = A B: structural pattern of C (sorted columns) and the
