@@ -335,6 +335,9 @@ amgr_status amgr_dist_create_auto(amgr_hier* global, const void* nccl_id128, int
 amgr_status amgr_dist_level_dims(const amgr_dist* d, int level, int64_t* dims);
 /* owned: n_own global row ids; nnz_map: nnz global entry ids (either may be NULL). */
 amgr_status amgr_dist_level_maps(amgr_dist* d, int level, int64_t* owned, int64_t* nnz_map);
+/* bytes per entry of partitioned level `level`'s column stream in the row
+ * passes: 1 / 2 (coded, col = row + dict[code]) or 4 (int32 columns). */
+amgr_status amgr_dist_level_code(const amgr_dist* d, int level, int* col_bytes);
 /* Test transport: W ranks of ONE process (one host thread and one context
  * each, same device) exchange through stream-ordered device copies and host
  * barriers instead of NCCL, so the multi-rank device path can be checked on

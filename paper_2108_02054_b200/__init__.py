@@ -168,6 +168,7 @@ PROTOTYPES = {
     "amgr_dist_create_auto_loopback": (_I, [_V, _V, _I, _I, _L, _P(_V)]),
     "amgr_dist_level_dims": (_I, [_V, _I, _V]),
     "amgr_dist_level_maps": (_I, [_V, _I, _V, _V]),
+    "amgr_dist_level_code": (_I, [_V, _I, _V]),
     "amgr_dist_rebuild_local": (_I, [_V, _V, _I]),
     "amgr_dist_vcycle": (_I, [_V, _V, _V]),
     "amgr_dist_bicgstab": (_I, [_V, _V, _V, _P(_SolveParams), _P(_SolveStats)]),

@@ -814,7 +814,7 @@ static void levels_from_device_plan(DistHier& d, DevicePlan& P) {
         L.recv_off = s.recv_off;
         L.recv_cnt = s.recv_cnt;
         L.max_span = max_group_span(c, L.rp.get(), L.n_own);
-        encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc);
+        encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc, true);
     }
 }
 
@@ -907,9 +907,9 @@ static amgr_status dist_create_impl(amgr_hier* hg, int rank, int world, int top,
             }
             L.max_span = amgr::max_group_span(c, L.rp.get(), L.n_own);
             // local columns keep the stencil offsets of owned neighbours; halo
-            // columns (numbered after the owned rows) add distinct offsets, so
-            // the encoder only codes levels whose halos are small or absent
-            amgr::encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc);
+            // columns (numbered after the owned rows) add distinct offsets:
+            // 1-byte codes when there are few, 2-byte codes up to 65536
+            amgr::encode_columns(c, L.n_own, L.nnz, L.rp.get(), L.col.get(), L.cc, true);
         }
         amgr::dist_finish(*d, t_counts, t_count_total);
         CK(cudaStreamSynchronize(c.stream));
@@ -1023,6 +1023,13 @@ amgr_status amgr_dist_level_dims(const amgr_dist* d, int level, int64_t* dims) {
     dims[2] = L.nnz;
     dims[3] = L.n_cown;
     dims[4] = d->d->T;
+    return AMGR_OK;
+}
+
+amgr_status amgr_dist_level_code(const amgr_dist* d, int level, int* col_bytes) {
+    if (!d || !d->d || !col_bytes || level < 0 || level > d->d->T) return AMGR_E_INVALID_ARGUMENT;
+    const int m = d->d->lv[level].cc.mode;
+    *col_bytes = m == 1 ? 1 : m == 2 ? 2 : 4;
     return AMGR_OK;
 }
 

@@ -796,9 +796,11 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
     if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
-    // coded columns: uint8 only on <= 8 nnz/row, uint16 only above (encode_columns)
+    // coded columns: uint8 on <= 8 nnz/row, uint16 above (and on narrow partitioned levels)
     if (A.cmode == 1)
         launch_tma<Op, RP_CH, 0, uint8_t>(c, fam, bytes, A, op, g, s, grid);
+    else if (A.cmode == 2 && A.nnz <= 8 * A.n)  // a partitioned level 0 (encode_columns narrow16)
+        launch_tma<Op, RP_CH, 0, uint16_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.cmode == 2 && A.nnz > 12 * A.n)
         launch_tma<Op, RP_CH, 8, uint16_t>(c, fam, bytes, A, op, g, s, grid);
     else if (A.cmode == 2 && !fixed_grid)

@@ -1149,7 +1149,7 @@ __global__ void k_encode(int64_t n, const int* __restrict__ rp, const int* __res
 
 }  // namespace
 
-void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out) {
+void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out, bool narrow16) {
     out = ColCode{};
     // Default: uint8 codes on <= 8 entries/row (C3 level 0), uint16 codes on
     // 8..12 entries/row (level 1, read with 384-entry chunks: 211/227 ->
@@ -1160,9 +1160,12 @@ void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* co
     if (e && std::strcmp(e, "0") == 0) return;
     const bool wide_ok = e && std::strcmp(e, "16") == 0;
     if (nnz <= 0 || n <= 0) return;
-    const bool narrow = nnz <= 8 * n;
+    bool narrow = nnz <= 8 * n;
     if (nnz > 12 * n && !wide_ok) return;
-    const int limit = narrow ? 256 : 65536;
+    // narrow16: a narrow level with more than 256 offsets (a partitioned
+    // level 0: its halo columns are numbered after the owned rows) may take
+    // 2-byte codes instead of int32 columns
+    const int limit = narrow && !narrow16 ? 256 : 65536;
     DevArray<uint32_t> k0(nnz, c.stream), k1(nnz, c.stream);
     const unsigned grid = grid_for(n, SB, c.num_sms * 16);
     LAUNCH(c, "setup", 0.0, k_offset_keys, grid, SB, 0, n, rp, col, k0.get());
@@ -1181,6 +1184,7 @@ void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* co
     c.launches += 2;
     const int m = d2h_scalar(num.get(), c.stream);
     if (m > limit) return;
+    if (narrow && m > 256) narrow = false;  // narrow16: 2-byte codes
     out.ndict = m;
     out.dict.alloc(m, c.stream);
     // codes are read in 16-byte-rounded TMA ranges: zeroed slack past nnz

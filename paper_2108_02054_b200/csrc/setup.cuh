@@ -24,7 +24,8 @@ struct ColCode {
     DevArray<uint16_t> c16;
     DevArray<int> dict;
 };
-void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out);
+void encode_columns(Ctx& c, int64_t n, int64_t nnz, const int* rp, const int* col, ColCode& out,
+                    bool narrow16 = false);
 
 // First row (ascending) whose diagonal is missing or zero, or -1.
 // (strength_graph, coarsening.cpp:19-32; build_smoother, smoother.cpp:12-28)

@@ -177,6 +177,12 @@ class DistSolver:
         _check(lib().amgr_dist_bicgstab(self._p, f_ptr, u_ptr, C.byref(sp), C.byref(st)), self.h.ctx.ptr)
         return SolveStats(int(st.iterations), float(st.relative_residual), bool(st.converged), bool(st.breakdown))
 
+    def level_col_bytes(self, level: int) -> int:
+        """Bytes per entry of the partitioned level's column stream (1/2: coded, 4: int32)."""
+        v = C.c_int(0)
+        _check(lib().amgr_dist_level_code(self._p, int(level), C.byref(v)), self.h.ctx.ptr)
+        return int(v.value)
+
     def close(self):
         if self._p and self.h.ctx._p:
             lib().amgr_dist_destroy(self._p)

@@ -92,6 +92,8 @@ def test_dist_multirank_loopback_matches_single_gpu(world, overlap, monkeypatch)
         h = amg.setup(A, ctx=ctx)
         ds = D.DistSolver(h, r, world, replicate_below=300, loopback=lb)
         assert ds.plan.top >= 1 and (world == 1 or sum(len(L.halo) for L in ds.plan.levels) > 0)
+        # level 0 keeps a coded column stream despite its halo columns (2 bytes at most)
+        assert ds.level_col_bytes(0) in (1, 2), ds.level_col_bytes(0)
         own = torch.from_numpy(ds.owned0).cuda()
         ranks.append({"ctx": ctx, "h": h, "ds": ds, "own": own})
     torch.cuda.synchronize()
