@@ -1,5 +1,6 @@
 // Micro-benchmark of the coarsest-level dense kernels (LU factor / inverse)
-// on a 149 x 149 system like the C3 hierarchy's coarsest level.
+// on a 149 x 149 system like the C3 hierarchy's coarsest level (argument 2 "s":
+// sparse, ~7 entries per row, diagonally dominant; default dense random).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 --expt-relaxed-constexpr
 //      -I paper_2108_02054_b200/csrc -I include tools/ubench_dense.cu -o tools/ubench_dense
 #include "../paper_2108_02054_b200/csrc/kernels_core.cu"
@@ -18,8 +19,29 @@ int main(int argc, char** argv) {
     std::vector<double> a(n * n);
     std::mt19937_64 g(1);
     std::uniform_real_distribution<double> u(-1, 1);
-    for (auto& x : a) x = u(g);
-    for (int i = 0; i < n; ++i) a[i * n + i] += 4.0;
+    const bool sparse = argc > 2 && argv[2][0] == 's';  // like the C3 coarsest level: ~7 entries per row
+    if (sparse) {
+        std::uniform_int_distribution<int> col(0, n - 1);
+        for (int i = 0; i < n; ++i) {
+            double d = 1.0;
+            for (int t = 0; t < 6; ++t) {
+                const int j = col(g);
+                if (j == i) continue;
+                const double v = -std::abs(u(g));
+                a[i * n + j] += v;
+                a[j * n + i] += v;
+            }
+        }
+        for (int i = 0; i < n; ++i) {
+            double r = 1.0;
+            for (int j = 0; j < n; ++j)
+                if (j != i) r += std::abs(a[i * n + j]);
+            a[i * n + i] = r;
+        }
+    } else {
+        for (auto& x : a) x = u(g);
+        for (int i = 0; i < n; ++i) a[i * n + i] += 4.0;
+    }
     double *da, *dm, *di;
     int64_t* piv;
     int* st;
@@ -46,9 +68,9 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(amgr::k_dense_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 160 * 160);
     timeit("dense_reg LU", [&] {
         cudaMemcpyAsync(dm, da, 8 * n * n, cudaMemcpyDeviceToDevice);
-        amgr::k_dense_reg<false><<<1, amgr::DR_THREADS, 8 * n * n>>>(n, dm, dm, piv, st);
+        amgr::k_dense_reg<false><<<1, amgr::DR_THREADS, 8 * n * n>>>(n, dm, dm, piv, st, nullptr);
     });
-    timeit("dense_reg GJ inverse", [&] { amgr::k_dense_reg<true><<<1, amgr::DR_THREADS>>>(n, da, di, piv, st); });
+    timeit("dense_reg GJ inverse", [&] { amgr::k_dense_reg<true><<<1, amgr::DR_THREADS>>>(n, da, di, piv, st, nullptr); });
     cudaFuncSetAttribute(amgr::k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
     timeit("lu_factor (smem)", [&] {
         cudaMemcpyAsync(dm, da, 8 * n * n, cudaMemcpyDeviceToDevice);
@@ -57,7 +79,7 @@ int main(int argc, char** argv) {
     timeit("memcpy only", [&] { cudaMemcpyAsync(dm, da, 8 * n * n, cudaMemcpyDeviceToDevice); });
     // check GJ inverse: || A * inv - I ||
     std::vector<double> inv(n * n);
-    amgr::k_dense_reg<true><<<1, amgr::DR_THREADS>>>(n, da, di, piv, st);
+    amgr::k_dense_reg<true><<<1, amgr::DR_THREADS>>>(n, da, di, piv, st, nullptr);
     cudaMemcpy(inv.data(), di, 8 * n * n, cudaMemcpyDeviceToHost);
     double err = 0;
     for (int i = 0; i < n; ++i)
@@ -71,7 +93,7 @@ int main(int argc, char** argv) {
     std::vector<double> l1(n * n), l2(n * n);
     std::vector<int64_t> p1(n), p2(n);
     cudaMemcpy(dm, da, 8 * n * n, cudaMemcpyDeviceToDevice);
-    amgr::k_dense_reg<false><<<1, amgr::DR_THREADS, 8 * n * n>>>(n, dm, dm, piv, st);
+    amgr::k_dense_reg<false><<<1, amgr::DR_THREADS, 8 * n * n>>>(n, dm, dm, piv, st, nullptr);
     cudaMemcpy(l1.data(), dm, 8 * n * n, cudaMemcpyDeviceToHost);
     cudaMemcpy(p1.data(), piv, 8 * n, cudaMemcpyDeviceToHost);
     cudaMemcpy(dm, da, 8 * n * n, cudaMemcpyDeviceToDevice);
