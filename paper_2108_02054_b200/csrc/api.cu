@@ -156,6 +156,7 @@ void amgr_ctx_destroy(amgr_ctx* ctx) {
         cudaEventDestroy(ctx->c.fork_ev);
         cudaEventDestroy(ctx->c.join_ev);
     }
+    for (cudaEvent_t e : ctx->c.clock_pool) cudaEventDestroy(e);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
 }

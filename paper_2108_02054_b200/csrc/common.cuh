@@ -82,6 +82,10 @@ struct Ctx {
     cudaEvent_t snap_ev = nullptr, d2h_done_ev = nullptr;
     double* snap = nullptr;
     int64_t snap_n = 0;
+    // timing events of the per-call phase clocks, created once and reused
+    // (creating ~30 events per rebuild starved the short small-level kernels)
+    std::vector<cudaEvent_t> clock_pool;
+    size_t clock_used = 0;
 };
 
 // Run fn with c.stream temporarily redirected to the side stream, ordered

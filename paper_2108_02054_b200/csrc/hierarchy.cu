@@ -42,18 +42,19 @@ enum Phase { PH_TRANSFER = 0, PH_GALERKIN = 1, PH_SMOOTHER = 2, PH_COARSE = 3 };
 struct PhaseClock {
     Ctx& c;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
-    explicit PhaseClock(Ctx& cc) : c(cc) {}
-    ~PhaseClock() {
-        for (auto& v : ev)
-            for (auto& p : v) {
-                cudaEventDestroy(p.first);
-                cudaEventDestroy(p.second);
-            }
+    size_t base;
+    explicit PhaseClock(Ctx& cc) : c(cc), base(cc.clock_used) {}
+    ~PhaseClock() { c.clock_used = base; }  // events return to the context's pool
+    cudaEvent_t take() {
+        if (c.clock_used == c.clock_pool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            c.clock_pool.push_back(e);
+        }
+        return c.clock_pool[c.clock_used++];
     }
     void begin(Phase ph) {
-        cudaEvent_t a, b;
-        CK(cudaEventCreate(&a));
-        CK(cudaEventCreate(&b));
+        cudaEvent_t a = take(), b = take();
         CK(cudaEventRecord(a, c.stream));
         ev[ph].push_back({a, b});
     }
@@ -225,9 +226,7 @@ void check_rebuild_errors(Hier& h, const char* what) {
 
 void reset_err(Hier& h) {
     Work& W = work(h);
-    std::vector<int> e(h.lv.size() + 1, 0x7fffffff);
-    e.back() = -1;
-    h2d(W.err.get(), e.data(), static_cast<int64_t>(e.size()), h.ctx->stream);
+    reset_error_slots(*h.ctx, W.err.get(), static_cast<int64_t>(h.lv.size()));
 }
 
 // ---- smoothed aggregation (extension; oracle/amg_oracle.c) -------------------

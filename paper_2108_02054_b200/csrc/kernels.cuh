@@ -176,6 +176,8 @@ struct GrpArgs {
     int* bad_f = nullptr;
 };
 void rap_grp(Ctx& c, const GrpArgs& a, int64_t nf, int64_t nc, int64_t nnz_f, int64_t nnz_c);
+// the per-level first-bad-row slots (0x7fffffff) and the LU status slot (-1)
+void reset_error_slots(Ctx& c, int* err, int64_t nlevels);
 // Jacobi: w[i] = 1.0 / a_ii (smoother.cpp:8-32); records the first bad row.
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* diag_pos, double* w,
                     int* bad_row);

@@ -2809,6 +2809,12 @@ void rap_rows(Ctx& c, const RapRowsArgs& a, int maxlen, int64_t nf, int64_t nnz_
         launch_rap_rows<32>(c, a, bytes);
 }
 
+__global__ void k_reset_err(int64_t nl, int* err) {
+    for (int64_t i = threadIdx.x; i <= nl; i += blockDim.x) err[i] = i < nl ? 0x7fffffff : -1;
+}
+void reset_error_slots(Ctx& c, int* err, int64_t nlevels) {
+    LAUNCH(c, "setup", 0.0, k_reset_err, 1, 64, 0, nlevels, err);
+}
 void jacobi_rebuild(Ctx& c, int64_t n, const double* val, const int* dpos, double* w, int* bad) {
     if (n == 0) return;
     LAUNCH(c, "smoother", 20.0 * n, k_jacobi, grid_for(n, 256, c.num_sms * 16), 256, 0, static_cast<int>(n),
