@@ -382,11 +382,12 @@ def test_spai0_smoother_vs_oracle(ctx):
     assert st.converged and abs(st.iterations - so.iterations) <= 1
 
 
-@pytest.mark.parametrize("n", [72, 75, 78, 150])
+@pytest.mark.parametrize("n", [72, 75, 78, 150, 160, 161, 400])
 def test_direct_solve_sizes_around_the_smem_opt_in(ctx, n):
     """Stalled coarsening (no strong couplings) -> the whole matrix is the
     coarsest system; n = 72..78 is where dynamic + static shared memory of the
-    register LU kernel first exceeds 48 KB (regression: missing opt-in)."""
+    register LU kernel first exceeds 48 KB (regression: missing opt-in);
+    160 | 161 is the register kernel's limit (k_dense_reg -> k_lu_factor)."""
     A = P.random_csr(n, n, 0.05, 3, diag=4.0)
     kw = dict(eps=0.99)
     h = amg.setup(A, amg.AmgParams(**kw), ctx=ctx)
@@ -785,3 +786,65 @@ def test_single_operator_entry_points(ctx):
     sing = P.csr_from_dense_rows([[(0, 1.0), (1, 1.0)], [(0, 1.0), (1, 1.0)]], 2)
     with pytest.raises(amg.RuntimeFailure, match="singular"):
         amg.coarse_factorize(sing, ctx=ctx)
+
+
+def test_tiny_and_empty_systems_match_reference(ctx):
+    """Edge sizes (hierarchy.cpp:45-105, dense_lu.cpp, bicgstab.cpp): the
+    empty matrix is rejected with the reference's text; 1x1 and 2x2 systems
+    are a single direct level whose factor, V-cycle and BiCGStab (iterations,
+    iterate, residual) are bit-identical to the reference's."""
+    empty = (np.array([0]), np.array([], dtype=np.int64), np.array([]))
+    with pytest.raises(ref.RefError, match="setup: empty matrix"):
+        ref.setup(empty)
+    with pytest.raises(amg.InvalidArgument, match="setup: empty matrix"):
+        amg.setup(empty, ctx=ctx)
+    systems = [((np.array([0, 1]), np.array([0]), np.array([4.0])), np.array([2.0])),
+               (P.csr_from_dense_rows([[(0, 4.0), (1, -1.0)], [(0, -1.0), (1, 4.0)]], 2), np.array([1.0, 2.0])),
+               # pivoting: |a_10| > |a_00|
+               (P.csr_from_dense_rows([[(0, 1.0), (1, 2.0)], [(0, 3.0), (1, 1.0)]], 2), np.array([1.0, -1.0]))]
+    for A, f in systems:
+        h = amg.setup(A, ctx=ctx)
+        r = ref.setup(A)
+        assert h.num_levels() == len(r.levels) == 1
+        assert_same_hierarchy(h, r)
+        assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r, f, fixed=True)))
+        u, st = amg.bicgstab(h, f)
+        rs = ref.bicgstab(r, f, fixed=True)
+        assert st.iterations == rs.iterations and bool(st.converged) == rs.converged
+        assert np.array_equal(_bits(u), _bits(rs.u))
+        r.free()
+
+
+def test_isolated_rows_and_ragged_lengths_match_reference(ctx):
+    """Rows with only a diagonal entry (no strong neighbours: singleton
+    aggregates, coarsening.cpp:77-120) mixed with long rows: hierarchy, partial
+    update and V-cycle bit-exact."""
+    n = 600
+    rng = np.random.default_rng(5)
+    rows = []
+    for i in range(n):
+        if i % 7 == 3:
+            rows.append([(i, 2.5)])  # isolated
+            continue
+        cols = {i}
+        k = 2 if i % 11 else 40  # a few long rows
+        for j in rng.integers(0, n, k):
+            if int(j) % 7 != 3:
+                cols.add(int(j))
+        ent = [(j, -rng.uniform(0.1, 1.0)) for j in sorted(cols) if j != i]
+        ent.append((i, 1.0 + sum(-v for _, v in ent)))
+        rows.append(sorted(ent))
+    A = P.csr_from_dense_rows(rows, n)
+    prm = dict(coarse_enough=20)
+    h = amg.setup(A, amg.AmgParams(**prm), ctx=ctx)
+    r = ref.setup(A, ref.params(**prm))
+    assert h.num_levels() >= 2
+    assert_same_hierarchy(h, r)
+    A2 = (A[0], A[1], A[2] * rng.uniform(0.9, 1.1, len(A[2])))
+    h.rebuild_values(A2[2])
+    r2 = ref.partial_update(r, A2, ref.params(**prm))
+    assert_same_hierarchy(h, r2)
+    f = np.random.default_rng(6).uniform(-1, 1, n)
+    assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r2, f, fixed=True, prm=ref.params(**prm))))
+    r2.free()
+    r.free()
