@@ -113,6 +113,61 @@ __global__ void k_rank_sum(int world, int k, const double* __restrict__ parts, d
     *outs[t] = s;
 }
 
+// ---- sequential-dot parity mode (Ctx::seq_dots) --------------------------------
+// The reference sums every dot left to right over the GLOBAL index
+// (bicgstab.cpp:11-17).  Each rank forms its rounded products a_i*b_i in local
+// order, one padded allgather brings all of them to every rank, and one
+// thread per rank sums them in global order through gpos (global row ->
+// position in the gathered blocks): the same bits as the reference's dot.
+__global__ void k_dist_prod(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                            double* __restrict__ out, Gate g) {
+    if (gated_off(g)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __dmul_rn(a[i], b[i]);
+}
+
+// gathered owned ids (as doubles, -1 = padding) -> gpos
+__global__ void k_dist_gpos(int64_t total, const double* __restrict__ ids, int64_t* __restrict__ gpos) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = ids[k];
+        if (v >= 0.0) gpos[static_cast<int64_t>(v)] = k;
+    }
+}
+
+constexpr int GS_THREADS = 256, GS_CH = 2048;
+
+// s = sum_{i < n} prod[gpos[i]] left to right; warps 1.. stage the next chunk
+// into shared memory while thread 0 sums the current one
+__global__ void __launch_bounds__(GS_THREADS) k_dist_seq_sum(int64_t n, const double* __restrict__ prod,
+                                                             const int64_t* __restrict__ gpos, double* out, Gate g) {
+    if (gated_off(g)) return;
+    __shared__ double buf[2][GS_CH];
+    const int tid = threadIdx.x;
+    const int64_t nch = (n + GS_CH - 1) / GS_CH;
+    auto fill = [&](int64_t ch, double* dst, int t0, int nt) {
+        const int64_t base = ch * GS_CH;
+        const int len = static_cast<int>(n - base < GS_CH ? n - base : GS_CH);
+        for (int i = t0; i < len; i += nt) dst[i] = prod[gpos[base + i]];
+    };
+    if (nch > 0) fill(0, buf[0], tid, GS_THREADS);
+    __syncthreads();
+    double s = 0.0;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        if (tid >= 32) {
+            if (ch + 1 < nch) fill(ch + 1, buf[(ch + 1) & 1], tid - 32, GS_THREADS - 32);
+        } else if (tid == 0) {
+            const int64_t base = ch * GS_CH;
+            const int len = static_cast<int>(n - base < GS_CH ? n - base : GS_CH);
+            const double* p = buf[ch & 1];
+            for (int i = 0; i < len; ++i) s = __dadd_rn(s, p[i]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *out = s;
+}
+
 // ---- partitioned rebuild (rank-local values) ----------------------------------
 // local diagonal positions: owned row r has local column r (linear scan, the
 // local columns are not sorted: halo ids follow the owned ones)
@@ -300,6 +355,10 @@ struct DistHier {
     DevArray<double> kr, krt, kp, kv, ks, kt, kph, ksh, ku;
     DevArray<double> dloc, dall;  // local dot results (up to 2) and the gathered partials
     DevArray<double*> douts;      // table of dot output pointer sets (out_slot)
+    // sequential-dot parity mode: products, their padded allgather, global order
+    int64_t spad = 0, n_global = 0;
+    DevArray<double> sprod, sall, kq;
+    DevArray<int64_t> gpos;
     std::vector<std::vector<double*>> dtab;
     std::vector<int64_t> dtab_off;
 };
@@ -418,6 +477,58 @@ static void allsum(DistHier& d, int k, std::initializer_list<double*> outs) {
     double* const* slot = out_slot(d, outs);
     allgather(d, d.dloc.get(), d.dall.get(), k);
     LAUNCH(c, "dist", 0.0, k_rank_sum, 1, 32, 0, d.world, k, d.dall.get(), const_cast<double**>(slot));
+}
+
+// sequential-dot mode: global positions of every rank's level-0 rows (once,
+// outside any capture: one allgather of the row counts, one of the ids)
+static void seq_prepare(DistHier& d) {
+    if (d.gpos.size() > 0) return;
+    Ctx& c = *d.ctx;
+    const DistLevel& L0 = d.lv[0];
+    d.n_global = d.g->lv.front().pat->n;
+    DevArray<double> cnt, cnts;
+    cnt.alloc(1, c.stream);
+    cnts.alloc(d.world, c.stream);
+    const double me = static_cast<double>(L0.n_own);
+    h2d(cnt.get(), &me, 1, c.stream);
+    allgather(d, cnt.get(), cnts.get(), 1);
+    std::vector<double> hc(static_cast<size_t>(d.world));
+    d2h(hc.data(), cnts.get(), d.world, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    int64_t pad = 1, tot = 0;
+    for (double v : hc) {
+        pad = std::max(pad, static_cast<int64_t>(v));
+        tot += static_cast<int64_t>(v);
+    }
+    if (tot != d.n_global) fail(AMGR_E_RUNTIME, "dist: level-0 rows of all ranks do not cover the global level");
+    d.spad = pad;
+    d.sprod.alloc(pad, c.stream);
+    d.sall.alloc(pad * d.world, c.stream);
+    d.kq.alloc(std::max<int64_t>(L0.n_own, 1), c.stream);
+    d.gpos.alloc(d.n_global, c.stream);
+    std::vector<int> ids(static_cast<size_t>(L0.n_own));
+    d2h(ids.data(), L0.owned.get(), L0.n_own, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    std::vector<double> idd(static_cast<size_t>(pad), -1.0);
+    for (int64_t i = 0; i < L0.n_own; ++i) idd[i] = ids[i];
+    h2d(d.sprod.get(), idd.data(), pad, c.stream);
+    allgather(d, d.sprod.get(), d.sall.get(), pad);
+    LAUNCH(c, "dist", 0.0, k_dist_gpos, grid_for(pad * d.world, 256, c.num_sms * 8), 256, 0, pad * d.world,
+           d.sall.get(), d.gpos.get());
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+// *out = the reference's dot(a, b) over the global vector (after the
+// rank-ordered blocked value the same field held; gated like its producer)
+static void seq_dot_dist(DistHier& d, const double* a, const double* b, double* out, Gate g = {}) {
+    Ctx& c = *d.ctx;
+    const int64_t n = d.lv[0].n_own;
+    if (n > 0)
+        LAUNCH(c, "seq_dot", 16.0 * n, k_dist_prod, grid_for(n, 256, c.num_sms * 8), 256, 0, n, a, b, d.sprod.get(),
+               g);
+    allgather(d, d.sprod.get(), d.sall.get(), d.spad);
+    LAUNCH(c, "seq_dot", 16.0 * d.n_global, k_dist_seq_sum, 1, GS_THREADS, 0, d.n_global, d.sall.get(),
+           d.gpos.get(), out, g);
 }
 
 static DotSink local_sink(DistHier& d, int slot) {
@@ -1109,10 +1220,27 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
         CK(cudaStreamSynchronize(c.stream));
         return s;
     };
+    // sequential-dot parity mode (amgr_ctx_set_dot_order on this rank's
+    // context; every rank must use the same order): after each rank-ordered
+    // dot the reference's left-to-right global dot overwrites the field, at
+    // the same places as the single-GPU solver (hierarchy.cu::bicgstab)
+    const bool seq = c.seq_dots;
+    if (seq) seq_prepare(d);
+    auto SD = [&](const double* a, const double* b, double* o, Gate g = {}) {
+        if (seq) seq_dot_dist(d, a, b, o, g);
+    };
+    // ||f - A u||^2 into *o: rank-ordered, then (sequential mode) the
+    // reference's sum over r = f - A u written to a scratch vector
+    auto true_resid = [&](double* u_, double* o, Gate g) {
+        resid_norm(c, A, f, u_, seq ? d.kq.get() : nullptr, nullptr, local_sink(d, 0), g);
+        allsum(d, 1, {o});
+        SD(d.kq.get(), d.kq.get(), o, g);
+    };
     KState s0;
     h2d(st, &s0, 1, c.stream);
     dot(c, n, f, f, local_sink(d, 0));
     allsum(d, 1, {&st->d_true});
+    SD(f, f, &st->d_true);
     KState s = rd();
     const double normf = std::sqrt(s.d_true);
     if (normf == 0.0) {
@@ -1126,6 +1254,8 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
     resid_norm(c, A, f, uu, d.kr.get(), d.krt.get(), local_sink(d, 0));
     dot(c, n, d.krt.get(), d.kr.get(), local_sink(d, 1));
     allsum(d, 2, {&st->d_rr, &st->d_rtr});
+    SD(d.kr.get(), d.kr.get(), &st->d_rr);
+    SD(d.krt.get(), d.kr.get(), &st->d_rtr);
     s = rd();
     out.relative_residual = std::sqrt(s.d_rr) / normf;
     if (out.relative_residual <= sp.tol) {
@@ -1159,29 +1289,34 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
         halo(d, L0, d.kph.get(), G);
         spmv_dot(c, A, d.kph.get(), d.kv.get(), d.krt.get(), local_sink(d, 0), G);
         allsum(d, 1, {&st->d_rtv});
+        SD(d.krt.get(), d.kv.get(), &st->d_rtv, G);
         bicg_alpha(c, st);
         bicg_s(c, st, n, d.kr.get(), d.kv.get(), d.ks.get(), local_sink(d, 0));
         allsum(d, 1, {&st->d_ss});
+        SD(d.ks.get(), d.ks.get(), &st->d_ss, G);
         bicg_half_test(c, st);
         bicg_half_u(c, st, n, uu, d.kph.get());
         halo(d, L0, uu, GH);
-        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GH);
-        allsum(d, 1, {&st->d_true});
+        true_resid(uu, &st->d_true, GH);
         bicg_half_check(c, st);
         bicg_half_r(c, st, n, d.kr.get(), d.ks.get(), d.krt.get(), local_sink(d, 0));
         allsum(d, 1, {&st->d_rtr});  // stale when gated off; bicg_update rewrites d_rtr then
+        SD(d.krt.get(), d.kr.get(), &st->d_rtr, GH);
         dist_vcycle(d, d.ks.get(), d.ksh.get(), GF);
         halo(d, L0, d.ksh.get(), GF);
         spmv_dot2(c, A, d.ksh.get(), d.kt.get(), d.ks.get(), local_sink(d, 0), GF);
         allsum(d, 2, {&st->d_ts, &st->d_tt});
+        SD(d.kt.get(), d.ks.get(), &st->d_ts, GF);
+        SD(d.kt.get(), d.kt.get(), &st->d_tt, GF);
         bicg_omega(c, st);
         bicg_update(c, st, n, uu, d.kph.get(), d.ksh.get(), d.kr.get(), d.ks.get(), d.kt.get(), d.krt.get(),
                     local_sink(d, 0));
         allsum(d, 2, {&st->d_rr, &st->d_rtr});
+        SD(d.kr.get(), d.kr.get(), &st->d_rr, GF);
+        SD(d.krt.get(), d.kr.get(), &st->d_rtr, GF);
         bicg_end_test(c, st);
         halo(d, L0, uu, GC);
-        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0), GC);
-        allsum(d, 1, {&st->d_true});
+        true_resid(uu, &st->d_true, GC);
         bicg_end_check(c, st);
     };
     run_iterations(h, iter, s, d.lb == nullptr && !std::getenv("AMGR_DIST_NO_GRAPH"));
@@ -1192,8 +1327,7 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
     } else {
         out.breakdown = (s.flags & KF_BREAKDOWN) ? 1 : 0;
         halo(d, L0, uu, Gate{});
-        resid_norm(c, A, f, uu, nullptr, nullptr, local_sink(d, 0));
-        allsum(d, 1, {&st->d_true});
+        true_resid(uu, &st->d_true, Gate{});
         s = rd();
         out.relative_residual = std::sqrt(s.d_true) / normf;
         out.converged = (out.relative_residual <= sp.tol && !out.breakdown) ? 1 : 0;

@@ -400,6 +400,80 @@ def test_device_built_plan_c4_rank_counts_bit_exact(world, g):
     lb.close()
 
 
+@pytest.mark.parametrize("world,g", [(1, 20), (2, 20), (3, 32), (4, 48), (8, 128)])
+def test_dist_sequential_dots_bit_identical(world, g):
+    """Sequential-dot parity mode on the partition (every rank's context set
+    to AMGR_DOTS_SEQUENTIAL): each dot is the reference's left-to-right sum
+    over the GLOBAL index (products allgathered, summed through the global
+    order), so the row-partitioned BiCGStab after a rank-local rebuild is the
+    reference's bicgstab on partial_update(A_k) bit for bit — same iteration
+    count, same assembled iterate, same residual — at any rank count.  Up to
+    48^3 the comparison is against oracle/_ref itself; at 128^3 against the
+    single-GPU sequential-dot solve (pinned to the reference at that size by
+    test_gpu_parity_large.test_seq_dots_bicgstab_bit_identical_128).
+    World 1 runs over NCCL (graph-captured), the others through loopback."""
+    import torch
+
+    from oracle import ref
+    from paper_2108_02054_b200 import distributed as D
+
+    A = P.grid3d_values("dambreak", g, 9)
+    A2 = P.grid3d_values("dambreak", g, 30)
+    n = g ** 3
+    fr = P.rhs(n)
+    if g <= 48:
+        r0 = ref.setup(A)
+        r2 = ref.partial_update(r0, A2)
+        rs = ref.bicgstab(r2, fr, fixed=True)
+        want_u, want_it, want_res = rs.u, rs.iterations, rs.relative_residual
+        r2.free()
+        r0.free()
+    else:
+        sc = amg.Context(0)
+        sc.sequential_dots = True
+        hs = amg.setup(A, amg.AmgParams(coarse_solve="exact"), ctx=sc)
+        hs.rebuild_values(A2[2])
+        want_u, st = amg.bicgstab(hs, fr)
+        want_it, want_res = st.iterations, st.relative_residual
+        del hs
+
+    lb = D.Loopback(world) if world > 1 else None
+    ranks = []
+    for r in range(world):
+        ctx = amg.Context(0)
+        ctx.sequential_dots = True
+        h = amg.setup(A, amg.AmgParams(coarse_solve="exact"), ctx=ctx)
+        ds = D.DistSolver(h, r, world, D.nccl_unique_id() if lb is None else None, replicate_below=2000,
+                          loopback=lb, device_plan=True)
+        ranks.append({"ctx": ctx, "ds": ds, "own": ds.owned0})
+
+    def fn(r):
+        R = ranks[r]
+        ds = R["ds"]
+        ds.rebuild_local(ds.local_values(A2[2]))
+        frd = torch.from_numpy(fr[R["own"]]).cuda()
+        ur = torch.zeros(ds.n_local, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        st = ds.bicgstab(frd.data_ptr(), ur.data_ptr())
+        return st, ur.cpu().numpy()
+
+    out, errs = _run_ranks(world, fn)
+    assert not errs, errs
+    assert all(o is not None for o in out), "a rank did not finish"
+    x = np.zeros(n)
+    for r in range(world):
+        st = out[r][0]
+        assert st.converged and st.iterations == want_it, (r, st, want_it)
+        assert np.float64(st.relative_residual).view(np.int64) == np.float64(want_res).view(np.int64), \
+            (st.relative_residual, want_res)
+        x[ranks[r]["own"]] = out[r][1]
+    np.testing.assert_array_equal(x.view(np.int64), np.asarray(want_u).view(np.int64))
+    for R in ranks:
+        R["ds"].close()
+    if lb:
+        lb.close()
+
+
 def test_device_built_plan_world1_nccl(ctx):
     """World 1 over NCCL on a device-built plan (no halos, no send lists):
     rank-local rebuild + BiCGStab equal the single-GPU path."""
