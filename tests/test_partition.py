@@ -5,7 +5,8 @@ the local rows with halo exchanges (send/recv) and the transition allgather,
 and the assembled result must equal the single-domain V-cycle of the C oracle
 bit for bit (every row sum and restriction keeps the reference's order).
 A distributed BiCGStab with rank-ordered dot reductions converges within +-1
-iteration of the oracle.  The numpy executor is test infrastructure standing
+iteration of the oracle; with the sequential-dot mode's global-order dots it
+is the oracle's BiCGStab bit for bit.  The numpy executor is test infrastructure standing
 in for the kernels (which are the single-GPU ones, tested in -m gpu)."""
 import os
 import socket
@@ -77,6 +78,19 @@ class Comm:
         self.dist.all_gather(out, tp)
         return np.concatenate([o.numpy()[:int(s.item())] for o, s in zip(out, sizes)])
 
+    def dot_global_order(self, a, b, owned, n):
+        """the sequential-dot mode's algorithm (dist.cu seq_dot_dist): rounded
+        local products, one allgather, the reference's left-to-right sum over
+        the global index (bicgstab.cpp:11-17) through the gathered owned ids"""
+        prods = self.allgather_concat(np.asarray(a) * np.asarray(b))
+        ids = self.allgather_concat(np.asarray(owned, np.float64)).astype(np.int64)
+        g = np.empty(n)
+        g[ids] = prods
+        s = 0.0
+        for v in g.tolist():
+            s += v
+        return s
+
     def sum_ordered(self, x):
         """deterministic: gather per-rank partials, add in rank order"""
         parts = self.allgather_concat(np.array([x]))
@@ -132,13 +146,18 @@ def replicated_vcycle(H, start, f):
     return u
 
 
-def local_bicgstab(plan, H, f_own, comm, tol=1e-8, max_iter=100):
-    """bicgstab.cpp:21-135 with distributed SpMV and rank-ordered dots."""
+def local_bicgstab(plan, H, f_own, comm, tol=1e-8, max_iter=100, seq=False):
+    """bicgstab.cpp:21-135 with distributed SpMV and rank-ordered dots (seq:
+    the reference's global-order dots)."""
     L0 = plan.levels[0]
     val0 = H.levels[0].A[2][L0.nnz_map]
     A = lambda x: spmv_seq(L0.rp, L0.col, val0, comm.halo(L0, x))  # noqa: E731
     M = lambda x: local_vcycle(plan, H, x, comm)  # noqa: E731
-    dot = lambda a, b: comm.sum_ordered(float(np.dot(a, b)))  # noqa: E731
+    if seq:
+        n = len(H.levels[0].A[0]) - 1
+        dot = lambda a, b: comm.dot_global_order(a, b, L0.owned, n)  # noqa: E731
+    else:
+        dot = lambda a, b: comm.sum_ordered(float(np.dot(a, b)))  # noqa: E731
     nf = np.sqrt(dot(f_own, f_own))
     u = np.zeros_like(f_own)
     r = f_own - A(u)
@@ -189,7 +208,9 @@ def _worker(rank, world, port, out_path):
     u_own = local_vcycle(plan, H, f[plan.levels[0].owned], comm)
     fr = P.rhs(n)
     us, it, conv = local_bicgstab(plan, H, fr[plan.levels[0].owned], comm)
+    uq, itq, convq = local_bicgstab(plan, H, fr[plan.levels[0].owned], comm, seq=True)
     np.savez(out_path + f".{rank}.npz", owned=plan.levels[0].owned, u=u_own, us=us, it=it, conv=conv,
+             uq=uq, itq=itq, convq=convq,
              top=plan.top, halos=[len(L.halo) for L in plan.levels])
     dist.destroy_process_group()
 
@@ -309,3 +330,10 @@ def test_distributed_vcycle_and_bicgstab_gloo(tmp_path):
     assert its[0] == its[1] and abs(its[0] - so.iterations) <= 1
     res = np.linalg.norm(P.rhs(n) - O.spmv(A, us)) / np.linalg.norm(P.rhs(n))
     assert res <= 1e-8
+    # global-order dots: the oracle's BiCGStab iteration for iteration
+    uq = np.zeros(n)
+    for r in range(world):
+        d = np.load(out + f".{r}.npz")
+        uq[d["owned"]] = d["uq"]
+        assert bool(d["convq"]) and int(d["itq"]) == so.iterations, (int(d["itq"]), so.iterations)
+    np.testing.assert_array_equal(uq.view(np.int64), np.asarray(so.u).view(np.int64))
