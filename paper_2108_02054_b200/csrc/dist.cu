@@ -1225,6 +1225,23 @@ void dist_bicgstab(DistHier& d, const double* f, double* u, const amgr_solve_par
     // dot the reference's left-to-right global dot overwrites the field, at
     // the same places as the single-GPU solver (hierarchy.cu::bicgstab)
     const bool seq = c.seq_dots;
+    if (d.world > 1) {
+        // every rank must sum its dots the same way (a mismatch would leave
+        // the ranks in different collective sequences): agree first, fail
+        // together with a message otherwise
+        DevArray<double> mine, all;
+        mine.alloc(1, c.stream);
+        all.alloc(d.world, c.stream);
+        const double flag = seq ? 1.0 : 0.0;
+        h2d(mine.get(), &flag, 1, c.stream);
+        allgather(d, mine.get(), all.get(), 1);
+        std::vector<double> flags(static_cast<size_t>(d.world));
+        d2h(flags.data(), all.get(), d.world, c.stream);
+        CK(cudaStreamSynchronize(c.stream));
+        for (double v : flags)
+            if (v != flags[0])
+                fail(AMGR_E_INVALID_ARGUMENT, "dist bicgstab: the ranks' contexts use different dot orders");
+    }
     if (seq) seq_prepare(d);
     auto SD = [&](const double* a, const double* b, double* o, Gate g = {}) {
         if (seq) seq_dot_dist(d, a, b, o, g);

@@ -464,6 +464,44 @@ def test_dist_sequential_dots_bit_identical(world, g):
         lb.close()
 
 
+def test_dist_mixed_dot_orders_fail_on_every_rank():
+    """Ranks whose contexts disagree on the dot order would run different
+    collective sequences: every rank raises instead of hanging."""
+    import torch
+
+    from paper_2108_02054_b200 import distributed as D
+
+    g, world = 16, 2
+    A = P.grid3d_values("dambreak", g, 9)
+    fr = P.rhs(g ** 3)
+    lb = D.Loopback(world)
+    ranks = []
+    for r in range(world):
+        ctx = amg.Context(0)
+        ctx.sequential_dots = r == 0
+        h = amg.setup(A, ctx=ctx)
+        ds = D.DistSolver(h, r, world, replicate_below=300, loopback=lb, device_plan=True)
+        ranks.append({"ctx": ctx, "ds": ds, "own": ds.owned0})
+
+    def fn(r):
+        R = ranks[r]
+        frd = torch.from_numpy(fr[R["own"]]).cuda()
+        ur = torch.zeros(R["ds"].n_local, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        try:
+            R["ds"].bicgstab(frd.data_ptr(), ur.data_ptr())
+        except amg.InvalidArgument as e:
+            return str(e)
+        return None
+
+    out, errs = _run_ranks(world, fn)
+    assert not errs, errs
+    assert all(o is not None and "different dot orders" in o for o in out), out
+    for R in ranks:
+        R["ds"].close()
+    lb.close()
+
+
 def test_device_built_plan_world1_nccl(ctx):
     """World 1 over NCCL on a device-built plan (no halos, no send lists):
     rank-local rebuild + BiCGStab equal the single-GPU path."""
