@@ -407,6 +407,12 @@ amgr_status amgr_hier_level_dims(const amgr_hier* h, int level, int64_t* dims);
  * 1 / 2 = coded column stream col = row + dict[code]), *ndict = dictionary
  * size (0 when uncoded).  Either pointer may be NULL. */
 amgr_status amgr_hier_level_layout(const amgr_hier* h, int level, int32_t* col_bytes, int32_t* ndict);
+/* Symmetric-stencil form of A_level (no reference counterpart):
+ * *pairs = K > 0 when the row passes currently read A_level as its diagonal
+ * plus K upper diagonals (columns i + {0, +-off[k]}, values bitwise symmetric,
+ * checked at every rebuild), 0 when they read the CSR arrays; off (K ints,
+ * may be NULL) receives the offsets. */
+amgr_status amgr_hier_level_stencil(const amgr_hier* h, int level, int32_t* pairs, int32_t* off);
 /* A_level as int64 CSR (row_ptr nrows+1, col nnz, values nnz) into host buffers. */
 amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col,
                               double* values);

@@ -129,6 +129,7 @@ PROTOTYPES = {
     "amgr_hier_num_levels": (_I, [_V]),
     "amgr_hier_level_dims": (_I, [_V, _I, _V]),
     "amgr_hier_level_layout": (_I, [_V, _I, _V, _V]),
+    "amgr_hier_level_stencil": (_I, [_V, _I, _V, _V]),
     "amgr_hier_level_A": (_I, [_V, _I, _V, _V, _V]),
     "amgr_hier_level_P": (_I, [_V, _I, _V]),
     "amgr_hier_level_R": (_I, [_V, _I, _V, _V]),
@@ -414,6 +415,15 @@ class Hierarchy:
         cb, nd = C.c_int32(), C.c_int32()
         _check(lib().amgr_hier_level_layout(self._p, lvl, C.byref(cb), C.byref(nd)), self.ctx.ptr)
         return {"col_bytes": int(cb.value), "ndict": int(nd.value)}
+
+    def level_stencil(self, lvl: int):
+        """(K, offsets) when the row passes read A_lvl in its symmetric-stencil
+        form (diagonal + K upper diagonals), (0, ()) when they read the CSR
+        arrays (amgr_hier_level_stencil)."""
+        k = C.c_int32()
+        off = np.zeros(3, np.int32)
+        _check(lib().amgr_hier_level_stencil(self._p, lvl, C.byref(k), off.ctypes.data), self.ctx.ptr)
+        return int(k.value), tuple(int(x) for x in off[:k.value])
 
     def finest_size(self) -> int:
         return self.level_dims(0)["nrows"]

@@ -425,6 +425,18 @@ amgr_status amgr_hier_level_layout(const amgr_hier* h, int level, int32_t* col_b
     });
 }
 
+amgr_status amgr_hier_level_stencil(const amgr_hier* h, int level, int32_t* pairs, int32_t* off) {
+    if (!h || !pairs) return AMGR_E_INVALID_ARGUMENT;
+    return guard_c(ctx_of(h), [&] {
+        const amgr::Hier& H = *h->h;
+        if (level < 0 || level >= static_cast<int>(H.lv.size())) amgr::invalid("level out of range");
+        const amgr::Level& L = H.lv[level];
+        *pairs = L.dia_on ? L.pat->dia_k : 0;
+        if (off && L.dia_on)
+            for (int k = 0; k < L.pat->dia_k; ++k) off[k] = L.pat->doff[k];
+    });
+}
+
 amgr_status amgr_hier_level_A(const amgr_hier* h, int level, int64_t* row_ptr, int64_t* col, double* values) {
     if (!h) return AMGR_E_INVALID_ARGUMENT;
     return guard_c(ctx_of(h), [&] {

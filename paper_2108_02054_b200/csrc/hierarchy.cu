@@ -207,6 +207,67 @@ void throw_lu(int st) {
     fail(AMGR_E_RUNTIME, os.str());
 }
 
+// ---- symmetric-stencil form of level 0 (sym_dia) ------------------------------
+// A level-0 pattern whose columns are i + {0, +-o_0, .., +-o_{K-1}} (K = 2, 3:
+// the 5-/7-point grid stencils of C1-C5), sorted and structurally symmetric,
+// whose values are BITWISE symmetric (a(i,j) == a(j,i), re-checked at every
+// rebuild) is also kept as D | U_0..U_{K-1}: the row passes then read
+// 8 (K+1) + 1 bytes per row instead of 9 nnz/n + 4 (k_dia), with the same
+// entries summed in the same order.  AMGR_SYM_DIA=0 disables it.
+static bool sym_dia_enabled() {
+    const char* e = std::getenv("AMGR_SYM_DIA");
+    return !(e && e[0] == '0');
+}
+
+// eligibility of a pattern (examined once; host sync)
+static bool sym_dia_pattern(Ctx& c, Pattern& P) {
+    if (P.dia_k >= 0) return P.dia_k > 0;
+    P.dia_k = 0;
+    if (P.cc.mode != 1 || P.cc.ndict < 5 || P.cc.ndict > 7 || P.n != P.ncols) return false;
+    std::vector<int> d(static_cast<size_t>(P.cc.ndict));
+    d2h(d.data(), P.cc.dict.get(), P.cc.ndict, c.stream);
+    CK(cudaStreamSynchronize(c.stream));
+    std::vector<int> pos;
+    bool zero = false;
+    for (int x : d) {
+        if (x == 0) zero = true;
+        if (x > 0) pos.push_back(x);
+    }
+    std::sort(pos.begin(), pos.end());
+    const int K = static_cast<int>(pos.size());
+    if (!zero || K < 2 || K > 3 || 2 * K + 1 != P.cc.ndict) return false;
+    for (int o : pos)
+        if (std::find(d.begin(), d.end(), -o) == d.end()) return false;
+    DevArray<uint8_t> m(P.n, c.stream);
+    if (!dia_masks(c, csr_view(P, nullptr), K, pos.data(), m.get())) return false;
+    P.dmask = std::move(m);
+    for (int k = 0; k < K; ++k) P.doff[k] = pos[k];
+    P.dia_k = K;
+    return true;
+}
+
+// level-0 values -> D | U (enqueued on the current stream); the bit-symmetry
+// verdict is read by sym_dia_commit after the rebuild's sync
+static bool sym_dia_prepare(Hier& h) {
+    Level& L0 = h.lv.front();
+    L0.dia_on = false;
+    return h.lv.size() > 1 && sym_dia_enabled() && sym_dia_pattern(*h.ctx, *L0.pat);
+}
+static void sym_dia_values(Hier& h) {
+    Ctx& c = *h.ctx;
+    Level& L0 = h.lv.front();
+    const Pattern& P = *L0.pat;
+    const int64_t need = (P.dia_k + 1) * P.n;
+    if (L0.dia.size() != need) L0.dia.alloc(need, c.stream);
+    if (L0.dia_flag.size() != 1) L0.dia_flag.alloc(1, c.stream);
+    dia_values(c, csr_view(P, L0.view().val), P.dia_k, P.doff, P.dmask.get(), L0.dia.get(), L0.dia_flag.get());
+}
+static void sym_dia_commit(Hier& h) {
+    Level& L0 = h.lv.front();
+    if (L0.dia_flag.size() != 1 || L0.pat->dia_k <= 0 || !sym_dia_enabled()) return;
+    L0.dia_on = d2h_scalar(L0.dia_flag.get(), h.ctx->stream) == 0;
+}
+
 // Read the per-level smoother bad-row slots and the LU status in one sync
 // and throw the first error in the reference's order.
 void check_rebuild_errors(Hier& h, const char* what) {
@@ -215,6 +276,7 @@ void check_rebuild_errors(Hier& h, const char* what) {
     std::vector<int> e(L + 1);
     d2h(e.data(), W.err.get(), static_cast<int64_t>(L + 1), h.ctx->stream);
     CK(cudaStreamSynchronize(h.ctx->stream));
+    sym_dia_commit(h);
     for (size_t l = 0; l + 1 < L; ++l)
         if (e[l] != 0x7fffffff) {
             std::ostringstream os;
@@ -413,6 +475,9 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
     const char* fe = std::getenv("AMGR_FUSE_JACOBI");
     const bool jac = h.prm.smoother == AMGR_SMOOTHER_JACOBI && fe && fe[0] == '1';
     std::vector<char> wdone(L, 0);
+    // level 0's symmetric-stencil copy on the side stream, concurrent with
+    // the Galerkin chain (both only read A_0)
+    if (start == 0 && sym_dia_prepare(h)) on_side(c, [&] { sym_dia_values(h); });
     build_grp_plans(h, start);
     for (size_t i = start; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
@@ -772,8 +837,10 @@ std::unique_ptr<Hier> setup(Ctx& c, const amgr_csr& A, const AmgP& p) {
     clk.begin(PH_COARSE);
     coarse_factorize(*h, lu_status.get());
     clk.end(PH_COARSE);
+    if (sym_dia_prepare(*h)) sym_dia_values(*h);
     const int st = d2h_scalar(lu_status.get(), c.stream);
     if (st >= 0) throw_lu(st);
+    sym_dia_commit(*h);
     h->tm = clk.collect();
     work(*h);
     if (trace) {

@@ -32,6 +32,11 @@ struct Pattern {
     DevArray<int> rp, col, diag;
     ColCode cc;  // coded column stream for the row passes (mode 0: none)
     int lag_groups = -1;  // max |j - i| / 32 + 2 of a coded pattern (k_rowpass_lag), lazily
+    // symmetric-stencil form (level 0): -1 not examined, 0 not a symmetric
+    // stencil, else the number K of offset pairs (doff ascending) + row masks
+    int dia_k = -1;
+    int doff[3] = {0, 0, 0};
+    DevArray<uint8_t> dmask;
 };
 inline void set_code(CsrView& v, const ColCode& cc) {
     v.cmode = cc.mode;
@@ -87,6 +92,11 @@ struct Level {
     double om = -1.0;  // per-level Jacobi weight of an SA hierarchy (sa_jacobi_weights); < 0: prm's
     std::shared_ptr<Transfer> T;   // null on the coarsest level
     std::shared_ptr<RapPlan> rap;  // null on the coarsest level
+    // symmetric-stencil copy of this level's values (level 0; D | U_0..U_{K-1})
+    // and its bit-symmetry flag; dia_on when the last rebuild found them equal
+    DevArray<double> dia;
+    DevArray<int> dia_flag;
+    bool dia_on = false;
     CsrView view() const {
         CsrView v;
         v.n = pat->n;
@@ -97,6 +107,12 @@ struct Level {
         v.val = ext_val ? ext_val : val.get();
         v.max_span = pat->max_span;
         set_code(v, pat->cc);
+        if (dia_on) {
+            v.dia = dia.get();
+            v.dmask = pat->dmask.get();
+            v.dk = pat->dia_k;
+            for (int k = 0; k < 3; ++k) v.doff[k] = pat->doff[k];
+        }
         return v;
     }
 };

@@ -25,6 +25,14 @@ struct CsrView {
     int ndict = 0;
     const void* code = nullptr;
     const int* dict = nullptr;
+    // symmetric-stencil form of level 0 (sym_dia, hierarchy.cu): when dia is
+    // set, the row passes read D | U_0 .. U_{dk-1} (n values each; U_k[i] =
+    // a(i, i + doff[k]), and a(i, i - doff[k]) = U_k[i - doff[k]]) and a
+    // presence mask per row instead of the CSR arrays
+    const double* dia = nullptr;
+    const uint8_t* dmask = nullptr;
+    int dk = 0;
+    int doff[3] = {0, 0, 0};
 };
 
 // Deterministic multi-block dot products: per-block partials + last-block
@@ -37,6 +45,15 @@ struct DotSink {
 
 // Fixed grid for dot-producing kernels so the reduction order never changes.
 int dot_grid(const Ctx& c);
+
+// ---- symmetric-stencil form (level 0) -----------------------------------------
+// presence masks of a pattern whose columns are i + {-off[K-1]..-off[0], 0,
+// off[0]..off[K-1]} in ascending order and structurally symmetric; false (and
+// no mask) otherwise.  Host sync.
+bool dia_masks(Ctx& c, const CsrView& A, int K, const int* off, uint8_t* mask);
+// D | U_0..U_{K-1} from the CSR values; *flag |= 1 when a(i, j) and a(j, i)
+// differ in any bit (the form is then unusable for these values)
+void dia_values(Ctx& c, const CsrView& A, int K, const int* off, const uint8_t* mask, double* dia, int* flag);
 
 // ---- row-pass (CSR SpMV family) --------------------------------------------
 void spmv(Ctx& c, const CsrView& A, const double* x, double* y, Gate g = {});

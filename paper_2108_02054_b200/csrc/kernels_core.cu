@@ -787,6 +787,78 @@ void launch_tma(Ctx& c, const char* fam, double bytes, const CsrView& A, const O
     LAUNCH_PDL(c, fam, bytes, (k_rowpass<Op, CH, GATHER, CT>), grid, RP_BLOCK, smem, A, op, g, s);
 }
 
+// ---- k_dia: row pass over the symmetric-stencil form of level 0 -------------
+// Thread per row (grid-stride).  Row i's entries in ascending column order:
+// the lower neighbours i - off[K-1] .. i - off[0] (values U_k[i - off[k]],
+// i.e. the neighbour's own upper entry: the form is only active when the
+// values are bitwise symmetric), the diagonal D[i], the upper neighbours
+// i + off[0] .. i + off[K-1] (U_k[i]); absent entries (mask) are skipped, so
+// the sum s = 0 + a x + ... visits exactly the reference's entries in the
+// reference's order (csr.cpp:79-84).  Every load is coalesced (shifted
+// streams; the lower values and operands are L2 hits), no column stream, no
+// row pointers: 8 (K + 1) + 1 bytes per row instead of 9 nnz/n + 4.
+// Rows are dealt to lanes exactly as k_rowpass deals them (warp w of block b
+// takes 32-row groups b*RP_WARPS + w, + RP_WARPS*grid, ...; lane l row
+// 32 G + l) on k_rowpass's grid and block, so the per-thread dot partials and
+// their block/grid reduction are k_rowpass's too: dots, and hence BiCGStab
+// iterates, are bit-identical with and without the form.
+template <class Op, int K>
+__global__ void __launch_bounds__(RP_BLOCK, RP_BLOCKS_PER_SM) k_dia(CsrView A, Op op, Gate g, DotSink sink) {
+    pdl_enter();
+    if (gated_off(g)) return;
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    constexpr int NE = 2 * K + 1;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    const int n = static_cast<int>(A.n);
+    const int64_t nl = A.n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ngroups = (n + 31) >> 5;
+    const int W = gridDim.x * RP_WARPS;
+    const double* __restrict__ D = A.dia;
+    for (int G = blockIdx.x * RP_WARPS + w; G < ngroups; G += W) {
+        const int i = G * 32 + lane;
+        if (i >= n) continue;
+        const unsigned m = __ldg(A.dmask + i);
+        const auto q = op.load(i);
+        double av[NE], xv[NE];
+#pragma unroll
+        for (int b = 0; b < NE; ++b) {
+            const bool on = (m >> b) & 1u;
+            int j;
+            const double* src;
+            if (b < K) {  // lower: k = K - 1 - b
+                j = i - A.doff[K - 1 - b];
+                src = D + static_cast<int64_t>(K - b) * nl + j;
+            } else if (b == K) {
+                j = i;
+                src = D + i;
+            } else {  // upper: k = b - K - 1
+                j = i + A.doff[b - K - 1];
+                src = D + static_cast<int64_t>(b - K) * nl + i;
+            }
+            av[b] = on ? __ldg(src) : 0.0;
+            xv[b] = on ? op.x(j) : 0.0;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < NE; ++b)
+            if ((m >> b) & 1u) s = dadd(s, dmul(av[b], xv[b]));
+        op.finish(i, s, q, dots);
+    }
+    if constexpr (Op::NDOT > 0) block_dots<Op::NDOT>(dots, sink);
+}
+
+template <class Op>
+void launch_dia(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g, DotSink s,
+                unsigned grid) {
+    if (A.dk == 3)
+        LAUNCH_PDL(c, fam, bytes, (k_dia<Op, 3>), grid, RP_BLOCK, 0, A, op, g, s);
+    else
+        LAUNCH_PDL(c, fam, bytes, (k_dia<Op, 2>), grid, RP_BLOCK, 0, A, op, g, s);
+}
+
 template <class Op>
 void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, const Op& op, Gate g,
                     DotSink s, bool fixed_grid) {
@@ -796,6 +868,10 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
     int64_t cap = static_cast<int64_t>(c.num_sms) * RP_BLOCKS_PER_SM;
     unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
     if (fixed_grid) grid = static_cast<unsigned>(cap);  // deterministic dot order
+    if (A.dia) {  // symmetric-stencil form of level 0 (same grid and row deal)
+        launch_dia(c, fam, bytes, A, op, g, s, grid);
+        return;
+    }
     // coded columns: uint8 on <= 8 nnz/row, uint16 above (and on narrow partitioned levels)
     if (A.cmode == 1)
         launch_tma<Op, RP_CH, 0, uint8_t>(c, fam, bytes, A, op, g, s, grid);
@@ -831,7 +907,15 @@ void launch_rowpass(Ctx& c, const char* fam, double bytes, const CsrView& A, con
 // 1-/2-byte code of a coded column stream)
 double entry_bytes(const CsrView& A) { return A.cmode == 1 ? 9.0 : A.cmode == 2 ? 10.0 : 12.0; }
 
+// bytes of one pass over the operator itself (values + index structure)
+double mat_bytes(const CsrView& A) {
+    if (A.dia) return (8.0 * (A.dk + 1) + 1.0) * A.n;
+    return entry_bytes(A) * A.nnz + 4.0 * (A.n + 1);
+}
+
 double spmv_bytes(const CsrView& A) {
+    // symmetric-stencil form: D + K upper diagonals + the mask per row
+    if (A.dia) return (8.0 * (A.dk + 1) + 1.0) * A.n + 8.0 * A.ncols + 8.0 * A.n;
     // value + column per entry + row_ptr + x read once + y written once
     return entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.ncols + 8.0 * A.n;
 }
@@ -2591,7 +2675,7 @@ void vc_premul(Ctx& c, int64_t n, const double* f, const double* w, double om, d
 }
 void vc_down(Ctx& c, const CsrView& A, const double* f, const double* u0, double* r, Gate g) {
     // A + f read once, u0 gathered (read once), r written once
-    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    const double bytes = mat_bytes(A) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDown{f, u0, r}, g, {}, false);
 }
 void vc_restrict_general(Ctx& c, const CsrView& R, const double* r, double* fc, const double* wc, double om,
@@ -2604,7 +2688,7 @@ void vc_prolong_general(Ctx& c, const CsrView& P, const double* u, const double*
     launch_rowpass(c, "prolong", bytes, P, OpProlongG{e, u, out}, g, {}, false);
 }
 void vc_down_premul(Ctx& c, const CsrView& A, const double* f, const double* w, double om, double* r, Gate g) {
-    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 24.0 * A.n;
+    const double bytes = mat_bytes(A) + 24.0 * A.n;
     launch_rowpass(c, "vcycle_down", bytes, A, OpDownP{f, w, om, r}, g, {}, false);
 }
 // AMGR_VEC4=0: the scalar grid-stride prolongation kernels (A/B)
@@ -2653,7 +2737,7 @@ void vc_smooth_rows(Ctx& c, const CsrView& A, const int* rows, int64_t nrows, co
 }
 void vc_smooth(Ctx& c, const CsrView& A, const double* f, const double* w, double om, const double* u,
                double* out, Gate g) {
-    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n;
+    const double bytes = mat_bytes(A) + 32.0 * A.n;
     launch_rowpass(c, "vcycle_smooth", bytes, A, OpSmooth{f, w, om, u, out}, g, {}, false);
 }
 void vc_prolong(Ctx& c, int64_t n, const double* u, const int* agg, const double* uc, double* out,
@@ -2707,7 +2791,7 @@ bool smooth_then_spmv(Ctx& c, const CsrView& A, const double* f, const double* w
                       Gate g) {
     if (A.cmode != 1 || A.n == 0 || dgroups <= 0) return false;
     // one DRAM sweep of A (+ the vectors of both passes); the second sweep is L2
-    const double bytes = entry_bytes(A) * A.nnz + 4.0 * (A.n + 1) + 32.0 * A.n + (kind == 1 ? 24.0 : 24.0) * A.n;
+    const double bytes = mat_bytes(A) + 32.0 * A.n + (kind == 1 ? 24.0 : 24.0) * A.n;
     const OpSmooth op1{f, w, om, u, out};
     if (kind == 1) return launch_lag(c, A, op1, OpSpmvDotL2{out, y, ab}, g, s, done, dgroups, bytes);
     return launch_lag(c, A, op1, OpSpmvDot2L2{out, y, ab}, g, s, done, dgroups, bytes);
@@ -3010,6 +3094,107 @@ int max_group_span(Ctx& c, const int* rp, int64_t n) {
 void compare_i32(Ctx& c, const int* a, const int* b, int64_t n, int* diff) {
     if (n == 0) return;
     LAUNCH(c, "io", 0.0, k_compare_i32, grid_for(n, 256, c.num_sms * 16), 256, 0, a, b, n, diff);
+}
+
+
+// ---- symmetric-stencil form: masks (per pattern) and values (per rebuild) ----
+namespace {
+struct DiaOff {
+    int k;
+    int o[3];
+};
+// bit of column offset d in the mask order (ascending column), -1 if none
+__device__ __forceinline__ int dia_bit(const DiaOff& f, int64_t d) {
+    if (d == 0) return f.k;
+    for (int k = 0; k < f.k; ++k) {
+        if (d == -f.o[k]) return f.k - 1 - k;
+        if (d == f.o[k]) return f.k + 1 + k;
+    }
+    return -1;
+}
+__global__ void k_dia_mask(CsrView A, DiaOff f, uint8_t* mask, int* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < A.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        unsigned m = 0;
+        int last = -1;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const int b = dia_bit(f, static_cast<int64_t>(A.col[e]) - i);
+            if (b <= last) {  // unknown offset, unsorted or repeated column
+                atomicOr(bad, 1);
+                break;
+            }
+            m |= 1u << b;
+            last = b;
+        }
+        mask[i] = static_cast<uint8_t>(m);
+    }
+}
+// structural symmetry: (i, i+o_k) present <=> (i+o_k, i) present
+__global__ void k_dia_symm(int64_t n, DiaOff f, const uint8_t* mask, int* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned m = mask[i];
+        for (int k = 0; k < f.k; ++k) {
+            const bool up = (m >> (f.k + 1 + k)) & 1u, lo = (m >> (f.k - 1 - k)) & 1u;
+            const int64_t ju = i + f.o[k], jl = i - f.o[k];
+            const bool pu = ju < n && ((mask[ju] >> (f.k - 1 - k)) & 1u);
+            const bool pl = jl >= 0 && ((mask[jl] >> (f.k + 1 + k)) & 1u);
+            if (up != pu || lo != pl) atomicOr(bad, 1);
+        }
+    }
+}
+__global__ void k_dia_values(CsrView A, DiaOff f, const uint8_t* __restrict__ mask, double* __restrict__ dia,
+                             int* flag) {
+    const int64_t n = A.n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned m = mask[i];
+        const int base = __ldg(A.rp + i);
+        bool diff = false;
+        dia[i] = 0.0;
+        for (int k = 0; k < f.k; ++k) dia[static_cast<int64_t>(k + 1) * n + i] = 0.0;
+        for (int b = 0; b < 2 * f.k + 1; ++b) {
+            if (!((m >> b) & 1u)) continue;
+            const double v = __ldg(A.val + base + __popc(m & ((1u << b) - 1u)));
+            if (b == f.k) {
+                dia[i] = v;
+            } else if (b > f.k) {
+                dia[static_cast<int64_t>(b - f.k) * n + i] = v;
+            } else {  // lower entry k: must equal the partner's upper entry bit for bit
+                const int k = f.k - 1 - b;
+                const int64_t j = i - f.o[k];
+                const unsigned mj = mask[j];
+                const int bj = f.k + 1 + k;
+                const double u = __ldg(A.val + __ldg(A.rp + j) + __popc(mj & ((1u << bj) - 1u)));
+                diff |= __double_as_longlong(u) != __double_as_longlong(v);
+            }
+        }
+        if (diff) atomicOr(flag, 1);
+    }
+}
+DiaOff dia_off(int K, const int* off) {
+    DiaOff f{};
+    f.k = K;
+    for (int k = 0; k < K; ++k) f.o[k] = off[k];
+    return f;
+}
+}  // namespace
+
+bool dia_masks(Ctx& c, const CsrView& A, int K, const int* off, uint8_t* mask) {
+    if (A.n == 0 || K < 1 || K > 3) return false;
+    DevArray<int> bad(1, c.stream);
+    CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), c.stream));
+    const DiaOff f = dia_off(K, off);
+    LAUNCH(c, "setup", 0.0, k_dia_mask, grid_for(A.n, 256, c.num_sms * 8), 256, 0, A, f, mask, bad.get());
+    LAUNCH(c, "setup", 0.0, k_dia_symm, grid_for(A.n, 256, c.num_sms * 8), 256, 0, A.n, f, mask, bad.get());
+    return d2h_scalar(bad.get(), c.stream) == 0;
+}
+
+void dia_values(Ctx& c, const CsrView& A, int K, const int* off, const uint8_t* mask, double* dia, int* flag) {
+    if (A.n == 0) return;
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
+    LAUNCH(c, "dia", (12.0 + 8.0 * (K + 1) + 1.0) * A.n + 8.0 * A.nnz, k_dia_values,
+           grid_for(A.n, 256, c.num_sms * 8), 256, 0, A, dia_off(K, off), mask, dia, flag);
 }
 
 }  // namespace amgr

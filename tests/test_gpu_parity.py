@@ -848,3 +848,50 @@ def test_isolated_rows_and_ragged_lengths_match_reference(ctx):
     assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r2, f, fixed=True, prm=ref.params(**prm))))
     r2.free()
     r.free()
+
+
+def test_symmetric_stencil_form_bit_exact(ctx, monkeypatch):
+    """Level 0 of a grid stencil with bitwise-symmetric values runs its row
+    passes on the symmetric-stencil form (diagonal + K upper diagonals, k_dia):
+    V-cycle, level SpMV and partial update stay bit-exact against the
+    reference; values that are not bitwise symmetric (one a_ij != a_ji)
+    switch the passes back to the CSR arrays at that rebuild, and back again
+    when symmetry returns; AMGR_SYM_DIA=0 gives the same bits."""
+    A = P.grid3d_values("dambreak", 24, 7)
+    n = 24 ** 3
+    f = np.random.default_rng(8).uniform(-1, 1, n)
+    h = amg.setup(A, ctx=ctx)
+    r = ref.setup(A)
+    assert h.level_stencil(0) == (3, (1, 24, 576))
+    assert h.level_stencil(1) == (0, ())
+    assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r, f, fixed=True)))
+    assert np.array_equal(_bits(h.spmv(0, f)), _bits(ref.spmv(A, f)))
+    # one asymmetric entry: a(i, i+1) != a(i+1, i)
+    rp, ci, v = (np.asarray(x) for x in A)
+    i = 5000
+    e = rp[i] + int(np.nonzero(ci[rp[i]:rp[i + 1]] == i + 1)[0][0])
+    v2 = v.copy()
+    v2[e] = np.nextafter(v2[e], 0.0)
+    A2 = (rp, ci, v2)
+    h.rebuild_values(v2)
+    assert h.level_stencil(0) == (0, ())
+    r2 = ref.partial_update(r, A2)
+    assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(ref.vcycle(r2, f, fixed=True)))
+    assert np.array_equal(_bits(h.spmv(0, f)), _bits(ref.spmv(A2, f)))
+    r2.free()
+    h.rebuild_values(v)
+    assert h.level_stencil(0) == (3, (1, 24, 576))
+    u_on = amg.vcycle(h, f)
+    assert np.array_equal(_bits(u_on), _bits(ref.vcycle(r, f, fixed=True)))
+    _, st_on = amg.bicgstab(h, P.rhs(n))
+    monkeypatch.setenv("AMGR_SYM_DIA", "0")
+    h.rebuild_values(v)
+    assert h.level_stencil(0) == (0, ())
+    assert np.array_equal(_bits(amg.vcycle(h, f)), _bits(u_on))
+    _, st_off = amg.bicgstab(h, P.rhs(n))
+    assert abs(st_on.iterations - st_off.iterations) <= 1
+    monkeypatch.delenv("AMGR_SYM_DIA")
+    # 2D 5-point stencil: K = 2
+    h2 = amg.setup(P.poisson2d(64), ctx=ctx)
+    assert h2.level_stencil(0) == (2, (1, 64))
+    r.free()
