@@ -579,13 +579,21 @@ def run_replicas(a, rank, world, local):
         pass
     lvl0 = h.level_dims(0)
     cb0 = h.level_layout(0)["col_bytes"]
+    sk0, soff0 = h.level_stencil(0)
     csr_bytes = 12 * lvl0["nnz"] + 4 * (lvl0["nrows"] + 1) + 32 * lvl0["nrows"]
+    if sk0:
+        kern0 = f"k_dia<OpSmooth,{sk0}> level 0 (post-smoothing sweep, symmetric-stencil form)"
+        form0 = (f"(8*({sk0}+1)+1)*n + 32*n  (diagonal + {sk0} upper diagonals {list(soff0)} + 1-byte row mask, "
+                 f"then x, f, w read and the output written; DESIGN.md 3.1b)")
+    else:
+        kern0 = "k_rowpass<OpSmooth> level 0 (post-smoothing sweep)"
+        form0 = (f"(8+{cb0})*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads; "
+                 f"{cb0}-byte column codes, DESIGN.md 2)")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "k_rowpass<OpSmooth> level 0 (post-smoothing sweep)",
+                "kernel": kern0,
                 "bytes_per_launch": pbytes / cnt if cnt else None,
-                "bytes_formula": f"(8+{cb0})*nnz + 4*(n+1) + 32*n  (SURVEY.md 8(d) SpMV + f,w reads; "
-                                 f"{cb0}-byte column codes, DESIGN.md 2)",
+                "bytes_formula": form0,
                 "csr_equivalent_GB_s": (csr_bytes / (pms / cnt) / 1e6) if cnt else None,
                 "nnz": lvl0["nnz"], "n": lvl0["nrows"], "peak_source": peak_kind, "kernels": extra}
 
@@ -599,6 +607,8 @@ def run_replicas(a, rank, world, local):
     jac_b = sum(20 * nl[i] for i in range(Lh - 1))
     cbl = [h.level_layout(l)["col_bytes"] for l in range(Lh)]
     spmv = [(8 + cbl[i]) * zl[i] + 4 * (nl[i] + 1) + 16 * nl[i] for i in range(Lh)]
+    if sk0:  # level 0 in symmetric-stencil form
+        spmv[0] = (8 * (sk0 + 1) + 1) * nl[0] + 16 * nl[0]
     vc_b = sum(2 * spmv[i] + 64 * nl[i] for i in range(Lh - 1))
     it_b = 2 * vc_b + 2 * spmv[0] + 192 * nl[0]
     # one V-cycle, device time (stream-launched, 10 repetitions)
@@ -621,12 +631,18 @@ def run_replicas(a, rank, world, local):
         return {"algorithmic_GB": bytes_ / 1e9, "ms": ms, "GB_s": gbs, "frac_measured_peak": gbs / peak,
                 "frac_8TBs_nominal": gbs / 8000.0}
 
-    phases = {"rebuild": phase(rap_b + jac_b, rebuild_ms), "vcycle": phase(vc_b, vc_ms),
+    # the rebuild also refreshes level 0's symmetric-stencil copy (read the CSR
+    # values + row starts + masks, write D | U): bytes the reference does not move
+    dia_b = ((12 + 8 * (sk0 + 1) + 1) * nl[0] + 8 * zl[0]) if sk0 else 0
+    phases = {"rebuild": phase(rap_b + jac_b, rebuild_ms),
+              "rebuild_incl_level0_layout": phase(rap_b + jac_b + dia_b, rebuild_ms),
+              "vcycle": phase(vc_b, vc_ms),
               "bicgstab_iteration": phase(it_b, it_ms),
               "bytes_formulas": "SURVEY.md 8(d): RAP 12nnz_i+8nnz_i+1+4n_i+4(n_i+1 +1), Jacobi 20n_i, "
                                 "V-cycle sum(2 SpMV_i + 64 n_i), iteration 2 V + 2 SpMV_0 + 192 n_0; "
-                                "SpMV_i with (8 + column bytes) per entry",
-              "column_bytes_per_level": cbl}
+                                "SpMV_i with (8 + column bytes) per entry (level 0 in symmetric-stencil form: "
+                                "8 (K+1) + 1 bytes per row)",
+              "column_bytes_per_level": cbl, "level0_stencil_pairs": sk0}
     del vz
 
     # ---- e2e through the C-ABI with host buffers ----

@@ -475,9 +475,15 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
     const char* fe = std::getenv("AMGR_FUSE_JACOBI");
     const bool jac = h.prm.smoother == AMGR_SMOOTHER_JACOBI && fe && fe[0] == '1';
     std::vector<char> wdone(L, 0);
-    // level 0's symmetric-stencil copy on the side stream, concurrent with
-    // the Galerkin chain (both only read A_0)
-    if (start == 0 && sym_dia_prepare(h)) on_side(c, [&] { sym_dia_values(h); });
+    // level 0's symmetric-stencil copy: forked onto the side stream once the
+    // wide Galerkin levels are done (AMGR_DIA_FORK, default after level 1),
+    // so it overlaps the latency-bound small levels of the chain (next to the
+    // level-0 product it would compete for bandwidth; next to the one-CTA
+    // coarse factorization it cannot run: that CTA needs a whole SM)
+    const bool dia = start == 0 && sym_dia_prepare(h);
+    bool dia_done = false;
+    const char* dfe = std::getenv("AMGR_DIA_FORK");
+    const size_t dia_fork = dfe ? static_cast<size_t>(std::atoi(dfe)) : 1;
     build_grp_plans(h, start);
     for (size_t i = start; i + 1 < L; ++i) {
         c.cur_level = static_cast<int>(i);
@@ -559,6 +565,10 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
                         B.val.get(), A.pat->nnz, A.rap->max_chunk);
         }
         clk.end(PH_GALERKIN);
+        if (dia && !dia_done && i >= dia_fork) {
+            on_side(c, [&] { sym_dia_values(h); });
+            dia_done = true;
+        }
     }
     c.cur_level = static_cast<int>(L - 1);
     on_side(c, [&] {
@@ -573,6 +583,7 @@ void numeric_pass(Hier& h, PhaseClock& clk, size_t start = 0) {
         build_smoother(c, h.lv[i], h.prm, W.err.get() + i);
         clk.end(PH_SMOOTHER);
     }
+    if (dia && !dia_done) sym_dia_values(h);
     join_side(c);
     c.cur_level = -1;
     sa_jacobi_weights(h);

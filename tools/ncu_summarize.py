@@ -15,9 +15,10 @@ N0, Z0 = 16777216, 117047296   # level 0
 N1, Z1 = 8347648, 91350080     # level 1
 N2, Z2 = 2605983, 38621109     # level 2
 ALG = {  # name: (key, algorithmic bytes per launch, formula)
-    # level 0 runs the smoothing sweep on the uint8 coded column stream
-    "smooth_L0": ("vcycle_smooth@0", 9 * Z0 + 4 * (N0 + 1) + 32 * N0, "9*nnz + 4*(n+1) + 32*n (1-byte column codes)"),
-    "down_L0": ("vcycle_down@0", 9 * Z0 + 4 * (N0 + 1) + 24 * N0, "9*nnz + 4*(n+1) + 24*n (1-byte codes; u0 folded: w replaces u0)"),
+    # level 0 runs in symmetric-stencil form (k_dia): diagonal +
+    # 3 upper diagonals + a 1-byte row mask = 33 bytes per row
+    "smooth_L0": ("vcycle_smooth@0", 33 * N0 + 32 * N0, "33*n + 32*n (D + 3 upper diagonals + mask; x, f, w, out)"),
+    "down_L0": ("vcycle_down@0", 33 * N0 + 24 * N0, "33*n + 24*n (symmetric-stencil form; u0 folded: w replaces u0)"),
     "down_L1": ("vcycle_down@1", 10 * Z1 + 4 * (N1 + 1) + 24 * N1, "10*nnz + 4*(n+1) + 24*n (2-byte column codes)"),
     # k_rap_grp (round 2): the Galerkin product + the fine level's fused damped-Jacobi rebuild
     "rap_L0": ("rap@0", 12 * Z0 + 8 * Z1 + 4 * N0 + 4 * (N1 + 1) + 20 * N0,

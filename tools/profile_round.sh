@@ -14,10 +14,11 @@ python tools/region_driver.py 256 all > gpurun_out/plain_all.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
       --log-file gpurun_out/${R}_launches.csv python tools/region_driver.py 256 all > gpurun_out/ncu_list.log 2>&1
 python tools/region_driver.py 256 vcycle > gpurun_out/plain_v.log 2>&1 && {
-  # V-cycle launch order of ^k_rowpass$: down L0..L13 (14), up L13..L0 (14)
-  full smooth_L0 vcycle '^k_rowpass$' 27
-  full down_L0 vcycle '^k_rowpass$' 0
-  full down_L1 vcycle '^k_rowpass$' 1
+  # level 0 runs k_dia (symmetric-stencil form): down L0 (0), smooth L0 (1);
+  # ^k_rowpass$ then carries down L1..L13 and up L13..L1
+  full smooth_L0 vcycle '^k_dia$' 1
+  full down_L0 vcycle '^k_dia$' 0
+  full down_L1 vcycle '^k_rowpass$' 0
 }
 python tools/region_driver.py 256 rebuild > gpurun_out/plain_r.log 2>&1 && {
   full rap_L0 rebuild '^k_rap_grp$' 0
