@@ -3195,8 +3195,10 @@ void dia_values(Ctx& c, const CsrView& A, int K, const int* off, const uint8_t* 
     CK(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
     // 6 of 8 block slots per SM (measured: the full grid slows the Galerkin
     // levels it overlaps more than it gains)
+    const char* e = std::getenv("AMGR_DIA_BLOCKS");
+    const int per_sm = e ? std::max(1, std::atoi(e)) : 6;
     LAUNCH(c, "dia", (12.0 + 8.0 * (K + 1) + 1.0) * A.n + 8.0 * A.nnz, k_dia_values,
-           grid_for(A.n, 256, c.num_sms * 6), 256, 0, A, dia_off(K, off), mask, dia, flag);
+           grid_for(A.n, 256, static_cast<int64_t>(c.num_sms) * per_sm), 256, 0, A, dia_off(K, off), mask, dia, flag);
 }
 
 }  // namespace amgr
